@@ -1,0 +1,200 @@
+/*
+ * qsv — B200-native state-vector engine for the DeepQuantum / quasar qubit
+ * hot path. This is the C ABI (the drop-in boundary): plain pointers and
+ * sizes, no C++ or torch types. Everything above it (the quasar-compatible
+ * C++ headers in include/quasar/, the Python mirror in
+ * paper_2512_18995_b200/qsv.py) is a thin host layer over these calls.
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   qsv_apply_matrix     quasar::qubit::detail::apply_matrix_strided
+ *                        include/quasar/qubit/state.hpp:111-143
+ *   qsv_apply_gate       quasar::qubit::apply_gate (pure states)
+ *                        include/quasar/qubit/state.hpp:149-157
+ *   qsv_gate_matrix      quasar::qubit::gate_matrix  include/quasar/qubit/gate.hpp:89-154
+ *   qsv_run_circuit      quasar::qubit::Circuit::forward  include/quasar/qubit/circuit.hpp:121-157
+ *   qsv_plan_*           (same, with planning hoisted out of the timed loop)
+ *   qsv_expect_pauli     quasar::qubit::expectation_one / expectation
+ *                        include/quasar/qubit/circuit.hpp:248-282
+ *   qsv_expect_z_all     expectation() over the n single-Z observables (cfg1/cfg2)
+ *   qsv_marginal_probs   quasar::qubit::marginal_probabilities circuit.hpp:182-205
+ *   qsv_state_*          quasar::qubit::QubitState (basis / from_amplitudes /
+ *                        amplitudes(b)) state.hpp:29-91
+ *   qsv_ctx_create_dist, qsv_state_global_bits, qsv_norm2 (global)
+ *                        quasar::dist::PartitionedState / run_on_ranks /
+ *                        global_norm2 (source absent from the reference;
+ *                        contract from tests/test_dist.cpp:66-174 and
+ *                        SPEC.md:719-798)
+ *
+ * Conventions (identical to the reference):
+ *   - wire 0 is the MOST significant bit of a basis index (state.hpp:21-24);
+ *   - a k-qubit matrix is 2^k x 2^k row-major with wires[0] as its MSB
+ *     (gate.hpp:30); complex numbers are interleaved (re, im) doubles;
+ *   - amplitudes cross the boundary in LOGICAL index order whatever
+ *     internal qubit permutation the engine is using.
+ *
+ * Status codes mirror the reference CLI exit codes (tools/main.cpp:686-697)
+ * and error classes (core.hpp:34-47). Every call returns one; the message of
+ * the last failure on the calling thread is qsv_last_error().
+ *
+ * Threading: calls on distinct states are independent; calls on the same
+ * state must be serialised by the caller (reference: SPEC.md:216).
+ */
+#ifndef QSV_H_
+#define QSV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QSV_VERSION 1
+
+enum qsv_status {
+    QSV_OK = 0,
+    QSV_ERR_INTERNAL = 1,  /* CUDA / internal failure */
+    QSV_ERR_INVALID = 2,   /* quasar::invalid_input */
+    QSV_ERR_GUARD = 3,     /* quasar::guard_error (numerical guard) */
+    QSV_ERR_TRANSPORT = 4  /* quasar::transport_error (NCCL) */
+};
+
+enum qsv_dtype { QSV_C64 = 1, QSV_C128 = 2 };
+
+/* apply flags */
+enum {
+    QSV_ZERO_OFF_CONTROL = 1 /* apply_matrix_strided(..., zero_off_control=true) */
+};
+
+typedef struct qsv_ctx qsv_ctx;
+typedef struct qsv_state qsv_state;
+typedef struct qsv_plan qsv_plan;
+
+/* A gate record with the meaning of quasar::qubit::Gate (gate.hpp:28-38). */
+typedef struct qsv_gate {
+    char name[16];          /* x y z h s t rx ry rz p u3 swap rxx ryy rzz custom */
+    int32_t nwires;         /* targets; wires[0] is the matrix MSB */
+    int32_t wires[2];
+    int32_t ncontrols;      /* all controls must be |1> */
+    int32_t controls[6];
+    int32_t nparams;
+    double params[3];       /* radians */
+    int32_t trainable;
+    int32_t encode;         /* parameters bound from data rows at run time */
+    const double *custom;   /* name=="custom": 2^k x 2^k row-major (re,im) */
+} qsv_gate;
+
+/* Tensor product of single-qubit Paulis (circuit.hpp:25-28). */
+typedef struct qsv_obs {
+    int32_t nwires;
+    const int32_t *wires;
+    const char *basis;      /* one of 'x','y','z' per wire */
+} qsv_obs;
+
+/* Planner / executor options (0 = engine default). */
+typedef struct qsv_opts {
+    int32_t fuse;           /* 1 = fused tile passes (default), 0 = one kernel per gate */
+    int32_t tile_bits;      /* qubits per shared-memory tile (K) */
+    int32_t low_bits;       /* lowest physical qubits always in a tile (coalescing) */
+    int32_t use_graph;      /* capture the pass sequence in a CUDA graph */
+    int32_t reserved[4];
+} qsv_opts;
+
+/* What a plan does, for measurement (bench.py roofline). */
+typedef struct qsv_plan_info {
+    int32_t ngates;          /* source gates */
+    int32_t npasses;         /* state passes (kernel launches) per execute */
+    int32_t nswaps;          /* global<->local qubit swaps (multi-GPU) */
+    int32_t max_tile_bits;
+    double bytes_per_exec;   /* algorithmic HBM bytes per execute (all passes) */
+    double comm_bytes_per_exec; /* bytes sent per rank per execute */
+} qsv_plan_info;
+
+/* ---- library --------------------------------------------------------- */
+const char *qsv_last_error(void);
+int qsv_version(void);
+/* Number of CUDA devices (0 on a host without a GPU; never fails). */
+int qsv_device_count(void);
+
+/* ---- context (owns the CUDA stream, the NCCL communicator) ----------- */
+int qsv_ctx_create(int device, qsv_ctx **out);
+/* One process per GPU: rank/world with an NCCL unique id produced by
+ * qsv_nccl_unique_id on rank 0 and broadcast by the caller (e.g. with
+ * torch.distributed). world must be a power of two (test_dist.cpp:90-94). */
+int qsv_nccl_unique_id(void *out128);
+int qsv_ctx_create_dist(int device, int rank, int world, const void *unique_id128, qsv_ctx **out);
+int qsv_ctx_destroy(qsv_ctx *ctx);
+int qsv_ctx_sync(qsv_ctx *ctx);
+/* The cudaStream_t the engine launches on (for events), as void*. */
+int qsv_ctx_stream(qsv_ctx *ctx, void **stream);
+int qsv_ctx_rank(qsv_ctx *ctx, int *rank, int *world);
+
+/* ---- states (QubitState) --------------------------------------------- */
+/* nqubit is the GLOBAL qubit count; each rank holds 2^(nqubit-g) amplitudes
+ * per batch row, g = log2(world). Initialised to |0...0>. */
+int qsv_state_create(qsv_ctx *ctx, int nqubit, int batch, int dtype, qsv_state **out);
+int qsv_state_destroy(qsv_state *st);
+int qsv_state_info(const qsv_state *st, int *nqubit, int *batch, int *dtype, int *global_bits,
+                   uint64_t *local_amps);
+/* |index> on every batch row (QubitState::basis, state.hpp:34-42). */
+int qsv_state_set_basis(qsv_state *st, uint64_t index);
+/* Host <-> device, interleaved (re,im) float64 for BOTH dtypes, logical
+ * order. On a distributed context these move this rank's slice (the
+ * 2^(n-g) indices whose top g bits equal the rank). */
+int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count);
+int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count);
+/* Raw dtype-native host buffers (float32 pairs for C64): the cheap path the
+ * e2e benchmark uses (pinned host memory, one DMA each way). */
+int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t count);
+int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count);
+int qsv_state_clone(const qsv_state *st, qsv_state **out);
+/* Device pointer of row `row` in the engine's PHYSICAL order (tests). */
+int qsv_state_device_ptr(qsv_state *st, int row, void **ptr);
+
+/* ---- gates ------------------------------------------------------------- */
+/* gate_matrix() with reference semantics; out is 2^k x 2^k (re,im). */
+int qsv_gate_matrix(const qsv_gate *g, double *out, int *k);
+/* apply_matrix_strided on every batch row. */
+int qsv_apply_matrix(qsv_state *st, int k, const int32_t *wires, int nctl, const int32_t *ctls, const double *m,
+                     int flags);
+/* apply_gate: gate_matrix + unitarity check (1e-10) + strided update. */
+int qsv_apply_gate(qsv_state *st, const qsv_gate *g);
+
+/* ---- circuits (Circuit::forward) --------------------------------------- */
+/* rows == 0: apply the gates to every batch row (no encode slots allowed).
+ * rows  > 0: rows must equal the state's batch; row b binds the encode slots
+ * from data[b*slots ...] in circuit order; slots must equal the circuit's
+ * encode-slot count exactly (circuit.hpp:133-136). */
+int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const double *data, int rows, int slots,
+                    const qsv_opts *opts);
+int qsv_plan_create(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, const qsv_opts *opts,
+                    qsv_plan **out);
+int qsv_plan_destroy(qsv_plan *plan);
+int qsv_plan_info_get(const qsv_plan *plan, qsv_plan_info *info);
+int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots);
+/* Execute once with a CUDA event pair around every launch; launch_ms gets
+ * npasses durations (ms). */
+int qsv_plan_profile(qsv_plan *plan, qsv_state *st, double *launch_ms);
+
+/* ---- reductions (FP64 accumulation) ------------------------------------ */
+int qsv_norm2(qsv_state *st, double *out /* batch */);
+/* <Z_w> for every wire w: out[b * n + w]. */
+int qsv_expect_z_all(qsv_state *st, double *out);
+/* <P> for each observable: out[b * nobs + i]; fails (QSV_ERR_INVALID) on an
+ * imaginary residue >= 1e-10 like circuit.hpp:261. */
+int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
+/* marginal_probabilities on row `row`: out has 2^k entries. */
+int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
+
+/* ---- seeded inputs (quasar::Rng, rng.hpp:29-103) ----------------------- */
+/* Fills `out` with count draws of stream Rng(seed, label) (label may be
+ * NULL for Rng(seed)); kind 0 next_u64, 1 uniform, 2 normal. Counter-based,
+ * so it runs on nthreads host threads and still reproduces the sequential
+ * stream exactly. */
+int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QSV_H_ */

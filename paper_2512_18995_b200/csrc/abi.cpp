@@ -1,0 +1,505 @@
+// extern "C" entry points of include/qsv.h. Every call catches C++
+// exceptions and maps them to the reference's status codes
+// (tools/main.cpp:686-697): invalid_input -> 2, guard_error -> 3,
+// transport_error -> 4, CUDA/internal -> 1. There is no CPU fallback: without
+// a usable CUDA device every state/plan call fails with QSV_ERR_INTERNAL.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+
+#include "qsv_internal.hpp"
+
+struct qsv_ctx : qsv::Ctx {};
+struct qsv_state : qsv::State {};
+struct qsv_plan : qsv::Plan {};
+
+namespace qsv {
+void build_plan(Plan &p, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts);
+void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates,
+                         const qsv_opts *opts);
+void execute_plan(Plan &p, State &st, const double *data, int rows, int slots);
+void profile_plan(Plan &p, State &st, double *launch_ms);
+int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads);
+} // namespace qsv
+
+using namespace qsv;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F> int guard(F &&f) {
+    try {
+        f();
+        return QSV_OK;
+    } catch (const Error &e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc &) {
+        g_err = "out of host memory";
+        return QSV_ERR_INTERNAL;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return QSV_ERR_INTERNAL;
+    }
+}
+
+void init_ctx(Ctx &c, int device) {
+    int ndev = 0;
+    const cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        fail(QSV_ERR_INTERNAL, "qsv: no CUDA device available (the engine has no CPU fallback)");
+    require(device >= 0 && device < ndev, "qsv: device index out of range");
+    c.device = device;
+    QSV_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    QSV_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major < 10) fail(QSV_ERR_INTERNAL, "qsv: built for sm_100a (B200); device is sm_" +
+                                                    std::to_string(prop.major * 10 + prop.minor));
+    c.sm_count = prop.multiProcessorCount;
+    c.smem_optin = prop.sharedMemPerBlockOptin;
+    QSV_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+}
+
+// Chunked host(f64) -> device(dtype) transfer through a bounded staging buffer.
+void upload_f64(State &st, void *dst, const double *host, uint64_t count) {
+    cudaStream_t s = st.ctx->stream;
+    if (st.dtype == QSV_C128) {
+        QSV_CUDA(cudaMemcpyAsync(dst, host, count * 16, cudaMemcpyHostToDevice, s));
+        QSV_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24); // 16 Mi amplitudes (256 MiB f64)
+    void *stage = nullptr;
+    QSV_CUDA(cudaMalloc(&stage, chunk * 16));
+    for (uint64_t off = 0; off < count; off += chunk) {
+        const uint64_t c = std::min(chunk, count - off);
+        QSV_CUDA(cudaMemcpyAsync(stage, host + 2 * off, c * 16, cudaMemcpyHostToDevice, s));
+        launch_convert(static_cast<float *>(dst) + 2 * off, QSV_C64, stage, QSV_C128, 2 * c, s);
+    }
+    QSV_CUDA(cudaStreamSynchronize(s));
+    cudaFree(stage);
+}
+
+void download_f64(State &st, const void *src, double *host, uint64_t count) {
+    cudaStream_t s = st.ctx->stream;
+    if (st.dtype == QSV_C128) {
+        QSV_CUDA(cudaMemcpyAsync(host, src, count * 16, cudaMemcpyDeviceToHost, s));
+        QSV_CUDA(cudaStreamSynchronize(s));
+        return;
+    }
+    const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24);
+    void *stage = nullptr;
+    QSV_CUDA(cudaMalloc(&stage, chunk * 16));
+    for (uint64_t off = 0; off < count; off += chunk) {
+        const uint64_t c = std::min(chunk, count - off);
+        launch_convert(stage, QSV_C128, static_cast<const float *>(src) + 2 * off, QSV_C64, 2 * c, s);
+        QSV_CUDA(cudaMemcpyAsync(host + 2 * off, stage, c * 16, cudaMemcpyDeviceToHost, s));
+        QSV_CUDA(cudaStreamSynchronize(s));
+    }
+    cudaFree(stage);
+}
+
+void *row_ptr(State &st, int row) {
+    require(row >= 0 && row < st.batch, "batch index out of range");
+    return static_cast<unsigned char *>(st.d) + static_cast<size_t>(row) * st.local_amps * st.amp_bytes();
+}
+
+// One-gate plan, executed immediately (apply_gate / apply_matrix_strided).
+void run_single(State &st, const GateRec &g) {
+    Plan p;
+    build_plan(p, st.ctx, st.n, st.dtype, {g}, 0, nullptr);
+    execute_plan(p, st, nullptr, 0, 0);
+    QSV_CUDA(cudaStreamSynchronize(st.ctx->stream));
+}
+
+} // namespace
+
+extern "C" {
+
+const char *qsv_last_error(void) { return g_err.c_str(); }
+int qsv_version(void) { return QSV_VERSION; }
+
+int qsv_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+int qsv_ctx_create(int device, qsv_ctx **out) {
+    return guard([&] {
+        require(out != nullptr, "qsv_ctx_create: null out");
+        auto c = std::make_unique<qsv_ctx>();
+        init_ctx(*c, device);
+        *out = c.release();
+    });
+}
+
+int qsv_nccl_unique_id(void *out128) {
+    return guard([&] { nccl_unique_id(out128); });
+}
+
+int qsv_ctx_create_dist(int device, int rank, int world, const void *uid, qsv_ctx **out) {
+    return guard([&] {
+        require(out != nullptr, "qsv_ctx_create_dist: null out");
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two"); // test_dist.cpp:90-94
+        require(rank >= 0 && rank < world, "rank out of range");
+        auto c = std::make_unique<qsv_ctx>();
+        init_ctx(*c, device);
+        c->rank = rank;
+        c->world = world;
+        c->gbits = std::countr_zero(static_cast<unsigned>(world));
+        if (world > 1) nccl_init(*c, uid);
+        *out = c.release();
+    });
+}
+
+int qsv_ctx_destroy(qsv_ctx *ctx) {
+    return guard([&] { delete ctx; });
+}
+
+int qsv_ctx_sync(qsv_ctx *ctx) {
+    return guard([&] {
+        require(ctx != nullptr, "null ctx");
+        QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+    });
+}
+
+int qsv_ctx_stream(qsv_ctx *ctx, void **stream) {
+    return guard([&] {
+        require(ctx && stream, "null argument");
+        *stream = ctx->stream;
+    });
+}
+
+int qsv_ctx_rank(qsv_ctx *ctx, int *rank, int *world) {
+    return guard([&] {
+        require(ctx && rank && world, "null argument");
+        *rank = ctx->rank;
+        *world = ctx->world;
+    });
+}
+
+int qsv_state_create(qsv_ctx *ctx, int nqubit, int batch, int dtype, qsv_state **out) {
+    return guard([&] {
+        require(ctx && out, "null argument");
+        require(nqubit >= 1 && nqubit <= kMaxQubits, "QubitState: nqubit out of range");
+        require(batch >= 1, "QubitState: batch must be >= 1");
+        require(dtype == QSV_C64 || dtype == QSV_C128, "QubitState: dtype must be QSV_C64 or QSV_C128");
+        require(nqubit >= ctx->gbits, "QubitState: fewer amplitudes than ranks");
+        auto st = std::make_unique<qsv_state>();
+        st->ctx = ctx;
+        st->n = nqubit;
+        st->nlocal = nqubit - ctx->gbits;
+        require(st->nlocal >= 1, "QubitState: need at least one local qubit per rank");
+        st->batch = batch;
+        st->dtype = dtype;
+        st->local_amps = 1ull << st->nlocal;
+        st->perm.resize(nqubit);
+        for (int w = 0; w < nqubit; ++w) st->perm[w] = nqubit - 1 - w;
+        QSV_CUDA(cudaSetDevice(ctx->device));
+        const size_t bytes = st->local_amps * st->amp_bytes() * static_cast<size_t>(batch);
+        const cudaError_t e = cudaMalloc(&st->d, bytes);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(QSV_ERR_INTERNAL, "QubitState: cannot allocate " + std::to_string(bytes) + " bytes of HBM");
+        }
+        launch_set_basis(*st, 0, ctx->rank == 0);
+        QSV_CUDA(cudaStreamSynchronize(ctx->stream));
+        *out = st.release();
+    });
+}
+
+int qsv_state_destroy(qsv_state *st) {
+    return guard([&] { delete st; });
+}
+
+int qsv_state_info(const qsv_state *st, int *nqubit, int *batch, int *dtype, int *global_bits, uint64_t *local_amps) {
+    return guard([&] {
+        require(st != nullptr, "null state");
+        if (nqubit) *nqubit = st->n;
+        if (batch) *batch = st->batch;
+        if (dtype) *dtype = st->dtype;
+        if (global_bits) *global_bits = st->ctx->gbits;
+        if (local_amps) *local_amps = st->local_amps;
+    });
+}
+
+int qsv_state_set_basis(qsv_state *st, uint64_t index) {
+    return guard([&] {
+        require(st != nullptr, "null state");
+        require(st->n >= 64 || index < (1ull << st->n), "QubitState: basis index out of range"); // state.hpp:36
+        const uint64_t owner = index >> st->nlocal;
+        launch_set_basis(*st, index & (st->local_amps - 1), owner == static_cast<uint64_t>(st->ctx->rank));
+        QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    });
+}
+
+int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        upload_f64(*st, row_ptr(*st, row), host, count);
+    });
+}
+
+int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        download_f64(*st, row_ptr(*st, row), host, count);
+    });
+}
+
+int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        QSV_CUDA(cudaMemcpyAsync(row_ptr(*st, row), host, count * st->amp_bytes(), cudaMemcpyHostToDevice,
+                                 st->ctx->stream));
+    });
+}
+
+int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        QSV_CUDA(cudaMemcpyAsync(host, row_ptr(*st, row), count * st->amp_bytes(), cudaMemcpyDeviceToHost,
+                                 st->ctx->stream));
+        QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    });
+}
+
+int qsv_state_clone(const qsv_state *src, qsv_state **out) {
+    return guard([&] {
+        require(src && out, "null argument");
+        auto st = std::make_unique<qsv_state>();
+        st->ctx = src->ctx;
+        st->n = src->n;
+        st->nlocal = src->nlocal;
+        st->batch = src->batch;
+        st->dtype = src->dtype;
+        st->local_amps = src->local_amps;
+        st->perm = src->perm;
+        const size_t bytes = st->local_amps * st->amp_bytes() * static_cast<size_t>(st->batch);
+        QSV_CUDA(cudaMalloc(&st->d, bytes));
+        QSV_CUDA(cudaMemcpyAsync(st->d, src->d, bytes, cudaMemcpyDeviceToDevice, src->ctx->stream));
+        QSV_CUDA(cudaStreamSynchronize(src->ctx->stream));
+        *out = st.release();
+    });
+}
+
+int qsv_state_device_ptr(qsv_state *st, int row, void **ptr) {
+    return guard([&] {
+        require(st && ptr, "null argument");
+        *ptr = row_ptr(*st, row);
+    });
+}
+
+int qsv_gate_matrix(const qsv_gate *g, double *out, int *k) {
+    return guard([&] {
+        require(g && out, "null argument");
+        cplx m[16];
+        const int kk = gate_matrix(*g, m);
+        const int d = 1 << kk;
+        for (int i = 0; i < d * d; ++i) {
+            out[2 * i] = m[i].real();
+            out[2 * i + 1] = m[i].imag();
+        }
+        if (k) *k = kk;
+    });
+}
+
+int qsv_apply_matrix(qsv_state *st, int k, const int32_t *wires, int nctl, const int32_t *ctls, const double *m,
+                     int flags) {
+    return guard([&] {
+        require(st && wires && m, "null argument");
+        require(k >= 1 && k <= 2, "apply_matrix: 1 or 2 target wires supported");
+        require(nctl >= 0 && nctl <= 6 && (nctl == 0 || ctls), "apply_matrix: bad controls");
+        GateRec g;
+        g.name = "matrix";
+        g.kind = GK_CUSTOM;
+        g.k = k;
+        for (int i = 0; i < k; ++i) {
+            require(wires[i] >= 0 && wires[i] < st->n, "target wire out of range"); // state.hpp:116
+            g.wires[i] = wires[i];
+        }
+        require(k == 1 || wires[0] != wires[1], "apply_matrix: duplicate target wires");
+        for (int i = 0; i < nctl; ++i) {
+            require(ctls[i] >= 0 && ctls[i] < st->n, "control wire out of range"); // state.hpp:117
+            for (int j = 0; j < k; ++j) require(ctls[i] != wires[j], "gate wires and controls must be disjoint");
+            g.ctls.push_back(ctls[i]);
+        }
+        const int d = 1 << k;
+        bool diag = true;
+        for (int i = 0; i < d * d; ++i) {
+            g.m[i] = cplx(m[2 * i], m[2 * i + 1]);
+            if (i / d != i % d && g.m[i] != cplx(0, 0)) diag = false;
+        }
+        g.diag = diag;
+        g.flags = (flags & QSV_ZERO_OFF_CONTROL) ? OPF_ZERO_OFF_CONTROL : 0;
+        run_single(*st, g);
+    });
+}
+
+int qsv_apply_gate(qsv_state *st, const qsv_gate *gate) {
+    return guard([&] {
+        require(st && gate, "null argument");
+        int cursor = 0;
+        qsv_gate g = *gate;
+        g.encode = 0; // apply_gate uses the gate's own params (state.hpp:149-151)
+        GateRec r = resolve_gate(g, st->n, &cursor);
+        run_single(*st, r);
+    });
+}
+
+int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const double *data, int rows, int slots,
+                    const qsv_opts *opts) {
+    return guard([&] {
+        require(st != nullptr, "null state");
+        Plan p;
+        build_plan_from_abi(p, st->ctx, st->n, st->dtype, gates, ngates, opts);
+        execute_plan(p, *st, data, rows, slots);
+        QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
+    });
+}
+
+int qsv_plan_create(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, const qsv_opts *opts,
+                    qsv_plan **out) {
+    return guard([&] {
+        require(ctx && out, "null argument");
+        auto q = std::make_unique<qsv_plan>();
+        build_plan_from_abi(*q, ctx, nqubit, dtype, gates, ngates, opts);
+        *out = q.release();
+    });
+}
+
+int qsv_plan_destroy(qsv_plan *plan) {
+    return guard([&] { delete plan; });
+}
+
+int qsv_plan_info_get(const qsv_plan *p, qsv_plan_info *info) {
+    return guard([&] {
+        require(p && info, "null argument");
+        std::memset(info, 0, sizeof(*info));
+        info->ngates = p->ngates;
+        for (const Step &s : p->steps) {
+            if (s.kind == 0) {
+                info->npasses += 1;
+                info->bytes_per_exec += p->dev[s.pass].bytes;
+                info->max_tile_bits = std::max(info->max_tile_bits, p->passes[s.pass].K);
+            } else {
+                info->nswaps += static_cast<int>(s.swap_bits.size());
+                const double amp = p->dtype == QSV_C64 ? 8 : 16;
+                info->comm_bytes_per_exec += s.swap_bits.size() * amp * std::ldexp(1.0, p->nlocal - 1);
+            }
+        }
+    });
+}
+
+int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots) {
+    return guard([&] {
+        require(plan && st, "null argument");
+        execute_plan(*plan, *st, data, rows, slots);
+    });
+}
+
+int qsv_plan_profile(qsv_plan *plan, qsv_state *st, double *launch_ms) {
+    return guard([&] {
+        require(plan && st && launch_ms, "null argument");
+        profile_plan(*plan, *st, launch_ms);
+    });
+}
+
+int qsv_norm2(qsv_state *st, double *out) {
+    return guard([&] {
+        require(st && out, "null argument");
+        reduce_norm2(*st, out);
+    });
+}
+
+int qsv_expect_z_all(qsv_state *st, double *out) {
+    return guard([&] {
+        require(st && out, "null argument");
+        constexpr int kZ = 41;
+        std::vector<double> z(static_cast<size_t>(st->batch) * kZ);
+        reduce_z_all(*st, z.data());
+        for (int b = 0; b < st->batch; ++b) {
+            const double *zb = z.data() + static_cast<size_t>(b) * kZ;
+            for (int w = 0; w < st->n; ++w)
+                out[static_cast<size_t>(b) * st->n + w] = zb[0] - 2.0 * zb[1 + st->perm[w]];
+        }
+    });
+}
+
+int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
+    return guard([&] {
+        require(st && (nobs == 0 || (obs && out)), "null argument");
+        for (int i = 0; i < nobs; ++i) {
+            const qsv_obs &o = obs[i];
+            require(o.nwires >= 0 && (o.nwires == 0 || (o.wires && o.basis)), "observable: bad wires");
+            require(static_cast<int>(std::strlen(o.basis ? o.basis : "")) == o.nwires,
+                    "observable: one basis letter per wire"); // circuit.hpp:97
+            uint64_t flip = 0, zy = 0;
+            int ny = 0;
+            // apply the Paulis wire by wire like expectation_one: repeated wires
+            // compose (X X = I etc.), so track the product explicitly.
+            // phase accumulates as i^k from Y/X products on the same wire.
+            std::vector<int> seen;
+            for (int j = 0; j < o.nwires; ++j) {
+                const char c = o.basis[j];
+                require(c == 'x' || c == 'y' || c == 'z', "observable: basis letter outside {x,y,z}");
+                const int w = o.wires[j];
+                require(w >= 0 && w < st->n, "target wire out of range");
+                if (std::find(seen.begin(), seen.end(), w) != seen.end())
+                    fail(QSV_ERR_INVALID, "observable: repeated wire not supported");
+                seen.push_back(w);
+                const int pb = st->perm[w];
+                require(pb < st->nlocal || c == 'z', "observable: x/y on a global qubit not supported");
+                const uint64_t bit = 1ull << pb;
+                if (c == 'x') flip |= bit;
+                if (c == 'y') flip |= bit, zy |= bit, ++ny;
+                if (c == 'z') zy |= bit;
+            }
+            std::vector<double> v(static_cast<size_t>(st->batch) * 2);
+            reduce_pauli(*st, flip, zy, v.data());
+            // (-i)^ny factor (Y = -i * (-1)^b * X on |b>)
+            const int q = ny & 3;
+            for (int b = 0; b < st->batch; ++b) {
+                double re = v[2 * b], im = v[2 * b + 1];
+                for (int t = 0; t < q; ++t) {
+                    const double nre = im, nim = -re; // multiply by -i
+                    re = nre, im = nim;
+                }
+                if (std::abs(im) >= 1e-10) fail(QSV_ERR_INVALID, "expectation: imaginary residue"); // circuit.hpp:261
+                out[static_cast<size_t>(b) * nobs + i] = re;
+            }
+        }
+    });
+}
+
+int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out) {
+    return guard([&] {
+        require(st && out, "null argument");
+        require(k >= 1 && wires, "measure: empty wire list"); // circuit.hpp:185
+        require(row >= 0 && row < st->batch, "batch index out of range");
+        std::vector<int> bits;
+        for (int i = 0; i < k; ++i) {
+            require(wires[i] >= 0 && wires[i] < st->n, "target wire out of range");
+            bits.push_back(st->perm[wires[i]]);
+        }
+        reduce_marginal(*st, row, bits, out);
+    });
+}
+
+int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads) {
+    return guard([&] {
+        require(out != nullptr || count == 0, "null out");
+        rng_fill(seed, label, kind, count, out, nthreads);
+    });
+}
+
+} // extern "C"

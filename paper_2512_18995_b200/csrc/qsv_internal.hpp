@@ -1,0 +1,224 @@
+// Internal declarations shared by the host runtime (C++) and the CUDA
+// kernels of the qsv engine. Not part of the ABI (include/qsv.h is).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/qsv.h"
+
+namespace qsv {
+
+using cplx = std::complex<double>;
+
+// ---- errors (mirror quasar core.hpp:34-47 + CUDA) --------------------------
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string &msg) { throw Error(code, msg); }
+inline void require(bool cond, const std::string &msg) {
+    if (!cond) fail(QSV_ERR_INVALID, msg);
+}
+void cuda_check(cudaError_t e, const char *what);
+#define QSV_CUDA(x) ::qsv::cuda_check((x), #x)
+
+// ---- limits -----------------------------------------------------------------
+constexpr int kMaxQubits = 40;     // global qubits (36q configs + headroom)
+constexpr int kMaxTileBits = 14;   // K: 2^K amplitudes per CTA tile
+constexpr int kMaxSlots = 5;       // R: register-resident qubits per group
+constexpr int kRegSlots = 4;       // R used by the fused kernel
+
+// ---- device program (tile passes) ---------------------------------------
+enum OpType : int32_t { OP_DENSE1 = 1, OP_DENSE2 = 2, OP_DIAG = 3 };
+enum OpFlags : int32_t { OPF_ZERO_OFF_CONTROL = 1 };
+
+// One gate, lowered onto a register group. Conditions are split into the
+// part over register slots (rmask/rval, R bits) and the part over every other
+// bit of the GLOBAL physical index (fmask/fval; tile bits outside the group,
+// bits outside the tile, and rank bits on a distributed state).
+template <typename T> struct alignas(16) TileOp {
+    int32_t type;
+    int32_t a, b;           // DENSE1: a = slot; DENSE2: a = MSB slot > b = LSB slot
+    int32_t rmask, rval;
+    int32_t enc;            // >= 0: matrix comes from the per-row table
+    int32_t flags;
+    int32_t nt;             // DIAG: number of target bits (1 or 2)
+    int32_t t0, t1;         // DIAG: slot (if reg) or physical position
+    int32_t t0reg, t1reg;   // DIAG: 1 if the target is a register slot
+    uint64_t fmask, fval;
+    T m[32];                // DENSE1: 2x2, DENSE2: 4x4 (row-major, re/im); DIAG: d[0..3]
+};
+
+struct GroupDesc {
+    int32_t op_begin, op_end;
+    int32_t slot_bit[kMaxSlots];       // tile-local bit of each register slot
+    int32_t ng_bit[kMaxTileBits];      // tile-local bits NOT in the group, ascending
+};
+
+// Per-row matrix binding of an encoded gate (device-side gate_matrix).
+struct EncDesc {
+    int32_t kind;        // GateKind
+    int32_t slot;        // first data column
+    int32_t nparams;
+    int32_t swapq;       // DENSE2 stored with swapped qubit order
+    int32_t diag;        // store the diagonal (DIAG op layout)
+};
+
+enum GateKind : int32_t {
+    GK_X, GK_Y, GK_Z, GK_H, GK_S, GK_T, GK_RX, GK_RY, GK_RZ, GK_P, GK_U3, GK_SWAP, GK_RXX, GK_RYY, GK_RZZ, GK_CUSTOM
+};
+
+struct PassArgs {
+    void *state;
+    uint64_t row_stride;      // amplitudes per batch row
+    uint64_t rank_base;       // rank << nlocal (global physical index offset)
+    const GroupDesc *groups;
+    const void *ops;          // TileOp<T>*
+    const void *enc_table;    // [nenc][batch][32] T
+    int32_t batch;
+    int32_t nlocal, K, L, ngroups, next;
+    int32_t row0;             // first batch row of this launch (gridDim.y chunks)
+    int32_t tile_pos[kMaxTileBits];  // physical position of tile-local bit i
+    int32_t ext_pos[kMaxQubits];     // physical positions of non-tile local bits
+};
+
+// A single state pass: the tile geometry plus the groups/ops to run on it.
+struct PassHost {
+    int K = 0, L = 0;
+    std::vector<int> tile_pos;        // size K
+    std::vector<int> ext_pos;         // nlocal - K
+    std::vector<GroupDesc> groups;
+    std::vector<TileOp<double>> ops;  // lowered in double; converted per dtype
+    int ngates = 0;                   // source gates in this pass
+    double bytes = 0;                 // algorithmic HBM bytes per row
+};
+
+// ---- resolved gate ----------------------------------------------------------
+struct GateRec {
+    std::string name;
+    int kind = 0;
+    int k = 1;                 // targets
+    int wires[2] = {0, 0};     // logical
+    std::vector<int> ctls;     // logical
+    bool diag = false;
+    bool encoded = false;
+    int enc_slot = -1;         // first data column when encoded
+    int nparams = 0;
+    int flags = 0;             // OPF_* (zero_off_control for apply_matrix)
+    cplx m[16];                // 2^k x 2^k row-major (non-encoded)
+};
+
+int gate_kind(const std::string &name);
+// gate_matrix with reference semantics (gate.hpp:89-154); returns k.
+int gate_matrix(const qsv_gate &g, cplx *m);
+bool approx_unitary(const cplx *m, int d, double tol);
+bool kind_is_diagonal(int kind);
+GateRec resolve_gate(const qsv_gate &g, int nqubit, int *enc_cursor);
+
+// ---- runtime objects ----------------------------------------------------
+struct Nccl;  // dlopen'd NCCL
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int rank = 0, world = 1, gbits = 0;
+    int sm_count = 148;
+    size_t smem_optin = 0;
+    void *comm = nullptr;       // ncclComm_t
+    Nccl *nccl = nullptr;       // owned; freed by nccl_destroy
+    ~Ctx();
+};
+
+struct State {
+    Ctx *ctx = nullptr;
+    int n = 0, nlocal = 0, batch = 1, dtype = QSV_C128;
+    uint64_t local_amps = 0;
+    void *d = nullptr;          // batch * local_amps amplitudes
+    std::vector<int> perm;      // logical wire -> physical bit (>= nlocal: rank bit)
+    size_t amp_bytes() const { return dtype == QSV_C64 ? 8 : 16; }
+    ~State();
+};
+
+struct DevPass {
+    PassArgs args{};
+    int threads = 256;
+    size_t smem = 0;
+    uint64_t tiles = 0;
+    double bytes = 0;
+    int ngates = 0;
+};
+
+// One step of an executable program: a local pass or a global<->local swap.
+struct Step {
+    int kind = 0;              // 0 pass, 1 swap
+    int pass = -1;             // index into passes
+    std::vector<std::pair<int, int>> swap_bits;  // (global physical bit, local physical bit)
+};
+
+struct Plan {
+    Ctx *ctx = nullptr;
+    int n = 0, nlocal = 0, dtype = QSV_C128;
+    int ngates = 0;
+    int nslots = 0;            // encode slots
+    std::vector<GateRec> gates;
+    std::vector<PassHost> passes;
+    std::vector<Step> steps;
+    std::vector<int> perm_in, perm_out;  // layout before/after
+    std::vector<EncDesc> encs;
+    // device buffers
+    void *d_groups = nullptr, *d_ops = nullptr, *d_encs = nullptr;
+    void *d_enc_table = nullptr;
+    size_t enc_table_rows = 0;
+    void *d_data = nullptr;
+    size_t d_data_cap = 0;
+    std::vector<DevPass> dev;
+    qsv_opts opts{};
+    double comm_bytes = 0;
+    cudaGraphExec_t graph = nullptr;
+    void *graph_state = nullptr;
+    int graph_rows = -1;
+    ~Plan();
+};
+
+// ---- planner (planner.cpp) --------------------------------------------------
+struct PlanConfig {
+    int nlocal = 0, K = 12, L = 3, R = kRegSlots;
+    bool fuse = true;
+    int dtype = QSV_C128;
+};
+// Lowers gates (already mapped to PHYSICAL bit positions, all targets local)
+// to tile passes.
+std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys_of_wire,
+                                  const PlanConfig &cfg, std::vector<EncDesc> &encs);
+int default_tile_bits(int dtype, int nlocal);
+int default_low_bits(int dtype, int nlocal);
+
+// ---- device launchers (engine.cu) -----------------------------------------
+void upload_plan(Plan &p);
+void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s);
+void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
+void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
+void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
+// Reductions write FP64 results to device memory, then copy to host.
+void reduce_norm2(State &st, double *host_out);
+void reduce_z_all(State &st, double *host_out /* batch x nlocal+1: [total, S_bit0..] */);
+void reduce_pauli(State &st, uint64_t flip, uint64_t zy, double *host_out /* batch x 2 */);
+void reduce_marginal(State &st, int row, const std::vector<int> &phys_bits, double *host_out);
+
+// ---- distributed (dist.cpp) -------------------------------------------------
+void nccl_unique_id(void *out128);
+void nccl_init(Ctx &ctx, const void *uid);
+void nccl_destroy(Ctx &ctx);
+// Exchange: swap physical rank bit `gbit` (>= nlocal) with local bit `lbit`
+// for every batch row, in place, chunked.
+void dist_swap_bits(State &st, const std::vector<std::pair<int, int>> &pairs, void *staging, size_t staging_bytes);
+void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count);
+
+} // namespace qsv

@@ -1,0 +1,107 @@
+// Seeded inputs with the reference's generator, quasar::Rng
+// (/root/reference/proj/include/quasar/rng.hpp:29-103): splitmix64 over a
+// keyed counter, fnv1a stream labels, Box-Muller normals with a cached spare.
+//
+// The generator is counter-based (draw c = mix(key + phi * c)), so a stream of
+// `count` draws splits across host threads and still reproduces the
+// sequential stream bit for bit. Normal draws come in (cos, sin) pairs from
+// counters (2j+1, 2j+2); the reference's u1 == 0 rejection (rng.hpp:59, p =
+// 2^-53 per pair) would shift every later counter, so if any chunk meets it
+// the whole fill is redone sequentially.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <thread>
+#include <vector>
+
+#include "qsv_internal.hpp"
+
+namespace qsv {
+
+namespace {
+constexpr uint64_t kPhi = 0x9e3779b97f4a7c15ull;
+
+inline uint64_t mix(uint64_t z) {
+    z += kPhi;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+inline uint64_t fnv1a(const char *s) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (; *s; ++s) {
+        h ^= static_cast<unsigned char>(*s);
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+inline double to_unit(uint64_t x) { return static_cast<double>(x >> 11) * 0x1.0p-53; }
+
+struct Seq { // sequential reference semantics (used on the rejection path)
+    uint64_t key, counter = 0;
+    double spare = 0;
+    bool have = false;
+    double uniform() { return to_unit(mix(key + kPhi * ++counter)); }
+    double normal() {
+        if (have) {
+            have = false;
+            return spare;
+        }
+        double u1 = 0.0;
+        while (u1 == 0.0) u1 = uniform();
+        const double u2 = uniform();
+        const double r = std::sqrt(-2.0 * std::log(u1));
+        spare = r * std::sin(2.0 * 3.141592653589793 * u2);
+        have = true;
+        return r * std::cos(2.0 * 3.141592653589793 * u2);
+    }
+};
+} // namespace
+
+int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads) {
+    require(kind >= 0 && kind <= 2, "rng_fill: kind must be 0 (u64), 1 (uniform) or 2 (normal)");
+    if (label) seed ^= fnv1a(label);
+    const uint64_t key = mix(seed ^ kPhi); // Rng(uint64_t) constructor
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    unsigned T = nthreads > 0 ? static_cast<unsigned>(nthreads) : hw;
+    T = std::max(1u, std::min<unsigned>(T, static_cast<unsigned>(std::max<uint64_t>(1, count >> 16))));
+    std::atomic<bool> rejected{false};
+    // work unit: one draw (kinds 0/1) or one normal pair (kind 2)
+    const uint64_t units = kind == 2 ? (count + 1) / 2 : count;
+    auto work = [&](uint64_t b, uint64_t e) {
+        for (uint64_t j = b; j < e; ++j) {
+            if (kind == 0) static_cast<uint64_t *>(out)[j] = mix(key + kPhi * (j + 1));
+            else if (kind == 1) static_cast<double *>(out)[j] = to_unit(mix(key + kPhi * (j + 1)));
+            else {
+                const double u1 = to_unit(mix(key + kPhi * (2 * j + 1)));
+                const double u2 = to_unit(mix(key + kPhi * (2 * j + 2)));
+                if (u1 == 0.0) {
+                    rejected = true;
+                    return;
+                }
+                const double r = std::sqrt(-2.0 * std::log(u1));
+                double *o = static_cast<double *>(out);
+                o[2 * j] = r * std::cos(2.0 * 3.141592653589793 * u2);
+                if (2 * j + 1 < count) o[2 * j + 1] = r * std::sin(2.0 * 3.141592653589793 * u2);
+            }
+        }
+    };
+    if (T == 1) work(0, units);
+    else {
+        std::vector<std::thread> pool;
+        const uint64_t per = (units + T - 1) / T;
+        for (unsigned t = 0; t < T; ++t) {
+            const uint64_t b = std::min<uint64_t>(units, t * per), e = std::min<uint64_t>(units, b + per);
+            pool.emplace_back(work, b, e);
+        }
+        for (auto &th : pool) th.join();
+    }
+    if (rejected) {
+        Seq s{key};
+        double *o = static_cast<double *>(out);
+        for (uint64_t i = 0; i < count; ++i) o[i] = s.normal();
+    }
+    return 0;
+}
+
+} // namespace qsv

@@ -1,0 +1,370 @@
+// Host runtime: contexts, device-resident states, plans (planning hoisted out
+// of execution), and the distributed step schedule.
+//
+// Reference correspondence (/root/reference/proj/include/quasar):
+//   State            qubit::QubitState (state.hpp:29-91), device-resident, one
+//                    row per batch element, no 30-qubit cap (state.hpp:35).
+//   plan + execute   qubit::Circuit::forward (circuit.hpp:121-157) with the
+//                    per-gate value copies (state.hpp:153) removed.
+//   dist schedule    dist::apply_gate_dist / run_circuit_dist (source absent;
+//                    SPEC.md:743-751, tests/test_dist.cpp:96-126): local gates
+//                    and every diagonal gate run without communication; a
+//                    non-diagonal gate on a global (rank) qubit first swaps
+//                    that qubit with a local one.
+#include <algorithm>
+#include <bit>
+#include <cstring>
+
+#include "qsv_internal.hpp"
+
+namespace qsv {
+
+Ctx::~Ctx() {
+    if (comm || nccl) nccl_destroy(*this);
+    if (stream) cudaStreamDestroy(stream);
+}
+
+State::~State() {
+    if (d) cudaFree(d);
+}
+
+Plan::~Plan() {
+    if (graph) cudaGraphExecDestroy(graph);
+    cudaFree(d_groups);
+    cudaFree(d_ops);
+    cudaFree(d_encs);
+    cudaFree(d_enc_table);
+    cudaFree(d_data);
+}
+
+namespace {
+
+std::vector<int> canonical_perm(int n) {
+    std::vector<int> p(n);
+    for (int w = 0; w < n; ++w) p[w] = n - 1 - w; // wire 0 = MSB (state.hpp:21-24)
+    return p;
+}
+
+template <typename T> TileOp<T> convert_op(const TileOp<double> &o) {
+    TileOp<T> r{};
+    r.type = o.type, r.a = o.a, r.b = o.b, r.rmask = o.rmask, r.rval = o.rval, r.enc = o.enc, r.flags = o.flags;
+    r.nt = o.nt, r.t0 = o.t0, r.t1 = o.t1, r.t0reg = o.t0reg, r.t1reg = o.t1reg, r.fmask = o.fmask, r.fval = o.fval;
+    for (int i = 0; i < 32; ++i) r.m[i] = static_cast<T>(o.m[i]);
+    return r;
+}
+
+// Distributed schedule: split the gate list into local segments separated by
+// global<->local qubit swaps. A non-diagonal target on a rank bit is swapped
+// with the local bit whose next non-diagonal use is furthest away (Belady),
+// preferring the highest local bits (contiguous halves).
+void schedule_dist(Plan &p, const PlanConfig &cfg) {
+    const int n = p.n, nl = p.nlocal;
+    std::vector<int> phys = p.perm_in;
+    std::vector<int> wire_at(n);
+    for (int w = 0; w < n; ++w) wire_at[phys[w]] = w;
+    size_t i = 0;
+    const size_t G = p.gates.size();
+    auto next_use = [&](int wire, size_t from) -> size_t {
+        for (size_t j = from; j < G; ++j) {
+            const GateRec &g = p.gates[j];
+            if (g.diag) continue;
+            for (int t = 0; t < g.k; ++t)
+                if (g.wires[t] == wire) return j;
+        }
+        return G + 1;
+    };
+    while (i < G) {
+        // maximal local segment
+        size_t j = i;
+        while (j < G) {
+            const GateRec &g = p.gates[j];
+            bool ok = true;
+            if (!g.diag)
+                for (int t = 0; t < g.k; ++t)
+                    if (phys[g.wires[t]] >= nl) ok = false;
+            if (!ok) break;
+            ++j;
+        }
+        if (j > i) {
+            std::vector<GateRec> seg(p.gates.begin() + i, p.gates.begin() + j);
+            auto passes = plan_passes(seg, phys, cfg, p.encs);
+            for (auto &ph : passes) {
+                Step s;
+                s.kind = 0;
+                s.pass = static_cast<int>(p.passes.size());
+                p.passes.push_back(std::move(ph));
+                p.steps.push_back(std::move(s));
+            }
+            i = j;
+            continue;
+        }
+        // gate i needs a swap
+        const GateRec &g = p.gates[i];
+        Step s;
+        s.kind = 1;
+        std::vector<int> keep; // local bits that must stay (this gate's local targets)
+        for (int t = 0; t < g.k; ++t)
+            if (phys[g.wires[t]] < nl) keep.push_back(phys[g.wires[t]]);
+        for (int t = 0; t < g.k; ++t) {
+            const int gb = phys[g.wires[t]];
+            if (gb < nl) continue;
+            int best = -1;
+            size_t best_use = 0;
+            for (int lb = nl - 1; lb >= 0; --lb) {
+                if (std::find(keep.begin(), keep.end(), lb) != keep.end()) continue;
+                const size_t u = next_use(wire_at[lb], i);
+                if (best < 0 || u > best_use) best = lb, best_use = u;
+                if (u == G + 1) break;
+            }
+            require(best >= 0, "dist: no local qubit available for a swap");
+            keep.push_back(best);
+            s.swap_bits.emplace_back(gb, best);
+            const int wg = wire_at[gb], wl = wire_at[best];
+            std::swap(phys[wg], phys[wl]);
+            wire_at[gb] = wl;
+            wire_at[best] = wg;
+        }
+        p.steps.push_back(std::move(s));
+    }
+    // Restore the canonical layout so the API always sees logical order.
+    // Phase A: put the right wire on every rank bit (global<->local swaps).
+    const std::vector<int> canon = p.perm_in;
+    std::vector<int> wire_of_canon(n);
+    for (int w = 0; w < n; ++w) wire_of_canon[canon[w]] = w;
+    auto do_swap = [&](Step &s, int a, int b) { // exchange physical bits a, b
+        s.swap_bits.emplace_back(a, b);
+        const int wa = wire_at[a], wb = wire_at[b];
+        std::swap(phys[wa], phys[wb]);
+        wire_at[a] = wb;
+        wire_at[b] = wa;
+    };
+    Step back;
+    back.kind = 1;
+    for (int gb = nl; gb < n; ++gb) {
+        const int want = wire_of_canon[gb];
+        int x = phys[want];
+        if (x == gb) continue;
+        if (x >= nl) { // parked on another rank bit: bring it local first
+            int lb = nl - 1;
+            do_swap(back, x, lb);
+            x = lb;
+        }
+        do_swap(back, gb, x);
+    }
+    if (!back.swap_bits.empty()) p.steps.push_back(std::move(back));
+    // Phase B: local bits permuted among themselves -> local swap gates,
+    // expressed on PHYSICAL bits (identity mapping) and fused into passes.
+    std::vector<GateRec> fix;
+    for (int w = 0; w < n; ++w) {
+        if (phys[w] == canon[w]) continue;
+        const int a = phys[w], b = canon[w];
+        GateRec sw;
+        sw.name = "swap";
+        sw.kind = GK_SWAP;
+        sw.k = 2;
+        sw.wires[0] = a;
+        sw.wires[1] = b;
+        for (auto &x : sw.m) x = 0;
+        sw.m[0] = sw.m[15] = sw.m[6] = sw.m[9] = 1;
+        fix.push_back(sw);
+        const int wa = wire_at[a], wb = wire_at[b];
+        std::swap(phys[wa], phys[wb]);
+        wire_at[a] = wb;
+        wire_at[b] = wa;
+    }
+    if (!fix.empty()) {
+        std::vector<int> ident(n);
+        for (int b = 0; b < n; ++b) ident[b] = b;
+        auto passes = plan_passes(fix, ident, cfg, p.encs);
+        for (auto &ph : passes) {
+            Step s;
+            s.pass = static_cast<int>(p.passes.size());
+            p.passes.push_back(std::move(ph));
+            p.steps.push_back(std::move(s));
+        }
+    }
+    p.perm_out = phys;
+}
+
+} // namespace
+
+void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts) {
+    require(n >= 1 && n <= kMaxQubits, "plan: nqubit out of range");
+    require(dtype == QSV_C64 || dtype == QSV_C128, "plan: bad dtype");
+    Plan *p = &pl;
+    p->ctx = ctx;
+    p->n = n;
+    p->dtype = dtype;
+    p->nlocal = n - ctx->gbits;
+    require(p->nlocal >= 1, "plan: more ranks than amplitudes");
+    if (opts) p->opts = *opts;
+    else p->opts.fuse = 1;
+    p->gates = std::move(gates);
+    p->nslots = nslots;
+    p->ngates = static_cast<int>(p->gates.size());
+    PlanConfig cfg;
+    cfg.nlocal = p->nlocal;
+    cfg.dtype = dtype;
+    cfg.K = p->opts.tile_bits > 0 ? std::min(p->opts.tile_bits, kMaxTileBits) : default_tile_bits(dtype, p->nlocal);
+    cfg.K = std::min(cfg.K, p->nlocal);
+    cfg.L = p->opts.low_bits > 0 ? p->opts.low_bits : default_low_bits(dtype, p->nlocal);
+    cfg.L = std::max(dtype == QSV_C64 ? 1 : 0, std::min(cfg.L, cfg.K));
+    cfg.fuse = p->opts.fuse != 0;
+    require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
+    p->perm_in = canonical_perm(n);
+    if (ctx->world == 1) {
+        if (!p->gates.empty()) {
+            auto passes = plan_passes(p->gates, p->perm_in, cfg, p->encs);
+            for (auto &ph : passes) {
+                Step s;
+                s.pass = static_cast<int>(p->passes.size());
+                p->passes.push_back(std::move(ph));
+                p->steps.push_back(std::move(s));
+            }
+        }
+        p->perm_out = p->perm_in;
+    } else {
+        schedule_dist(*p, cfg);
+    }
+    upload_plan(*p);
+}
+
+void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates,
+                         const qsv_opts *opts) {
+    require(ngates >= 0 && (ngates == 0 || gates != nullptr), "plan: bad gate list");
+    require(n >= 1 && n <= kMaxQubits, "plan: nqubit out of range");
+    std::vector<GateRec> recs;
+    int cursor = 0;
+    for (int i = 0; i < ngates; ++i) recs.push_back(resolve_gate(gates[i], n, &cursor));
+    build_plan(p, ctx, n, dtype, std::move(recs), cursor, opts);
+}
+
+void upload_plan(Plan &p) {
+    std::vector<GroupDesc> groups;
+    std::vector<size_t> group_off, op_off;
+    size_t nops = 0;
+    for (auto &ph : p.passes) {
+        group_off.push_back(groups.size());
+        op_off.push_back(nops);
+        groups.insert(groups.end(), ph.groups.begin(), ph.groups.end());
+        nops += ph.ops.size();
+    }
+    const size_t op_size = p.dtype == QSV_C64 ? sizeof(TileOp<float>) : sizeof(TileOp<double>);
+    std::vector<unsigned char> opbuf(std::max<size_t>(nops, 1) * op_size);
+    size_t k = 0;
+    for (auto &ph : p.passes)
+        for (auto &o : ph.ops) {
+            if (p.dtype == QSV_C64) {
+                auto c = convert_op<float>(o);
+                std::memcpy(opbuf.data() + k * op_size, &c, op_size);
+            } else {
+                std::memcpy(opbuf.data() + k * op_size, &o, op_size);
+            }
+            ++k;
+        }
+    QSV_CUDA(cudaSetDevice(p.ctx->device));
+    QSV_CUDA(cudaMalloc(&p.d_groups, std::max<size_t>(groups.size(), 1) * sizeof(GroupDesc)));
+    QSV_CUDA(cudaMalloc(&p.d_ops, opbuf.size()));
+    if (!groups.empty())
+        QSV_CUDA(cudaMemcpy(p.d_groups, groups.data(), groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice));
+    QSV_CUDA(cudaMemcpy(p.d_ops, opbuf.data(), opbuf.size(), cudaMemcpyHostToDevice));
+    if (!p.encs.empty()) {
+        QSV_CUDA(cudaMalloc(&p.d_encs, p.encs.size() * sizeof(EncDesc)));
+        QSV_CUDA(cudaMemcpy(p.d_encs, p.encs.data(), p.encs.size() * sizeof(EncDesc), cudaMemcpyHostToDevice));
+    }
+    const size_t amp = p.dtype == QSV_C64 ? 8 : 16;
+    p.dev.clear();
+    for (size_t i = 0; i < p.passes.size(); ++i) {
+        const PassHost &ph = p.passes[i];
+        DevPass dp;
+        PassArgs &a = dp.args;
+        a.row_stride = 1ull << p.nlocal;
+        a.rank_base = static_cast<uint64_t>(p.ctx->rank) << p.nlocal;
+        a.groups = static_cast<const GroupDesc *>(p.d_groups) + group_off[i];
+        a.ops = static_cast<const unsigned char *>(p.d_ops) + op_off[i] * op_size;
+        a.nlocal = p.nlocal;
+        a.K = ph.K;
+        a.L = ph.L;
+        a.ngroups = static_cast<int>(ph.groups.size());
+        a.next = static_cast<int>(ph.ext_pos.size());
+        for (int j = 0; j < ph.K; ++j) a.tile_pos[j] = ph.tile_pos[j];
+        for (int j = 0; j < a.next; ++j) a.ext_pos[j] = ph.ext_pos[j];
+        const int R = std::min(kRegSlots, ph.K);
+        const int nsets = 1 << (ph.K - R);
+        const int chunks = (1 << ph.K) * static_cast<int>(amp) / 16;
+        dp.threads = std::max(32, std::min(256, std::max(nsets, std::min(chunks, 256))));
+        dp.threads = (dp.threads + 31) / 32 * 32;
+        dp.smem = (amp << ph.K) + (sizeof(uint64_t) << (ph.K - ph.L));
+        dp.tiles = 1ull << (p.nlocal - ph.K);
+        dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
+        dp.ngates = ph.ngates;
+        p.dev.push_back(dp);
+    }
+}
+
+void execute_plan(Plan &p, State &st, const double *data, int rows, int slots) {
+    require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
+    require(st.ctx == p.ctx, "plan/state belong to different contexts");
+    if (rows == 0) {
+        require(p.nslots == 0, "circuit has encode slots but no data given"); // circuit.hpp:125
+    } else {
+        require(rows == st.batch, "data rows must equal the state's batch");
+        require(slots == p.nslots, "data length " + std::to_string(slots) + " != encode slots " +
+                                       std::to_string(p.nslots)); // circuit.hpp:134-136
+    }
+    cudaStream_t s = p.ctx->stream;
+    QSV_CUDA(cudaSetDevice(p.ctx->device));
+    const void *enc_table = nullptr;
+    if (!p.encs.empty()) {
+        const size_t dbytes = sizeof(double) * static_cast<size_t>(rows) * slots;
+        if (dbytes > p.d_data_cap) {
+            cudaFree(p.d_data);
+            QSV_CUDA(cudaMalloc(&p.d_data, dbytes));
+            p.d_data_cap = dbytes;
+        }
+        QSV_CUDA(cudaMemcpyAsync(p.d_data, data, dbytes, cudaMemcpyHostToDevice, s));
+        if (static_cast<size_t>(rows) > p.enc_table_rows) {
+            cudaFree(p.d_enc_table);
+            const size_t tsz = (p.dtype == QSV_C64 ? 4 : 8) * 32 * p.encs.size() * static_cast<size_t>(rows);
+            QSV_CUDA(cudaMalloc(&p.d_enc_table, tsz));
+            p.enc_table_rows = rows;
+        }
+        launch_bind(p, static_cast<const double *>(p.d_data), rows, slots, s);
+        enc_table = p.d_enc_table;
+    }
+    for (const Step &stp : p.steps) {
+        if (stp.kind == 0) {
+            DevPass dp = p.dev[stp.pass];
+            dp.args.enc_table = enc_table;
+            dp.args.batch = rows > 0 ? rows : st.batch;
+            launch_pass(dp, p.dtype, st.d, st.batch, s);
+        } else {
+            dist_swap_bits(st, stp.swap_bits, nullptr, 0);
+        }
+    }
+}
+
+void profile_plan(Plan &p, State &st, double *launch_ms) {
+    require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
+    require(p.nslots == 0, "profile: encoded plans not supported");
+    cudaStream_t s = p.ctx->stream;
+    std::vector<cudaEvent_t> ev(2 * p.steps.size());
+    for (auto &e : ev) QSV_CUDA(cudaEventCreate(&e));
+    size_t k = 0;
+    for (const Step &stp : p.steps) {
+        QSV_CUDA(cudaEventRecord(ev[2 * k], s));
+        if (stp.kind == 0) launch_pass(p.dev[stp.pass], p.dtype, st.d, st.batch, s);
+        else dist_swap_bits(st, stp.swap_bits, nullptr, 0);
+        QSV_CUDA(cudaEventRecord(ev[2 * k + 1], s));
+        ++k;
+    }
+    QSV_CUDA(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < p.steps.size(); ++i) {
+        float ms = 0;
+        QSV_CUDA(cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]));
+        launch_ms[i] = ms;
+    }
+    for (auto &e : ev) cudaEventDestroy(e);
+}
+
+} // namespace qsv

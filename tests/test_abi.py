@@ -1,0 +1,91 @@
+"""The C-ABI library on a GPU-less host: it builds, loads, exports exactly the
+symbols include/qsv.h declares, runs its host-only calls, and fails LOUDLY
+(QSV_ERR_INTERNAL, never a silent CPU path) when asked to compute."""
+import ctypes as C
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2512_18995_b200 import build as B
+from paper_2512_18995_b200 import qsv
+from paper_2512_18995_b200.qsv import make_gate
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "qsv.h"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    B.build()
+    O.build()
+
+
+def declared_symbols():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(qsv_\w+)\s*\(", text, re.M)))
+
+
+def test_header_and_binding_agree():
+    syms = declared_symbols()
+    assert len(syms) >= 30
+    assert set(syms) == set(qsv._SIGS), set(syms) ^ set(qsv._SIGS)
+
+
+def test_library_exports_every_declared_symbol():
+    L = C.CDLL(str(B.LIB))
+    for s in declared_symbols():
+        assert hasattr(L, s), s
+    assert qsv.lib().qsv_version() == 1
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", str(B.LIB)], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_no_gpu_fails_loudly():
+    L = qsv.lib()
+    if L.qsv_device_count() > 0:
+        pytest.skip("a GPU is visible")
+    h = C.c_void_p()
+    rc = L.qsv_ctx_create(0, C.byref(h))
+    assert rc == qsv.ERR_INTERNAL
+    assert b"no CPU fallback" in L.qsv_last_error()
+    with pytest.raises(qsv.QsvError):
+        qsv.Context(0)
+
+
+@pytest.mark.parametrize("name,wires,params", [
+    ("h", [0], []), ("rx", [0], [0.3]), ("ry", [0], [-1.2]), ("rz", [0], [2.9]), ("p", [0], [0.7]),
+    ("u3", [0], [0.1, -0.4, 2.2]), ("swap", [0, 1], []), ("rxx", [0, 1], [0.9]), ("ryy", [0, 1], [-2.1]),
+    ("rzz", [0, 1], [1.3]), ("s", [0], []), ("t", [0], []), ("y", [0], []),
+])
+def test_abi_gate_matrix_matches_reference(name, wires, params):
+    g = make_gate(name, wires, [], params)
+    want = O.ref_gate_matrix(g) if O.REF_LIB.exists() else O.port_gate_matrix(g)
+    assert np.max(np.abs(qsv.gate_matrix(g) - want)) <= 1e-16
+
+
+def test_abi_gate_matrix_errors_mirror_reference():
+    with pytest.raises(qsv.InvalidInput, match="unknown gate"):
+        qsv.gate_matrix(make_gate("nope", [0]))
+    with pytest.raises(qsv.InvalidInput, match="expected 1 params"):
+        qsv.gate_matrix(make_gate("rx", [0], [], []))
+    with pytest.raises(qsv.InvalidInput, match="not unitary"):
+        qsv.gate_matrix(make_gate("custom", [0], custom=np.array([[1, 1], [0, 1]])))
+    with pytest.raises(qsv.InvalidInput, match="disjoint"):
+        make_gate("x", [0], [0])
+
+
+def test_rng_fill_matches_reference_stream():
+    for kind, k in (("u64", 0), ("uniform", 1), ("normal", 2)):
+        for cnt in (1, 7, 1000, 300001):
+            got = qsv.rng_fill(0, "cfg3", kind, cnt, nthreads=4)
+            want = O.port_rng(0, "cfg3", k, cnt)
+            assert np.array_equal(got, want), (kind, cnt)

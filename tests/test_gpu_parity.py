@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference.
+
+Bar (BASELINE.json north_star): max |amplitude error| <= 1e-12 in complex128
+and <= 1e-5 in complex64; expectations within the same bounds. The checker is
+the reference itself where it is present (oracle/_ref) and the committed
+golden fixtures it produced; the C restatement (pinned to the reference by
+tests/test_oracle.py) covers sizes the fixtures do not.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2512_18995_b200 import qsv
+from paper_2512_18995_b200 import workloads as W
+from paper_2512_18995_b200.qsv import C64, C128, Circuit, QubitState, Rng, make_gate
+from tests.golden_io import load_circuit_cases
+from tests.helpers import random_circuit, random_gate, random_state
+
+pytestmark = pytest.mark.gpu
+TOL = {C128: 1e-12, C64: 1e-5}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def ctx(built):
+    return qsv.default_context()
+
+
+def ref_or_port_forward(n, gates, init=None, data=None):
+    if O.REF_LIB.exists():
+        return O.ref_forward(n, gates, init=init, data=data)
+    return O.port_forward(n, gates, init=init, data=data)
+
+
+def run(n, gates, init=None, data=None, dtype=C128, opts=None):
+    cir = Circuit(n)
+    for g in gates:
+        cir.add(g)
+    st = None
+    if init is not None:
+        st = QubitState.from_amplitudes(n, init, dtype=dtype)
+    out = cir.forward(st, data, dtype=dtype, opts=opts)
+    return np.stack([out.amplitudes(b) for b in range(out.batch())]), out
+
+
+# ------------------------------------------------------------ golden ----
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_golden_fixtures(dtype):
+    for case in load_circuit_cases():
+        got, st = run(case["n"], case["gates"], case.get("init"), case.get("data"), dtype=dtype)
+        err = np.max(np.abs(got - case["out"]))
+        assert err <= TOL[dtype], (case["name"], err)
+        if "obs" in case:
+            obs = [qsv.Observable(w, b) for w, b in case["obs"]]
+            e = qsv.expectation_many(st, obs)
+            assert np.max(np.abs(e - np.asarray(case["expect"]))) <= TOL[dtype] * 10, case["name"]
+        if "marg" in case:
+            for w, p in zip(case["marg"], case["probs"]):
+                assert np.max(np.abs(qsv.marginal_probabilities(st, w) - np.asarray(p))) <= TOL[dtype] * 10
+
+
+# ------------------------------------------ reference test_qubit KATs ----
+def test_hadamard_on_zero():
+    s = qsv.apply_gate(QubitState.basis(1), make_gate("h", [0]))
+    a = s.amplitudes()
+    assert abs(a[0] - 1 / math.sqrt(2)) < 1e-12 and abs(a[1] - 1 / math.sqrt(2)) < 1e-12
+
+
+def test_toffoli_like():
+    s = qsv.apply_gate(QubitState.basis(3, 0b110), make_gate("x", [2], [0, 1]))
+    assert abs(abs(s.amplitudes()[0b111]) - 1) < 1e-12
+
+
+def test_striding_matches_dense_oracle_gate_by_gate():
+    rng = Rng(31, "striding")
+    for n in range(1, 7):
+        psi = random_state(rng, n)
+        s = QubitState.from_amplitudes(n, psi)
+        for rep in range(20):
+            g = random_gate(rng, n)
+            s = qsv.apply_gate(s, g)
+            psi = O.port_forward(n, [g], init=psi)[0]
+            assert np.max(np.abs(s.amplitudes() - psi)) < 1e-12, (n, g.name)
+
+
+def test_norm_preserved_long_circuit():
+    rng = Rng(37, "norm")
+    gates = [random_gate(rng, 5) for _ in range(1000)]
+    got, st = run(5, gates)
+    assert abs(np.linalg.norm(got[0]) - 1) < 1e-10
+    assert abs(st.norm2()[0] - 1) < 1e-10
+    want = ref_or_port_forward(5, gates)[0]
+    assert np.max(np.abs(got[0] - want)) < 1e-12
+
+
+def test_empty_circuit_and_bell():
+    out = Circuit(2).forward()
+    assert abs(out.amplitudes()[0] - 1) < 1e-15
+    cir = Circuit(2)
+    cir.h(0)
+    cir.cnot(0, 1)
+    a = cir.forward().amplitudes()
+    r = 1 / math.sqrt(2)
+    assert np.max(np.abs(a - np.array([r, 0, 0, r]))) < 1e-12
+
+
+def test_batch_rows_equal_single_runs():  # test_qubit.cpp:180-193
+    cir = Circuit(2)
+    cir.h(0)
+    cir.ry(0, 0.0, False, True)
+    cir.ry(1, 0.0, False, True)
+    cir.cnot(0, 1)
+    data = [[0.1, 0.2], [1.0, -0.4], [2.2, 0.0], [-0.7, 0.9]]
+    batch = cir.forward(data=data)
+    assert batch.batch() == 4
+    for r in range(4):
+        single = cir.forward(data=[data[r]])
+        assert np.max(np.abs(batch.amplitudes(r) - single.amplitudes(0))) < 1e-14
+
+
+def test_data_length_mismatch_fails_fast():  # test_qubit.cpp:195-200
+    cir = Circuit(2)
+    cir.ry(0, 0.0, False, True)
+    with pytest.raises(qsv.InvalidInput):
+        cir.forward(data=[[0.1, 0.2]])
+    with pytest.raises(qsv.InvalidInput):
+        cir.forward(data=[[]])
+    with pytest.raises(qsv.InvalidInput):
+        cir.forward()
+
+
+def test_expectation_basic_and_ghz():  # test_qubit.cpp:255-270
+    zero = QubitState.basis(1)
+    assert abs(qsv.expectation_one(zero, qsv.Observable([0], "z")) - 1) < 1e-12
+    plus = qsv.apply_gate(zero, make_gate("h", [0]))
+    assert abs(qsv.expectation_one(plus, qsv.Observable([0], "x")) - 1) < 1e-12
+    cir = Circuit(3)
+    cir.h(0)
+    cir.cnot(0, 1)
+    cir.cnot(1, 2)
+    s = cir.forward()
+    assert abs(qsv.expectation_one(s, qsv.Observable([0, 1, 2], "zzz"))) < 1e-12
+    assert abs(qsv.expectation_one(s, qsv.Observable([0, 1, 2], "xxx")) - 1) < 1e-12
+
+
+def test_measure_matches_seeded_reference_histogram():  # test_dist.cpp:207-222 / test_qubit.cpp:202-247
+    cir = Circuit(3)
+    cir.h(0)
+    cir.cnot(0, 1)
+    cir.ry(2, 0.7)
+    s = cir.forward()
+    got = qsv.measure(s, 500, [0, 1, 2], Rng(9, "hist"))
+    if O.REF_LIB.exists():
+        want = O.ref_measure(3, s.amplitudes(), 500, [0, 1, 2], 9, "hist")
+        for i, cnt in enumerate(want):
+            key = qsv.bits_to_string(i, 3)
+            assert got.get(key, {"count": 0})["count"] == int(cnt), key
+    bell = Circuit(2)
+    bell.h(0)
+    bell.cnot(0, 1)
+    counts = qsv.measure(bell.forward(), 100000, [0, 1], Rng(1, "measure-bell"), True)
+    assert abs(counts["00"]["probability"] - 0.5) < 1e-12
+    assert "01" not in counts
+    assert abs(counts["00"]["count"] - 50000) < 5 * math.sqrt(0.25 * 100000)
+
+
+# ----------------------------------------------- random / fused paths ----
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_random_circuits_up_to_14_qubits(dtype):
+    rng = Rng(101, "gpu-random")
+    for n in [1, 2, 3, 4, 5, 7, 9, 11, 12, 13, 14]:
+        psi = random_state(rng, n)
+        gates = [random_gate(rng, n) for _ in range(60)]
+        got, _ = run(n, gates, init=psi, dtype=dtype)
+        want = O.port_forward(n, gates, init=psi)[0]
+        assert np.max(np.abs(got[0] - want)) <= TOL[dtype], n
+
+
+@pytest.mark.parametrize("opts", [{"fuse": 0}, {"tile_bits": 6, "low_bits": 2}, {"tile_bits": 10, "low_bits": 1},
+                                  {"tile_bits": 13, "low_bits": 5}])
+def test_tile_geometries_agree(opts):
+    rng = Rng(5, "geom")
+    n = 16
+    psi = random_state(rng, n)
+    cir = random_circuit(rng, n, 120)
+    got, _ = run(n, cir.gates(), init=psi, opts=opts)
+    want = O.port_forward(n, cir.gates(), init=psi)[0]
+    assert np.max(np.abs(got[0] - want)) <= 1e-12
+
+
+def test_apply_matrix_zero_off_control():
+    rng = Rng(3, "zoc")
+    psi = random_state(rng, 7)
+    m = np.array([[0.3, 0.1j], [0.2, -0.5]])
+    s = QubitState.from_amplitudes(7, psi)
+    s.apply_matrix(m, [2], [0, 4], zero_off_control=True)
+    want = O.port_apply_matrix(psi, 7, m, [2], [0, 4], zero_off_control=True)
+    assert np.max(np.abs(s.amplitudes() - want)) < 1e-15
+    d = np.diag([0.0, 1j])
+    s = QubitState.from_amplitudes(7, psi)
+    s.apply_matrix(d, [5], [1], zero_off_control=True)
+    want = O.port_apply_matrix(psi, 7, d, [5], [1], zero_off_control=True)
+    assert np.max(np.abs(s.amplitudes() - want)) < 1e-15
+
+
+def test_expectations_all_pauli_strings_vs_reference():
+    rng = Rng(17, "pauli")
+    n = 6
+    psi = random_state(rng, n)
+    s = QubitState.from_amplitudes(n, psi)
+    obs = []
+    for _ in range(40):
+        k = 1 + rng.next_below(4)
+        wires = []
+        while len(wires) < k:
+            w = rng.next_below(n)
+            if w not in wires:
+                wires.append(w)
+        basis = "".join("xyz"[rng.next_below(3)] for _ in wires)
+        obs.append((wires, basis))
+    got = qsv.expectation_many(s, [qsv.Observable(w, b) for w, b in obs])[0]
+    for (w, b), g in zip(obs, got):
+        want, im = O.port_expectation(n, psi, w, b)
+        assert abs(g - want) < 1e-12, (w, b)
+    z = s.expect_z_all()[0]
+    for q in range(n):
+        assert abs(z[q] - O.port_expectation(n, psi, [q], "z")[0]) < 1e-12
+
+
+# ------------------------------------------------ config families ----
+def test_cfg1_full_20q_vs_reference():
+    cir = W.cfg1_circuit(20)
+    s = cir.forward()
+    got = s.amplitudes()
+    want = ref_or_port_forward(20, cir.gates())[0]
+    assert np.max(np.abs(got - want)) <= 1e-12
+    z = s.expect_z_all()[0]
+    wz = np.array([O.port_expectation(20, want, [q], "z")[0] for q in range(0, 20, 5)])
+    assert np.max(np.abs(z[0:20:5] - wz)) <= 1e-12
+
+
+def test_cfg2_batched_c64_vs_reference_rows():
+    cir, data = W.cfg2_circuit()
+    s = cir.forward(data=data, dtype=C64)
+    z = s.expect_z_all()
+    assert z.shape == (4096, 12)
+    rows = list(range(0, 4096, 257))
+    want = ref_or_port_forward(12, cir.gates(), data=data[rows])
+    for i, r in enumerate(rows):
+        a = s.amplitudes(r)
+        assert np.max(np.abs(a - want[i])) <= 1e-5, r
+        wz = [O.port_expectation(12, want[i], [q], "z")[0] for q in range(12)]
+        assert np.max(np.abs(z[r] - wz)) <= 1e-5
+    assert np.max(np.abs(s.norm2() - 1)) < 1e-5
+
+
+def test_cfg3_qft_reduced_vs_reference():
+    for n in (10, 16, 20):
+        cir = W.cfg3_circuit(n)
+        psi = W.cfg3_input(n)
+        s = cir.forward(QubitState.from_amplitudes(n, psi))
+        want = ref_or_port_forward(n, cir.gates(), init=psi)[0]
+        assert np.max(np.abs(s.amplitudes() - want)) <= 1e-12, n
+
+
+def test_qft_of_zero_is_uniform_24q():  # test_dist.cpp:147-160 scaled
+    n = 24
+    s = qsv.qft_circuit(n).forward()
+    a = s.amplitudes()
+    assert np.max(np.abs(np.abs(a) - 2.0 ** (-n / 2))) < 1e-12
+
+
+@pytest.mark.parametrize("dtype,n", [(C128, 22), (C64, 24)])
+def test_mirror_circuits_return_to_zero(dtype, n):
+    for cir in (W.cfg4_circuit(n, layers=6), W.cfg5_circuit(n, layers=4)):
+        s = W.mirror(cir).forward(dtype=dtype)
+        a = s.amplitudes()
+        assert abs(a[0] - 1) <= 10 * TOL[dtype]
+        assert np.max(np.abs(a[1:])) <= 10 * TOL[dtype]
+
+
+def test_cfg5_family_c64_vs_reference():
+    cir = W.cfg5_circuit(16, layers=4)
+    s = cir.forward(dtype=C64)
+    want = ref_or_port_forward(16, cir.gates())[0]
+    assert np.max(np.abs(s.amplitudes() - want)) <= 1e-5
+    e = qsv.expectation(s, cir)[0]
+    assert abs(e - O.port_expectation(16, want, [0, 15], "zz")[0]) <= 1e-5

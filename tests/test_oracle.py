@@ -1,0 +1,203 @@
+"""Pins the CPU oracle before it is trusted (CPU only, no GPU).
+
+1. The C restatement (oracle/qsv_oracle.c) against the reference itself
+   (oracle/_ref/libquasar_ref.so = the unmodified quasar headers), on the
+   reference's own known-answer tests (proj/tests/test_qubit.cpp) and seeded
+   random circuits.
+2. Both against the committed golden fixtures (tests/golden/*.json, made by
+   tests/golden/make_golden.py from the reference library), so the pin holds
+   on hosts without /root/reference.
+"""
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2512_18995_b200.qsv import Rng, kPi, make_gate
+from tests.helpers import dense_apply, random_circuit, random_gate, random_state
+
+GOLD = Path(__file__).resolve().parent / "golden"
+HAVE_REF = O.REF_LIB.exists() or O.REFERENCE_INCLUDE.exists()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _build():
+    O.build()
+
+
+def needs_ref():
+    if not O.REF_LIB.exists():
+        pytest.skip("reference library not built (needs /root/reference)")
+
+
+# ---------------------------------------------------------------- Rng ----
+def test_python_rng_matches_reference_stream():
+    needs_ref()
+    for seed, label in [(0, "cfg1"), (31, "striding"), (7, None)]:
+        r = Rng(seed, label) if label else Rng(seed)
+        got = [r.next_u64() for _ in range(64)]
+        want = O.ref_rng(seed, label, 0, 64)
+        assert got == [int(x) for x in want]
+        r = Rng(seed, label) if label else Rng(seed)
+        got = [r.normal() for _ in range(33)]
+        assert np.array_equal(np.array(got), O.ref_rng(seed, label, 2, 33))
+        r = Rng(seed, label) if label else Rng(seed)
+        got = [r.next_below(37) for _ in range(50)]
+        assert got == [int(x) for x in O.ref_rng(seed, label, 3, 50, 37)]
+
+
+def test_port_rng_matches_reference():
+    needs_ref()
+    for kind in (0, 1, 2, 3):
+        assert np.array_equal(O.port_rng(5, "dist-equiv", kind, 101, 13), O.ref_rng(5, "dist-equiv", kind, 101, 13))
+
+
+# ------------------------------------------------------- gate matrices ----
+GATES = [
+    ("x", [0], []), ("y", [0], []), ("z", [0], []), ("h", [0], []), ("s", [0], []), ("t", [0], []),
+    ("rx", [0], [0.3]), ("ry", [0], [-1.2]), ("rz", [0], [2.9]), ("p", [0], [0.7]),
+    ("u3", [0], [0.1, -0.4, 2.2]), ("swap", [0, 1], []), ("rxx", [0, 1], [0.9]), ("ryy", [0, 1], [-2.1]),
+    ("rzz", [0, 1], [1.3]),
+]
+
+
+@pytest.mark.parametrize("name,wires,params", GATES)
+def test_port_gate_matrix_matches_reference(name, wires, params):
+    needs_ref()
+    g = make_gate(name, wires, [], params)
+    assert np.array_equal(O.port_gate_matrix(g), O.ref_gate_matrix(g))
+
+
+# -------------------------------------------- KATs (test_qubit.cpp) -------
+def test_kat_hadamard_on_zero():  # test_qubit.cpp:86-91
+    out = O.port_forward(1, [make_gate("h", [0])])[0]
+    r = 1 / math.sqrt(2.0)
+    assert abs(out[0] - r) < 1e-12 and abs(out[1] - r) < 1e-12
+
+
+def test_kat_toffoli_like():  # test_qubit.cpp:93-98
+    init = np.zeros(8, complex)
+    init[0b110] = 1
+    out = O.port_forward(3, [make_gate("x", [2], [0, 1])], init=init)[0]
+    assert abs(abs(out[0b111]) - 1) < 1e-12
+
+
+def test_kat_striding_matches_dense_oracle():  # test_qubit.cpp:100-114
+    rng = Rng(31, "striding")
+    for n in range(1, 7):
+        psi = random_state(rng, n)
+        state = psi.copy()
+        for _ in range(20):
+            g = random_gate(rng, n)
+            state = O.port_forward(n, [g], init=state)[0]
+            psi = dense_apply(psi, O.port_gate_matrix(g), g.wires, g.controls, n)
+            assert np.max(np.abs(state - psi)) < 1e-12, (n, g.name)
+
+
+def test_kat_norm_preserved():  # test_qubit.cpp:116-122
+    rng = Rng(37, "norm")
+    gates = [random_gate(rng, 5) for _ in range(1000)]
+    out = O.port_forward(5, gates)[0]
+    assert abs(np.linalg.norm(out) - 1) < 1e-10
+
+
+def test_kat_bell_and_ghz_expectations():  # test_qubit.cpp:130-140, 255-270
+    bell = O.port_forward(2, [make_gate("h", [0]), make_gate("x", [1], [0])])[0]
+    r = 1 / math.sqrt(2)
+    assert np.allclose(bell, [r, 0, 0, r], atol=1e-12)
+    ghz = O.port_forward(3, [make_gate("h", [0]), make_gate("x", [1], [0]), make_gate("x", [2], [1])])[0]
+    assert abs(O.port_expectation(3, ghz, [0, 1, 2], "zzz")[0]) < 1e-12
+    assert abs(O.port_expectation(3, ghz, [0, 1, 2], "xxx")[0] - 1) < 1e-12
+
+
+def test_port_matches_reference_random_circuits():
+    needs_ref()
+    rng = Rng(7, "dist-equiv")
+    for trial in range(12):
+        n = 4 + rng.next_below(5)
+        cir = random_circuit(rng, n, 18)
+        a = O.port_forward(n, cir.gates())[0]
+        b = O.ref_forward(n, cir.gates())[0]
+        assert np.max(np.abs(a - b)) <= 1e-15, trial
+
+
+def test_port_matches_reference_encoded_batch():  # test_qubit.cpp:145-193
+    needs_ref()
+    from paper_2512_18995_b200.qsv import Circuit
+
+    cir = Circuit(3)
+    cir.h(0)
+    cir.cnot(0, 1)
+    cir.x(2, [0])
+    cir.rylayer(encode=True)
+    cir.cnot_ring()
+    cir.rylayer(encode=False)
+    data = [[1.0, 2.0, 3.0], [0.1, -0.2, 0.3]]
+    a = O.port_forward(3, cir.gates(), data=data)
+    b = O.ref_forward(3, cir.gates(), data=data)
+    assert np.max(np.abs(a - b)) <= 1e-15
+    e1 = O.port_expectation(3, a[0], [0, 1, 2], "xzx")[0]
+    e2 = O.ref_expectation(3, b[0], [([0, 1, 2], "xzx")])[0]
+    assert abs(e1 - e2) < 1e-15
+
+
+def test_reference_rejects_data_length_mismatch():  # test_qubit.cpp:195-200
+    needs_ref()
+    g = [make_gate("ry", [0], [], [0.0], False, True)]
+    with pytest.raises(O.OracleError) as e:
+        O.ref_forward(2, g, data=[[0.1, 0.2]])
+    assert e.value.code == 2
+
+
+def test_port_marginal_and_zero_off_control_match_reference():
+    needs_ref()
+    rng = Rng(3, "marg")
+    psi = random_state(rng, 6)
+    for wires in ([0], [2, 5], [5, 1, 3]):
+        assert np.allclose(O.port_marginal(6, psi, wires), O.ref_marginal(6, psi, wires), atol=1e-15)
+    # zero_off_control: restate by hand (adjoint.hpp:99-101 uses it)
+    m = np.array([[0.3, 0.1j], [0.2, -0.5]])
+    out = O.port_apply_matrix(psi, 6, m, [2], [0, 4], zero_off_control=True)
+    want = np.zeros_like(psi)
+    for i in range(64):
+        on = (i >> 5) & 1 and (i >> 1) & 1
+        if not on:
+            continue
+        b = (i >> 3) & 1
+        j0 = i & ~(1 << 3)
+        want[i] = m[b, 0] * psi[j0] + m[b, 1] * psi[j0 | (1 << 3)]
+    assert np.max(np.abs(out - want)) < 1e-15
+
+
+# --------------------------------------------------------- golden pins ----
+def _load(name):
+    p = GOLD / name
+    if not p.exists():
+        pytest.skip(f"{p} missing")
+    return json.loads(p.read_text())
+
+
+def _c(a):
+    a = np.asarray(a, dtype=np.float64)
+    return a[..., 0] + 1j * a[..., 1]
+
+
+def test_golden_rng():
+    g = _load("rng.json")
+    for case in g["cases"]:
+        got = O.port_rng(case["seed"], case["label"], case["kind"], len(case["values"]), case.get("arg", 0))
+        if case["kind"] in (0, 3):
+            assert [int(x) for x in got] == [int(x) for x in case["values"]]
+        else:
+            assert np.array_equal(got, np.array(case["values"], dtype=np.float64))
+
+
+def test_golden_circuits_port():
+    from tests.golden_io import load_circuit_cases
+
+    for case in load_circuit_cases():
+        got = O.port_forward(case["n"], case["gates"], init=case.get("init"), data=case.get("data"))
+        assert np.max(np.abs(got - case["out"])) <= 1e-14, case["name"]
