@@ -1,0 +1,302 @@
+"""Benchmark: BASELINE.json metric "gate passes/sec and achieved HBM GB/s per
+pass at n qubits" on config 3 -- the 30-qubit complex128 QFT (+ final swaps)
+on the seeded, normalised Gaussian input state, one B200 (16 GiB state).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Arms
+  default      the engine (libqsv.so, fused sm_100a tile passes) through the C
+               ABI. A step = one full execution of the 495-gate circuit on the
+               HBM-resident state. value = source gates applied per second
+               (one "gate pass" = one reference gate applied to all 2^30
+               amplitudes). Under torchrun (N > 1) the state is sharded over N
+               GPUs (top log2 N qubits global, NCCL qubit swaps): strong scaling.
+  reference    the reference's own CPU path (oracle/_ref: the unmodified
+               quasar headers, quasar::qubit::apply_gate) on this host, a
+               bounded sample of the same workload: each step applies one
+               gate of the same circuit to the same 30-qubit state.
+
+Timing: W warm-up steps, then K steps bracketed by barrier +
+cudaStreamSynchronize, CUDA events on the engine's own stream, max over
+ranks; the state (16 GiB) is far larger than L2 (126 MB), so no flush is
+needed. Per-launch CUDA events inside the timed region give the dominant
+kernel's average duration for the roofline.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_QUBITS = 30
+WORKLOAD = "cfg3: 30-qubit complex128 QFT + 15 final swaps on a seeded normalised Gaussian state"
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def cpu_reference_sample(cir, n, psi, gates_per_step, steps):
+    """The reference CPU path on a bounded sample: quasar::qubit::apply_gate
+    over `gates_per_step` gates of the same circuit, `steps` times."""
+    from oracle import oracle as O
+
+    gl = cir.gates()
+    times = []
+    state = psi
+    for s in range(steps):
+        sample = [gl[(s * gates_per_step + j) % len(gl)] for j in range(gates_per_step)]
+        sec, state = O.ref_time_apply(n, sample, state)
+        times.append(sec)
+    return times
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2512_18995_b200 import workloads as W
+
+    if not O.REF_LIB.exists():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libquasar_ref.so not built"}))
+        return 0
+    n = N_QUBITS
+    cir = W.cfg3_circuit(n)
+    psi = W.cfg3_input(n)
+    times = cpu_reference_sample(cir, n, psi, 1, args.warmup + args.steps)[args.warmup:]
+    t = float(np.sum(times))
+    value = args.steps / t
+    line = {
+        "metric": "gate passes/sec at n qubits (source gates applied to the full state per second)",
+        "value": value, "unit": "gates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state)",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD, "n_qubits": n, "sample": "1 gate of the circuit per step, in order"},
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "reference",
+                         "sample": f"{args.steps} gates of cfg3 at n=30 via quasar::qubit::apply_gate "
+                                   "(single-threaded reference path; parallel_for is unused by it)"},
+        "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="qsv")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=N_QUBITS, help="(diagnostics only) qubit count")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+
+    from paper_2512_18995_b200 import build as B
+
+    B.build()
+    from paper_2512_18995_b200 import qsv
+    from paper_2512_18995_b200 import workloads as W
+
+    rank, world, local = dist_env()
+    assert world == args.gpus or "WORLD_SIZE" not in os.environ, "--gpus must match the torchrun world size"
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo", init_method="env://")
+        uid = [qsv.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx = qsv.Context(local, rank, world, uid[0])
+    else:
+        ctx = qsv.Context(local)
+    qsv.set_default_context(ctx)
+    n = args.n
+    cir = W.cfg3_circuit(n)
+    psi = W.cfg3_input(n)  # full logical state on the host (16 GiB at n = 30)
+    g = int(np.log2(world))
+    nl = n - g
+    mine = psi[rank << nl:(rank + 1) << nl]
+    plan = qsv.Plan(n, cir.gates(), dtype=qsv.C128, ctx=ctx)
+    st = qsv.QubitState(n, dtype=qsv.C128, ctx=ctx)
+    st.upload(mine)
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        plan.execute(st)
+    ctx.sync()
+    barrier()
+    npass = plan.info["npasses"]
+    launch_ms = []
+    with Clocks(local) as clk:
+        ctx.sync()
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            launch_ms.append(plan.profile(st))  # one execution, events around every launch
+        e1.record(stream)
+        e1.synchronize()
+        ctx.sync()
+        barrier()
+    t_ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([t_ms], dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+    ngates = plan.info["ngates"]
+    value = args.steps * ngates / (t_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (tile_pass_kernel) ----
+    lm = np.array(launch_ms)[:, :npass]  # steps x passes (swap steps excluded when world == 1)
+    amp_bytes = 16
+    bytes_per_launch = 2.0 * amp_bytes * (1 << nl)  # read + write of every local amplitude
+    avg_launch_ms = float(lm.mean())
+    hbm_peak, peak_kind = peaks()
+    achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+
+    # ---- end to end through the C ABI with pinned host buffers ----
+    e2e = None
+    if args.e2e_steps > 0:
+        host_in = torch.from_numpy(mine.view(np.float64)).pin_memory()
+        host_out = torch.empty_like(host_in).pin_memory()
+        L = qsv.lib()
+        cnt = 1 << nl
+        ctx.sync()
+        barrier()
+        t0 = time.perf_counter()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.e2e_steps):
+            qsv.check(L.qsv_state_upload_raw(st.h, 0, host_in.data_ptr(), cnt))
+            plan.execute(st)
+            qsv.check(L.qsv_state_download_raw(st.h, 0, host_out.data_ptr(), cnt))
+        f1.record(stream)
+        f1.synchronize()
+        barrier()
+        e2e_ms = f0.elapsed_time(f1)
+        if world > 1:
+            t = torch.tensor([e2e_ms], dtype=torch.float64)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": args.e2e_steps * ngates / (e2e_ms / 1e3), "unit": "gates/s",
+               "h2d_bytes_per_step": cnt * 16, "d2h_bytes_per_step": cnt * 16,
+               "ms_per_step": e2e_ms / args.e2e_steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+
+        if O.REF_LIB.exists():
+            times = cpu_reference_sample(cir, n, psi, 1, 2)
+            cpu = {"value": 2 / float(np.sum(times)), "unit": "gates/s", "cores": 1, "kind": "reference",
+                   "sample": "first 2 gates of cfg3 (h(0), cp(1,0)) at n=30 via quasar::qubit::apply_gate, "
+                             "single thread"}
+    if rank == 0:
+        line = {
+            "metric": "gate passes/sec at n qubits (source gates applied to the full state per second)",
+            "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state, normalised in FP64)",
+            "config": {"workload": WORKLOAD, "n_qubits": n, "gates": ngates, "passes_per_step": npass,
+                       "swaps_per_step": plan.info["nswaps"], "parallelism": f"state sharded over {world} GPU(s)",
+                       "l2": "state (16 GiB) >> L2 (126 MB); no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                         "kernel": "tile_pass_kernel", "bytes_per_launch": bytes_per_launch,
+                         "avg_launch_ms": avg_launch_ms,
+                         "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
+            "gpu_launches": args.steps * npass,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -97,7 +97,9 @@ typedef struct qsv_opts {
     int32_t tile_bits;      /* qubits per shared-memory tile (K) */
     int32_t low_bits;       /* lowest physical qubits always in a tile (coalescing) */
     int32_t use_graph;      /* capture the pass sequence in a CUDA graph */
-    int32_t reserved[4];
+    int32_t no_fuse_1q;     /* 1 = keep runs of single-qubit gates unfused */
+    int32_t no_phase_flush; /* 1 = apply every diagonal gate eagerly */
+    int32_t reserved[2];
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */

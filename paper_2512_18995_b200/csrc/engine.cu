@@ -149,9 +149,90 @@ __device__ __forceinline__ void diag_op(typename Vec2<T>::type (&v)[1 << R], con
     }
 }
 
+template <typename T, int R, int J>
+__device__ __forceinline__ void dense1r(typename Vec2<T>::type (&v)[1 << R], const T *__restrict__ m, bool fok,
+                                        int rmask, int rval) {
+    using V = typename Vec2<T>::type;
+    const T a = m[0], b = m[2], c = m[4], d = m[6];
+#pragma unroll
+    for (int r = 0; r < (1 << R); ++r) {
+        if (r & (1 << J)) continue;
+        const int r1 = r | (1 << J);
+        if (fok && ((r & rmask) == rval)) {
+            const V x0 = v[r], x1 = v[r1];
+            v[r] = V{a * x0.x + b * x1.x, a * x0.y + b * x1.y};
+            v[r1] = V{c * x0.x + d * x1.x, c * x0.y + d * x1.y};
+        }
+    }
+}
+
+template <typename T, int R, int J>
+__device__ __forceinline__ void x1(typename Vec2<T>::type (&v)[1 << R], bool fok, int rmask, int rval) {
+    using V = typename Vec2<T>::type;
+#pragma unroll
+    for (int r = 0; r < (1 << R); ++r) {
+        if (r & (1 << J)) continue;
+        const int r1 = r | (1 << J);
+        const bool on = fok && ((r & rmask) == rval);
+        const V x0 = v[r], x1v = v[r1];
+        v[r] = on ? x1v : x0;
+        v[r1] = on ? x0 : x1v;
+    }
+}
+
+template <typename T, int R, int J>
+__device__ __forceinline__ void scale_slot(typename Vec2<T>::type (&v)[1 << R], typename Vec2<T>::type f) {
+#pragma unroll
+    for (int r = 0; r < (1 << R); ++r)
+        if (r & (1 << J)) v[r] = cmul(v[r], f);
+}
+
+// value of a phase record on the bits of `pb` (1 when its condition fails)
+template <typename V>
+__device__ __forceinline__ V eval_rec(const DiagRec &rc, uint64_t pb) {
+    using T = decltype(V{}.x);
+    if ((pb & rc.fmask) != rc.fval) return V{1, 0};
+    int idx = 0;
+    if (rc.nt >= 1) idx = static_cast<int>((pb >> rc.tpos0) & 1ull);
+    if (rc.nt == 2) idx = (idx << 1) | static_cast<int>((pb >> rc.tpos1) & 1ull);
+    return V{static_cast<T>(rc.val[2 * idx]), static_cast<T>(rc.val[2 * idx + 1])};
+}
+
+// Context a FLUSH needs besides the registers.
+template <typename V> struct FlushCtx {
+    const FlushTarget *targets;
+    const DiagRec *recs;
+    const V *tables;
+    const V *E;  // shared memory, per-CTA external factors
+    int s;       // set index
+};
+
+template <typename T, int R>
+__device__ __forceinline__ void flush_op(typename Vec2<T>::type (&v)[1 << R], const TileOp<T> &o,
+                                         const FlushCtx<typename Vec2<T>::type> &fc, uint64_t pb) {
+    using V = typename Vec2<T>::type;
+    for (int ti = o.a; ti < o.b; ++ti) {
+        const FlushTarget ft = fc.targets[ti];
+        V f = ft.eidx >= 0 ? fc.E[ft.eidx] : V{1, 0};
+        if (ft.table >= 0) f = cmul(f, fc.tables[ft.table + fc.s]);
+        for (int k = ft.mix_begin; k < ft.mix_end; ++k) f = cmul(f, eval_rec<V>(fc.recs[k], pb));
+        switch (ft.slot) {
+        case -1:
+#pragma unroll
+            for (int r = 0; r < (1 << R); ++r) v[r] = cmul(v[r], f);
+            break;
+        case 0: scale_slot<T, R, 0>(v, f); break;
+        case 1: if constexpr (R > 1) scale_slot<T, R, 1>(v, f); break;
+        case 2: if constexpr (R > 2) scale_slot<T, R, 2>(v, f); break;
+        case 3: if constexpr (R > 3) scale_slot<T, R, 3>(v, f); break;
+        }
+    }
+}
+
 template <typename T, int R>
 __device__ __forceinline__ void run_op(typename Vec2<T>::type (&v)[1 << R], const TileOp<T> &o,
-                                       const T *__restrict__ enc_table, int batch, int row, uint64_t pb) {
+                                       const T *__restrict__ enc_table, int batch, int row, uint64_t pb,
+                                       const FlushCtx<typename Vec2<T>::type> &fc) {
     const bool fok = (pb & o.fmask) == o.fval;
     const T *m = o.enc >= 0 ? enc_table + (static_cast<size_t>(o.enc) * batch + row) * 32 : o.m;
     const bool zoc = (o.flags & OPF_ZERO_OFF_CONTROL) != 0;
@@ -178,6 +259,23 @@ __device__ __forceinline__ void run_op(typename Vec2<T>::type (&v)[1 << R], cons
         }
         break;
     case OP_DIAG: diag_op<T, R>(v, o, m, pb, fok, zoc); break;
+    case OP_DENSE1R:
+        switch (o.a) {
+        case 0: dense1r<T, R, 0>(v, m, fok, o.rmask, o.rval); break;
+        case 1: if constexpr (R > 1) dense1r<T, R, 1>(v, m, fok, o.rmask, o.rval); break;
+        case 2: if constexpr (R > 2) dense1r<T, R, 2>(v, m, fok, o.rmask, o.rval); break;
+        case 3: if constexpr (R > 3) dense1r<T, R, 3>(v, m, fok, o.rmask, o.rval); break;
+        }
+        break;
+    case OP_X1:
+        switch (o.a) {
+        case 0: x1<T, R, 0>(v, fok, o.rmask, o.rval); break;
+        case 1: if constexpr (R > 1) x1<T, R, 1>(v, fok, o.rmask, o.rval); break;
+        case 2: if constexpr (R > 2) x1<T, R, 2>(v, fok, o.rmask, o.rval); break;
+        case 3: if constexpr (R > 3) x1<T, R, 3>(v, fok, o.rmask, o.rval); break;
+        }
+        break;
+    case OP_FLUSH: flush_op<T, R>(v, o, fc, pb); break;
     }
 }
 
@@ -220,8 +318,21 @@ __global__ void __launch_bounds__(256, 2) tile_pass_kernel(const PassArgs a) {
 
     const uint64_t pbase = a.rank_base | tb;
     const int nsets = 1 << (K - R);
+    __shared__ V E[kMaxExtTargets];
+    FlushCtx<V> fc{a.targets, a.recs, reinterpret_cast<const V *>(a.tables), E, 0};
     for (int gi = 0; gi < a.ngroups; ++gi) {
         const GroupDesc &gd = a.groups[gi];
+        if (gd.tgt_end > gd.tgt_begin) {
+            // per-CTA factors of records over bits outside the tile
+            for (int t = gd.tgt_begin + threadIdx.x; t < gd.tgt_end; t += blockDim.x) {
+                const FlushTarget ft = a.targets[t];
+                if (ft.eidx < 0) continue;
+                V f{1, 0};
+                for (int k = ft.ext_begin; k < ft.ext_end; ++k) f = cmul(f, eval_rec<V>(a.recs[k], pbase));
+                E[ft.eidx] = f;
+            }
+            __syncthreads();
+        }
         int uoff[1 << R];
         uoff[0] = 0;
 #pragma unroll
@@ -243,7 +354,8 @@ __global__ void __launch_bounds__(256, 2) tile_pass_kernel(const PassArgs a) {
             V v[1 << R];
 #pragma unroll
             for (int r = 0; r < (1 << R); ++r) v[r] = tile[swz<V>(ub | uoff[r])];
-            for (int oi = ob; oi < oe; ++oi) run_op<T, R>(v, ops[oi], enc_table, a.batch, row, pb);
+            fc.s = s;
+            for (int oi = ob; oi < oe; ++oi) run_op<T, R>(v, ops[oi], enc_table, a.batch, row, pb, fc);
 #pragma unroll
             for (int r = 0; r < (1 << R); ++r) tile[swz<V>(ub | uoff[r])] = v[r];
         }

@@ -25,6 +25,7 @@
 // The same greedy, with capacity R over tile qubits, forms the groups.
 #include <algorithm>
 #include <bit>
+#include <cmath>
 #include <cstring>
 
 #include "qsv_internal.hpp"
@@ -90,7 +91,330 @@ void set_m(TileOp<double> &op, const cplx *m, int d) {
 
 } // namespace
 
-std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys,
+// ---- single-qubit run fusion ----------------------------------------------
+std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates) {
+    std::vector<GateRec> out;
+    std::vector<int> open(kMaxQubits, -1); // wire -> index in `out` of an open run
+    for (const GateRec &g : gates) {
+        const bool fusable = g.k == 1 && g.ctls.empty() && !g.encoded && g.flags == 0;
+        if (fusable) {
+            const int w = g.wires[0];
+            if (open[w] >= 0) {
+                GateRec &f = out[open[w]];
+                cplx m[4];
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 2; ++c) m[r * 2 + c] = g.m[r * 2] * f.m[c] + g.m[r * 2 + 1] * f.m[2 + c];
+                for (int i = 0; i < 4; ++i) f.m[i] = m[i];
+                f.diag = (m[1] == cplx(0, 0) && m[2] == cplx(0, 0));
+                f.name = "fused1q";
+                f.kind = GK_CUSTOM;
+                continue;
+            }
+            out.push_back(g);
+            open[w] = static_cast<int>(out.size()) - 1;
+            continue;
+        }
+        for (int t = 0; t < g.k; ++t) open[g.wires[t]] = -1;
+        for (int c : g.ctls) open[c] = -1;
+        out.push_back(g);
+    }
+    return out;
+}
+
+namespace {
+
+bool is_unitary_diag(const GateRec &g) {
+    const int d = 1 << g.k;
+    for (int i = 0; i < d; ++i)
+        if (std::abs(std::abs(g.m[i * d + i]) - 1.0) > 1e-12) return false;
+    return true;
+}
+
+cplx eval_rec(const DiagRec &r, uint64_t pb) {
+    if ((pb & r.fmask) != r.fval) return cplx(1, 0);
+    int idx = 0;
+    if (r.nt >= 1) idx = static_cast<int>((pb >> r.tpos0) & 1);
+    if (r.nt == 2) idx = (idx << 1) | static_cast<int>((pb >> r.tpos1) & 1);
+    return cplx(r.val[2 * idx], r.val[2 * idx + 1]);
+}
+
+uint64_t rec_deps(const DiagRec &r) {
+    uint64_t d = r.fmask;
+    if (r.nt >= 1) d |= 1ull << r.tpos0;
+    if (r.nt == 2) d |= 1ull << r.tpos1;
+    return d;
+}
+
+// Lowers the admitted gates of one register group into device ops. Unitary
+// diagonal gates that depend on at most one register slot are not applied
+// where they stand: their phase becomes a per-slot (or per-set "uniform")
+// factor that floats forward -- diagonal gates commute with each other and
+// with every gate not acting non-diagonally on their slot -- and is applied
+// by one FLUSH right before the next non-diagonal gate on that slot, or at
+// the end of the group. Each factor is split by the bits it reads:
+//   EXT    only bits outside the tile: one value per CTA (shared memory);
+//   TILE   only tile bits outside the group: a host-precomputed table over
+//          the set index, shared by every CTA;
+//   MIXED  both: evaluated per register set.
+struct GroupLowering {
+    PassHost &ph;
+    const std::vector<GateRec> &gates;
+    const std::vector<int> &phys;
+    const int *slot_of_phys;
+    int R;
+    std::vector<EncDesc> &encs;
+    bool flush_enabled;
+    std::vector<int> ng_phys;                 // physical bits of the set index, LSB first
+    std::vector<std::vector<DiagRec>> pend;   // per slot
+    std::vector<DiagRec> pend_u;
+    int n_ext = 0;
+
+    GroupLowering(PassHost &p, const std::vector<GateRec> &g, const std::vector<int> &ph_, const int *sop, int r,
+                  std::vector<EncDesc> &e, bool fe)
+        : ph(p), gates(g), phys(ph_), slot_of_phys(sop), R(r), encs(e), flush_enabled(fe), pend(r) {}
+
+    int slot(int wire) const {
+        const int b = phys[wire];
+        return b < 64 ? slot_of_phys[b] : -1;
+    }
+
+    void emit_target(int slot_id, const std::vector<DiagRec> &recs) {
+        if (recs.empty()) return;
+        uint64_t ngmask = 0;
+        for (int b : ng_phys) ngmask |= 1ull << b;
+        const uint64_t tilemask = ngmask;
+        FlushTarget t{};
+        t.slot = slot_id;
+        t.table = -1;
+        t.eidx = -1;
+        std::vector<DiagRec> ext, tile, mix;
+        for (const DiagRec &r : recs) {
+            const uint64_t d = rec_deps(r);
+            if ((d & ngmask) == 0) ext.push_back(r); // no tile dependence (tile group bits never appear)
+            else if ((d & ~tilemask) == 0) tile.push_back(r);
+            else mix.push_back(r);
+        }
+        if (!ext.empty() && n_ext >= kMaxExtTargets) {
+            mix.insert(mix.end(), ext.begin(), ext.end());
+            ext.clear();
+        }
+        t.ext_begin = static_cast<int>(ph.recs.size());
+        ph.recs.insert(ph.recs.end(), ext.begin(), ext.end());
+        t.ext_end = static_cast<int>(ph.recs.size());
+        if (!ext.empty()) t.eidx = n_ext++;
+        t.mix_begin = static_cast<int>(ph.recs.size());
+        ph.recs.insert(ph.recs.end(), mix.begin(), mix.end());
+        t.mix_end = static_cast<int>(ph.recs.size());
+        if (!tile.empty()) {
+            const int nset = 1 << ng_phys.size();
+            t.table = static_cast<int>(ph.tables.size());
+            for (int s = 0; s < nset; ++s) {
+                uint64_t pb = 0;
+                for (size_t i = 0; i < ng_phys.size(); ++i)
+                    if ((s >> i) & 1) pb |= 1ull << ng_phys[i];
+                cplx f(1, 0);
+                for (const DiagRec &r : tile) f *= eval_rec(r, pb);
+                ph.tables.push_back(f);
+            }
+        }
+        ph.targets.push_back(t);
+    }
+
+    void flush(const std::vector<int> &slots, bool with_u) {
+        const int t0 = static_cast<int>(ph.targets.size());
+        for (int j : slots) {
+            emit_target(j, pend[j]);
+            pend[j].clear();
+        }
+        if (with_u) {
+            emit_target(-1, pend_u);
+            pend_u.clear();
+        }
+        const int t1 = static_cast<int>(ph.targets.size());
+        if (t1 > t0) {
+            TileOp<double> op{};
+            op.type = OP_FLUSH;
+            op.enc = -1;
+            op.a = t0;
+            op.b = t1;
+            ph.ops.push_back(op);
+        }
+    }
+
+    // Returns true when the diagonal gate was absorbed into pending factors.
+    bool try_defer(const GateRec &g) {
+        if (!flush_enabled || !g.diag || g.encoded || g.flags || !is_unitary_diag(g)) return false;
+        DiagRec base{};
+        int rc = -1, nrc = 0;
+        for (int c : g.ctls) {
+            const int s = slot(c);
+            if (s >= 0) rc = s, ++nrc;
+            else {
+                base.fmask |= 1ull << phys[c];
+                base.fval |= 1ull << phys[c];
+            }
+        }
+        int rt = -1, rtpos = -1, nrt = 0;
+        for (int t = 0; t < g.k; ++t)
+            if (slot(g.wires[t]) >= 0) rt = slot(g.wires[t]), rtpos = t, ++nrt;
+        const int d = 1 << g.k;
+        cplx dv[4];
+        for (int i = 0; i < d; ++i) dv[i] = g.m[i * d + i];
+        auto setv = [](DiagRec &r, int i, cplx v) {
+            r.val[2 * i] = v.real();
+            r.val[2 * i + 1] = v.imag();
+        };
+        if (nrc + nrt == 0) {
+            DiagRec r = base;
+            r.nt = g.k;
+            r.tpos0 = phys[g.wires[0]];
+            if (g.k == 2) r.tpos1 = phys[g.wires[1]];
+            for (int i = 0; i < d; ++i) setv(r, i, dv[i]);
+            pend_u.push_back(r);
+            return true;
+        }
+        if (nrc == 1 && nrt == 0) {
+            DiagRec r = base;
+            r.nt = g.k;
+            r.tpos0 = phys[g.wires[0]];
+            if (g.k == 2) r.tpos1 = phys[g.wires[1]];
+            for (int i = 0; i < d; ++i) setv(r, i, dv[i]);
+            pend[rc].push_back(r);
+            return true;
+        }
+        if (nrc == 0 && nrt == 1) {
+            DiagRec u = base, f = base;
+            if (g.k == 1) {
+                u.nt = f.nt = 0;
+                setv(u, 0, dv[0]);
+                setv(f, 0, dv[1] / dv[0]);
+            } else {
+                const int other = 1 - rtpos;
+                u.nt = f.nt = 1;
+                u.tpos0 = f.tpos0 = phys[g.wires[other]];
+                for (int ob = 0; ob < 2; ++ob) {
+                    const int i0 = rtpos == 0 ? (0 << 1) | ob : (ob << 1) | 0;
+                    const int i1 = rtpos == 0 ? (1 << 1) | ob : (ob << 1) | 1;
+                    setv(u, ob, dv[i0]);
+                    setv(f, ob, dv[i1] / dv[i0]);
+                }
+            }
+            pend_u.push_back(u);
+            pend[rt].push_back(f);
+            return true;
+        }
+        return false;
+    }
+
+    void add(int gi) {
+        const GateRec &g = gates[gi];
+        if (try_defer(g)) return;
+        if (!g.diag) { // flush the pending factors of the slots it acts on non-diagonally
+            std::vector<int> need;
+            for (int t = 0; t < g.k; ++t) {
+                const int s = slot(g.wires[t]);
+                if (s >= 0 && !pend[s].empty()) need.push_back(s);
+            }
+            if (!need.empty()) flush(need, false);
+        }
+        lower(g);
+    }
+
+    void finish() {
+        std::vector<int> all;
+        for (int j = 0; j < R; ++j)
+            if (!pend[j].empty()) all.push_back(j);
+        flush(all, true);
+    }
+
+    void lower(const GateRec &g) {
+        TileOp<double> op{};
+        op.enc = -1;
+        op.flags = g.flags & OPF_ZERO_OFF_CONTROL;
+        for (int c : g.ctls) {
+            const int s = slot(c);
+            if (s >= 0) {
+                op.rmask |= 1 << s;
+                op.rval |= 1 << s;
+            } else {
+                op.fmask |= 1ull << phys[c];
+                op.fval |= 1ull << phys[c];
+            }
+        }
+        const int d = 1 << g.k;
+        if (g.diag) {
+            op.type = OP_DIAG;
+            op.nt = g.k;
+            int *tt[2] = {&op.t0, &op.t1};
+            int *tr[2] = {&op.t0reg, &op.t1reg};
+            for (int t = 0; t < g.k; ++t) {
+                const int s = slot(g.wires[t]);
+                *tt[t] = s >= 0 ? s : phys[g.wires[t]];
+                *tr[t] = s >= 0 ? 1 : 0;
+            }
+            if (!g.encoded)
+                for (int i = 0; i < d; ++i) {
+                    op.m[2 * i] = g.m[i * d + i].real();
+                    op.m[2 * i + 1] = g.m[i * d + i].imag();
+                }
+        } else if (g.k == 1) {
+            op.a = slot(g.wires[0]);
+            op.type = OP_DENSE1;
+            if (!g.encoded) {
+                set_m(op, g.m, 2);
+                const bool real = g.m[0].imag() == 0 && g.m[1].imag() == 0 && g.m[2].imag() == 0 &&
+                                  g.m[3].imag() == 0;
+                if (real) op.type = OP_DENSE1R;
+                if (g.m[0] == cplx(0, 0) && g.m[3] == cplx(0, 0) && g.m[1] == cplx(1, 0) && g.m[2] == cplx(1, 0) &&
+                    !(g.flags & OPF_ZERO_OFF_CONTROL))
+                    op.type = OP_X1;
+            }
+        } else {
+            op.type = OP_DENSE2;
+            const int s0 = slot(g.wires[0]), s1 = slot(g.wires[1]);
+            const bool swapq = s0 < s1;
+            op.a = swapq ? s1 : s0;
+            op.b = swapq ? s0 : s1;
+            if (!g.encoded) {
+                cplx mm[16];
+                for (int r = 0; r < 4; ++r)
+                    for (int c = 0; c < 4; ++c) {
+                        const int rr = swapq ? ((r & 1) << 1) | (r >> 1) : r;
+                        const int cc = swapq ? ((c & 1) << 1) | (c >> 1) : c;
+                        mm[r * 4 + c] = g.m[rr * 4 + cc];
+                    }
+                set_m(op, mm, 4);
+            }
+            if (g.encoded) {
+                EncDesc e{};
+                e.kind = g.kind;
+                e.slot = g.enc_slot;
+                e.nparams = g.nparams;
+                e.swapq = swapq ? 1 : 0;
+                e.diag = 0;
+                op.enc = static_cast<int>(encs.size());
+                encs.push_back(e);
+            }
+            ph.ops.push_back(op);
+            return;
+        }
+        if (g.encoded) {
+            EncDesc e{};
+            e.kind = g.kind;
+            e.slot = g.enc_slot;
+            e.nparams = g.nparams;
+            e.swapq = 0;
+            e.diag = g.diag ? 1 : 0;
+            op.enc = static_cast<int>(encs.size());
+            encs.push_back(e);
+        }
+        ph.ops.push_back(op);
+    }
+};
+
+} // namespace
+
+std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const std::vector<int> &phys,
                                   const PlanConfig &cfg, std::vector<EncDesc> &encs) {
     const int nl = cfg.nlocal;
     const int K = std::min(cfg.K, nl);
@@ -98,6 +422,8 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::
     const int R = std::min(cfg.R, K);
     require(K >= 1, "planner: empty local state");
     const uint64_t localmask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
+    const std::vector<GateRec> fused = cfg.fuse_1q ? fuse_single_qubit_runs(gates_in) : gates_in;
+    const std::vector<GateRec> &gates = fused;
 
     std::vector<PG> pg(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) {
@@ -153,7 +479,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::
 
         // ---- groups (capacity R over tile qubits) ---------------------------
         std::vector<int> gorder = pass_gates[p];
-        ph.ngates = static_cast<int>(gorder.size());
+        ph.ngates = static_cast<int>(gorder.size()); // (after 1q fusion)
         while (!gorder.empty()) {
             uint64_t gact = 0;
             std::vector<int> took = admit(gorder, pg, gact, R, active);
@@ -177,79 +503,13 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::
             for (int t = 0; t < K; ++t)
                 if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) gd.ng_bit[q++] = t;
 
-            for (int gi : took) {
-                const GateRec &g = gates[gi];
-                TileOp<double> op{};
-                op.enc = -1;
-                op.flags = g.flags & OPF_ZERO_OFF_CONTROL;
-                // controls
-                for (int c : g.ctls) {
-                    const int b = phys[c];
-                    if (b < 64 && slot_of_phys[b] >= 0) {
-                        op.rmask |= 1 << slot_of_phys[b];
-                        op.rval |= 1 << slot_of_phys[b];
-                    } else {
-                        op.fmask |= 1ull << b;
-                        op.fval |= 1ull << b;
-                    }
-                }
-                const int d = 1 << g.k;
-                if (g.diag) {
-                    op.type = OP_DIAG;
-                    op.nt = g.k;
-                    int *tt[2] = {&op.t0, &op.t1};
-                    int *tr[2] = {&op.t0reg, &op.t1reg};
-                    for (int t = 0; t < g.k; ++t) {
-                        const int b = phys[g.wires[t]];
-                        if (slot_of_phys[b] >= 0) {
-                            *tt[t] = slot_of_phys[b];
-                            *tr[t] = 1;
-                        } else {
-                            *tt[t] = b;
-                            *tr[t] = 0;
-                        }
-                    }
-                    if (!g.encoded)
-                        for (int i = 0; i < d; ++i) {
-                            op.m[2 * i] = g.m[i * d + i].real();
-                            op.m[2 * i + 1] = g.m[i * d + i].imag();
-                        }
-                } else if (g.k == 1) {
-                    op.type = OP_DENSE1;
-                    op.a = slot_of_phys[phys[g.wires[0]]];
-                    if (!g.encoded) set_m(op, g.m, 2);
-                } else {
-                    op.type = OP_DENSE2;
-                    const int s0 = slot_of_phys[phys[g.wires[0]]], s1 = slot_of_phys[phys[g.wires[1]]];
-                    const bool swapq = s0 < s1;
-                    op.a = swapq ? s1 : s0;
-                    op.b = swapq ? s0 : s1;
-                    if (!g.encoded) {
-                        cplx mm[16];
-                        for (int r = 0; r < 4; ++r)
-                            for (int c = 0; c < 4; ++c) {
-                                // swap the two qubits of the row/column index
-                                const int rr = swapq ? ((r & 1) << 1) | (r >> 1) : r;
-                                const int cc = swapq ? ((c & 1) << 1) | (c >> 1) : c;
-                                mm[r * 4 + c] = g.m[rr * 4 + cc];
-                            }
-                        set_m(op, mm, 4);
-                    }
-                    if (g.encoded) op.flags |= swapq ? 2 : 0;
-                }
-                if (g.encoded) {
-                    EncDesc e{};
-                    e.kind = g.kind;
-                    e.slot = g.enc_slot;
-                    e.nparams = g.nparams;
-                    e.swapq = (op.type == OP_DENSE2 && (op.flags & 2)) ? 1 : 0;
-                    e.diag = g.diag ? 1 : 0;
-                    op.enc = static_cast<int>(encs.size());
-                    encs.push_back(e);
-                }
-                op.flags &= ~2; // (bit 1 was scratch for the qubit swap)
-                ph.ops.push_back(op);
-            }
+            GroupLowering low(ph, gates, phys, slot_of_phys, R, encs, cfg.phase_flush);
+            low.ng_phys.clear();
+            for (int i = 0; i < K - R; ++i) low.ng_phys.push_back(ph.tile_pos[gd.ng_bit[i]]);
+            gd.tgt_begin = static_cast<int>(ph.targets.size());
+            for (int gi : took) low.add(gi);
+            low.finish();
+            gd.tgt_end = static_cast<int>(ph.targets.size());
             gd.op_end = static_cast<int>(ph.ops.size());
             ph.groups.push_back(gd);
         }

@@ -36,7 +36,14 @@ constexpr int kMaxSlots = 5;       // R: register-resident qubits per group
 constexpr int kRegSlots = 4;       // R used by the fused kernel
 
 // ---- device program (tile passes) ---------------------------------------
-enum OpType : int32_t { OP_DENSE1 = 1, OP_DENSE2 = 2, OP_DIAG = 3 };
+enum OpType : int32_t {
+    OP_DENSE1 = 1,   // complex 2x2 on one register slot
+    OP_DENSE2 = 2,   // complex 4x4 on two register slots
+    OP_DIAG = 3,     // diagonal applied eagerly per register (>= 2 register deps / non-unitary)
+    OP_DENSE1R = 4,  // real 2x2 (h, ry, ...): half the FLOPs
+    OP_X1 = 5,       // Pauli-X on one slot: a predicated register swap, no FLOPs
+    OP_FLUSH = 6     // apply pending phase factors: targets [a, b)
+};
 enum OpFlags : int32_t { OPF_ZERO_OFF_CONTROL = 1 };
 
 // One gate, lowered onto a register group. Conditions are split into the
@@ -45,7 +52,7 @@ enum OpFlags : int32_t { OPF_ZERO_OFF_CONTROL = 1 };
 // bits outside the tile, and rank bits on a distributed state).
 template <typename T> struct alignas(16) TileOp {
     int32_t type;
-    int32_t a, b;           // DENSE1: a = slot; DENSE2: a = MSB slot > b = LSB slot
+    int32_t a, b;           // DENSE1: a = slot; DENSE2: a = MSB slot > b = LSB slot; FLUSH: target range
     int32_t rmask, rval;
     int32_t enc;            // >= 0: matrix comes from the per-row table
     int32_t flags;
@@ -56,10 +63,37 @@ template <typename T> struct alignas(16) TileOp {
     T m[32];                // DENSE1: 2x2, DENSE2: 4x4 (row-major, re/im); DIAG: d[0..3]
 };
 
+// A phase factor that depends only on bits OUTSIDE the register group
+// ("fixed" bits of a register set): value = cond ? val[index of the fixed
+// target bits] : 1, cond = (index & fmask) == fval.
+struct alignas(16) DiagRec {
+    uint64_t fmask, fval;
+    int32_t nt;             // fixed target bits (0..2)
+    int32_t tpos0, tpos1;   // their physical positions (tpos0 is the MSB of the index)
+    int32_t pad;
+    double val[8];          // up to 4 complex values
+};
+
+// One factor applied at a FLUSH: to every register (slot < 0) or to the
+// registers whose slot bit is 1. factor = E[eidx] (per CTA: records over bits
+// outside the tile) * table[s] (host-precomputed over the set index s:
+// records over tile bits outside the group) * prod(mixed records, per set).
+struct FlushTarget {
+    int32_t slot;
+    int32_t table;          // offset (complex entries) into the pass's table, or -1
+    int32_t ext_begin, ext_end;
+    int32_t mix_begin, mix_end;
+    int32_t eidx;           // index into the CTA's shared E array, or -1
+    int32_t pad;
+};
+
+constexpr int kMaxExtTargets = 64;
+
 struct GroupDesc {
     int32_t op_begin, op_end;
     int32_t slot_bit[kMaxSlots];       // tile-local bit of each register slot
     int32_t ng_bit[kMaxTileBits];      // tile-local bits NOT in the group, ascending
+    int32_t tgt_begin, tgt_end;        // flush targets with per-CTA (E) factors to precompute
 };
 
 // Per-row matrix binding of an encoded gate (device-side gate_matrix).
@@ -82,6 +116,9 @@ struct PassArgs {
     const GroupDesc *groups;
     const void *ops;          // TileOp<T>*
     const void *enc_table;    // [nenc][batch][32] T
+    const FlushTarget *targets;
+    const DiagRec *recs;
+    const void *tables;       // complex T
     int32_t batch;
     int32_t nlocal, K, L, ngroups, next;
     int32_t row0;             // first batch row of this launch (gridDim.y chunks)
@@ -96,6 +133,9 @@ struct PassHost {
     std::vector<int> ext_pos;         // nlocal - K
     std::vector<GroupDesc> groups;
     std::vector<TileOp<double>> ops;  // lowered in double; converted per dtype
+    std::vector<FlushTarget> targets;
+    std::vector<DiagRec> recs;
+    std::vector<cplx> tables;
     int ngates = 0;                   // source gates in this pass
     double bytes = 0;                 // algorithmic HBM bytes per row
 };
@@ -174,6 +214,7 @@ struct Plan {
     std::vector<EncDesc> encs;
     // device buffers
     void *d_groups = nullptr, *d_ops = nullptr, *d_encs = nullptr;
+    void *d_targets = nullptr, *d_recs = nullptr, *d_tables = nullptr;
     void *d_enc_table = nullptr;
     size_t enc_table_rows = 0;
     void *d_data = nullptr;
@@ -190,9 +231,14 @@ struct Plan {
 // ---- planner (planner.cpp) --------------------------------------------------
 struct PlanConfig {
     int nlocal = 0, K = 12, L = 3, R = kRegSlots;
-    bool fuse = true;
+    bool fuse = true;       // tile passes with many gates (false: one gate per pass)
+    bool fuse_1q = true;    // pre-multiply runs of single-qubit gates
+    bool phase_flush = true;  // lazy phase factors for diagonal gates
     int dtype = QSV_C128;
 };
+// Host-side gate fusion: runs of uncontrolled, non-encoded single-qubit gates
+// on the same wire (nothing else touching it in between) become one matrix.
+std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates);
 // Lowers gates (already mapped to PHYSICAL bit positions, all targets local)
 // to tile passes.
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys_of_wire,

@@ -32,6 +32,9 @@ Plan::~Plan() {
     if (graph) cudaGraphExecDestroy(graph);
     cudaFree(d_groups);
     cudaFree(d_ops);
+    cudaFree(d_targets);
+    cudaFree(d_recs);
+    cudaFree(d_tables);
     cudaFree(d_encs);
     cudaFree(d_enc_table);
     cudaFree(d_data);
@@ -210,6 +213,8 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.L = p->opts.low_bits > 0 ? p->opts.low_bits : default_low_bits(dtype, p->nlocal);
     cfg.L = std::max(dtype == QSV_C64 ? 1 : 0, std::min(cfg.L, cfg.K));
     cfg.fuse = p->opts.fuse != 0;
+    cfg.fuse_1q = p->opts.no_fuse_1q == 0;
+    cfg.phase_flush = p->opts.no_phase_flush == 0;
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
     if (ctx->world == 1) {
@@ -241,12 +246,21 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
 
 void upload_plan(Plan &p) {
     std::vector<GroupDesc> groups;
-    std::vector<size_t> group_off, op_off;
+    std::vector<FlushTarget> targets;
+    std::vector<DiagRec> recs;
+    std::vector<cplx> tables;
+    std::vector<size_t> group_off, op_off, tgt_off, rec_off, tab_off;
     size_t nops = 0;
     for (auto &ph : p.passes) {
         group_off.push_back(groups.size());
         op_off.push_back(nops);
+        tgt_off.push_back(targets.size());
+        rec_off.push_back(recs.size());
+        tab_off.push_back(tables.size());
         groups.insert(groups.end(), ph.groups.begin(), ph.groups.end());
+        targets.insert(targets.end(), ph.targets.begin(), ph.targets.end());
+        recs.insert(recs.end(), ph.recs.begin(), ph.recs.end());
+        tables.insert(tables.end(), ph.tables.begin(), ph.tables.end());
         nops += ph.ops.size();
     }
     const size_t op_size = p.dtype == QSV_C64 ? sizeof(TileOp<float>) : sizeof(TileOp<double>);
@@ -268,6 +282,24 @@ void upload_plan(Plan &p) {
     if (!groups.empty())
         QSV_CUDA(cudaMemcpy(p.d_groups, groups.data(), groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice));
     QSV_CUDA(cudaMemcpy(p.d_ops, opbuf.data(), opbuf.size(), cudaMemcpyHostToDevice));
+    auto up = [](void **dst, const void *src, size_t bytes) {
+        QSV_CUDA(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
+        if (bytes) QSV_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
+    };
+    up(&p.d_targets, targets.data(), targets.size() * sizeof(FlushTarget));
+    up(&p.d_recs, recs.data(), recs.size() * sizeof(DiagRec));
+    const size_t tsz = p.dtype == QSV_C64 ? 8 : 16;
+    std::vector<unsigned char> tabbuf(tables.size() * tsz);
+    for (size_t i = 0; i < tables.size(); ++i) {
+        if (p.dtype == QSV_C64) {
+            const float f[2] = {static_cast<float>(tables[i].real()), static_cast<float>(tables[i].imag())};
+            std::memcpy(tabbuf.data() + i * tsz, f, tsz);
+        } else {
+            const double f[2] = {tables[i].real(), tables[i].imag()};
+            std::memcpy(tabbuf.data() + i * tsz, f, tsz);
+        }
+    }
+    up(&p.d_tables, tabbuf.data(), tabbuf.size());
     if (!p.encs.empty()) {
         QSV_CUDA(cudaMalloc(&p.d_encs, p.encs.size() * sizeof(EncDesc)));
         QSV_CUDA(cudaMemcpy(p.d_encs, p.encs.data(), p.encs.size() * sizeof(EncDesc), cudaMemcpyHostToDevice));
@@ -282,6 +314,9 @@ void upload_plan(Plan &p) {
         a.rank_base = static_cast<uint64_t>(p.ctx->rank) << p.nlocal;
         a.groups = static_cast<const GroupDesc *>(p.d_groups) + group_off[i];
         a.ops = static_cast<const unsigned char *>(p.d_ops) + op_off[i] * op_size;
+        a.targets = static_cast<const FlushTarget *>(p.d_targets) + tgt_off[i];
+        a.recs = static_cast<const DiagRec *>(p.d_recs) + rec_off[i];
+        a.tables = static_cast<const unsigned char *>(p.d_tables) + tab_off[i] * tsz;
         a.nlocal = p.nlocal;
         a.K = ph.K;
         a.L = ph.L;
