@@ -1,13 +1,5 @@
-// sm_100a kernels of the qsv engine.
-//
-//   tile_pass_kernel   the fused gate pass (the hot loop). Replaces the
-//                      reference's per-gate strided sweep
-//                      (apply_matrix_strided, /root/reference/proj/include/
-//                      quasar/qubit/state.hpp:111-143) with one HBM read+write
-//                      per PASS of many gates: cp.async 16-byte staging of a
-//                      2^K-amplitude tile into XOR-swizzled shared memory,
-//                      register-resident groups of R qubits, coalesced
-//                      streaming stores.
+// sm_100a support kernels of the qsv engine (the fused gate pass lives in
+// tile_pass.cu):
 //   bind_kernel        device-side gate_matrix for encoded (per-row) gates
 //                      (gate.hpp:89-154, circuit.hpp:139-147).
 //   zsum/pauli/norm    FP64 warp->block->grid reductions for expectation_one
@@ -19,6 +11,8 @@
 
 #include "qsv_internal.hpp"
 
+#include "device_util.cuh"
+
 namespace qsv {
 
 void cuda_check(cudaError_t e, const char *what) {
@@ -26,349 +20,8 @@ void cuda_check(cudaError_t e, const char *what) {
 }
 
 namespace {
-
-template <typename T> struct Vec2;
-template <> struct Vec2<float> { using type = float2; };
-template <> struct Vec2<double> { using type = double2; };
-
-template <typename V> __device__ __forceinline__ V cmul(V a, V b) {
-    V r;
-    r.x = a.x * b.x - a.y * b.y;
-    r.y = a.x * b.y + a.y * b.x;
-    return r;
-}
-template <typename V> __device__ __forceinline__ V cfma(V a, V b, V acc) { // acc + a*b
-    acc.x += a.x * b.x - a.y * b.y;
-    acc.y += a.x * b.y + a.y * b.x;
-    return acc;
-}
-
-// XOR-swizzle of a tile-local amplitude index into its shared-memory slot so
-// that lanes walking any tile bit spread over the 8 sixteen-byte columns of a
-// 128-byte bank row. Bijective inside the tile (only the low bits change).
-template <typename V> __device__ __forceinline__ int swz(int u);
-template <> __device__ __forceinline__ int swz<double2>(int u) {
-    const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12);
-    return u ^ (f & 7);
-}
-template <> __device__ __forceinline__ int swz<float2>(int u) {
-    const int w = u >> 1; // 16-byte unit = 2 amplitudes, kept adjacent
-    const int f = (w >> 3) ^ (w >> 6) ^ (w >> 9) ^ (w >> 12);
-    return ((w ^ (f & 7)) << 1) | (u & 1);
-}
-
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
-__device__ __forceinline__ void st_cs16(void *gmem, float4 v) {
-    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\n" ::"l"(gmem), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-                 : "memory");
-}
-
-// ---- register-group gate application ---------------------------------------
-template <typename T, int R, int J>
-__device__ __forceinline__ void dense1(typename Vec2<T>::type (&v)[1 << R], const T *__restrict__ m, bool fok,
-                                       int rmask, int rval, bool zoc) {
-    using V = typename Vec2<T>::type;
-    const V m00 = {m[0], m[1]}, m01 = {m[2], m[3]}, m10 = {m[4], m[5]}, m11 = {m[6], m[7]};
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r) {
-        if (r & (1 << J)) continue;
-        const int r1 = r | (1 << J);
-        const bool on = fok && ((r & rmask) == rval);
-        if (on) {
-            const V x0 = v[r], x1 = v[r1];
-            v[r] = cfma(m01, x1, cmul(m00, x0));
-            v[r1] = cfma(m11, x1, cmul(m10, x0));
-        } else if (zoc) {
-            v[r] = V{0, 0};
-            v[r1] = V{0, 0};
-        }
-    }
-}
-
-template <typename T, int R, int A, int B>
-__device__ __forceinline__ void dense2(typename Vec2<T>::type (&v)[1 << R], const T *__restrict__ m, bool fok,
-                                       int rmask, int rval, bool zoc) {
-    using V = typename Vec2<T>::type;
-    // matrix entries are re-read (L1-resident, warp-uniform) instead of held
-    // in 32 registers: the 2^R amplitudes already occupy the register budget.
-    const V *mv = reinterpret_cast<const V *>(m);
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r) {
-        if (r & ((1 << A) | (1 << B))) continue;
-        const int idx[4] = {r, r | (1 << B), r | (1 << A), r | (1 << A) | (1 << B)};
-        const bool on = fok && ((r & rmask) == rval);
-        if (on) {
-            V x[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) x[q] = v[idx[q]];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                V acc = cmul(__ldg(mv + q * 4), x[0]);
-                acc = cfma(__ldg(mv + q * 4 + 1), x[1], acc);
-                acc = cfma(__ldg(mv + q * 4 + 2), x[2], acc);
-                acc = cfma(__ldg(mv + q * 4 + 3), x[3], acc);
-                v[idx[q]] = acc;
-            }
-        } else if (zoc) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) v[idx[q]] = V{0, 0};
-        }
-    }
-}
-
-template <typename T, int R>
-__device__ __forceinline__ void diag_op(typename Vec2<T>::type (&v)[1 << R], const TileOp<T> &o,
-                                        const T *__restrict__ m, uint64_t pb, bool fok, bool zoc) {
-    using V = typename Vec2<T>::type;
-    const V d0 = {m[0], m[1]}, d1 = {m[2], m[3]};
-    V d2 = d0, d3 = d1;
-    const int nt = o.nt;
-    if (nt == 2) {
-        d2 = V{m[4], m[5]};
-        d3 = V{m[6], m[7]};
-    }
-    const int t0 = o.t0, t1 = o.t1;
-    const bool t0r = o.t0reg, t1r = o.t1reg;
-    const int f0 = t0r ? 0 : int((pb >> t0) & 1ull);
-    const int f1 = (nt == 2 && !t1r) ? int((pb >> t1) & 1ull) : 0;
-    const int rmask = o.rmask, rval = o.rval;
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r) {
-        const int b0 = t0r ? ((r >> t0) & 1) : f0;
-        int sel = b0;
-        if (nt == 2) sel = (b0 << 1) | (t1r ? ((r >> t1) & 1) : f1);
-        const V d = sel == 0 ? d0 : sel == 1 ? d1 : sel == 2 ? d2 : d3;
-        if (fok && ((r & rmask) == rval)) v[r] = cmul(v[r], d);
-        else if (zoc) v[r] = V{0, 0};
-    }
-}
-
-template <typename T, int R, int J>
-__device__ __forceinline__ void dense1r(typename Vec2<T>::type (&v)[1 << R], const T *__restrict__ m, bool fok,
-                                        int rmask, int rval) {
-    using V = typename Vec2<T>::type;
-    const T a = m[0], b = m[2], c = m[4], d = m[6];
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r) {
-        if (r & (1 << J)) continue;
-        const int r1 = r | (1 << J);
-        if (fok && ((r & rmask) == rval)) {
-            const V x0 = v[r], x1 = v[r1];
-            v[r] = V{a * x0.x + b * x1.x, a * x0.y + b * x1.y};
-            v[r1] = V{c * x0.x + d * x1.x, c * x0.y + d * x1.y};
-        }
-    }
-}
-
-template <typename T, int R, int J>
-__device__ __forceinline__ void x1(typename Vec2<T>::type (&v)[1 << R], bool fok, int rmask, int rval) {
-    using V = typename Vec2<T>::type;
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r) {
-        if (r & (1 << J)) continue;
-        const int r1 = r | (1 << J);
-        const bool on = fok && ((r & rmask) == rval);
-        const V x0 = v[r], x1v = v[r1];
-        v[r] = on ? x1v : x0;
-        v[r1] = on ? x0 : x1v;
-    }
-}
-
-template <typename T, int R, int J>
-__device__ __forceinline__ void scale_slot(typename Vec2<T>::type (&v)[1 << R], typename Vec2<T>::type f) {
-#pragma unroll
-    for (int r = 0; r < (1 << R); ++r)
-        if (r & (1 << J)) v[r] = cmul(v[r], f);
-}
-
-// value of a phase record on the bits of `pb` (1 when its condition fails)
-template <typename V>
-__device__ __forceinline__ V eval_rec(const DiagRec &rc, uint64_t pb) {
-    using T = decltype(V{}.x);
-    if ((pb & rc.fmask) != rc.fval) return V{1, 0};
-    int idx = 0;
-    if (rc.nt >= 1) idx = static_cast<int>((pb >> rc.tpos0) & 1ull);
-    if (rc.nt == 2) idx = (idx << 1) | static_cast<int>((pb >> rc.tpos1) & 1ull);
-    return V{static_cast<T>(rc.val[2 * idx]), static_cast<T>(rc.val[2 * idx + 1])};
-}
-
-// Context a FLUSH needs besides the registers.
-template <typename V> struct FlushCtx {
-    const FlushTarget *targets;
-    const DiagRec *recs;
-    const V *tables;
-    const V *E;  // shared memory, per-CTA external factors
-    int s;       // set index
-};
-
-template <typename T, int R>
-__device__ __forceinline__ void flush_op(typename Vec2<T>::type (&v)[1 << R], const TileOp<T> &o,
-                                         const FlushCtx<typename Vec2<T>::type> &fc, uint64_t pb) {
-    using V = typename Vec2<T>::type;
-    for (int ti = o.a; ti < o.b; ++ti) {
-        const FlushTarget ft = fc.targets[ti];
-        V f = ft.eidx >= 0 ? fc.E[ft.eidx] : V{1, 0};
-        if (ft.table >= 0) f = cmul(f, fc.tables[ft.table + fc.s]);
-        for (int k = ft.mix_begin; k < ft.mix_end; ++k) f = cmul(f, eval_rec<V>(fc.recs[k], pb));
-        switch (ft.slot) {
-        case -1:
-#pragma unroll
-            for (int r = 0; r < (1 << R); ++r) v[r] = cmul(v[r], f);
-            break;
-        case 0: scale_slot<T, R, 0>(v, f); break;
-        case 1: if constexpr (R > 1) scale_slot<T, R, 1>(v, f); break;
-        case 2: if constexpr (R > 2) scale_slot<T, R, 2>(v, f); break;
-        case 3: if constexpr (R > 3) scale_slot<T, R, 3>(v, f); break;
-        }
-    }
-}
-
-template <typename T, int R>
-__device__ __forceinline__ void run_op(typename Vec2<T>::type (&v)[1 << R], const TileOp<T> &o,
-                                       const T *__restrict__ enc_table, int batch, int row, uint64_t pb,
-                                       const FlushCtx<typename Vec2<T>::type> &fc) {
-    const bool fok = (pb & o.fmask) == o.fval;
-    const T *m = o.enc >= 0 ? enc_table + (static_cast<size_t>(o.enc) * batch + row) * 32 : o.m;
-    const bool zoc = (o.flags & OPF_ZERO_OFF_CONTROL) != 0;
-    switch (o.type) {
-    case OP_DENSE1:
-        switch (o.a) {
-        case 0: dense1<T, R, 0>(v, m, fok, o.rmask, o.rval, zoc); break;
-        case 1: if constexpr (R > 1) dense1<T, R, 1>(v, m, fok, o.rmask, o.rval, zoc); break;
-        case 2: if constexpr (R > 2) dense1<T, R, 2>(v, m, fok, o.rmask, o.rval, zoc); break;
-        case 3: if constexpr (R > 3) dense1<T, R, 3>(v, m, fok, o.rmask, o.rval, zoc); break;
-        }
-        break;
-    case OP_DENSE2:
-        if constexpr (R > 1) {
-            const int ab = o.a * 8 + o.b;
-            switch (ab) {
-            case 1 * 8 + 0: dense2<T, R, 1, 0>(v, m, fok, o.rmask, o.rval, zoc); break;
-            case 2 * 8 + 0: if constexpr (R > 2) dense2<T, R, 2, 0>(v, m, fok, o.rmask, o.rval, zoc); break;
-            case 2 * 8 + 1: if constexpr (R > 2) dense2<T, R, 2, 1>(v, m, fok, o.rmask, o.rval, zoc); break;
-            case 3 * 8 + 0: if constexpr (R > 3) dense2<T, R, 3, 0>(v, m, fok, o.rmask, o.rval, zoc); break;
-            case 3 * 8 + 1: if constexpr (R > 3) dense2<T, R, 3, 1>(v, m, fok, o.rmask, o.rval, zoc); break;
-            case 3 * 8 + 2: if constexpr (R > 3) dense2<T, R, 3, 2>(v, m, fok, o.rmask, o.rval, zoc); break;
-            }
-        }
-        break;
-    case OP_DIAG: diag_op<T, R>(v, o, m, pb, fok, zoc); break;
-    case OP_DENSE1R:
-        switch (o.a) {
-        case 0: dense1r<T, R, 0>(v, m, fok, o.rmask, o.rval); break;
-        case 1: if constexpr (R > 1) dense1r<T, R, 1>(v, m, fok, o.rmask, o.rval); break;
-        case 2: if constexpr (R > 2) dense1r<T, R, 2>(v, m, fok, o.rmask, o.rval); break;
-        case 3: if constexpr (R > 3) dense1r<T, R, 3>(v, m, fok, o.rmask, o.rval); break;
-        }
-        break;
-    case OP_X1:
-        switch (o.a) {
-        case 0: x1<T, R, 0>(v, fok, o.rmask, o.rval); break;
-        case 1: if constexpr (R > 1) x1<T, R, 1>(v, fok, o.rmask, o.rval); break;
-        case 2: if constexpr (R > 2) x1<T, R, 2>(v, fok, o.rmask, o.rval); break;
-        case 3: if constexpr (R > 3) x1<T, R, 3>(v, fok, o.rmask, o.rval); break;
-        }
-        break;
-    case OP_FLUSH: flush_op<T, R>(v, o, fc, pb); break;
-    }
-}
-
-// One fused pass. grid = (tiles per row, rows); block handles one tile.
-template <typename T, int R>
-__global__ void __launch_bounds__(256, 2) tile_pass_kernel(const PassArgs a) {
-    using V = typename Vec2<T>::type;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    V *tile = reinterpret_cast<V *>(smem_raw);
-    uint64_t *hi_off = reinterpret_cast<uint64_t *>(smem_raw + (sizeof(V) << a.K));
-    const int row = a.row0 + blockIdx.y;
-    V *st = reinterpret_cast<V *>(a.state) + static_cast<size_t>(row) * a.row_stride;
-    const TileOp<T> *ops = reinterpret_cast<const TileOp<T> *>(a.ops);
-    const T *enc_table = reinterpret_cast<const T *>(a.enc_table);
-
-    // tile base: blockIdx.x scattered over the non-tile local bits
-    uint64_t tb = 0;
-    {
-        const uint64_t bid = blockIdx.x;
-        for (int i = 0; i < a.next; ++i) tb |= ((bid >> i) & 1ull) << a.ext_pos[i];
-    }
-    const int K = a.K, L = a.L, H = K - L;
-    for (int h = threadIdx.x; h < (1 << H); h += blockDim.x) {
-        uint64_t o = 0;
-        for (int i = 0; i < H; ++i) o |= static_cast<uint64_t>((h >> i) & 1) << a.tile_pos[L + i];
-        hi_off[h] = o;
-    }
-    __syncthreads();
-
-    constexpr int APU = 16 / sizeof(V); // amplitudes per 16-byte chunk
-    const int nchunks = (1 << K) / APU;
-    const int lmask = (1 << L) - 1;
-    for (int c = threadIdx.x; c < nchunks; c += blockDim.x) {
-        const int u = c * APU;
-        const uint64_t g = tb + hi_off[u >> L] + (u & lmask);
-        cp_async16(&tile[swz<V>(u)], &st[g]);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-
-    const uint64_t pbase = a.rank_base | tb;
-    const int nsets = 1 << (K - R);
-    __shared__ V E[kMaxExtTargets];
-    FlushCtx<V> fc{a.targets, a.recs, reinterpret_cast<const V *>(a.tables), E, 0};
-    for (int gi = 0; gi < a.ngroups; ++gi) {
-        const GroupDesc &gd = a.groups[gi];
-        if (gd.tgt_end > gd.tgt_begin) {
-            // per-CTA factors of records over bits outside the tile
-            for (int t = gd.tgt_begin + threadIdx.x; t < gd.tgt_end; t += blockDim.x) {
-                const FlushTarget ft = a.targets[t];
-                if (ft.eidx < 0) continue;
-                V f{1, 0};
-                for (int k = ft.ext_begin; k < ft.ext_end; ++k) f = cmul(f, eval_rec<V>(a.recs[k], pbase));
-                E[ft.eidx] = f;
-            }
-            __syncthreads();
-        }
-        int uoff[1 << R];
-        uoff[0] = 0;
-#pragma unroll
-        for (int j = 0; j < R; ++j) {
-            const int bit = 1 << gd.slot_bit[j];
-#pragma unroll
-            for (int r = 0; r < (1 << j); ++r) uoff[r | (1 << j)] = uoff[r] | bit;
-        }
-        const int ob = gd.op_begin, oe = gd.op_end;
-        for (int s = threadIdx.x; s < nsets; s += blockDim.x) {
-            int ub = 0;
-            uint64_t pb = pbase;
-            for (int i = 0; i < K - R; ++i) {
-                const int bit = (s >> i) & 1;
-                const int tbit = gd.ng_bit[i];
-                ub |= bit << tbit;
-                pb |= static_cast<uint64_t>(bit) << a.tile_pos[tbit];
-            }
-            V v[1 << R];
-#pragma unroll
-            for (int r = 0; r < (1 << R); ++r) v[r] = tile[swz<V>(ub | uoff[r])];
-            fc.s = s;
-            for (int oi = ob; oi < oe; ++oi) run_op<T, R>(v, ops[oi], enc_table, a.batch, row, pb, fc);
-#pragma unroll
-            for (int r = 0; r < (1 << R); ++r) tile[swz<V>(ub | uoff[r])] = v[r];
-        }
-        __syncthreads();
-    }
-
-    for (int c = threadIdx.x; c < nchunks; c += blockDim.x) {
-        const int u = c * APU;
-        const uint64_t g = tb + hi_off[u >> L] + (u & lmask);
-        const float4 val = *reinterpret_cast<const float4 *>(&tile[swz<V>(u)]);
-        st_cs16(&st[g], val);
-    }
-}
+using dev::Vec2;
+using dev::warp_sum;
 
 // ---- encoded gates: device-side gate_matrix (gate.hpp:89-154) -------------
 template <typename T>
@@ -465,12 +118,6 @@ __global__ void f32_to_f64_kernel(double *dst, const float *src, uint64_t n) {
         dst[i] = static_cast<double>(src[i]);
 }
 
-// ---- reductions -----------------------------------------------------------
-__device__ __forceinline__ double warp_sum(double x) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-    return x;
-}
 
 constexpr int kZ = 41; // total + one accumulator per physical local bit (<= 40)
 
@@ -595,27 +242,6 @@ __global__ void __launch_bounds__(256) marginal_kernel(const typename Vec2<T>::t
         out_partial[static_cast<size_t>(blockIdx.x) * nb + j] = hist[j];
 }
 
-template <typename T, int R> void set_attrs(size_t smem) {
-    static size_t done = 0;
-    if (smem > done) {
-        QSV_CUDA(cudaFuncSetAttribute(tile_pass_kernel<T, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        done = smem;
-    }
-}
-
-template <typename T, int R> void launch_tile(const DevPass &dp, void *state, int rows, cudaStream_t s) {
-    set_attrs<T, R>(dp.smem);
-    PassArgs a = dp.args;
-    a.state = state;
-    for (int r0 = 0; r0 < rows; r0 += 65535) {
-        a.row0 = r0;
-        const dim3 grid(static_cast<unsigned>(dp.tiles), static_cast<unsigned>(std::min(rows - r0, 65535)));
-        tile_pass_kernel<T, R><<<grid, dp.threads, dp.smem, s>>>(a);
-    }
-    QSV_CUDA(cudaGetLastError());
-}
-
 int grid_for(uint64_t work, int threads, int sm_count) {
     const uint64_t want = (work + threads - 1) / threads;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 8;
@@ -623,26 +249,6 @@ int grid_for(uint64_t work, int threads, int sm_count) {
 }
 
 } // namespace
-
-// ---------------------------------------------------------------- launchers --
-void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s) {
-    const int R = std::min(kRegSlots, dp.args.K);
-    if (dtype == QSV_C64) {
-        switch (R) {
-        case 1: launch_tile<float, 1>(dp, state, rows, s); break;
-        case 2: launch_tile<float, 2>(dp, state, rows, s); break;
-        case 3: launch_tile<float, 3>(dp, state, rows, s); break;
-        default: launch_tile<float, 4>(dp, state, rows, s); break;
-        }
-    } else {
-        switch (R) {
-        case 1: launch_tile<double, 1>(dp, state, rows, s); break;
-        case 2: launch_tile<double, 2>(dp, state, rows, s); break;
-        case 3: launch_tile<double, 3>(dp, state, rows, s); break;
-        default: launch_tile<double, 4>(dp, state, rows, s); break;
-        }
-    }
-}
 
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s) {
     const int nenc = static_cast<int>(p.encs.size());

@@ -29,11 +29,7 @@ State::~State() {
 }
 
 Plan::~Plan() {
-    if (graph) cudaGraphExecDestroy(graph);
-    cudaFree(d_groups);
-    cudaFree(d_ops);
-    cudaFree(d_targets);
-    cudaFree(d_recs);
+    cudaFree(d_blob);
     cudaFree(d_tables);
     cudaFree(d_encs);
     cudaFree(d_enc_table);
@@ -46,14 +42,6 @@ std::vector<int> canonical_perm(int n) {
     std::vector<int> p(n);
     for (int w = 0; w < n; ++w) p[w] = n - 1 - w; // wire 0 = MSB (state.hpp:21-24)
     return p;
-}
-
-template <typename T> TileOp<T> convert_op(const TileOp<double> &o) {
-    TileOp<T> r{};
-    r.type = o.type, r.a = o.a, r.b = o.b, r.rmask = o.rmask, r.rval = o.rval, r.enc = o.enc, r.flags = o.flags;
-    r.nt = o.nt, r.t0 = o.t0, r.t1 = o.t1, r.t0reg = o.t0reg, r.t1reg = o.t1reg, r.fmask = o.fmask, r.fval = o.fval;
-    for (int i = 0; i < 32; ++i) r.m[i] = static_cast<T>(o.m[i]);
-    return r;
 }
 
 // Distributed schedule: split the gate list into local segments separated by
@@ -245,78 +233,61 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
 }
 
 void upload_plan(Plan &p) {
-    std::vector<GroupDesc> groups;
-    std::vector<FlushTarget> targets;
-    std::vector<DiagRec> recs;
-    std::vector<cplx> tables;
-    std::vector<size_t> group_off, op_off, tgt_off, rec_off, tab_off;
-    size_t nops = 0;
-    for (auto &ph : p.passes) {
-        group_off.push_back(groups.size());
-        op_off.push_back(nops);
-        tgt_off.push_back(targets.size());
-        rec_off.push_back(recs.size());
-        tab_off.push_back(tables.size());
-        groups.insert(groups.end(), ph.groups.begin(), ph.groups.end());
-        targets.insert(targets.end(), ph.targets.begin(), ph.targets.end());
-        recs.insert(recs.end(), ph.recs.begin(), ph.recs.end());
-        tables.insert(tables.end(), ph.tables.begin(), ph.tables.end());
-        nops += ph.ops.size();
-    }
-    const size_t op_size = p.dtype == QSV_C64 ? sizeof(TileOp<float>) : sizeof(TileOp<double>);
-    std::vector<unsigned char> opbuf(std::max<size_t>(nops, 1) * op_size);
-    size_t k = 0;
-    for (auto &ph : p.passes)
-        for (auto &o : ph.ops) {
+    // one device blob holding every pass program (each 16-byte aligned), one
+    // table array
+    std::vector<unsigned char> blob;
+    std::vector<unsigned char> tables;
+    const size_t tsz = p.dtype == QSV_C64 ? 8 : 16;
+    struct Off {
+        size_t blob, bytes, table;
+        int ot, orc, oo;
+    };
+    std::vector<Off> offs;
+    for (const PassHost &ph : p.passes) {
+        Off o{};
+        std::vector<unsigned char> b = serialize_program(ph, p.dtype, &o.ot, &o.orc, &o.oo);
+        o.blob = blob.size();
+        o.bytes = (b.size() + 15) / 16 * 16;
+        b.resize(o.bytes, 0);
+        blob.insert(blob.end(), b.begin(), b.end());
+        o.table = tables.size() / tsz;
+        for (const cplx &c : ph.tables) {
+            unsigned char buf[16];
             if (p.dtype == QSV_C64) {
-                auto c = convert_op<float>(o);
-                std::memcpy(opbuf.data() + k * op_size, &c, op_size);
+                const float f[2] = {static_cast<float>(c.real()), static_cast<float>(c.imag())};
+                std::memcpy(buf, f, 8);
             } else {
-                std::memcpy(opbuf.data() + k * op_size, &o, op_size);
+                const double f[2] = {c.real(), c.imag()};
+                std::memcpy(buf, f, 16);
             }
-            ++k;
+            tables.insert(tables.end(), buf, buf + tsz);
         }
+        offs.push_back(o);
+    }
     QSV_CUDA(cudaSetDevice(p.ctx->device));
-    QSV_CUDA(cudaMalloc(&p.d_groups, std::max<size_t>(groups.size(), 1) * sizeof(GroupDesc)));
-    QSV_CUDA(cudaMalloc(&p.d_ops, opbuf.size()));
-    if (!groups.empty())
-        QSV_CUDA(cudaMemcpy(p.d_groups, groups.data(), groups.size() * sizeof(GroupDesc), cudaMemcpyHostToDevice));
-    QSV_CUDA(cudaMemcpy(p.d_ops, opbuf.data(), opbuf.size(), cudaMemcpyHostToDevice));
     auto up = [](void **dst, const void *src, size_t bytes) {
         QSV_CUDA(cudaMalloc(dst, std::max<size_t>(bytes, 16)));
         if (bytes) QSV_CUDA(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice));
     };
-    up(&p.d_targets, targets.data(), targets.size() * sizeof(FlushTarget));
-    up(&p.d_recs, recs.data(), recs.size() * sizeof(DiagRec));
-    const size_t tsz = p.dtype == QSV_C64 ? 8 : 16;
-    std::vector<unsigned char> tabbuf(tables.size() * tsz);
-    for (size_t i = 0; i < tables.size(); ++i) {
-        if (p.dtype == QSV_C64) {
-            const float f[2] = {static_cast<float>(tables[i].real()), static_cast<float>(tables[i].imag())};
-            std::memcpy(tabbuf.data() + i * tsz, f, tsz);
-        } else {
-            const double f[2] = {tables[i].real(), tables[i].imag()};
-            std::memcpy(tabbuf.data() + i * tsz, f, tsz);
-        }
-    }
-    up(&p.d_tables, tabbuf.data(), tabbuf.size());
-    if (!p.encs.empty()) {
-        QSV_CUDA(cudaMalloc(&p.d_encs, p.encs.size() * sizeof(EncDesc)));
-        QSV_CUDA(cudaMemcpy(p.d_encs, p.encs.data(), p.encs.size() * sizeof(EncDesc), cudaMemcpyHostToDevice));
-    }
+    up(&p.d_blob, blob.data(), blob.size());
+    up(&p.d_tables, tables.data(), tables.size());
+    if (!p.encs.empty()) up(&p.d_encs, p.encs.data(), p.encs.size() * sizeof(EncDesc));
     const size_t amp = p.dtype == QSV_C64 ? 8 : 16;
     p.dev.clear();
     for (size_t i = 0; i < p.passes.size(); ++i) {
         const PassHost &ph = p.passes[i];
+        const Off &o = offs[i];
         DevPass dp;
         PassArgs &a = dp.args;
         a.row_stride = 1ull << p.nlocal;
         a.rank_base = static_cast<uint64_t>(p.ctx->rank) << p.nlocal;
-        a.groups = static_cast<const GroupDesc *>(p.d_groups) + group_off[i];
-        a.ops = static_cast<const unsigned char *>(p.d_ops) + op_off[i] * op_size;
-        a.targets = static_cast<const FlushTarget *>(p.d_targets) + tgt_off[i];
-        a.recs = static_cast<const DiagRec *>(p.d_recs) + rec_off[i];
-        a.tables = static_cast<const unsigned char *>(p.d_tables) + tab_off[i] * tsz;
+        a.tiles_per_row = 1ull << (p.nlocal - ph.K);
+        a.blob = static_cast<const unsigned char *>(p.d_blob) + o.blob;
+        a.blob_bytes = static_cast<int>(o.bytes);
+        a.off_targets = o.ot;
+        a.off_recs = o.orc;
+        a.off_ops = o.oo;
+        a.tables = static_cast<const unsigned char *>(p.d_tables) + o.table * tsz;
         a.nlocal = p.nlocal;
         a.K = ph.K;
         a.L = ph.L;
@@ -324,13 +295,15 @@ void upload_plan(Plan &p) {
         a.next = static_cast<int>(ph.ext_pos.size());
         for (int j = 0; j < ph.K; ++j) a.tile_pos[j] = ph.tile_pos[j];
         for (int j = 0; j < a.next; ++j) a.ext_pos[j] = ph.ext_pos[j];
-        const int R = std::min(kRegSlots, ph.K);
-        const int nsets = 1 << (ph.K - R);
-        const int chunks = (1 << ph.K) * static_cast<int>(amp) / 16;
+        dp.R = ph.R;
+        const int nsets = 1 << (ph.K - ph.R);
+        const int chunks = static_cast<int>(((1ull << ph.K) * amp) / 16);
         dp.threads = std::max(32, std::min(256, std::max(nsets, std::min(chunks, 256))));
         dp.threads = (dp.threads + 31) / 32 * 32;
-        dp.smem = (amp << ph.K) + (sizeof(uint64_t) << (ph.K - ph.L));
-        dp.tiles = 1ull << (p.nlocal - ph.K);
+        dp.smem = (amp << ph.K) + (sizeof(uint64_t) << (ph.K - ph.L)) + o.bytes;
+        require(dp.smem + 1024 <= p.ctx->smem_optin || p.ctx->smem_optin == 0,
+                "plan: pass program does not fit in shared memory");
+        dp.grid = std::max(1, tile_kernel_blocks_per_sm(p.dtype, dp.R, dp.threads, dp.smem)) * p.ctx->sm_count;
         dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
         dp.ngates = ph.ngates;
         p.dev.push_back(dp);

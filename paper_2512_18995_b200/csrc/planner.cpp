@@ -33,7 +33,7 @@
 namespace qsv {
 
 int default_tile_bits(int dtype, int nlocal) {
-    const int k = dtype == QSV_C64 ? 13 : 12; // 64 KiB tiles: 3 CTAs per SM
+    const int k = dtype == QSV_C64 ? 13 : 12; // 64 KiB tiles: 2-3 CTAs per SM
     return std::min(k, nlocal);
 }
 int default_low_bits(int dtype, int nlocal) {
@@ -41,60 +41,10 @@ int default_low_bits(int dtype, int nlocal) {
     return std::min(l, nlocal);
 }
 
-namespace {
-
-struct PG {
-    int idx;            // gate index
-    uint64_t nmask = 0; // physical bits acted on non-diagonally
-    uint64_t dmask = 0; // physical bits acted on diagonally (controls, diag targets)
-};
-
-inline bool conflicts(const PG &g, uint64_t bN, uint64_t bD) {
-    return (g.nmask & (bN | bD)) || (g.dmask & bN);
-}
-
-// Greedy admission: returns admitted gate indices (positions into `order`),
-// the qubits they claimed, and leaves the rest in `order`.
-std::vector<int> admit(std::vector<int> &order, const std::vector<PG> &pg, uint64_t &active, int cap,
-                       uint64_t allowed) {
-    int cnt = std::popcount(active);
-    uint64_t bN = 0, bD = 0;
-    std::vector<int> took, rest;
-    for (int i : order) {
-        const PG &g = pg[i];
-        bool ok = !conflicts(g, bN, bD);
-        if (ok) {
-            const uint64_t need = g.nmask & ~active;
-            if ((need & ~allowed) || cnt + std::popcount(need) > cap) ok = false;
-            else {
-                active |= need;
-                cnt += std::popcount(need);
-            }
-        }
-        if (ok) took.push_back(i);
-        else {
-            bN |= g.nmask;
-            bD |= g.dmask;
-            rest.push_back(i);
-        }
-    }
-    order.swap(rest);
-    return took;
-}
-
-void set_m(TileOp<double> &op, const cplx *m, int d) {
-    for (int i = 0; i < d * d; ++i) {
-        op.m[2 * i] = m[i].real();
-        op.m[2 * i + 1] = m[i].imag();
-    }
-}
-
-} // namespace
-
 // ---- single-qubit run fusion ----------------------------------------------
 std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates) {
     std::vector<GateRec> out;
-    std::vector<int> open(kMaxQubits, -1); // wire -> index in `out` of an open run
+    std::vector<int> open(64, -1); // wire -> index in `out` of an open run
     for (const GateRec &g : gates) {
         const bool fusable = g.k == 1 && g.ctls.empty() && !g.encoded && g.flags == 0;
         if (fusable) {
@@ -123,6 +73,42 @@ std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates) {
 
 namespace {
 
+struct PG {
+    uint64_t nmask = 0; // physical bits acted on non-diagonally
+    uint64_t dmask = 0; // physical bits acted on diagonally (controls, diag targets)
+};
+
+inline bool conflicts(const PG &g, uint64_t bN, uint64_t bD) { return (g.nmask & (bN | bD)) || (g.dmask & bN); }
+
+// Greedy admission over `order` (ascending gate indices). Admitted gates are
+// returned; the rest stay in `order`.
+std::vector<int> admit(std::vector<int> &order, const std::vector<PG> &pg, uint64_t &active, int cap,
+                       uint64_t allowed) {
+    int cnt = std::popcount(active);
+    uint64_t bN = 0, bD = 0;
+    std::vector<int> took, rest;
+    for (int i : order) {
+        const PG &g = pg[i];
+        bool ok = !conflicts(g, bN, bD);
+        if (ok) {
+            const uint64_t need = g.nmask & ~active;
+            if ((need & ~allowed) || cnt + std::popcount(need) > cap) ok = false;
+            else {
+                active |= need;
+                cnt += std::popcount(need);
+            }
+        }
+        if (ok) took.push_back(i);
+        else {
+            bN |= g.nmask;
+            bD |= g.dmask;
+            rest.push_back(i);
+        }
+    }
+    order.swap(rest);
+    return took;
+}
+
 bool is_unitary_diag(const GateRec &g) {
     const int d = 1 << g.k;
     for (int i = 0; i < d; ++i)
@@ -145,17 +131,28 @@ uint64_t rec_deps(const DiagRec &r) {
     return d;
 }
 
-// Lowers the admitted gates of one register group into device ops. Unitary
-// diagonal gates that depend on at most one register slot are not applied
-// where they stand: their phase becomes a per-slot (or per-set "uniform")
-// factor that floats forward -- diagonal gates commute with each other and
-// with every gate not acting non-diagonally on their slot -- and is applied
-// by one FLUSH right before the next non-diagonal gate on that slot, or at
-// the end of the group. Each factor is split by the bits it reads:
-//   EXT    only bits outside the tile: one value per CTA (shared memory);
-//   TILE   only tile bits outside the group: a host-precomputed table over
-//          the set index, shared by every CTA;
-//   MIXED  both: evaluated per register set.
+void setv(DiagRec &r, int i, cplx v) {
+    r.val[2 * i] = v.real();
+    r.val[2 * i + 1] = v.imag();
+}
+
+// Lowers the admitted gates of one register group into HostOps.
+//
+// Unitary diagonal gates are not applied where they stand. Diagonal gates
+// commute with each other and with every gate that is not non-diagonal on
+// one of their qubits, so their phases are deferred and applied by a FLUSH
+// right before the next non-diagonal gate on a register slot they depend on,
+// or at the end of the group:
+//   * phases over register slots only (no other bit) multiply into one
+//     2^R-entry register table, computed here;
+//   * phases over exactly one register slot plus fixed bits become per-slot
+//     factors, phases over fixed bits only a per-set uniform factor. Each is
+//     split by the fixed bits it reads: EXT (only bits outside the tile: one
+//     value per tile, computed by the CTA), TILE (only tile bits outside the
+//     group: a host table over the set index, shared by every CTA), MIXED
+//     (both: evaluated per register set);
+//   * anything else (two register slots AND fixed bits, non-unitary, or
+//     encoded) is applied where it stands (OP_DIAG).
 struct GroupLowering {
     PassHost &ph;
     const std::vector<GateRec> &gates;
@@ -167,22 +164,24 @@ struct GroupLowering {
     std::vector<int> ng_phys;                 // physical bits of the set index, LSB first
     std::vector<std::vector<DiagRec>> pend;   // per slot
     std::vector<DiagRec> pend_u;
+    std::vector<cplx> pend_reg;               // register table
+    unsigned pend_reg_slots = 0;
     int n_ext = 0;
 
     GroupLowering(PassHost &p, const std::vector<GateRec> &g, const std::vector<int> &ph_, const int *sop, int r,
                   std::vector<EncDesc> &e, bool fe)
-        : ph(p), gates(g), phys(ph_), slot_of_phys(sop), R(r), encs(e), flush_enabled(fe), pend(r) {}
+        : ph(p), gates(g), phys(ph_), slot_of_phys(sop), R(r), encs(e), flush_enabled(fe), pend(r),
+          pend_reg(1u << r, cplx(1, 0)) {}
 
     int slot(int wire) const {
         const int b = phys[wire];
         return b < 64 ? slot_of_phys[b] : -1;
     }
 
-    void emit_target(int slot_id, const std::vector<DiagRec> &recs) {
-        if (recs.empty()) return;
+    int emit_target(int slot_id, const std::vector<DiagRec> &recs) {
+        if (recs.empty()) return 0;
         uint64_t ngmask = 0;
         for (int b : ng_phys) ngmask |= 1ull << b;
-        const uint64_t tilemask = ngmask;
         FlushTarget t{};
         t.slot = slot_id;
         t.table = -1;
@@ -190,8 +189,8 @@ struct GroupLowering {
         std::vector<DiagRec> ext, tile, mix;
         for (const DiagRec &r : recs) {
             const uint64_t d = rec_deps(r);
-            if ((d & ngmask) == 0) ext.push_back(r); // no tile dependence (tile group bits never appear)
-            else if ((d & ~tilemask) == 0) tile.push_back(r);
+            if ((d & ngmask) == 0) ext.push_back(r);      // bits outside the tile only
+            else if ((d & ~ngmask) == 0) tile.push_back(r); // tile bits outside the group only
             else mix.push_back(r);
         }
         if (!ext.empty() && n_ext >= kMaxExtTargets) {
@@ -218,53 +217,71 @@ struct GroupLowering {
             }
         }
         ph.targets.push_back(t);
+        return 1;
     }
 
-    void flush(const std::vector<int> &slots, bool with_u) {
-        const int t0 = static_cast<int>(ph.targets.size());
-        for (int j : slots) {
-            emit_target(j, pend[j]);
-            pend[j].clear();
-        }
+    void flush(unsigned slots, bool with_u, bool with_reg) {
+        HostOp op;
+        op.code = OP_FLUSH;
+        op.flush.tgt_begin = static_cast<int>(ph.targets.size());
+        for (int j = 0; j < R; ++j)
+            if ((slots >> j) & 1) {
+                emit_target(j, pend[j]);
+                pend[j].clear();
+            }
         if (with_u) {
             emit_target(-1, pend_u);
             pend_u.clear();
         }
-        const int t1 = static_cast<int>(ph.targets.size());
-        if (t1 > t0) {
-            TileOp<double> op{};
-            op.type = OP_FLUSH;
-            op.enc = -1;
-            op.a = t0;
-            op.b = t1;
-            ph.ops.push_back(op);
+        op.flush.tgt_end = static_cast<int>(ph.targets.size());
+        if (with_reg && pend_reg_slots) {
+            for (int r = 0; r < (1 << R); ++r)
+                if (pend_reg[r] != cplx(1, 0)) op.flush.regmask |= 1u << r;
+            if (op.flush.regmask) op.regtab = pend_reg;
+            std::fill(pend_reg.begin(), pend_reg.end(), cplx(1, 0));
+            pend_reg_slots = 0;
         }
+        if (op.flush.tgt_end > op.flush.tgt_begin || op.flush.regmask) ph.ops.push_back(std::move(op));
     }
 
-    // Returns true when the diagonal gate was absorbed into pending factors.
+    // Returns true when the diagonal gate was absorbed into pending phases.
     bool try_defer(const GateRec &g) {
         if (!flush_enabled || !g.diag || g.encoded || g.flags || !is_unitary_diag(g)) return false;
         DiagRec base{};
-        int rc = -1, nrc = 0;
+        unsigned rc_slots = 0;
         for (int c : g.ctls) {
             const int s = slot(c);
-            if (s >= 0) rc = s, ++nrc;
+            if (s >= 0) rc_slots |= 1u << s;
             else {
                 base.fmask |= 1ull << phys[c];
                 base.fval |= 1ull << phys[c];
             }
         }
-        int rt = -1, rtpos = -1, nrt = 0;
-        for (int t = 0; t < g.k; ++t)
-            if (slot(g.wires[t]) >= 0) rt = slot(g.wires[t]), rtpos = t, ++nrt;
+        int tslot[2] = {-1, -1};
+        unsigned rt_slots = 0;
+        int nfixed_t = 0;
+        for (int t = 0; t < g.k; ++t) {
+            tslot[t] = slot(g.wires[t]);
+            if (tslot[t] >= 0) rt_slots |= 1u << tslot[t];
+            else ++nfixed_t;
+        }
         const int d = 1 << g.k;
         cplx dv[4];
         for (int i = 0; i < d; ++i) dv[i] = g.m[i * d + i];
-        auto setv = [](DiagRec &r, int i, cplx v) {
-            r.val[2 * i] = v.real();
-            r.val[2 * i + 1] = v.imag();
-        };
-        if (nrc + nrt == 0) {
+        const unsigned reg = rc_slots | rt_slots;
+        const int nreg = std::popcount(reg);
+        // register-only phase -> register table
+        if (nreg >= 1 && base.fmask == 0 && nfixed_t == 0) {
+            for (int r = 0; r < (1 << R); ++r) {
+                if ((r & rc_slots) != rc_slots) continue;
+                int idx = 0;
+                for (int t = 0; t < g.k; ++t) idx = (idx << 1) | ((r >> tslot[t]) & 1);
+                pend_reg[r] *= dv[idx];
+            }
+            pend_reg_slots |= reg;
+            return true;
+        }
+        if (nreg == 0) {
             DiagRec r = base;
             r.nt = g.k;
             r.tpos0 = phys[g.wires[0]];
@@ -273,16 +290,19 @@ struct GroupLowering {
             pend_u.push_back(r);
             return true;
         }
-        if (nrc == 1 && nrt == 0) {
+        if (nreg == 1 && rt_slots == 0) { // one register control, targets fixed
+            const int j = std::countr_zero(rc_slots);
             DiagRec r = base;
             r.nt = g.k;
             r.tpos0 = phys[g.wires[0]];
             if (g.k == 2) r.tpos1 = phys[g.wires[1]];
             for (int i = 0; i < d; ++i) setv(r, i, dv[i]);
-            pend[rc].push_back(r);
+            pend[j].push_back(r);
             return true;
         }
-        if (nrc == 0 && nrt == 1) {
+        if (nreg == 1 && rc_slots == 0) { // one register target
+            const int j = std::countr_zero(rt_slots);
+            const int rtpos = tslot[0] == j ? 0 : 1;
             DiagRec u = base, f = base;
             if (g.k == 1) {
                 u.nt = f.nt = 0;
@@ -300,7 +320,7 @@ struct GroupLowering {
                 }
             }
             pend_u.push_back(u);
-            pend[rt].push_back(f);
+            pend[j].push_back(f);
             return true;
         }
         return false;
@@ -309,28 +329,26 @@ struct GroupLowering {
     void add(int gi) {
         const GateRec &g = gates[gi];
         if (try_defer(g)) return;
-        if (!g.diag) { // flush the pending factors of the slots it acts on non-diagonally
-            std::vector<int> need;
+        if (!g.diag) { // flush pending phases on the slots it acts on non-diagonally
+            unsigned need = 0;
             for (int t = 0; t < g.k; ++t) {
                 const int s = slot(g.wires[t]);
-                if (s >= 0 && !pend[s].empty()) need.push_back(s);
+                if (s >= 0) need |= 1u << s;
             }
-            if (!need.empty()) flush(need, false);
+            unsigned slots = 0;
+            for (int j = 0; j < R; ++j)
+                if (((need >> j) & 1) && !pend[j].empty()) slots |= 1u << j;
+            const bool reg = (pend_reg_slots & need) != 0;
+            if (slots || reg) flush(slots, false, reg);
         }
         lower(g);
     }
 
-    void finish() {
-        std::vector<int> all;
-        for (int j = 0; j < R; ++j)
-            if (!pend[j].empty()) all.push_back(j);
-        flush(all, true);
-    }
+    void finish() { flush((1u << R) - 1, true, true); }
 
     void lower(const GateRec &g) {
-        TileOp<double> op{};
-        op.enc = -1;
-        op.flags = g.flags & OPF_ZERO_OFF_CONTROL;
+        HostOp op;
+        if (g.flags & OPF_ZERO_OFF_CONTROL) op.flags |= OPF_ZERO_OFF_CONTROL;
         for (int c : g.ctls) {
             const int s = slot(c);
             if (s >= 0) {
@@ -341,78 +359,204 @@ struct GroupLowering {
                 op.fval |= 1ull << phys[c];
             }
         }
-        const int d = 1 << g.k;
-        if (g.diag) {
-            op.type = OP_DIAG;
-            op.nt = g.k;
-            int *tt[2] = {&op.t0, &op.t1};
-            int *tr[2] = {&op.t0reg, &op.t1reg};
-            for (int t = 0; t < g.k; ++t) {
-                const int s = slot(g.wires[t]);
-                *tt[t] = s >= 0 ? s : phys[g.wires[t]];
-                *tr[t] = s >= 0 ? 1 : 0;
-            }
-            if (!g.encoded)
-                for (int i = 0; i < d; ++i) {
-                    op.m[2 * i] = g.m[i * d + i].real();
-                    op.m[2 * i + 1] = g.m[i * d + i].imag();
-                }
-        } else if (g.k == 1) {
-            op.a = slot(g.wires[0]);
-            op.type = OP_DENSE1;
-            if (!g.encoded) {
-                set_m(op, g.m, 2);
-                const bool real = g.m[0].imag() == 0 && g.m[1].imag() == 0 && g.m[2].imag() == 0 &&
-                                  g.m[3].imag() == 0;
-                if (real) op.type = OP_DENSE1R;
-                if (g.m[0] == cplx(0, 0) && g.m[3] == cplx(0, 0) && g.m[1] == cplx(1, 0) && g.m[2] == cplx(1, 0) &&
-                    !(g.flags & OPF_ZERO_OFF_CONTROL))
-                    op.type = OP_X1;
-            }
-        } else {
-            op.type = OP_DENSE2;
-            const int s0 = slot(g.wires[0]), s1 = slot(g.wires[1]);
-            const bool swapq = s0 < s1;
-            op.a = swapq ? s1 : s0;
-            op.b = swapq ? s0 : s1;
-            if (!g.encoded) {
-                cplx mm[16];
-                for (int r = 0; r < 4; ++r)
-                    for (int c = 0; c < 4; ++c) {
-                        const int rr = swapq ? ((r & 1) << 1) | (r >> 1) : r;
-                        const int cc = swapq ? ((c & 1) << 1) | (c >> 1) : c;
-                        mm[r * 4 + c] = g.m[rr * 4 + cc];
-                    }
-                set_m(op, mm, 4);
-            }
-            if (g.encoded) {
-                EncDesc e{};
-                e.kind = g.kind;
-                e.slot = g.enc_slot;
-                e.nparams = g.nparams;
-                e.swapq = swapq ? 1 : 0;
-                e.diag = 0;
-                op.enc = static_cast<int>(encs.size());
-                encs.push_back(e);
-            }
-            ph.ops.push_back(op);
-            return;
-        }
+        if (op.rmask) op.flags |= OPF_RCOND;
+        if (op.fmask) op.flags |= OPF_FCOND;
         if (g.encoded) {
+            op.flags |= OPF_ENC;
             EncDesc e{};
             e.kind = g.kind;
             e.slot = g.enc_slot;
             e.nparams = g.nparams;
-            e.swapq = 0;
             e.diag = g.diag ? 1 : 0;
             op.enc = static_cast<int>(encs.size());
             encs.push_back(e);
         }
-        ph.ops.push_back(op);
+        const int d = 1 << g.k;
+        if (g.diag) {
+            op.code = OP_DIAG;
+            op.nt = static_cast<uint8_t>(g.k);
+            uint8_t *tt[2] = {&op.t0, &op.t1};
+            for (int t = 0; t < g.k; ++t) {
+                const int s = slot(g.wires[t]);
+                *tt[t] = static_cast<uint8_t>(s >= 0 ? s : phys[g.wires[t]]);
+                if (s >= 0) op.treg |= 1 << t;
+            }
+            if (!g.encoded)
+                for (int i = 0; i < d; ++i) op.pay.push_back(g.m[i * d + i]);
+        } else if (g.k == 1) {
+            op.a = static_cast<uint8_t>(slot(g.wires[0]));
+            op.code = OP_DENSE1;
+            if (!g.encoded) {
+                op.pay.assign(g.m, g.m + 4);
+                const bool real = g.m[0].imag() == 0 && g.m[1].imag() == 0 && g.m[2].imag() == 0 &&
+                                  g.m[3].imag() == 0;
+                if (real) op.code = OP_DENSE1R;
+                if (g.m[0] == cplx(0, 0) && g.m[3] == cplx(0, 0) && g.m[1] == cplx(1, 0) && g.m[2] == cplx(1, 0) &&
+                    !(op.flags & OPF_ZERO_OFF_CONTROL)) {
+                    op.code = OP_X1;
+                    op.pay.clear();
+                }
+            }
+        } else {
+            op.code = OP_DENSE2;
+            const int s0 = slot(g.wires[0]), s1 = slot(g.wires[1]);
+            const bool swapq = s0 < s1;
+            op.a = static_cast<uint8_t>(swapq ? s1 : s0);
+            op.b = static_cast<uint8_t>(swapq ? s0 : s1);
+            if (g.encoded) encs.back().swapq = swapq ? 1 : 0;
+            else {
+                op.pay.resize(16);
+                for (int r = 0; r < 4; ++r)
+                    for (int c = 0; c < 4; ++c) {
+                        const int rr = swapq ? ((r & 1) << 1) | (r >> 1) : r;
+                        const int cc = swapq ? ((c & 1) << 1) | (c >> 1) : c;
+                        op.pay[r * 4 + c] = g.m[rr * 4 + cc];
+                    }
+            }
+        }
+        ph.ops.push_back(std::move(op));
     }
 };
 
+PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg, const std::vector<int> &took,
+                    uint64_t active, const std::vector<int> &phys, const PlanConfig &cfg, int K, int L, int R,
+                    std::vector<EncDesc> &encs) {
+    const int nl = cfg.nlocal;
+    PassHost ph;
+    ph.K = K;
+    ph.L = L;
+    ph.R = R;
+    for (int b = 0; b < nl && std::popcount(active) < K; ++b) active |= 1ull << b; // lengthen contiguous runs
+    for (int b = 0; b < nl; ++b)
+        if (active & (1ull << b)) ph.tile_pos.push_back(b);
+        else ph.ext_pos.push_back(b);
+    require(static_cast<int>(ph.tile_pos.size()) == K, "planner: tile size");
+    int tile_of_phys[64];
+    for (int &x : tile_of_phys) x = -1;
+    for (int i = 0; i < K; ++i) tile_of_phys[ph.tile_pos[i]] = i;
+    std::vector<int> gorder = took;
+    ph.ngates = static_cast<int>(gorder.size());
+    while (!gorder.empty()) {
+        uint64_t gact = 0;
+        std::vector<int> gtook = admit(gorder, pg, gact, R, active);
+        require(!gtook.empty(), "planner: no group progress");
+        // slots: claimed tile bits, padded with the HIGHEST free tile bits so
+        // the lanes of a warp walk the low (contiguous) tile bits.
+        std::vector<int> slot_tile;
+        for (int b = 0; b < nl; ++b)
+            if (gact & (1ull << b)) slot_tile.push_back(tile_of_phys[b]);
+        for (int t = K - 1; t >= 0 && static_cast<int>(slot_tile.size()) < R; --t)
+            if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) slot_tile.push_back(t);
+        HostGroup hg;
+        int slot_of_phys[64];
+        for (int &x : slot_of_phys) x = -1;
+        for (int j = 0; j < R; ++j) {
+            hg.slot_bit[j] = slot_tile[j];
+            slot_of_phys[ph.tile_pos[slot_tile[j]]] = j;
+        }
+        int q = 0;
+        for (int t = 0; t < K; ++t)
+            if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) hg.ng_bit[q++] = t;
+        GroupLowering low(ph, gates, phys, slot_of_phys, R, encs, cfg.phase_flush);
+        for (int i = 0; i < K - R; ++i) low.ng_phys.push_back(ph.tile_pos[hg.ng_bit[i]]);
+        hg.op_begin = static_cast<int>(ph.ops.size());
+        hg.tgt_begin = static_cast<int>(ph.targets.size());
+        for (int gi : gtook) low.add(gi);
+        low.finish();
+        hg.op_end = static_cast<int>(ph.ops.size());
+        hg.tgt_end = static_cast<int>(ph.targets.size());
+        ph.groups.push_back(hg);
+    }
+    return ph;
+}
+
+size_t pass_program_bytes(const PassHost &ph, int dtype) {
+    size_t b = ph.groups.size() * sizeof(GroupDesc) + ph.targets.size() * sizeof(FlushTarget) +
+               ph.recs.size() * sizeof(DiagRec);
+    for (const HostOp &op : ph.ops) b += op_record_bytes(op, dtype, ph.R);
+    return b;
+}
+
 } // namespace
+
+size_t op_record_bytes(const HostOp &op, int dtype, int R) {
+    const size_t t = dtype == QSV_C64 ? 4 : 8;
+    size_t b = sizeof(OpHdr) + ((op.flags & OPF_FCOND) ? 16 : 0);
+    const bool enc = (op.flags & OPF_ENC) != 0;
+    switch (op.code) {
+    case OP_DENSE1: b += enc ? 0 : 8 * t; break;
+    case OP_DENSE1R: b += (4 * t + 15) / 16 * 16; break;
+    case OP_DENSE2: b += enc ? 0 : 32 * t; break;
+    case OP_DIAG: b += enc ? 0 : 8 * t; break;
+    case OP_X1: break;
+    case OP_FLUSH: b += sizeof(FlushPay) + (op.flush.regmask ? (2 * t << R) : 0); break;
+    }
+    return (b + 15) / 16 * 16;
+}
+
+std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int *off_targets, int *off_recs,
+                                             int *off_ops) {
+    const bool f32 = dtype == QSV_C64;
+    std::vector<size_t> op_off(ph.ops.size() + 1, 0);
+    for (size_t i = 0; i < ph.ops.size(); ++i) op_off[i + 1] = op_off[i] + op_record_bytes(ph.ops[i], dtype, ph.R);
+    const size_t g_bytes = ph.groups.size() * sizeof(GroupDesc);
+    const size_t t_bytes = ph.targets.size() * sizeof(FlushTarget);
+    const size_t r_bytes = ph.recs.size() * sizeof(DiagRec);
+    std::vector<unsigned char> blob(g_bytes + t_bytes + r_bytes + op_off.back(), 0);
+    *off_targets = static_cast<int>(g_bytes);
+    *off_recs = static_cast<int>(g_bytes + t_bytes);
+    *off_ops = static_cast<int>(g_bytes + t_bytes + r_bytes);
+    for (size_t i = 0; i < ph.groups.size(); ++i) {
+        const HostGroup &hg = ph.groups[i];
+        GroupDesc gd{};
+        gd.op_begin = static_cast<int>(op_off[hg.op_begin]);
+        gd.op_end = static_cast<int>(op_off[hg.op_end]);
+        for (int j = 0; j < kMaxSlots; ++j) gd.slot_bit[j] = hg.slot_bit[j];
+        for (int j = 0; j < kMaxTileBits; ++j) gd.ng_bit[j] = hg.ng_bit[j];
+        gd.tgt_begin = hg.tgt_begin;
+        gd.tgt_end = hg.tgt_end;
+        std::memcpy(blob.data() + i * sizeof(GroupDesc), &gd, sizeof(gd));
+    }
+    if (t_bytes) std::memcpy(blob.data() + g_bytes, ph.targets.data(), t_bytes);
+    if (r_bytes) std::memcpy(blob.data() + g_bytes + t_bytes, ph.recs.data(), r_bytes);
+    auto put = [&](unsigned char *&p, double v) {
+        if (f32) {
+            const float f = static_cast<float>(v);
+            std::memcpy(p, &f, 4);
+            p += 4;
+        } else {
+            std::memcpy(p, &v, 8);
+            p += 8;
+        }
+    };
+    for (size_t i = 0; i < ph.ops.size(); ++i) {
+        const HostOp &op = ph.ops[i];
+        unsigned char *p = blob.data() + *off_ops + op_off[i];
+        OpHdr h{};
+        h.code = op.code, h.a = op.a, h.b = op.b, h.flags = op.flags, h.rmask = op.rmask, h.rval = op.rval;
+        h.nt = op.nt, h.t0 = op.t0, h.t1 = op.t1, h.treg = op.treg;
+        h.enc = static_cast<uint16_t>(op.enc < 0 ? 0 : op.enc);
+        h.size = static_cast<uint16_t>(op_off[i + 1] - op_off[i]);
+        std::memcpy(p, &h, sizeof h);
+        p += sizeof h;
+        if (op.flags & OPF_FCOND) {
+            std::memcpy(p, &op.fmask, 8);
+            std::memcpy(p + 8, &op.fval, 8);
+            p += 16;
+        }
+        if (op.code == OP_FLUSH) {
+            std::memcpy(p, &op.flush, sizeof(FlushPay));
+            p += sizeof(FlushPay);
+            if (op.flush.regmask)
+                for (const cplx &c : op.regtab) put(p, c.real()), put(p, c.imag());
+        } else if (op.code == OP_DENSE1R) {
+            for (const cplx &c : op.pay) put(p, c.real());
+        } else {
+            for (const cplx &c : op.pay) put(p, c.real()), put(p, c.imag());
+        }
+    }
+    return blob;
+}
 
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const std::vector<int> &phys,
                                   const PlanConfig &cfg, std::vector<EncDesc> &encs) {
@@ -428,7 +572,6 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
     std::vector<PG> pg(gates.size());
     for (size_t i = 0; i < gates.size(); ++i) {
         const GateRec &g = gates[i];
-        pg[i].idx = static_cast<int>(i);
         for (int t = 0; t < g.k; ++t) {
             const uint64_t b = 1ull << phys[g.wires[t]];
             if (g.diag) pg[i].dmask |= b;
@@ -440,9 +583,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
         for (int c : g.ctls) pg[i].dmask |= 1ull << phys[c];
     }
 
-    // ---- passes -----------------------------------------------------------
-    std::vector<std::vector<int>> pass_gates;
-    std::vector<uint64_t> pass_active;
+    std::vector<PassHost> passes;
     std::vector<int> order(gates.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
     const uint64_t lowmask = (1ull << L) - 1;
@@ -457,61 +598,21 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             took.push_back(i);
         }
         require(!took.empty(), "planner: no progress");
-        pass_gates.push_back(std::move(took));
-        pass_active.push_back(active);
-    }
-
-    std::vector<PassHost> passes;
-    for (size_t p = 0; p < pass_gates.size(); ++p) {
-        PassHost ph;
-        ph.K = K;
-        ph.L = L;
-        uint64_t active = pass_active[p];
-        // pad with the lowest free bits: lengthens the contiguous runs
-        for (int b = 0; b < nl && std::popcount(active) < K; ++b) active |= 1ull << b;
-        for (int b = 0; b < nl; ++b)
-            if (active & (1ull << b)) ph.tile_pos.push_back(b);
-            else ph.ext_pos.push_back(b);
-        require(static_cast<int>(ph.tile_pos.size()) == K, "planner: tile size");
-        int tile_of_phys[64];
-        for (int &x : tile_of_phys) x = -1;
-        for (int i = 0; i < K; ++i) tile_of_phys[ph.tile_pos[i]] = i;
-
-        // ---- groups (capacity R over tile qubits) ---------------------------
-        std::vector<int> gorder = pass_gates[p];
-        ph.ngates = static_cast<int>(gorder.size()); // (after 1q fusion)
-        while (!gorder.empty()) {
-            uint64_t gact = 0;
-            std::vector<int> took = admit(gorder, pg, gact, R, active);
-            require(!took.empty(), "planner: no group progress");
-            // slots: claimed tile bits, padded with the HIGHEST free tile bits so
-            // the lanes of a warp walk the low (contiguous) tile bits.
-            std::vector<int> slot_tile;
-            for (int b = 0; b < nl; ++b)
-                if (gact & (1ull << b)) slot_tile.push_back(tile_of_phys[b]);
-            for (int t = K - 1; t >= 0 && static_cast<int>(slot_tile.size()) < R; --t)
-                if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) slot_tile.push_back(t);
-            GroupDesc gd{};
-            gd.op_begin = static_cast<int>(ph.ops.size());
-            int slot_of_phys[64];
-            for (int &x : slot_of_phys) x = -1;
-            for (int j = 0; j < R; ++j) {
-                gd.slot_bit[j] = slot_tile[j];
-                slot_of_phys[ph.tile_pos[slot_tile[j]]] = j;
-            }
-            int q = 0;
-            for (int t = 0; t < K; ++t)
-                if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) gd.ng_bit[q++] = t;
-
-            GroupLowering low(ph, gates, phys, slot_of_phys, R, encs, cfg.phase_flush);
-            low.ng_phys.clear();
-            for (int i = 0; i < K - R; ++i) low.ng_phys.push_back(ph.tile_pos[gd.ng_bit[i]]);
-            gd.tgt_begin = static_cast<int>(ph.targets.size());
-            for (int gi : took) low.add(gi);
-            low.finish();
-            gd.tgt_end = static_cast<int>(ph.targets.size());
-            gd.op_end = static_cast<int>(ph.ops.size());
-            ph.groups.push_back(gd);
+        size_t first_encs = encs.size();
+        PassHost ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
+        // keep the program within the shared-memory budget: give the tail of
+        // the admitted gates back (they commute with everything skipped before
+        // them, so they stay valid for a later pass)
+        while (pass_program_bytes(ph, cfg.dtype) > static_cast<size_t>(kProgramBudget) && took.size() > 1) {
+            const size_t keep = std::max<size_t>(1, took.size() * 2 / 3);
+            std::vector<int> back(took.begin() + keep, took.end());
+            took.resize(keep);
+            order.insert(order.end(), back.begin(), back.end());
+            std::sort(order.begin(), order.end());
+            active = lowmask;
+            for (int i : took) active |= pg[i].nmask;
+            encs.resize(first_encs);
+            ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         }
         passes.push_back(std::move(ph));
     }

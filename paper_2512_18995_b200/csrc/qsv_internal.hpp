@@ -30,37 +30,47 @@ void cuda_check(cudaError_t e, const char *what);
 #define QSV_CUDA(x) ::qsv::cuda_check((x), #x)
 
 // ---- limits -----------------------------------------------------------------
-constexpr int kMaxQubits = 40;     // global qubits (36q configs + headroom)
-constexpr int kMaxTileBits = 14;   // K: 2^K amplitudes per CTA tile
-constexpr int kMaxSlots = 5;       // R: register-resident qubits per group
-constexpr int kRegSlots = 4;       // R used by the fused kernel
+constexpr int kMaxQubits = 40;      // global qubits (36q configs + headroom)
+constexpr int kMaxTileBits = 14;    // K: 2^K amplitudes per CTA tile
+constexpr int kMaxSlots = 4;        // R: register-resident qubits per group
+constexpr int kRegSlots = 4;        // R used by the fused kernel
+constexpr int kMaxExtTargets = 64;  // per-CTA external phase factors per group
+constexpr int kProgramBudget = 40 * 1024;  // bytes of pass program staged in shared memory
 
 // ---- device program (tile passes) ---------------------------------------
-enum OpType : int32_t {
+// A pass program is one blob staged into shared memory by every CTA:
+//   [GroupDesc x ngroups][FlushTarget x ntargets][DiagRec x nrecs][op stream]
+// The op stream is a sequence of 16-byte-aligned variable-length records:
+//   OpHdr (16 B) [, uint64 fmask, fval (16 B) if OPF_FCOND] [, payload]
+// payload (T = float or double):
+//   DENSE1  4 complex T        DENSE1R  4 real T (padded to 16 B)
+//   DENSE2  16 complex T       DIAG     4 complex T        X1  none
+//   FLUSH   FlushPay (16 B) [, 2^R complex T register table if regmask]
+enum OpCode : uint8_t {
     OP_DENSE1 = 1,   // complex 2x2 on one register slot
-    OP_DENSE2 = 2,   // complex 4x4 on two register slots
-    OP_DIAG = 3,     // diagonal applied eagerly per register (>= 2 register deps / non-unitary)
-    OP_DENSE1R = 4,  // real 2x2 (h, ry, ...): half the FLOPs
-    OP_X1 = 5,       // Pauli-X on one slot: a predicated register swap, no FLOPs
-    OP_FLUSH = 6     // apply pending phase factors: targets [a, b)
+    OP_DENSE2 = 2,   // complex 4x4 on two register slots (a = MSB slot > b)
+    OP_DIAG = 3,     // diagonal applied where it stands (>= 2 register deps + fixed bits, or non-unitary)
+    OP_DENSE1R = 4,  // real 2x2 (h, ry, ...)
+    OP_X1 = 5,       // Pauli-X on one slot: register swap, no FLOPs
+    OP_FLUSH = 6     // apply pending phase factors
 };
-enum OpFlags : int32_t { OPF_ZERO_OFF_CONTROL = 1 };
+enum OpFlag : uint8_t { OPF_ZERO_OFF_CONTROL = 1, OPF_FCOND = 2, OPF_ENC = 4, OPF_RCOND = 8 };
 
-// One gate, lowered onto a register group. Conditions are split into the
-// part over register slots (rmask/rval, R bits) and the part over every other
-// bit of the GLOBAL physical index (fmask/fval; tile bits outside the group,
-// bits outside the tile, and rank bits on a distributed state).
-template <typename T> struct alignas(16) TileOp {
-    int32_t type;
-    int32_t a, b;           // DENSE1: a = slot; DENSE2: a = MSB slot > b = LSB slot; FLUSH: target range
-    int32_t rmask, rval;
-    int32_t enc;            // >= 0: matrix comes from the per-row table
-    int32_t flags;
-    int32_t nt;             // DIAG: number of target bits (1 or 2)
-    int32_t t0, t1;         // DIAG: slot (if reg) or physical position
-    int32_t t0reg, t1reg;   // DIAG: 1 if the target is a register slot
-    uint64_t fmask, fval;
-    T m[32];                // DENSE1: 2x2, DENSE2: 4x4 (row-major, re/im); DIAG: d[0..3]
+struct alignas(16) OpHdr {
+    uint8_t code, a, b, flags;
+    uint8_t rmask, rval;    // condition over register slots
+    uint8_t nt, t0, t1;     // DIAG: target count, slot or physical position
+    uint8_t treg;           // DIAG: bit0 t0 is a slot, bit1 t1 is a slot
+    uint16_t enc;           // encoded gate index (OPF_ENC)
+    uint16_t size;          // record size in bytes
+    uint16_t aux;
+};
+static_assert(sizeof(OpHdr) == 16, "OpHdr layout");
+
+struct alignas(16) FlushPay {
+    int32_t tgt_begin, tgt_end;
+    uint32_t regmask;       // registers multiplied by the register table
+    int32_t pad;
 };
 
 // A phase factor that depends only on bits OUTSIDE the register group
@@ -75,10 +85,10 @@ struct alignas(16) DiagRec {
 };
 
 // One factor applied at a FLUSH: to every register (slot < 0) or to the
-// registers whose slot bit is 1. factor = E[eidx] (per CTA: records over bits
-// outside the tile) * table[s] (host-precomputed over the set index s:
+// registers whose slot bit is 1. factor = E[eidx] (per tile: records over
+// bits outside the tile) * table[s] (host-precomputed over the set index s:
 // records over tile bits outside the group) * prod(mixed records, per set).
-struct FlushTarget {
+struct alignas(16) FlushTarget {
     int32_t slot;
     int32_t table;          // offset (complex entries) into the pass's table, or -1
     int32_t ext_begin, ext_end;
@@ -87,13 +97,11 @@ struct FlushTarget {
     int32_t pad;
 };
 
-constexpr int kMaxExtTargets = 64;
-
-struct GroupDesc {
-    int32_t op_begin, op_end;
+struct alignas(16) GroupDesc {
+    int32_t op_begin, op_end;          // byte offsets into the op stream
     int32_t slot_bit[kMaxSlots];       // tile-local bit of each register slot
     int32_t ng_bit[kMaxTileBits];      // tile-local bits NOT in the group, ascending
-    int32_t tgt_begin, tgt_end;        // flush targets with per-CTA (E) factors to precompute
+    int32_t tgt_begin, tgt_end;        // flush targets of this group (E precompute)
 };
 
 // Per-row matrix binding of an encoded gate (device-side gate_matrix).
@@ -113,31 +121,17 @@ struct PassArgs {
     void *state;
     uint64_t row_stride;      // amplitudes per batch row
     uint64_t rank_base;       // rank << nlocal (global physical index offset)
-    const GroupDesc *groups;
-    const void *ops;          // TileOp<T>*
-    const void *enc_table;    // [nenc][batch][32] T
-    const FlushTarget *targets;
-    const DiagRec *recs;
+    uint64_t tiles_per_row;
+    uint64_t total_tiles;     // tiles_per_row * rows
+    const void *blob;         // pass program (device)
     const void *tables;       // complex T
+    const void *enc_table;    // [nenc][batch][32] T
+    int32_t blob_bytes;
+    int32_t off_targets, off_recs, off_ops;
     int32_t batch;
     int32_t nlocal, K, L, ngroups, next;
-    int32_t row0;             // first batch row of this launch (gridDim.y chunks)
     int32_t tile_pos[kMaxTileBits];  // physical position of tile-local bit i
     int32_t ext_pos[kMaxQubits];     // physical positions of non-tile local bits
-};
-
-// A single state pass: the tile geometry plus the groups/ops to run on it.
-struct PassHost {
-    int K = 0, L = 0;
-    std::vector<int> tile_pos;        // size K
-    std::vector<int> ext_pos;         // nlocal - K
-    std::vector<GroupDesc> groups;
-    std::vector<TileOp<double>> ops;  // lowered in double; converted per dtype
-    std::vector<FlushTarget> targets;
-    std::vector<DiagRec> recs;
-    std::vector<cplx> tables;
-    int ngates = 0;                   // source gates in this pass
-    double bytes = 0;                 // algorithmic HBM bytes per row
 };
 
 // ---- resolved gate ----------------------------------------------------------
@@ -145,13 +139,13 @@ struct GateRec {
     std::string name;
     int kind = 0;
     int k = 1;                 // targets
-    int wires[2] = {0, 0};     // logical
+    int wires[2] = {0, 0};     // logical (or physical, for internal swap gates)
     std::vector<int> ctls;     // logical
     bool diag = false;
     bool encoded = false;
     int enc_slot = -1;         // first data column when encoded
     int nparams = 0;
-    int flags = 0;             // OPF_* (zero_off_control for apply_matrix)
+    int flags = 0;             // OPF_ZERO_OFF_CONTROL for apply_matrix
     cplx m[16];                // 2^k x 2^k row-major (non-encoded)
 };
 
@@ -161,6 +155,40 @@ int gate_matrix(const qsv_gate &g, cplx *m);
 bool approx_unitary(const cplx *m, int d, double tol);
 bool kind_is_diagonal(int kind);
 GateRec resolve_gate(const qsv_gate &g, int nqubit, int *enc_cursor);
+
+// ---- host-side program ---------------------------------------------------
+struct HostOp {
+    uint8_t code = 0, a = 0, b = 0, flags = 0, rmask = 0, rval = 0, nt = 0, t0 = 0, t1 = 0, treg = 0;
+    int enc = -1;
+    uint64_t fmask = 0, fval = 0;
+    std::vector<cplx> pay;     // DENSE1/DENSE1R: 4, DENSE2: 16, DIAG: 4
+    FlushPay flush{};
+    std::vector<cplx> regtab;  // FLUSH register table (2^R) when flush.regmask != 0
+};
+
+struct HostGroup {
+    int op_begin = 0, op_end = 0;   // indices into PassHost::ops
+    int slot_bit[kMaxSlots] = {};
+    int ng_bit[kMaxTileBits] = {};
+    int tgt_begin = 0, tgt_end = 0;
+};
+
+// A single state pass: the tile geometry plus the groups/ops to run on it.
+struct PassHost {
+    int K = 0, L = 0, R = kRegSlots;
+    std::vector<int> tile_pos;        // size K
+    std::vector<int> ext_pos;         // nlocal - K
+    std::vector<HostGroup> groups;
+    std::vector<HostOp> ops;
+    std::vector<FlushTarget> targets;
+    std::vector<DiagRec> recs;
+    std::vector<cplx> tables;
+    int ngates = 0;                   // gates in this pass (after 1q fusion)
+};
+// Serialised pass program for dtype.
+std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int *off_targets, int *off_recs,
+                                             int *off_ops);
+size_t op_record_bytes(const HostOp &op, int dtype, int R);
 
 // ---- runtime objects ----------------------------------------------------
 struct Nccl;  // dlopen'd NCCL
@@ -189,8 +217,9 @@ struct State {
 struct DevPass {
     PassArgs args{};
     int threads = 256;
+    int R = kRegSlots;
     size_t smem = 0;
-    uint64_t tiles = 0;
+    int grid = 0;               // persistent CTAs (occupancy x SMs)
     double bytes = 0;
     int ngates = 0;
 };
@@ -213,34 +242,29 @@ struct Plan {
     std::vector<int> perm_in, perm_out;  // layout before/after
     std::vector<EncDesc> encs;
     // device buffers
-    void *d_groups = nullptr, *d_ops = nullptr, *d_encs = nullptr;
-    void *d_targets = nullptr, *d_recs = nullptr, *d_tables = nullptr;
+    void *d_blob = nullptr, *d_tables = nullptr, *d_encs = nullptr;
     void *d_enc_table = nullptr;
     size_t enc_table_rows = 0;
     void *d_data = nullptr;
     size_t d_data_cap = 0;
     std::vector<DevPass> dev;
     qsv_opts opts{};
-    double comm_bytes = 0;
-    cudaGraphExec_t graph = nullptr;
-    void *graph_state = nullptr;
-    int graph_rows = -1;
     ~Plan();
 };
 
 // ---- planner (planner.cpp) --------------------------------------------------
 struct PlanConfig {
     int nlocal = 0, K = 12, L = 3, R = kRegSlots;
-    bool fuse = true;       // tile passes with many gates (false: one gate per pass)
-    bool fuse_1q = true;    // pre-multiply runs of single-qubit gates
+    bool fuse = true;         // tile passes with many gates (false: one gate per pass)
+    bool fuse_1q = true;      // pre-multiply runs of single-qubit gates
     bool phase_flush = true;  // lazy phase factors for diagonal gates
     int dtype = QSV_C128;
 };
 // Host-side gate fusion: runs of uncontrolled, non-encoded single-qubit gates
 // on the same wire (nothing else touching it in between) become one matrix.
 std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates);
-// Lowers gates (already mapped to PHYSICAL bit positions, all targets local)
-// to tile passes.
+// Lowers gates (wires mapped to PHYSICAL bits by phys_of_wire; every
+// non-diagonal target local) to tile passes.
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys_of_wire,
                                   const PlanConfig &cfg, std::vector<EncDesc> &encs);
 int default_tile_bits(int dtype, int nlocal);
@@ -252,13 +276,14 @@ void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
+int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);
-void reduce_z_all(State &st, double *host_out /* batch x nlocal+1: [total, S_bit0..] */);
+void reduce_z_all(State &st, double *host_out /* batch x kZ: [total, S_bit0..] */);
 void reduce_pauli(State &st, uint64_t flip, uint64_t zy, double *host_out /* batch x 2 */);
 void reduce_marginal(State &st, int row, const std::vector<int> &phys_bits, double *host_out);
 
-// ---- distributed (dist.cpp) -------------------------------------------------
+// ---- distributed (dist.cu) -------------------------------------------------
 void nccl_unique_id(void *out128);
 void nccl_init(Ctx &ctx, const void *uid);
 void nccl_destroy(Ctx &ctx);

@@ -178,7 +178,8 @@ def test_random_circuits_up_to_14_qubits(dtype):
 
 
 @pytest.mark.parametrize("opts", [{"fuse": 0}, {"tile_bits": 6, "low_bits": 2}, {"tile_bits": 10, "low_bits": 1},
-                                  {"tile_bits": 13, "low_bits": 5}])
+                                  {"tile_bits": 13, "low_bits": 5}, {"no_phase_flush": 1}, {"no_fuse_1q": 1},
+                                  {"fuse": 0, "no_phase_flush": 1, "no_fuse_1q": 1}])
 def test_tile_geometries_agree(opts):
     rng = Rng(5, "geom")
     n = 16
