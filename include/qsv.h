@@ -99,7 +99,8 @@ typedef struct qsv_opts {
     int32_t use_graph;      /* capture the pass sequence in a CUDA graph */
     int32_t no_fuse_1q;     /* 1 = keep runs of single-qubit gates unfused */
     int32_t no_phase_flush; /* 1 = apply every diagonal gate eagerly */
-    int32_t reserved[2];
+    int32_t jit;            /* 1 = specialised (NVRTC) pass kernels, -1 = interpreter, 0 = auto */
+    int32_t reserved;
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */

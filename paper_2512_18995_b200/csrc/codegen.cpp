@@ -1,0 +1,424 @@
+// Pass specialiser: emits the CUDA source of one fused tile pass with the
+// pass program compiled in (see jit.cpp for NVRTC + loading).
+//
+// The generated kernel has the structure of the interpreter in tile_pass.cu
+// (persistent CTAs, cp.async tile staging into swizzled shared memory,
+// register groups, streaming stores) but every gate is straight-line code:
+//   * matrix entries become exact hexfloat immediates; zero and +-1 terms are
+//     folded away, so h / x / ry / cz / diag phases cost only what they must;
+//   * register-slot conditions (controls inside the group) are resolved at
+//     generation time -- only the control-satisfied pairs are emitted;
+//   * bit scatters (tile index -> global offset, set index -> tile offset) are
+//     runs of constant shift/mask operations;
+//   * deferred phases (planner.cpp GroupLowering) keep their split: per-tile
+//     EXT factors in shared memory, TILE tables in global memory, MIXED
+//     records as inline predicated multiplies, register tables as constants.
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+#include <string>
+
+#include "qsv_internal.hpp"
+
+namespace qsv {
+
+namespace {
+
+std::string lit(double v, bool f32) {
+    char buf[64];
+    if (f32) {
+        std::snprintf(buf, sizeof buf, "%af", static_cast<double>(static_cast<float>(v)));
+    } else {
+        std::snprintf(buf, sizeof buf, "%a", v);
+    }
+    return buf;
+}
+
+// Runs of a bit scatter: source bit i -> destination bit pos[i] (ascending).
+struct Run {
+    int src, len, dst;
+};
+std::vector<Run> runs_of(const std::vector<int> &pos) {
+    std::vector<Run> rs;
+    for (size_t i = 0; i < pos.size(); ++i) {
+        if (!rs.empty() && rs.back().src + rs.back().len == static_cast<int>(i) &&
+            rs.back().dst + rs.back().len == pos[i])
+            rs.back().len++;
+        else rs.push_back({static_cast<int>(i), 1, pos[i]});
+    }
+    return rs;
+}
+std::string scatter(const std::string &x, const std::vector<int> &pos, bool wide) {
+    auto rs = runs_of(pos);
+    if (rs.empty()) return wide ? "0ull" : "0";
+    std::ostringstream o;
+    for (size_t k = 0; k < rs.size(); ++k) {
+        const Run &r = rs[k];
+        if (k) o << " | ";
+        const std::string mask = wide ? std::to_string((1ull << r.len) - 1) + "ull" : std::to_string((1u << r.len) - 1);
+        std::string src = wide ? "((unsigned long long)(" + x + "))" : "(" + x + ")";
+        o << "(((" << src << " >> " << r.src << ") & " << mask << ") << " << r.dst << ")";
+    }
+    return o.str();
+}
+
+struct Gen {
+    const PassHost &ph;
+    bool f32;
+    int R;
+    std::ostringstream o;
+    std::string T, V;
+
+    Gen(const PassHost &p, int dtype) : ph(p), f32(dtype == QSV_C64), R(p.R) {
+        T = f32 ? "float" : "double";
+        V = f32 ? "cf" : "cd";
+    }
+
+    std::string c(double x) const { return lit(x, f32); }
+
+    // dst = coefficient * x (complex), with constant folding; returns terms
+    // for the real and imaginary parts (appended to re/im lists)
+    void term(const cplx &m, const std::string &x, std::vector<std::string> &re, std::vector<std::string> &im) {
+        const double a = m.real(), b = m.imag();
+        auto mulstr = [&](double k, const std::string &v) -> std::string {
+            if (k == 1.0) return "+" + v;
+            if (k == -1.0) return "-" + v;
+            return "+" + c(k) + "*" + v;
+        };
+        // (a + ib)(x + iy) = (a x - b y) + i(a y + b x)
+        if (a != 0.0) {
+            re.push_back(mulstr(a, x + ".x"));
+            im.push_back(mulstr(a, x + ".y"));
+        }
+        if (b != 0.0) {
+            re.push_back(mulstr(-b, x + ".y"));
+            im.push_back(mulstr(b, x + ".x"));
+        }
+    }
+    static std::string sum(const std::vector<std::string> &ts) {
+        if (ts.empty()) return "0";
+        std::string s;
+        for (size_t i = 0; i < ts.size(); ++i) {
+            std::string t = ts[i];
+            if (i == 0 && t[0] == '+') t = t.substr(1);
+            s += t;
+        }
+        return s;
+    }
+
+    // v[r] = sum_k M[row][k] * x[k]
+    void matvec(const std::vector<int> &regs, const std::vector<cplx> &m, int d, const std::string &ind) {
+        o << ind << "{ ";
+        for (int k = 0; k < d; ++k) o << "const " << V << " x" << k << " = v" << regs[k] << "; ";
+        o << "\n";
+        for (int r = 0; r < d; ++r) {
+            std::vector<std::string> re, im;
+            for (int k = 0; k < d; ++k) term(m[r * d + k], "x" + std::to_string(k), re, im);
+            o << ind << "  v" << regs[r] << " = mk(" << sum(re) << ", " << sum(im) << ");\n";
+        }
+        o << ind << "}\n";
+    }
+
+    void cmul_const(int r, const cplx &f, const std::string &ind) {
+        if (f == cplx(1, 0)) return;
+        std::vector<std::string> re, im;
+        term(f, "v" + std::to_string(r), re, im);
+        o << ind << "v" << r << " = mk(" << sum(re) << ", " << sum(im) << ");\n";
+    }
+
+    std::string fcond(uint64_t fmask, uint64_t fval) {
+        std::ostringstream s;
+        s << "((pb & " << fmask << "ull) == " << fval << "ull)";
+        return s.str();
+    }
+
+    void emit_rec_factor(const DiagRec &r, const std::string &base, const std::string &f, const std::string &ind) {
+        // f = f * (cond(base) ? val[idx(base)] : 1)
+        std::string cond = r.fmask ? "((" + base + " & " + std::to_string(r.fmask) + "ull) == " +
+                                         std::to_string(r.fval) + "ull)"
+                                   : "true";
+        o << ind << "if (" << cond << ") {\n";
+        const int nv = 1 << r.nt;
+        if (nv == 1) {
+            o << ind << "  " << f << " = cmulv(" << f << ", mk(" << c(r.val[0]) << ", " << c(r.val[1]) << "));\n";
+        } else {
+            o << ind << "  const int ix = ";
+            if (r.nt == 1) o << "(int)((" << base << " >> " << r.tpos0 << ") & 1ull);\n";
+            else
+                o << "(int)(((" << base << " >> " << r.tpos0 << ") & 1ull) << 1 | ((" << base << " >> " << r.tpos1
+                  << ") & 1ull));\n";
+            o << ind << "  " << V << " q;\n";
+            for (int i = 0; i < nv; ++i)
+                o << ind << "  " << (i ? "else " : "") << "if (ix == " << i << ") q = mk(" << c(r.val[2 * i]) << ", "
+                  << c(r.val[2 * i + 1]) << ");\n";
+            o << ind << "  " << f << " = cmulv(" << f << ", q);\n";
+        }
+        o << ind << "}\n";
+    }
+
+    void emit_op(const HostOp &op, const std::string &ind) {
+        const int NR = 1 << R;
+        std::string ind2 = ind;
+        const bool fc = (op.flags & OPF_FCOND) != 0;
+        const bool zoc = (op.flags & OPF_ZERO_OFF_CONTROL) != 0;
+        const bool enc = (op.flags & OPF_ENC) != 0;
+        if (op.code == OP_FLUSH) {
+            emit_flush(op, ind);
+            return;
+        }
+        if (fc && !zoc) {
+            o << ind << "if " << fcond(op.fmask, op.fval) << " {\n";
+            ind2 = ind + "  ";
+        }
+        std::vector<cplx> m = op.pay;
+        if (enc) {
+            // matrix / diagonal from the per-row table
+            o << ind2 << "{ const " << T << " *em = a.enc_table + ((size_t)" << op.enc
+              << " * a.batch + row) * 32;\n";
+            const int cnt = op.code == OP_DENSE2 ? 16 : 4;
+            o << ind2 << "  " << V << " ";
+            for (int i = 0; i < cnt; ++i) o << (i ? ", " : "") << "e" << i << " = mk(em[" << 2 * i << "], em[" << 2 * i + 1 << "])";
+            o << ";\n";
+        }
+        auto pair_on = [&](int r) { return (r & op.rmask) == op.rval; };
+        auto zero_regs = [&](const std::vector<int> &regs, const std::string &in) {
+            for (int r : regs) o << in << "v" << r << " = mk(0, 0);\n";
+        };
+        switch (op.code) {
+        case OP_DENSE1:
+        case OP_DENSE1R:
+        case OP_X1: {
+            const int J = op.a;
+            if (op.code == OP_X1) m = {0, 1, 1, 0};
+            for (int r = 0; r < NR; ++r) {
+                if (r & (1 << J)) continue;
+                const int r1 = r | (1 << J);
+                std::vector<int> regs = {r, r1};
+                if (!pair_on(r)) {
+                    if (zoc) zero_regs(regs, ind2);
+                    continue;
+                }
+                if (zoc && fc) {
+                    o << ind2 << "if " << fcond(op.fmask, op.fval) << " {\n";
+                    emit_mv(regs, m, 2, enc, ind2 + "  ");
+                    o << ind2 << "} else {\n";
+                    zero_regs(regs, ind2 + "  ");
+                    o << ind2 << "}\n";
+                } else emit_mv(regs, m, 2, enc, ind2);
+            }
+            break;
+        }
+        case OP_DENSE2: {
+            const int A = op.a, B = op.b;
+            for (int r = 0; r < NR; ++r) {
+                if (r & ((1 << A) | (1 << B))) continue;
+                std::vector<int> regs = {r, r | (1 << B), r | (1 << A), r | (1 << A) | (1 << B)};
+                if (!pair_on(r)) {
+                    if (zoc) zero_regs(regs, ind2);
+                    continue;
+                }
+                if (zoc && fc) {
+                    o << ind2 << "if " << fcond(op.fmask, op.fval) << " {\n";
+                    emit_mv(regs, m, 4, enc, ind2 + "  ");
+                    o << ind2 << "} else {\n";
+                    zero_regs(regs, ind2 + "  ");
+                    o << ind2 << "}\n";
+                } else emit_mv(regs, m, 4, enc, ind2);
+            }
+            break;
+        }
+        case OP_DIAG: {
+            // value index from target bits: register bits are compile-time,
+            // fixed bits are read from pb
+            const bool t0r = op.treg & 1, t1r = (op.treg >> 1) & 1;
+            for (int r = 0; r < NR; ++r) {
+                const bool on = pair_on(r);
+                if (!on) {
+                    if (zoc) o << ind2 << "v" << r << " = mk(0, 0);\n";
+                    continue;
+                }
+                std::string body;
+                auto bitexpr = [&](bool reg, int t) -> std::string {
+                    if (reg) return std::to_string((r >> t) & 1);
+                    return "(int)((pb >> " + std::to_string(t) + ") & 1ull)";
+                };
+                const std::string b0 = bitexpr(t0r, op.t0);
+                const std::string idx = op.nt == 2 ? "((" + b0 + ") << 1 | (" + bitexpr(t1r, op.t1) + "))" : b0;
+                const bool static_idx = (t0r && (op.nt == 1 || t1r));
+                std::string in3 = ind2;
+                if (zoc && fc) {
+                    o << ind2 << "if " << fcond(op.fmask, op.fval) << " {\n";
+                    in3 = ind2 + "  ";
+                }
+                if (static_idx && !enc) {
+                    int ix = (r >> op.t0) & 1;
+                    if (op.nt == 2) ix = (ix << 1) | ((r >> op.t1) & 1);
+                    cmul_const(r, m[ix], in3);
+                } else {
+                    o << in3 << "{ const int ix = " << idx << "; " << V << " q = ";
+                    const int nv = 1 << op.nt;
+                    for (int i = 0; i < nv; ++i) {
+                        const std::string val = enc ? "e" + std::to_string(i)
+                                                    : "mk(" + c(m[i].real()) + ", " + c(m[i].imag()) + ")";
+                        if (i + 1 < nv) o << "ix == " << i << " ? " << val << " : ";
+                        else o << val;
+                    }
+                    o << "; v" << r << " = cmulv(v" << r << ", q); }\n";
+                }
+                if (zoc && fc) {
+                    o << ind2 << "} else {\n" << ind2 << "  v" << r << " = mk(0, 0);\n" << ind2 << "}\n";
+                }
+            }
+            break;
+        }
+        }
+        if (enc) o << ind2 << "}\n";
+        if (fc && !zoc) o << ind << "}\n";
+    }
+
+    void emit_mv(const std::vector<int> &regs, const std::vector<cplx> &m, int d, bool enc, const std::string &ind) {
+        if (!enc) {
+            matvec(regs, m, d, ind);
+            return;
+        }
+        o << ind << "{ ";
+        for (int k = 0; k < d; ++k) o << "const " << V << " x" << k << " = v" << regs[k] << "; ";
+        o << "\n";
+        for (int r = 0; r < d; ++r) {
+            o << ind << "  v" << regs[r] << " = ";
+            for (int k = 0; k < d; ++k) {
+                if (k == 0) o << "cmulv(e" << r * d << ", x0)";
+                else o << ";\n" << ind << "  v" << regs[r] << " = cfmav(e" << r * d + k << ", x" << k << ", v" << regs[r]
+                       << ")";
+            }
+            o << ";\n";
+        }
+        o << ind << "}\n";
+    }
+
+    void emit_flush(const HostOp &op, const std::string &ind) {
+        const int NR = 1 << R;
+        for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti) {
+            const FlushTarget &t = ph.targets[ti];
+            o << ind << "{ " << V << " f = " << (t.eidx >= 0 ? "E[" + std::to_string(t.eidx) + "]" : "mk(1, 0)")
+              << ";\n";
+            if (t.table >= 0) o << ind << "  f = cmulv(f, a.tables[" << t.table << " + s]);\n";
+            for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", "f", ind + "  ");
+            for (int r = 0; r < NR; ++r)
+                if (t.slot < 0 || ((r >> t.slot) & 1)) o << ind << "  v" << r << " = cmulv(v" << r << ", f);\n";
+            o << ind << "}\n";
+        }
+        if (op.flush.regmask)
+            for (int r = 0; r < NR; ++r)
+                if ((op.flush.regmask >> r) & 1) cmul_const(r, op.regtab[r], ind);
+    }
+
+    std::string source(const std::string &name) {
+        const int K = ph.K, L = ph.L, NR = 1 << R;
+        const int amp = f32 ? 8 : 16;
+        const int apu = 16 / amp;
+        const int nchunks = (1 << K) / apu;
+        const int nsets = 1 << (K - R);
+        int threads = std::max(32, std::min(256, std::max(nsets, std::min(nchunks, 256))));
+        threads = (threads + 31) / 32 * 32;
+        o << "// generated by qsv codegen.cpp: one fused tile pass\n";
+        o << "typedef unsigned long long u64;\n";
+        o << "struct __align__(" << (f32 ? 8 : 16) << ") " << V << " { " << T << " x, y; };\n";
+        o << "static __device__ __forceinline__ " << V << " mk(" << T << " x, " << T << " y) { " << V
+          << " r; r.x = x; r.y = y; return r; }\n";
+        o << "static __device__ __forceinline__ " << V << " cmulv(" << V << " a, " << V
+          << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
+        o << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
+          << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
+        if (f32)
+            o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; const int f = (w >> 3) ^ "
+                 "(w >> 6) ^ (w >> 9) ^ (w >> 12); return ((w ^ (f & 7)) << 1) | (u & 1); }\n";
+        else
+            o << "static __device__ __forceinline__ int swz(int u) { const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ "
+                 "(u >> 12); return u ^ (f & 7); }\n";
+        o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
+          << " *tables; const " << T << " *enc_table; int batch; int pad; };\n";
+        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", 2) " << name << "(const Args a) {\n";
+        o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+        o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
+        int next_max = 0;
+        for (const HostGroup &g : ph.groups) {
+            int ne = 0;
+            for (int ti = g.tgt_begin; ti < g.tgt_end; ++ti)
+                if (ph.targets[ti].eidx >= 0) ne = std::max(ne, ph.targets[ti].eidx + 1);
+            next_max = std::max(next_max, ne);
+        }
+        if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
+        std::vector<int> hi(ph.tile_pos.begin() + L, ph.tile_pos.end());
+        int tpr_log = static_cast<int>(ph.ext_pos.size());
+        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        o << "    const int row = (int)(t >> " << tpr_log << ");\n";
+        o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
+        o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
+        o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
+        o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
+        o << "      const int u = ch * " << apu << ";\n";
+        o << "      const u64 g = tb + (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") + (u & "
+          << ((1 << L) - 1) << ");\n";
+        o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&tile[swz(u)]);\n";
+        o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&st[g]) : "
+             "\"memory\");\n";
+        o << "    }\n";
+        o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+        o << "    __syncthreads();\n";
+        o << "    const u64 pbase = a.rank_base | tb;\n";
+        for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
+            const HostGroup &g = ph.groups[gi];
+            o << "    // ---- group " << gi << "\n";
+            bool any_ext = false;
+            for (int ti = g.tgt_begin; ti < g.tgt_end; ++ti) {
+                const FlushTarget &t = ph.targets[ti];
+                if (t.eidx < 0) continue;
+                any_ext = true;
+                o << "    if (threadIdx.x == " << (t.eidx % threads) << ") {\n      " << V << " f = mk(1, 0);\n";
+                for (int k = t.ext_begin; k < t.ext_end; ++k) emit_rec_factor(ph.recs[k], "pbase", "f", "      ");
+                o << "      E[" << t.eidx << "] = f;\n    }\n";
+            }
+            if (any_ext) o << "    __syncthreads();\n";
+            std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
+            for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
+            o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
+            o << "      const int ub = " << scatter("s", ngt, false) << ";\n";
+            o << "      const u64 pb = pbase | " << scatter("s", ngp, true) << ";\n";
+            (void)pb_unused;
+            std::vector<int> uoff(NR, 0);
+            for (int r = 0; r < NR; ++r)
+                for (int j = 0; j < R; ++j)
+                    if ((r >> j) & 1) uoff[r] |= 1 << g.slot_bit[j];
+            for (int r = 0; r < NR; ++r)
+                o << "      " << V << " v" << r << " = tile[swz(ub | " << uoff[r] << ")];\n";
+            for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
+            for (int r = 0; r < NR; ++r) o << "      tile[swz(ub | " << uoff[r] << ")] = v" << r << ";\n";
+            o << "      (void)pb;\n    }\n    __syncthreads();\n";
+        }
+        o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
+        o << "      const int u = ch * " << apu << ";\n";
+        o << "      const u64 g = tb + (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") + (u & "
+          << ((1 << L) - 1) << ");\n";
+        o << "      const float4 val = *(const float4 *)&tile[swz(u)];\n";
+        o << "      asm volatile(\"st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\\n\" :: \"l\"(&st[g]), \"f\"(val.x), "
+             "\"f\"(val.y), \"f\"(val.z), \"f\"(val.w) : \"memory\");\n";
+        o << "    }\n    __syncthreads();\n  }\n}\n";
+        return o.str();
+    }
+    int pb_unused = 0;
+};
+
+} // namespace
+
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads) {
+    Gen g(ph, dtype);
+    const int nsets = 1 << (ph.K - ph.R);
+    const int amp = dtype == QSV_C64 ? 8 : 16;
+    const int nchunks = (1 << ph.K) / (16 / amp);
+    int th = std::max(32, std::min(256, std::max(nsets, std::min(nchunks, 256))));
+    *threads = (th + 31) / 32 * 32;
+    return g.source(name);
+}
+
+} // namespace qsv

@@ -1,0 +1,221 @@
+// NVRTC compilation and loading of specialised pass kernels (codegen.cpp).
+//
+// libnvrtc is dlopen'ed (the CUDA 12.9 toolkit's, or the one torch ships) so
+// libqsv.so itself still loads on GPU-less hosts; kernels are compiled for
+// sm_100a only, loaded with cudaLibraryLoadData and launched like any other
+// kernel. Compiled cubins are cached in-process and, when writable, on disk
+// ($QSV_JIT_CACHE or ~/.cache/qsv_jit) keyed by a hash of the source; the
+// cache is an optimisation only -- nothing depends on it persisting.
+#include <dlfcn.h>
+#include <sys/stat.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "qsv_internal.hpp"
+
+namespace qsv {
+
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads);
+
+namespace {
+
+typedef int nvrtcResult;
+typedef struct _nvrtcProgram *nvrtcProgram;
+
+struct Nvrtc {
+    void *h = nullptr;
+    nvrtcResult (*CreateProgram)(nvrtcProgram *, const char *, const char *, int, const char *const *,
+                                 const char *const *) = nullptr;
+    nvrtcResult (*CompileProgram)(nvrtcProgram, int, const char *const *) = nullptr;
+    nvrtcResult (*GetCUBINSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetCUBIN)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*GetProgramLogSize)(nvrtcProgram, size_t *) = nullptr;
+    nvrtcResult (*GetProgramLog)(nvrtcProgram, char *) = nullptr;
+    nvrtcResult (*DestroyProgram)(nvrtcProgram *) = nullptr;
+    const char *(*GetErrorString)(nvrtcResult) = nullptr;
+};
+
+Nvrtc *nvrtc() {
+    static Nvrtc *inst = nullptr;
+    static std::mutex mu;
+    std::lock_guard<std::mutex> lk(mu);
+    if (inst) return inst;
+    auto *n = new Nvrtc();
+    const char *env = std::getenv("QSV_NVRTC_LIB");
+    const char *cands[] = {env, "/usr/local/cuda/lib64/libnvrtc.so.12", "libnvrtc.so.12", "libnvrtc.so"};
+    for (const char *c : cands) {
+        if (!c) continue;
+        n->h = dlopen(c, RTLD_NOW | RTLD_LOCAL);
+        if (n->h) break;
+    }
+    if (!n->h) {
+        delete n;
+        fail(QSV_ERR_INTERNAL, "NVRTC not found (set QSV_NVRTC_LIB to libnvrtc.so.12)");
+    }
+#define LOAD(f)                                                                                                        \
+    n->f = reinterpret_cast<decltype(n->f)>(dlsym(n->h, "nvrtc" #f));                                                  \
+    if (!n->f) fail(QSV_ERR_INTERNAL, "NVRTC symbol missing: nvrtc" #f);
+    LOAD(CreateProgram) LOAD(CompileProgram) LOAD(GetCUBINSize) LOAD(GetCUBIN) LOAD(GetProgramLogSize)
+    LOAD(GetProgramLog) LOAD(DestroyProgram) LOAD(GetErrorString)
+#undef LOAD
+    inst = n;
+    return inst;
+}
+
+uint64_t fnv64(const std::string &s) {
+    uint64_t h = 0xcbf29ce484222325ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
+std::string cache_dir() {
+    const char *env = std::getenv("QSV_JIT_CACHE");
+    if (env) return env;
+    const char *home = std::getenv("HOME");
+    return std::string(home ? home : "/tmp") + "/.cache/qsv_jit";
+}
+
+std::vector<char> compile(const std::string &src, const std::string &key) {
+    static std::map<std::string, std::vector<char>> mem;
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = mem.find(key);
+        if (it != mem.end()) return it->second;
+    }
+    const std::string path = cache_dir() + "/" + key + ".cubin";
+    {
+        std::ifstream f(path, std::ios::binary);
+        if (f) {
+            std::vector<char> b((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+            if (!b.empty()) {
+                std::lock_guard<std::mutex> lk(mu);
+                mem[key] = b;
+                return b;
+            }
+        }
+    }
+    Nvrtc *n = nvrtc();
+    nvrtcProgram prog = nullptr;
+    if (n->CreateProgram(&prog, src.c_str(), (key + ".cu").c_str(), 0, nullptr, nullptr) != 0)
+        fail(QSV_ERR_INTERNAL, "nvrtcCreateProgram failed");
+    const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--extra-device-vectorization"};
+    const nvrtcResult rc = n->CompileProgram(prog, 5, opts);
+    if (rc != 0) {
+        size_t ls = 0;
+        n->GetProgramLogSize(prog, &ls);
+        std::string log(ls, '\0');
+        n->GetProgramLog(prog, log.data());
+        n->DestroyProgram(&prog);
+        fail(QSV_ERR_INTERNAL, std::string("NVRTC compile failed: ") + n->GetErrorString(rc) + "\n" + log.substr(0, 4000));
+    }
+    size_t sz = 0;
+    n->GetCUBINSize(prog, &sz);
+    std::vector<char> cubin(sz);
+    n->GetCUBIN(prog, cubin.data());
+    n->DestroyProgram(&prog);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        mem[key] = cubin;
+    }
+    // best-effort disk cache (atomic rename)
+    const std::string dir = cache_dir();
+    mkdir((dir.substr(0, dir.rfind('/'))).c_str(), 0755);
+    mkdir(dir.c_str(), 0755);
+    const std::string tmp = path + ".tmp" + std::to_string(reinterpret_cast<uintptr_t>(&cubin));
+    {
+        std::ofstream f(tmp, std::ios::binary);
+        if (f) f.write(cubin.data(), static_cast<std::streamsize>(cubin.size()));
+    }
+    std::rename(tmp.c_str(), path.c_str());
+    return cubin;
+}
+
+} // namespace
+
+struct JitKernel {
+    cudaLibrary_t lib = nullptr;
+    cudaKernel_t kernel = nullptr;
+};
+
+// Compiles (or fetches) the specialised kernel of one pass and fills dp.
+void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
+    const std::string name = "qsv_pass";
+    int threads = 256;
+    std::string src = generate_pass_source(ph, dtype, name, &threads);
+    char key[32];
+    std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
+    std::vector<char> cubin = compile(src, key);
+    static std::map<std::string, JitKernel> loaded;
+    static std::mutex mu;
+    JitKernel jk;
+    int dev = 0;
+    QSV_CUDA(cudaGetDevice(&dev));
+    const std::string lkey = std::string(key) + ":" + std::to_string(dev);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = loaded.find(lkey);
+        if (it != loaded.end()) jk = it->second;
+        else {
+            QSV_CUDA(cudaLibraryLoadData(&jk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+            QSV_CUDA(cudaLibraryGetKernel(&jk.kernel, jk.lib, name.c_str()));
+            loaded[lkey] = jk;
+        }
+    }
+    const int amp = dtype == QSV_C64 ? 8 : 16;
+    dp.jit = reinterpret_cast<const void *>(jk.kernel);
+    dp.threads = threads;
+    dp.smem = static_cast<size_t>(amp) << ph.K;
+    int optin = 0;
+    QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    QSV_CUDA(cudaFuncGetAttributes(&fa, dp.jit));
+    QSV_CUDA(cudaFuncSetAttribute(dp.jit, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+    int blocks = 0;
+    QSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, dp.jit, dp.threads, dp.smem));
+    dp.grid = std::max(1, blocks) * sm_count;
+    dp.jit_regs = fa.numRegs;
+    dp.jit_spill = static_cast<int>(fa.localSizeBytes);
+}
+
+// Source of a pass's specialised kernel (diagnostics / tests).
+std::string jit_source(const PassHost &ph, int dtype) {
+    int threads = 0;
+    return generate_pass_source(ph, dtype, "qsv_pass", &threads);
+}
+
+void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s) {
+    struct JArgs {
+        void *state;
+        uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
+        const void *tables;
+        const void *enc_table;
+        int batch;
+        int pad;
+    } a{};
+    a.state = state;
+    a.row_stride = dp.args.row_stride;
+    a.rank_base = dp.args.rank_base;
+    a.tiles_per_row = dp.args.tiles_per_row;
+    a.total_tiles = dp.args.tiles_per_row * static_cast<uint64_t>(rows);
+    a.tables = dp.args.tables;
+    a.enc_table = dp.args.enc_table;
+    a.batch = dp.args.batch;
+    const uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(dp.grid, 1)));
+    void *args[] = {&a};
+    QSV_CUDA(cudaLaunchKernel(dp.jit, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
+}
+
+} // namespace qsv

@@ -300,10 +300,12 @@ void upload_plan(Plan &p) {
         const int chunks = static_cast<int>(((1ull << ph.K) * amp) / 16);
         dp.threads = std::max(32, std::min(256, std::max(nsets, std::min(chunks, 256))));
         dp.threads = (dp.threads + 31) / 32 * 32;
-        dp.smem = (amp << ph.K) + (sizeof(uint64_t) << (ph.K - ph.L)) + o.bytes;
+        dp.smem = tile_prog_offset(ph.K, ph.L, static_cast<int>(amp)) + o.bytes;
         require(dp.smem + 1024 <= p.ctx->smem_optin || p.ctx->smem_optin == 0,
                 "plan: pass program does not fit in shared memory");
         dp.grid = std::max(1, tile_kernel_blocks_per_sm(p.dtype, dp.R, dp.threads, dp.smem)) * p.ctx->sm_count;
+        const bool use_jit = p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
+        if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
         dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
         dp.ngates = ph.ngates;
         p.dev.push_back(dp);

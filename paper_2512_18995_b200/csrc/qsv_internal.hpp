@@ -134,6 +134,12 @@ struct PassArgs {
     int32_t ext_pos[kMaxQubits];     // physical positions of non-tile local bits
 };
 
+// Shared-memory layout of a tile CTA: [tile 2^K amps][hi_off 2^(K-L) u64][program]
+__host__ __device__ inline int tile_prog_offset(int K, int L, int amp_bytes) {
+    const int b = (amp_bytes << K) + (8 << (K - L));
+    return (b + 15) & ~15;
+}
+
 // ---- resolved gate ----------------------------------------------------------
 struct GateRec {
     std::string name;
@@ -220,6 +226,8 @@ struct DevPass {
     int R = kRegSlots;
     size_t smem = 0;
     int grid = 0;               // persistent CTAs (occupancy x SMs)
+    const void *jit = nullptr;  // specialised kernel (cudaKernel_t), else the interpreter
+    int jit_regs = 0, jit_spill = 0;
     double bytes = 0;
     int ngates = 0;
 };
@@ -277,6 +285,10 @@ void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaS
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
 int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
+// ---- pass specialisation (codegen.cpp, jit.cpp) ----------------------------
+void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
+void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s);
+std::string jit_source(const PassHost &ph, int dtype);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);
 void reduce_z_all(State &st, double *host_out /* batch x kZ: [total, S_bit0..] */);

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256, 2) tile_pass_kernel(const PassArgs a) {
     const int K = a.K, L = a.L, H = K - L;
     V *tile = reinterpret_cast<V *>(smem_raw);
     uint64_t *hi_off = reinterpret_cast<uint64_t *>(smem_raw + (sizeof(V) << K));
-    unsigned char *prog = reinterpret_cast<unsigned char *>(hi_off + (1 << H));
+    unsigned char *prog = smem_raw + tile_prog_offset(K, L, sizeof(V));
 
     // stage the pass program and the high-bit offset table once per CTA
     {
@@ -396,13 +396,24 @@ const void *select_kernel(int dtype, int R) {
 
 int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem) {
     const void *k = select_kernel(dtype, R);
-    QSV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int dev = 0, optin = 0;
+    QSV_CUDA(cudaGetDevice(&dev));
+    QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    // the limit is per kernel: always the device maximum, never a pass's own size
+    cudaFuncAttributes fa{};
+    QSV_CUDA(cudaFuncGetAttributes(&fa, k));
+    QSV_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
     int blocks = 0;
     QSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, threads, smem));
     return blocks;
 }
 
 void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s) {
+    if (dp.jit) {
+        launch_jit(dp, state, rows, s);
+        return;
+    }
     PassArgs a = dp.args;
     a.state = state;
     a.total_tiles = a.tiles_per_row * static_cast<uint64_t>(rows);

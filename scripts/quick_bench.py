@@ -20,7 +20,7 @@ def run(n, cir, dtype, opts=None, reps=3, label=""):
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 28
 run(n, W.cfg3_circuit(n), qsv.C128, label="cfg3")
-run(n, W.cfg3_circuit(n), qsv.C128, {"no_phase_flush": 1}, label="cfg3")
+run(n, W.cfg3_circuit(n), qsv.C128, {"jit": -1}, label="cfg3-int")
 run(n, W.cfg3_circuit(n), qsv.C128, {"tile_bits": 13, "low_bits": 3}, label="cfg3")
 run(n, W.cfg3_circuit(n), qsv.C128, {"tile_bits": 11, "low_bits": 3}, label="cfg3")
 run(n, W.cfg3_circuit(n), qsv.C128, {"tile_bits": 12, "low_bits": 2}, label="cfg3")

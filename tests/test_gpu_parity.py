@@ -46,9 +46,10 @@ def run(n, gates, init=None, data=None, dtype=C128, opts=None):
 
 # ------------------------------------------------------------ golden ----
 @pytest.mark.parametrize("dtype", [C128, C64])
-def test_golden_fixtures(dtype):
+@pytest.mark.parametrize("jit", [-1, 1])
+def test_golden_fixtures(dtype, jit):
     for case in load_circuit_cases():
-        got, st = run(case["n"], case["gates"], case.get("init"), case.get("data"), dtype=dtype)
+        got, st = run(case["n"], case["gates"], case.get("init"), case.get("data"), dtype=dtype, opts={"jit": jit})
         err = np.max(np.abs(got - case["out"]))
         assert err <= TOL[dtype], (case["name"], err)
         if "obs" in case:
@@ -167,19 +168,22 @@ def test_measure_matches_seeded_reference_histogram():  # test_dist.cpp:207-222 
 
 # ----------------------------------------------- random / fused paths ----
 @pytest.mark.parametrize("dtype", [C128, C64])
-def test_random_circuits_up_to_14_qubits(dtype):
+@pytest.mark.parametrize("jit", [-1, 1])
+def test_random_circuits_up_to_14_qubits(dtype, jit):
     rng = Rng(101, "gpu-random")
     for n in [1, 2, 3, 4, 5, 7, 9, 11, 12, 13, 14]:
         psi = random_state(rng, n)
         gates = [random_gate(rng, n) for _ in range(60)]
-        got, _ = run(n, gates, init=psi, dtype=dtype)
+        got, _ = run(n, gates, init=psi, dtype=dtype, opts={"jit": jit})
         want = O.port_forward(n, gates, init=psi)[0]
         assert np.max(np.abs(got[0] - want)) <= TOL[dtype], n
 
 
 @pytest.mark.parametrize("opts", [{"fuse": 0}, {"tile_bits": 6, "low_bits": 2}, {"tile_bits": 10, "low_bits": 1},
                                   {"tile_bits": 13, "low_bits": 5}, {"no_phase_flush": 1}, {"no_fuse_1q": 1},
-                                  {"fuse": 0, "no_phase_flush": 1, "no_fuse_1q": 1}])
+                                  {"fuse": 0, "no_phase_flush": 1, "no_fuse_1q": 1, "jit": -1},
+                                  {"jit": -1}, {"jit": 1, "tile_bits": 8, "low_bits": 2},
+                                  {"jit": 1, "no_phase_flush": 1}])
 def test_tile_geometries_agree(opts):
     rng = Rng(5, "geom")
     n = 16
