@@ -189,6 +189,13 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
 /* marginal_probabilities on row `row`: out has 2^k entries. */
 int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
 
+/* Plans on the host only (no device, no upload): fills info as
+ * qsv_plan_info_get would for a context of `world` ranks, and, when src is
+ * non-null, the generated CUDA source of pass `pass_index`. For tests and
+ * diagnostics on GPU-less hosts. */
+int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ngates, const qsv_opts *opts,
+                 qsv_plan_info *info, int pass_index, char *src, size_t cap);
+
 /* ---- seeded inputs (quasar::Rng, rng.hpp:29-103) ----------------------- */
 /* Fills `out` with count draws of stream Rng(seed, label) (label may be
  * NULL for Rng(seed)); kind 0 next_u64, 1 uniform, 2 normal. Counter-based,

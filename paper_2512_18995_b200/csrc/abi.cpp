@@ -495,6 +495,42 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
     });
 }
 
+int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ngates, const qsv_opts *opts,
+                 qsv_plan_info *info, int pass_index, char *src, size_t cap) {
+    return guard([&] {
+        require(world >= 1 && (world & (world - 1)) == 0, "world size must be a power of two");
+        Ctx ctx;
+        ctx.device = -1;
+        ctx.world = world;
+        ctx.gbits = std::countr_zero(static_cast<unsigned>(world));
+        Plan p;
+        build_plan_from_abi(p, &ctx, nqubit, dtype, gates, ngates, opts);
+        if (info) {
+            std::memset(info, 0, sizeof(*info));
+            info->ngates = p.ngates;
+            const double amp = dtype == QSV_C64 ? 8 : 16;
+            for (const Step &s : p.steps) {
+                if (s.kind == 0) {
+                    info->npasses += 1;
+                    info->bytes_per_exec += 2.0 * amp * std::ldexp(1.0, p.nlocal);
+                    info->max_tile_bits = std::max(info->max_tile_bits, p.passes[s.pass].K);
+                } else {
+                    info->nswaps += static_cast<int>(s.swap_bits.size());
+                    info->comm_bytes_per_exec += s.swap_bits.size() * amp * std::ldexp(1.0, p.nlocal - 1);
+                }
+            }
+        }
+        if (src && cap) {
+            src[0] = 0;
+            if (pass_index >= 0 && pass_index < static_cast<int>(p.passes.size())) {
+                const std::string s = jit_source(p.passes[pass_index], dtype);
+                std::snprintf(src, cap, "%s", s.c_str());
+            }
+        }
+        p.ctx = nullptr;
+    });
+}
+
 int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads) {
     return guard([&] {
         require(out != nullptr || count == 0, "null out");

@@ -302,7 +302,7 @@ struct Gen {
             const FlushTarget &t = ph.targets[ti];
             o << ind << "{ " << V << " f = " << (t.eidx >= 0 ? "E[" + std::to_string(t.eidx) + "]" : "mk(1, 0)")
               << ";\n";
-            if (t.table >= 0) o << ind << "  f = cmulv(f, a.tables[" << t.table << " + s]);\n";
+            if (t.table >= 0) o << ind << "  f = cmulv(f, tab" << ti << ");\n";
             for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", "f", ind + "  ");
             for (int r = 0; r < NR; ++r)
                 if (t.slot < 0 || ((r >> t.slot) & 1)) o << ind << "  v" << r << " = cmulv(v" << r << ", f);\n";
@@ -338,9 +338,13 @@ struct Gen {
                  "(u >> 12); return u ^ (f & 7); }\n";
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
           << " *tables; const " << T << " *enc_table; int batch; int pad; };\n";
-        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", 2) " << name << "(const Args a) {\n";
+        // Double buffering: while tile t is transformed in one shared buffer,
+        // the cp.async copies of tile t + gridDim are already in flight into
+        // the other (one CTA per SM, 2 x 2^K amplitudes).
+        const bool dbuf = double_buffer;
+        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (dbuf ? 1 : 2) << ") " << name
+          << "(const Args a) {\n";
         o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
-        o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
         int next_max = 0;
         for (const HostGroup &g : ph.groups) {
             int ne = 0;
@@ -351,21 +355,42 @@ struct Gen {
         if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
         std::vector<int> hi(ph.tile_pos.begin() + L, ph.tile_pos.end());
         int tpr_log = static_cast<int>(ph.ext_pos.size());
-        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        // tile -> (row pointer, base offset) and the cp.async issue loop
+        o << "  auto tile_base = [&](u64 t, " << V << " *&st) -> u64 {\n";
         o << "    const int row = (int)(t >> " << tpr_log << ");\n";
         o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
-        o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
-        o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
+        o << "    st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
+        o << "    return " << scatter("tl", ph.ext_pos, true) << ";\n  };\n";
+        o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
+        o << "    " << V << " *st; const u64 tb = tile_base(t, st);\n";
         o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
         o << "      const int u = ch * " << apu << ";\n";
         o << "      const u64 g = tb + (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") + (u & "
           << ((1 << L) - 1) << ");\n";
-        o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&tile[swz(u)]);\n";
+        o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[swz(u)]);\n";
         o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&st[g]) : "
              "\"memory\");\n";
-        o << "    }\n";
-        o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+        o << "    }\n  };\n";
+        if (dbuf) {
+            o << "  int cur = 0;\n";
+            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
+            o << "  asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
+        }
+        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        if (dbuf) {
+            o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
+            o << "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" << V << " *)smem_raw + ((cur ^ 1) << "
+              << K << "));\n";
+            o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 1;\\n\" ::: \"memory\");\n";
+        } else {
+            o << "    " << V << " *tile = (" << V << " *)smem_raw;\n";
+            o << "    issue(t, tile);\n";
+            o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+        }
         o << "    __syncthreads();\n";
+        o << "    " << V << " *st; const u64 tb = tile_base(t, st);\n";
+        o << "    const int row = (int)(t >> " << tpr_log << ");\n";
+        o << "    (void)row;\n";
         o << "    const u64 pbase = a.rank_base | tb;\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
@@ -385,7 +410,15 @@ struct Gen {
             o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
             o << "      const int ub = " << scatter("s", ngt, false) << ";\n";
             o << "      const u64 pb = pbase | " << scatter("s", ngp, true) << ";\n";
-            (void)pb_unused;
+            // phase tables: issue the (L2-resident) loads before the gate math
+            for (int oi = g.op_begin; oi < g.op_end; ++oi) {
+                const HostOp &op = ph.ops[oi];
+                if (op.code != OP_FLUSH) continue;
+                for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti)
+                    if (ph.targets[ti].table >= 0)
+                        o << "      const " << V << " tab" << ti << " = a.tables[" << ph.targets[ti].table
+                          << " + s];\n";
+            }
             std::vector<int> uoff(NR, 0);
             for (int r = 0; r < NR; ++r)
                 for (int j = 0; j < R; ++j)
@@ -403,16 +436,21 @@ struct Gen {
         o << "      const float4 val = *(const float4 *)&tile[swz(u)];\n";
         o << "      asm volatile(\"st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\\n\" :: \"l\"(&st[g]), \"f\"(val.x), "
              "\"f\"(val.y), \"f\"(val.z), \"f\"(val.w) : \"memory\");\n";
-        o << "    }\n    __syncthreads();\n  }\n}\n";
+        o << "    }\n    __syncthreads();\n";
+        if (dbuf) o << "    cur ^= 1;\n";
+        o << "  }\n";
+        if (dbuf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+        o << "}\n";
         return o.str();
     }
-    int pb_unused = 0;
+    bool double_buffer = true;
 };
 
 } // namespace
 
-std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads) {
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf) {
     Gen g(ph, dtype);
+    g.double_buffer = dbuf;
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const int nchunks = (1 << ph.K) / (16 / amp);

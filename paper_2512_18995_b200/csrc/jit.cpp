@@ -23,7 +23,11 @@
 
 namespace qsv {
 
-std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads);
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf);
+bool double_buffer_enabled() {
+    const char *e = std::getenv("QSV_DBUF");
+    return !(e && e[0] == '0');
+}
 
 namespace {
 
@@ -108,7 +112,17 @@ std::vector<char> compile(const std::string &src, const std::string &key) {
     }
     Nvrtc *n = nvrtc();
     nvrtcProgram prog = nullptr;
-    if (n->CreateProgram(&prog, src.c_str(), (key + ".cu").c_str(), 0, nullptr, nullptr) != 0)
+    // the source goes next to the cubin and names the program, so -lineinfo
+    // points ncu (--import-source) at the generated code
+    const std::string dir0 = cache_dir();
+    mkdir((dir0.substr(0, dir0.rfind('/'))).c_str(), 0755);
+    mkdir(dir0.c_str(), 0755);
+    const std::string src_path = dir0 + "/" + key + ".cu";
+    {
+        std::ofstream f(src_path);
+        if (f) f << src;
+    }
+    if (n->CreateProgram(&prog, src.c_str(), src_path.c_str(), 0, nullptr, nullptr) != 0)
         fail(QSV_ERR_INTERNAL, "nvrtcCreateProgram failed");
     const char *opts[] = {"-arch=sm_100a", "-std=c++17", "-default-device", "-lineinfo", "--extra-device-vectorization"};
     const nvrtcResult rc = n->CompileProgram(prog, 5, opts);
@@ -153,7 +167,8 @@ struct JitKernel {
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     const std::string name = "qsv_pass";
     int threads = 256;
-    std::string src = generate_pass_source(ph, dtype, name, &threads);
+    const bool dbuf = double_buffer_enabled();
+    std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf);
     char key[32];
     std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
     std::vector<char> cubin = compile(src, key);
@@ -176,7 +191,7 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     const int amp = dtype == QSV_C64 ? 8 : 16;
     dp.jit = reinterpret_cast<const void *>(jk.kernel);
     dp.threads = threads;
-    dp.smem = static_cast<size_t>(amp) << ph.K;
+    dp.smem = (static_cast<size_t>(amp) << ph.K) * (dbuf ? 2 : 1);
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
@@ -193,7 +208,7 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
 // Source of a pass's specialised kernel (diagnostics / tests).
 std::string jit_source(const PassHost &ph, int dtype) {
     int threads = 0;
-    return generate_pass_source(ph, dtype, "qsv_pass", &threads);
+    return generate_pass_source(ph, dtype, "qsv_pass", &threads, double_buffer_enabled());
 }
 
 void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s) {

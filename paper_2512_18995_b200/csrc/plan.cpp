@@ -219,7 +219,7 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     } else {
         schedule_dist(*p, cfg);
     }
-    upload_plan(*p);
+    if (ctx->stream || ctx->device >= 0) upload_plan(*p); // dry runs (qsv_plan_dry) stay on the host
 }
 
 void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates,

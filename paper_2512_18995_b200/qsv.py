@@ -127,7 +127,23 @@ _SIGS = {
     "qsv_expect_pauli": (C.c_int, [_P, C.c_int, C.POINTER(qsv_obs), C.c_void_p]),
     "qsv_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
     "qsv_rng_fill": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int]),
+    "qsv_plan_dry": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.POINTER(qsv_opts),
+                               C.POINTER(qsv_plan_info), C.c_int, C.c_char_p, C.c_size_t]),
 }
+
+
+def plan_dry(nqubit: int, gates, dtype: int = C128, world: int = 1, opts: dict | None = None,
+             source_of_pass: int = -1) -> tuple[dict, str]:
+    """Host-only planning (no GPU): plan statistics and, optionally, the
+    generated CUDA source of one pass."""
+    arr, keep = gate_array(gates)
+    o = make_opts(opts)
+    info = qsv_plan_info()
+    cap = 8 << 20 if source_of_pass >= 0 else 0
+    buf = C.create_string_buffer(cap) if cap else None
+    check(lib().qsv_plan_dry(nqubit, dtype, world, arr, len(gates), C.byref(o), C.byref(info), source_of_pass, buf,
+                             cap))
+    return {f: getattr(info, f) for f, _ in qsv_plan_info._fields_}, (buf.value.decode() if buf else "")
 
 _lib = None
 
