@@ -100,7 +100,7 @@ typedef struct qsv_opts {
     int32_t no_fuse_1q;     /* 1 = keep runs of single-qubit gates unfused */
     int32_t no_phase_flush; /* 1 = apply every diagonal gate eagerly */
     int32_t jit;            /* 1 = specialised (NVRTC) pass kernels, -1 = interpreter, 0 = auto */
-    int32_t reserved;
+    int32_t reg_slots;      /* qubits per register group R (1..4; 0 = 3 for C128, 4 for C64) */
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */

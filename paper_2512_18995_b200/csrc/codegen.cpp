@@ -62,6 +62,15 @@ std::string scatter(const std::string &x, const std::vector<int> &pos, bool wide
     return o.str();
 }
 
+// One register set per thread per group (up to 512 threads: 2 CTAs x 16 warps
+// per SM), at least one 16-byte chunk per thread for the tile copies.
+int kernel_threads(const PassHost &ph, int dtype) {
+    const int nsets = 1 << (ph.K - ph.R);
+    const int nchunks = (1 << ph.K) / (dtype == QSV_C64 ? 2 : 1);
+    const int th = std::max(32, std::min(512, std::max(nsets, std::min(nchunks, 256))));
+    return (th + 31) / 32 * 32;
+}
+
 struct Gen {
     const PassHost &ph;
     bool f32;
@@ -300,8 +309,8 @@ struct Gen {
         const int NR = 1 << R;
         for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti) {
             const FlushTarget &t = ph.targets[ti];
-            o << ind << "{ " << V << " f = " << (t.eidx >= 0 ? "E[" + std::to_string(t.eidx) + "]" : "mk(1, 0)")
-              << ";\n";
+            o << ind << "{ " << V << " f = "
+              << (t.eidx >= 0 ? "E[" + std::to_string(ebase[cur_group] + t.eidx) + "]" : "mk(1, 0)") << ";\n";
             if (t.table >= 0) o << ind << "  f = cmulv(f, tab" << ti << ");\n";
             for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", "f", ind + "  ");
             for (int r = 0; r < NR; ++r)
@@ -319,7 +328,7 @@ struct Gen {
         const int apu = 16 / amp;
         const int nchunks = (1 << K) / apu;
         const int nsets = 1 << (K - R);
-        int threads = std::max(32, std::min(256, std::max(nsets, std::min(nchunks, 256))));
+        int threads = kernel_threads(ph, f32 ? QSV_C64 : QSV_C128);
         threads = (threads + 31) / 32 * 32;
         o << "// generated by qsv codegen.cpp: one fused tile pass\n";
         o << "typedef unsigned long long u64;\n";
@@ -345,12 +354,16 @@ struct Gen {
         o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (dbuf ? 1 : 2) << ") " << name
           << "(const Args a) {\n";
         o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+        // per-tile external phase factors of ALL groups get distinct slots
+        ebase.assign(ph.groups.size(), 0);
         int next_max = 0;
-        for (const HostGroup &g : ph.groups) {
+        for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
+            const HostGroup &g = ph.groups[gi];
             int ne = 0;
             for (int ti = g.tgt_begin; ti < g.tgt_end; ++ti)
                 if (ph.targets[ti].eidx >= 0) ne = std::max(ne, ph.targets[ti].eidx + 1);
-            next_max = std::max(next_max, ne);
+            ebase[gi] = next_max;
+            next_max += ne;
         }
         if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
         std::vector<int> hi(ph.tile_pos.begin() + L, ph.tile_pos.end());
@@ -385,26 +398,36 @@ struct Gen {
         } else {
             o << "    " << V << " *tile = (" << V << " *)smem_raw;\n";
             o << "    issue(t, tile);\n";
-            o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 0;\\n\" ::: \"memory\");\n";
+            o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
         }
-        o << "    __syncthreads();\n";
         o << "    " << V << " *st; const u64 tb = tile_base(t, st);\n";
         o << "    const int row = (int)(t >> " << tpr_log << ");\n";
         o << "    (void)row;\n";
         o << "    const u64 pbase = a.rank_base | tb;\n";
+        // external phase factors of every group, one per thread spread over
+        // the warps, while the tile copies are in flight
+        {
+            int k = 0;
+            const int nwarps = threads / 32;
+            for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
+                const HostGroup &g = ph.groups[gi];
+                for (int ti = g.tgt_begin; ti < g.tgt_end; ++ti) {
+                    const FlushTarget &t = ph.targets[ti];
+                    if (t.eidx < 0) continue;
+                    const int thr = (k % nwarps) * 32 + (k / nwarps) % 32;
+                    ++k;
+                    o << "    if (threadIdx.x == " << thr << ") {\n      " << V << " f = mk(1, 0);\n";
+                    for (int q = t.ext_begin; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", "      ");
+                    o << "      E[" << ebase[gi] + t.eidx << "] = f;\n    }\n";
+                }
+            }
+        }
+        o << "    asm volatile(\"cp.async.wait_group " << (dbuf ? 1 : 0) << ";\\n\" ::: \"memory\");\n";
+        o << "    __syncthreads();\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
+            cur_group = static_cast<int>(gi);
             o << "    // ---- group " << gi << "\n";
-            bool any_ext = false;
-            for (int ti = g.tgt_begin; ti < g.tgt_end; ++ti) {
-                const FlushTarget &t = ph.targets[ti];
-                if (t.eidx < 0) continue;
-                any_ext = true;
-                o << "    if (threadIdx.x == " << (t.eidx % threads) << ") {\n      " << V << " f = mk(1, 0);\n";
-                for (int k = t.ext_begin; k < t.ext_end; ++k) emit_rec_factor(ph.recs[k], "pbase", "f", "      ");
-                o << "      E[" << t.eidx << "] = f;\n    }\n";
-            }
-            if (any_ext) o << "    __syncthreads();\n";
             std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
             o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
@@ -444,6 +467,8 @@ struct Gen {
         return o.str();
     }
     bool double_buffer = true;
+    std::vector<int> ebase; // first E slot of each group
+    int cur_group = 0;
 };
 
 } // namespace
@@ -454,7 +479,9 @@ std::string generate_pass_source(const PassHost &ph, int dtype, const std::strin
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const int nchunks = (1 << ph.K) / (16 / amp);
-    int th = std::max(32, std::min(256, std::max(nsets, std::min(nchunks, 256))));
+    int th = kernel_threads(ph, dtype);
+    (void)nsets;
+    (void)nchunks;
     *threads = (th + 31) / 32 * 32;
     return g.source(name);
 }
