@@ -339,6 +339,18 @@ struct Gen {
           << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
         o << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
           << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
+        // streaming (evict-first) 8/16-byte amplitude loads and stores
+        if (f32) {
+            o << "static __device__ __forceinline__ cf ldcs(const cf *p) { cf r; asm volatile(\"ld.global.cs.v2.f32 "
+                 "{%0,%1}, [%2];\" : \"=f\"(r.x), \"=f\"(r.y) : \"l\"(p)); return r; }\n";
+            o << "static __device__ __forceinline__ void stcs(cf *p, cf v) { asm volatile(\"st.global.cs.v2.f32 "
+                 "[%0], {%1,%2};\" :: \"l\"(p), \"f\"(v.x), \"f\"(v.y) : \"memory\"); }\n";
+        } else {
+            o << "static __device__ __forceinline__ cd ldcs(const cd *p) { cd r; asm volatile(\"ld.global.cs.v2.f64 "
+                 "{%0,%1}, [%2];\" : \"=d\"(r.x), \"=d\"(r.y) : \"l\"(p)); return r; }\n";
+            o << "static __device__ __forceinline__ void stcs(cd *p, cd v) { asm volatile(\"st.global.cs.v2.f64 "
+                 "[%0], {%1,%2};\" :: \"l\"(p), \"d\"(v.x), \"d\"(v.y) : \"memory\"); }\n";
+        }
         if (f32)
             o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; const int f = (w >> 3) ^ "
                  "(w >> 6) ^ (w >> 9) ^ (w >> 12); return ((w ^ (f & 7)) << 1) | (u & 1); }\n";
@@ -368,41 +380,24 @@ struct Gen {
         if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
         std::vector<int> hi(ph.tile_pos.begin() + L, ph.tile_pos.end());
         int tpr_log = static_cast<int>(ph.ext_pos.size());
-        // tile -> (row pointer, base offset) and the cp.async issue loop
-        o << "  auto tile_base = [&](u64 t, " << V << " *&st) -> u64 {\n";
-        o << "    const int row = (int)(t >> " << tpr_log << ");\n";
-        o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
-        o << "    st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
-        o << "    return " << scatter("tl", ph.ext_pos, true) << ";\n  };\n";
-        o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
-        o << "    " << V << " *st; const u64 tb = tile_base(t, st);\n";
-        o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
-        o << "      const int u = ch * " << apu << ";\n";
-        o << "      const u64 g = tb + (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") + (u & "
-          << ((1 << L) - 1) << ");\n";
-        o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[swz(u)]);\n";
-        o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&st[g]) : "
-             "\"memory\");\n";
-        o << "    }\n  };\n";
-        if (dbuf) {
-            o << "  int cur = 0;\n";
-            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
-            o << "  asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
-        }
+        // The first group reads its register sets straight from HBM and the
+        // last group writes them straight back; only the groups in between
+        // exchange amplitudes through the shared-memory tile. A one-group pass
+        // is a pure streaming kernel.
+        (void)dbuf;
+        (void)hi;
+        (void)apu;
+        (void)nchunks;
+        const int G = static_cast<int>(ph.groups.size());
+        const bool any_e = next_max > 0;
+        o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
+        o << "  (void)tile;\n";
         o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
-        if (dbuf) {
-            o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
-            o << "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" << V << " *)smem_raw + ((cur ^ 1) << "
-              << K << "));\n";
-            o << "    asm volatile(\"cp.async.commit_group;\\ncp.async.wait_group 1;\\n\" ::: \"memory\");\n";
-        } else {
-            o << "    " << V << " *tile = (" << V << " *)smem_raw;\n";
-            o << "    issue(t, tile);\n";
-            o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
-        }
-        o << "    " << V << " *st; const u64 tb = tile_base(t, st);\n";
         o << "    const int row = (int)(t >> " << tpr_log << ");\n";
         o << "    (void)row;\n";
+        o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
+        o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
+        o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
         o << "    const u64 pbase = a.rank_base | tb;\n";
         // external phase factors of every group, one per thread spread over
         // the warps, while the tile copies are in flight
@@ -422,17 +417,20 @@ struct Gen {
                 }
             }
         }
-        o << "    asm volatile(\"cp.async.wait_group " << (dbuf ? 1 : 0) << ";\\n\" ::: \"memory\");\n";
-        o << "    __syncthreads();\n";
+        if (any_e) o << "    __syncthreads();\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
             cur_group = static_cast<int>(gi);
+            const bool from_hbm = gi == 0, to_hbm = static_cast<int>(gi) == G - 1;
             o << "    // ---- group " << gi << "\n";
             std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
             o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
             o << "      const int ub = " << scatter("s", ngt, false) << ";\n";
-            o << "      const u64 pb = pbase | " << scatter("s", ngp, true) << ";\n";
+            o << "      const u64 ls = " << scatter("s", ngp, true) << ";\n";
+            o << "      const u64 pb = pbase | ls;\n";
+            o << "      const u64 gb = tb | ls;\n";
+            o << "      (void)ub; (void)gb;\n";
             // phase tables: issue the (L2-resident) loads before the gate math
             for (int oi = g.op_begin; oi < g.op_end; ++oi) {
                 const HostOp &op = ph.ops[oi];
@@ -443,26 +441,29 @@ struct Gen {
                           << " + s];\n";
             }
             std::vector<int> uoff(NR, 0);
+            std::vector<uint64_t> poff(NR, 0); // physical offsets of the register amplitudes
             for (int r = 0; r < NR; ++r)
                 for (int j = 0; j < R; ++j)
-                    if ((r >> j) & 1) uoff[r] |= 1 << g.slot_bit[j];
-            for (int r = 0; r < NR; ++r)
-                o << "      " << V << " v" << r << " = tile[swz(ub | " << uoff[r] << ")];\n";
+                    if ((r >> j) & 1) {
+                        uoff[r] |= 1 << g.slot_bit[j];
+                        poff[r] |= 1ull << ph.tile_pos[g.slot_bit[j]];
+                    }
+            for (int r = 0; r < NR; ++r) {
+                if (from_hbm)
+                    o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
+                else o << "      " << V << " v" << r << " = tile[swz(ub | " << uoff[r] << ")];\n";
+            }
             for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
-            for (int r = 0; r < NR; ++r) o << "      tile[swz(ub | " << uoff[r] << ")] = v" << r << ";\n";
-            o << "      (void)pb;\n    }\n    __syncthreads();\n";
+            for (int r = 0; r < NR; ++r) {
+                if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
+                else o << "      tile[swz(ub | " << uoff[r] << ")] = v" << r << ";\n";
+            }
+            o << "      (void)pb;\n    }\n";
+            if (!to_hbm) o << "    __syncthreads();\n";
         }
-        o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
-        o << "      const int u = ch * " << apu << ";\n";
-        o << "      const u64 g = tb + (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") + (u & "
-          << ((1 << L) - 1) << ");\n";
-        o << "      const float4 val = *(const float4 *)&tile[swz(u)];\n";
-        o << "      asm volatile(\"st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};\\n\" :: \"l\"(&st[g]), \"f\"(val.x), "
-             "\"f\"(val.y), \"f\"(val.z), \"f\"(val.w) : \"memory\");\n";
-        o << "    }\n    __syncthreads();\n";
-        if (dbuf) o << "    cur ^= 1;\n";
+        // the next tile's first group rewrites the shared tile / E
+        if (G >= 2 || any_e) o << "    __syncthreads();\n";
         o << "  }\n";
-        if (dbuf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
         o << "}\n";
         return o.str();
     }

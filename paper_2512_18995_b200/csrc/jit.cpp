@@ -191,7 +191,9 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     const int amp = dtype == QSV_C64 ? 8 : 16;
     dp.jit = reinterpret_cast<const void *>(jk.kernel);
     dp.threads = threads;
-    dp.smem = (static_cast<size_t>(amp) << ph.K) * (dbuf ? 2 : 1);
+    // groups between the first (loads from HBM) and the last (stores to HBM)
+    // exchange amplitudes through a shared tile; a one-group pass needs none
+    dp.smem = ph.groups.size() >= 2 ? (static_cast<size_t>(amp) << ph.K) : 0;
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
