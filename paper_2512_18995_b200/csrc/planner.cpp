@@ -391,6 +391,15 @@ struct GroupLowering {
                 const bool real = g.m[0].imag() == 0 && g.m[1].imag() == 0 && g.m[2].imag() == 0 &&
                                   g.m[3].imag() == 0;
                 if (real) op.code = OP_DENSE1R;
+                // c * (+-1 entries), e.g. h: apply the +-1 butterfly and defer c to
+                // one scale per pass (scalars commute with every gate)
+                const double c = std::abs(g.m[0].real());
+                if (real && c != 0.0 && c != 1.0 && !(op.flags & OPF_ZERO_OFF_CONTROL) && op.rmask == 0 &&
+                    op.fmask == 0 && std::abs(g.m[1].real()) == c && std::abs(g.m[2].real()) == c &&
+                    std::abs(g.m[3].real()) == c) {
+                    for (auto &x : op.pay) x /= c;
+                    ph.scale *= c;
+                }
                 if (g.m[0] == cplx(0, 0) && g.m[3] == cplx(0, 0) && g.m[1] == cplx(1, 0) && g.m[2] == cplx(1, 0) &&
                     !(op.flags & OPF_ZERO_OFF_CONTROL)) {
                     op.code = OP_X1;
@@ -466,6 +475,25 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
         hg.op_end = static_cast<int>(ph.ops.size());
         hg.tgt_end = static_cast<int>(ph.targets.size());
         ph.groups.push_back(hg);
+    }
+    if (ph.scale != 1.0) {
+        // the deferred butterfly normalisation: one real scale on every
+        // amplitude, folded into the last group's closing register table
+        HostGroup &last = ph.groups.back();
+        HostOp *fl = nullptr;
+        if (last.op_end > last.op_begin && ph.ops[last.op_end - 1].code == OP_FLUSH) fl = &ph.ops[last.op_end - 1];
+        if (!fl) {
+            HostOp op;
+            op.code = OP_FLUSH;
+            op.flush.tgt_begin = op.flush.tgt_end = static_cast<int>(ph.targets.size());
+            ph.ops.push_back(std::move(op));
+            last.op_end = static_cast<int>(ph.ops.size());
+            fl = &ph.ops.back();
+        }
+        if (fl->regtab.empty()) fl->regtab.assign(1u << R, cplx(1, 0));
+        for (auto &x : fl->regtab) x *= ph.scale;
+        fl->flush.regmask = (1u << (1u << R)) - 1;
+        ph.scale = 1.0;
     }
     return ph;
 }

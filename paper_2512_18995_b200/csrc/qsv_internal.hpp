@@ -190,6 +190,7 @@ struct PassHost {
     std::vector<DiagRec> recs;
     std::vector<cplx> tables;
     int ngates = 0;                   // gates in this pass (after 1q fusion)
+    double scale = 1.0;               // deferred real scale (butterfly normalisation)
 };
 // Serialised pass program for dtype.
 std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int *off_targets, int *off_recs,
