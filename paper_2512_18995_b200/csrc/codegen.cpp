@@ -13,6 +13,7 @@
 //   * deferred phases (planner.cpp GroupLowering) keep their split: per-tile
 //     EXT factors in shared memory, TILE tables in global memory, MIXED
 //     records as inline predicated multiplies, register tables as constants.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <sstream>
@@ -358,7 +359,7 @@ struct Gen {
             o << "static __device__ __forceinline__ int swz(int u) { const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ "
                  "(u >> 12); return u ^ (f & 7); }\n";
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
-          << " *tables; const " << T << " *enc_table; int batch; int pad; };\n";
+          << " *tables; const " << T << " *enc_table; int batch; int pad; void *out; };\n";
         // Double buffering: while tile t is transformed in one shared buffer,
         // the cp.async copies of tile t + gridDim are already in flight into
         // the other (one CTA per SM, 2 x 2^K amplitudes).
@@ -389,6 +390,7 @@ struct Gen {
         (void)apu;
         (void)nchunks;
         const int G = static_cast<int>(ph.groups.size());
+        const bool permuted = !ph.out_perm.empty();
         const bool any_e = next_max > 0;
         o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
         o << "  (void)tile;\n";
@@ -421,7 +423,7 @@ struct Gen {
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
             cur_group = static_cast<int>(gi);
-            const bool from_hbm = gi == 0, to_hbm = static_cast<int>(gi) == G - 1;
+            const bool from_hbm = gi == 0, to_hbm = static_cast<int>(gi) == G - 1 && !permuted;
             o << "    // ---- group " << gi << "\n";
             std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
@@ -461,8 +463,26 @@ struct Gen {
             o << "      (void)pb;\n    }\n";
             if (!to_hbm) o << "    __syncthreads();\n";
         }
+        if (permuted) {
+            // out-of-place copy-out in OUTPUT order: w enumerates the tile's
+            // output bit positions ascending (the L lowest output bits first,
+            // so the writes are contiguous runs); u is the same amplitude's
+            // input tile index.
+            std::vector<std::pair<int, int>> q; // (output position, input tile bit)
+            for (int i = 0; i < K; ++i) q.emplace_back(ph.out_perm[ph.tile_pos[i]], i);
+            std::sort(q.begin(), q.end());
+            std::vector<int> w2u, w2out, ext_out;
+            for (auto &pr : q) w2out.push_back(pr.first), w2u.push_back(pr.second);
+            for (int e : ph.ext_pos) ext_out.push_back(ph.out_perm[e]);
+            o << "    {\n      " << V << " *dst = (" << V << " *)a.out + (u64)row * a.row_stride;\n";
+            o << "      const u64 tbo = " << scatter("tl", ext_out, true) << ";\n";
+            o << "      for (int w = threadIdx.x; w < " << (1 << K) << "; w += " << threads << ") {\n";
+            o << "        const int u = " << scatter("w", w2u, false) << ";\n";
+            o << "        stcs(&dst[tbo | " << scatter("w", w2out, true) << "], tile[swz(u)]);\n";
+            o << "      }\n    }\n";
+        }
         // the next tile's first group rewrites the shared tile / E
-        if (G >= 2 || any_e) o << "    __syncthreads();\n";
+        if (G >= 2 || any_e || permuted) o << "    __syncthreads();\n";
         o << "  }\n";
         o << "}\n";
         return o.str();

@@ -193,7 +193,7 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     dp.threads = threads;
     // groups between the first (loads from HBM) and the last (stores to HBM)
     // exchange amplitudes through a shared tile; a one-group pass needs none
-    dp.smem = ph.groups.size() >= 2 ? (static_cast<size_t>(amp) << ph.K) : 0;
+    dp.smem = (ph.groups.size() >= 2 || !ph.out_perm.empty()) ? (static_cast<size_t>(amp) << ph.K) : 0;
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
@@ -213,7 +213,7 @@ std::string jit_source(const PassHost &ph, int dtype) {
     return generate_pass_source(ph, dtype, "qsv_pass", &threads, double_buffer_enabled());
 }
 
-void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s) {
+void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s) {
     struct JArgs {
         void *state;
         uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
@@ -221,8 +221,10 @@ void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s) {
         const void *enc_table;
         int batch;
         int pad;
+        void *out;
     } a{};
     a.state = state;
+    a.out = out;
     a.row_stride = dp.args.row_stride;
     a.rank_base = dp.args.rank_base;
     a.tiles_per_row = dp.args.tiles_per_row;

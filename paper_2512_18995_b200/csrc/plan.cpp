@@ -26,7 +26,10 @@ Ctx::~Ctx() {
 
 State::~State() {
     if (d) cudaFree(d);
+    if (scratch) cudaFree(scratch);
 }
+
+bool plan_uses_jit(const Plan &p);
 
 Plan::~Plan() {
     cudaFree(d_blob);
@@ -209,8 +212,19 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
     if (ctx->world == 1) {
+        // swaps as relabelings, the final layout folded into the last pass
+        const bool relabel = cfg.fuse && p->opts.no_relabel == 0 && plan_uses_jit(*p) && p->nslots == 0;
+        std::vector<GateRec> gl = p->gates;
+        std::vector<int> phys = p->perm_in, out_perm;
+        if (relabel) {
+            std::vector<int> fin;
+            gl = relabel_swaps(p->gates, p->perm_in, fin);
+            for (int b = 0; b < n; ++b) phys[b] = b; // gates now name physical bits
+            out_perm.assign(n, 0);
+            for (int w = 0; w < n; ++w) out_perm[fin[w]] = p->perm_in[w];
+        }
         if (!p->gates.empty()) {
-            auto passes = plan_passes(p->gates, p->perm_in, cfg, p->encs);
+            auto passes = plan_passes(gl, phys, cfg, p->encs, out_perm);
             for (auto &ph : passes) {
                 Step s;
                 s.pass = static_cast<int>(p->passes.size());
@@ -233,6 +247,28 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
     int cursor = 0;
     for (int i = 0; i < ngates; ++i) recs.push_back(resolve_gate(gates[i], n, &cursor));
     build_plan(p, ctx, n, dtype, std::move(recs), cursor, opts);
+}
+
+bool plan_uses_jit(const Plan &p) {
+    return p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
+}
+
+void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s) {
+    if (!dp.out_of_place) {
+        launch_pass(dp, dtype, st.d, st.batch, s);
+        return;
+    }
+    if (!st.scratch) {
+        const size_t bytes = st.local_amps * st.amp_bytes() * static_cast<size_t>(st.batch);
+        if (cudaMalloc(&st.scratch, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            st.scratch = nullptr;
+            fail(QSV_ERR_INTERNAL, "out-of-place pass: cannot allocate the scratch state (" + std::to_string(bytes) +
+                                       " bytes); plan with opts.no_relabel = 1");
+        }
+    }
+    launch_jit(dp, st.d, st.scratch, st.batch, s);
+    std::swap(st.d, st.scratch);
 }
 
 void upload_plan(Plan &p) {
@@ -307,7 +343,9 @@ void upload_plan(Plan &p) {
         require(dp.smem + 1024 <= p.ctx->smem_optin || p.ctx->smem_optin == 0,
                 "plan: pass program does not fit in shared memory");
         dp.grid = std::max(1, tile_kernel_blocks_per_sm(p.dtype, dp.R, dp.threads, dp.smem)) * p.ctx->sm_count;
-        const bool use_jit = p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
+        const bool use_jit = plan_uses_jit(p);
+        dp.out_of_place = !ph.out_perm.empty();
+        require(!dp.out_of_place || use_jit, "plan: permuting passes need the specialised kernels");
         if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
         dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
         dp.ngates = ph.ngates;
@@ -350,7 +388,7 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots) {
             DevPass dp = p.dev[stp.pass];
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
-            launch_pass(dp, p.dtype, st.d, st.batch, s);
+            run_pass(dp, p.dtype, st, s);
         } else {
             dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         }
@@ -366,7 +404,7 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
     size_t k = 0;
     for (const Step &stp : p.steps) {
         QSV_CUDA(cudaEventRecord(ev[2 * k], s));
-        if (stp.kind == 0) launch_pass(p.dev[stp.pass], p.dtype, st.d, st.batch, s);
+        if (stp.kind == 0) run_pass(p.dev[stp.pass], p.dtype, st, s);
         else dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         QSV_CUDA(cudaEventRecord(ev[2 * k + 1], s));
         ++k;

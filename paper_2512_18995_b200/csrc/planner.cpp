@@ -445,6 +445,13 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
     for (int i = 0; i < K; ++i) tile_of_phys[ph.tile_pos[i]] = i;
     std::vector<int> gorder = took;
     ph.ngates = static_cast<int>(gorder.size());
+    if (gorder.empty()) { // permutation-only pass: one empty group moves the data
+        HostGroup hg;
+        int j = 0;
+        for (int t = K - 1; t >= K - R; --t) hg.slot_bit[j++] = t;
+        for (int t = 0; t < K - R; ++t) hg.ng_bit[t] = t;
+        ph.groups.push_back(hg);
+    }
     while (!gorder.empty()) {
         uint64_t gact = 0;
         std::vector<int> gtook = admit(gorder, pg, gact, R, active);
@@ -587,7 +594,10 @@ std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int 
 }
 
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const std::vector<int> &phys,
-                                  const PlanConfig &cfg, std::vector<EncDesc> &encs) {
+                                  const PlanConfig &cfg, std::vector<EncDesc> &encs,
+                                  const std::vector<int> &out_perm) {
+    std::vector<int> last_took;
+    uint64_t last_active = 0;
     const int nl = cfg.nlocal;
     const int K = std::min(cfg.K, nl);
     const int L = std::min(cfg.L, K);
@@ -643,8 +653,56 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         }
         passes.push_back(std::move(ph));
+        last_took = took;
+        last_active = active;
+    }
+    // Final layout permutation: folded into the last pass when its tile can
+    // also hold the input bits that land on the L lowest output bits
+    // (coalesced permuted writes), else one extra permutation-only pass.
+    bool ident = true;
+    for (size_t b = 0; b < out_perm.size(); ++b) ident = ident && out_perm[b] == static_cast<int>(b);
+    if (!ident) {
+        uint64_t need = 0;
+        for (int b = 0; b < nl; ++b)
+            if (out_perm[b] < L) need |= 1ull << b;
+        bool done = false;
+        if (!passes.empty() && std::popcount(last_active | need) <= K) {
+            const size_t first_encs = encs.size();
+            (void)first_encs;
+            PassHost ph = lower_pass(gates, pg, last_took, last_active | need, phys, cfg, K, L, R, encs);
+            // the re-lowered pass re-registered its encoded gates: drop the old ones
+            if (pass_program_bytes(ph, cfg.dtype) <= static_cast<size_t>(kProgramBudget)) {
+                ph.out_perm = out_perm;
+                passes.back() = std::move(ph);
+                done = true;
+            }
+        }
+        if (!done) {
+            PassHost ph = lower_pass(gates, pg, {}, lowmask | need, phys, cfg, K, L, R, encs);
+            ph.out_perm = out_perm;
+            passes.push_back(std::move(ph));
+        }
     }
     return passes;
+}
+
+std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &gates, const std::vector<int> &phys_in,
+                                   std::vector<int> &final_phys) {
+    std::vector<int> phys = phys_in;
+    std::vector<GateRec> out;
+    out.reserve(gates.size());
+    for (const GateRec &g : gates) {
+        if (g.kind == GK_SWAP && g.k == 2 && g.ctls.empty() && !g.encoded && g.flags == 0) {
+            std::swap(phys[g.wires[0]], phys[g.wires[1]]);
+            continue;
+        }
+        GateRec p = g;
+        for (int t = 0; t < g.k; ++t) p.wires[t] = phys[g.wires[t]];
+        for (int &c : p.ctls) c = phys[c];
+        out.push_back(std::move(p));
+    }
+    final_phys = phys;
+    return out;
 }
 
 } // namespace qsv

@@ -191,6 +191,9 @@ struct PassHost {
     std::vector<cplx> tables;
     int ngates = 0;                   // gates in this pass (after 1q fusion)
     double scale = 1.0;               // deferred real scale (butterfly normalisation)
+    // Output bit permutation (input physical bit -> output physical bit);
+    // empty = identity. A permuting pass writes out of place (State::scratch).
+    std::vector<int> out_perm;
 };
 // Serialised pass program for dtype.
 std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int *off_targets, int *off_recs,
@@ -216,6 +219,7 @@ struct State {
     int n = 0, nlocal = 0, batch = 1, dtype = QSV_C128;
     uint64_t local_amps = 0;
     void *d = nullptr;          // batch * local_amps amplitudes
+    void *scratch = nullptr;    // same size; target of out-of-place (permuting) passes
     std::vector<int> perm;      // logical wire -> physical bit (>= nlocal: rank bit)
     size_t amp_bytes() const { return dtype == QSV_C64 ? 8 : 16; }
     ~State();
@@ -228,6 +232,7 @@ struct DevPass {
     size_t smem = 0;
     int grid = 0;               // persistent CTAs (occupancy x SMs)
     const void *jit = nullptr;  // specialised kernel (cudaKernel_t), else the interpreter
+    bool out_of_place = false;  // writes State::scratch (bit-permuting pass)
     int jit_regs = 0, jit_spill = 0;
     double bytes = 0;
     int ngates = 0;
@@ -269,26 +274,34 @@ struct PlanConfig {
     bool phase_flush = true;  // lazy phase factors for diagonal gates
     int dtype = QSV_C128;
 };
+// Swap gates as qubit relabelings: rewrites `gates` onto physical bits (the
+// returned gates' wires ARE physical bits), dropping uncontrolled swaps and
+// tracking the layout; `final_phys` receives the layout after the last gate.
+std::vector<GateRec> relabel_swaps(const std::vector<GateRec> &gates, const std::vector<int> &phys_in,
+                                   std::vector<int> &final_phys);
 // Host-side gate fusion: runs of uncontrolled, non-encoded single-qubit gates
 // on the same wire (nothing else touching it in between) become one matrix.
 std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates);
 // Lowers gates (wires mapped to PHYSICAL bits by phys_of_wire; every
 // non-diagonal target local) to tile passes.
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys_of_wire,
-                                  const PlanConfig &cfg, std::vector<EncDesc> &encs);
+                                  const PlanConfig &cfg, std::vector<EncDesc> &encs,
+                                  const std::vector<int> &out_perm = {});
 int default_tile_bits(int dtype, int nlocal);
 int default_low_bits(int dtype, int nlocal);
 
 // ---- device launchers (engine.cu) -----------------------------------------
 void upload_plan(Plan &p);
 void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s);
+// Runs one pass on `st`; an out-of-place pass writes State::scratch and swaps it in.
+void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s);
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
 int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
 // ---- pass specialisation (codegen.cpp, jit.cpp) ----------------------------
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
-void launch_jit(const DevPass &dp, void *state, int rows, cudaStream_t s);
+void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s);
 std::string jit_source(const PassHost &ph, int dtype);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);

@@ -411,7 +411,7 @@ int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem) {
 
 void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s) {
     if (dp.jit) {
-        launch_jit(dp, state, rows, s);
+        launch_jit(dp, state, state, rows, s);
         return;
     }
     PassArgs a = dp.args;

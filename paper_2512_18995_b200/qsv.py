@@ -78,7 +78,8 @@ class qsv_obs(C.Structure):
 
 class qsv_opts(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_bits", C.c_int32), ("low_bits", C.c_int32), ("use_graph", C.c_int32),
-                ("no_fuse_1q", C.c_int32), ("no_phase_flush", C.c_int32), ("jit", C.c_int32), ("reg_slots", C.c_int32)]
+                ("no_fuse_1q", C.c_int32), ("no_phase_flush", C.c_int32), ("jit", C.c_int32), ("reg_slots", C.c_int32),
+                ("no_relabel", C.c_int32), ("reserved", C.c_int32 * 3)]
 
 
 class qsv_plan_info(C.Structure):

@@ -269,6 +269,25 @@ def test_cfg3_qft_reduced_vs_reference():
         assert np.max(np.abs(s.amplitudes() - want)) <= 1e-12, n
 
 
+@pytest.mark.parametrize("opts", [{"jit": 1}, {"jit": 1, "no_relabel": 1}, {"jit": 1, "tile_bits": 9, "low_bits": 2},
+                                  {"jit": 1, "tile_bits": 12, "low_bits": 4}])
+def test_swaps_as_relabelings_match_reference(opts):
+    # swap gates become layout permutations folded into the last pass (out of
+    # place); the downloaded state must still be in logical order
+    rng = Rng(23, "relabel")
+    for n in (11, 17):
+        cir = random_circuit(rng, n, 80)
+        for i in range(n // 2):
+            cir.swap(i, n - 1 - i)
+        psi = random_state(rng, n)
+        got, st = run(n, cir.gates(), init=psi, opts=opts)
+        want = O.port_forward(n, cir.gates(), init=psi)[0]
+        assert np.max(np.abs(got[0] - want)) <= 1e-12, (n, opts)
+        z = st.expect_z_all()[0]
+        for q in (0, n - 1):
+            assert abs(z[q] - O.port_expectation(n, want, [q], "z")[0]) <= 1e-12
+
+
 def test_qft_of_zero_is_uniform_24q():  # test_dist.cpp:147-160 scaled
     n = 24
     s = qsv.qft_circuit(n).forward()
