@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <sstream>
 #include <string>
 
@@ -313,6 +314,11 @@ struct Gen {
             o << ind << "{ " << V << " f = "
               << (t.eidx >= 0 ? "E[" + std::to_string(ebase[cur_group] + t.eidx) + "]" : "mk(1, 0)") << ";\n";
             if (t.table >= 0) o << ind << "  f = cmulv(f, tab" << ti << ");\n";
+            if (t.table_lo >= 0)
+                o << ind << "  f = cmulv(f, stab[" << stab_off.at(t.table_lo) << " + (s & " << ((1 << t.lo_bits) - 1)
+                  << ")]);\n";
+            if (t.table_hi >= 0)
+                o << ind << "  f = cmulv(f, stab[" << stab_off.at(t.table_hi) << " + (s >> " << t.lo_bits << ")]);\n";
             for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", "f", ind + "  ");
             for (int r = 0; r < NR; ++r)
                 if (t.slot < 0 || ((r >> t.slot) & 1)) o << ind << "  v" << r << " = cmulv(v" << r << ", f);\n";
@@ -379,6 +385,27 @@ struct Gen {
             next_max += ne;
         }
         if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
+        // separable phase tables (low / high set-index bits) live in shared memory
+        {
+            std::vector<std::pair<int, int>> ranges; // (global offset, length)
+            for (const FlushTarget &t : ph.targets) {
+                const int nb = ph.K - ph.R;
+                if (t.table_lo >= 0) ranges.emplace_back(t.table_lo, 1 << t.lo_bits);
+                if (t.table_hi >= 0) ranges.emplace_back(t.table_hi, 1 << (nb - t.lo_bits));
+            }
+            int total = 0;
+            for (auto &r : ranges) {
+                stab_off[r.first] = total;
+                total += r.second;
+            }
+            if (total) {
+                o << "  __shared__ " << V << " stab[" << total << "];\n";
+                for (auto &r : ranges)
+                    o << "  for (int i = threadIdx.x; i < " << r.second << "; i += " << threads << ") stab["
+                      << stab_off[r.first] << " + i] = a.tables[" << r.first << " + i];\n";
+                o << "  __syncthreads();\n";
+            }
+        }
         std::vector<int> hi(ph.tile_pos.begin() + L, ph.tile_pos.end());
         int tpr_log = static_cast<int>(ph.ext_pos.size());
         // The first group reads its register sets straight from HBM and the
@@ -490,6 +517,7 @@ struct Gen {
     bool double_buffer = true;
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
+    std::map<int, int> stab_off; // global table offset -> shared-memory offset
 };
 
 } // namespace

@@ -204,18 +204,36 @@ struct GroupLowering {
         t.mix_begin = static_cast<int>(ph.recs.size());
         ph.recs.insert(ph.recs.end(), mix.begin(), mix.end());
         t.mix_end = static_cast<int>(ph.recs.size());
-        if (!tile.empty()) {
-            const int nset = 1 << ng_phys.size();
-            t.table = static_cast<int>(ph.tables.size());
-            for (int s = 0; s < nset; ++s) {
+        // tile records split by the set-index bits they read: low bits only,
+        // high bits only (two small separable tables), or both (full table)
+        const int nbits = static_cast<int>(ng_phys.size());
+        const int lo_bits = std::min(5, nbits);
+        uint64_t lomask = 0;
+        for (int i = 0; i < lo_bits; ++i) lomask |= 1ull << ng_phys[i];
+        std::vector<DiagRec> lo, hi, full;
+        for (const DiagRec &r : tile) {
+            const uint64_t d = rec_deps(r);
+            if ((d & ~lomask) == 0) lo.push_back(r);
+            else if ((d & lomask) == 0) hi.push_back(r);
+            else full.push_back(r);
+        }
+        auto make_table = [&](const std::vector<DiagRec> &rs, int first_bit, int bits) {
+            const int off = static_cast<int>(ph.tables.size());
+            for (int s = 0; s < (1 << bits); ++s) {
                 uint64_t pb = 0;
-                for (size_t i = 0; i < ng_phys.size(); ++i)
-                    if ((s >> i) & 1) pb |= 1ull << ng_phys[i];
+                for (int i = 0; i < bits; ++i)
+                    if ((s >> i) & 1) pb |= 1ull << ng_phys[first_bit + i];
                 cplx f(1, 0);
-                for (const DiagRec &r : tile) f *= eval_rec(r, pb);
+                for (const DiagRec &r : rs) f *= eval_rec(r, pb);
                 ph.tables.push_back(f);
             }
-        }
+            return off;
+        };
+        t.table_lo = t.table_hi = -1;
+        t.lo_bits = lo_bits;
+        if (!full.empty()) t.table = make_table(full, 0, nbits);
+        if (!lo.empty()) t.table_lo = make_table(lo, 0, lo_bits);
+        if (!hi.empty()) t.table_hi = make_table(hi, lo_bits, nbits - lo_bits);
         ph.targets.push_back(t);
         return 1;
     }

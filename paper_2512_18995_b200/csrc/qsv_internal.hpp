@@ -94,7 +94,9 @@ struct alignas(16) FlushTarget {
     int32_t ext_begin, ext_end;
     int32_t mix_begin, mix_end;
     int32_t eidx;           // index into the CTA's shared E array, or -1
-    int32_t pad;
+    // separable part of the tile records: table_lo[s & lo_mask] * table_hi[s >> lo_bits]
+    int32_t table_lo, table_hi, lo_bits;
+    int32_t pad[2];
 };
 
 struct alignas(16) GroupDesc {

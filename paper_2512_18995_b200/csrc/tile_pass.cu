@@ -191,6 +191,8 @@ __device__ __forceinline__ void flush_op(typename Vec2<T>::type (&v)[1 << R], co
         const FlushTarget ft = c.targets[ti];
         V f = ft.eidx >= 0 ? c.E[ft.eidx] : V{1, 0};
         if (ft.table >= 0) f = cmul(f, __ldg(c.tables + ft.table + c.s));
+        if (ft.table_lo >= 0) f = cmul(f, __ldg(c.tables + ft.table_lo + (c.s & ((1 << ft.lo_bits) - 1))));
+        if (ft.table_hi >= 0) f = cmul(f, __ldg(c.tables + ft.table_hi + (c.s >> ft.lo_bits)));
         for (int k = ft.mix_begin; k < ft.mix_end; ++k) f = cmul(f, eval_rec<V>(c.recs[k], c.pb));
         switch (ft.slot) {
         case -1:
