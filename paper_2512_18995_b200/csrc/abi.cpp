@@ -520,7 +520,49 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
                 }
             }
         }
-        if (src && cap) {
+        if (src && cap && pass_index == -2) { // the whole step schedule as JSON
+            std::string js = "{\"n\":" + std::to_string(p.n) + ",\"nlocal\":" + std::to_string(p.nlocal) +
+                             ",\"steps\":[";
+            char num[64];
+            auto dbl = [&](double v) {
+                std::snprintf(num, sizeof num, "%.17g", v);
+                return std::string(num);
+            };
+            for (size_t si = 0; si < p.steps.size(); ++si) {
+                const Step &s = p.steps[si];
+                if (si) js += ",";
+                if (s.kind == 1) {
+                    js += "{\"kind\":\"swap\",\"pairs\":[";
+                    for (size_t k = 0; k < s.swap_bits.size(); ++k)
+                        js += (k ? ",[" : "[") + std::to_string(s.swap_bits[k].first) + "," +
+                              std::to_string(s.swap_bits[k].second) + "]";
+                    js += "]}";
+                    continue;
+                }
+                const PassHost &ph = p.passes[s.pass];
+                js += "{\"kind\":\"pass\",\"tile\":[";
+                for (size_t k = 0; k < ph.tile_pos.size(); ++k) js += (k ? "," : "") + std::to_string(ph.tile_pos[k]);
+                js += "],\"out_perm\":[";
+                for (size_t k = 0; k < ph.out_perm.size(); ++k) js += (k ? "," : "") + std::to_string(ph.out_perm[k]);
+                js += "],\"gates\":[";
+                for (size_t gi = 0; gi < ph.exec_gates.size(); ++gi) {
+                    const GateRec &g = ph.exec_gates[gi];
+                    js += gi ? ",{" : "{";
+                    js += "\"t\":[" + std::to_string(g.wires[0]) + (g.k == 2 ? "," + std::to_string(g.wires[1]) : "") +
+                          "],\"c\":[";
+                    for (size_t c = 0; c < g.ctls.size(); ++c) js += (c ? "," : "") + std::to_string(g.ctls[c]);
+                    js += "],\"enc\":" + std::to_string(g.encoded ? g.enc_slot : -1) + ",\"m\":[";
+                    const int d = 1 << g.k;
+                    for (int i = 0; i < d * d; ++i)
+                        js += (i ? ",[" : "[") + dbl(g.m[i].real()) + "," + dbl(g.m[i].imag()) + "]";
+                    js += "]}";
+                }
+                js += "]}";
+            }
+            js += "]}";
+            require(js.size() + 1 <= cap, "plan_dry: schedule buffer too small");
+            std::memcpy(src, js.c_str(), js.size() + 1);
+        } else if (src && cap) {
             src[0] = 0;
             if (pass_index >= 0 && pass_index < static_cast<int>(p.passes.size())) {
                 const std::string s = jit_source(p.passes[pass_index], dtype);

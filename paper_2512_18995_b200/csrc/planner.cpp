@@ -495,7 +495,13 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
         for (int i = 0; i < K - R; ++i) low.ng_phys.push_back(ph.tile_pos[hg.ng_bit[i]]);
         hg.op_begin = static_cast<int>(ph.ops.size());
         hg.tgt_begin = static_cast<int>(ph.targets.size());
-        for (int gi : gtook) low.add(gi);
+        for (int gi : gtook) {
+            GateRec e = gates[gi];
+            for (int t = 0; t < e.k; ++t) e.wires[t] = phys[e.wires[t]];
+            for (int &c : e.ctls) c = phys[c];
+            ph.exec_gates.push_back(std::move(e));
+            low.add(gi);
+        }
         low.finish();
         hg.op_end = static_cast<int>(ph.ops.size());
         hg.tgt_end = static_cast<int>(ph.targets.size());

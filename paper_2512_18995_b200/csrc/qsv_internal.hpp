@@ -196,6 +196,9 @@ struct PassHost {
     // Output bit permutation (input physical bit -> output physical bit);
     // empty = identity. A permuting pass writes out of place (State::scratch).
     std::vector<int> out_perm;
+    // The pass's gates in execution order, wires mapped to physical bits
+    // (schedule export for host-side verification, qsv_plan_dry).
+    std::vector<GateRec> exec_gates;
 };
 // Serialised pass program for dtype.
 std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int *off_targets, int *off_recs,

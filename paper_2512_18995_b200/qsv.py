@@ -146,6 +146,21 @@ def plan_dry(nqubit: int, gates, dtype: int = C128, world: int = 1, opts: dict |
                              cap))
     return {f: getattr(info, f) for f, _ in qsv_plan_info._fields_}, (buf.value.decode() if buf else "")
 
+
+def plan_schedule(nqubit: int, gates, dtype: int = C128, world: int = 1, opts: dict | None = None) -> dict:
+    """Host-only: the executable step list (local passes with their gates on
+    physical bits, global<->local swap steps) the engine would run on `world`
+    ranks. Used to verify the distributed schedule on CPU."""
+    import json
+
+    arr, keep = gate_array(gates)
+    o = make_opts(opts)
+    info = qsv_plan_info()
+    cap = 64 << 20
+    buf = C.create_string_buffer(cap)
+    check(lib().qsv_plan_dry(nqubit, dtype, world, arr, len(gates), C.byref(o), C.byref(info), -2, buf, cap))
+    return json.loads(buf.value.decode())
+
 _lib = None
 
 
