@@ -233,6 +233,10 @@ def main():
     avg_launch_ms = float(lm.mean())
     hbm_peak, peak_kind = peaks()
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
+    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this workload
+    tp = ROOT / "profiles" / "r01_traffic_cfg3_30q.json"
+    if tp.exists() and n == N_QUBITS and world == 1:
+        traffic = json.loads(tp.read_text())["traffic_per_launch_bytes"]
 
     # ---- end to end through the C ABI with pinned host buffers ----
     e2e = None
@@ -283,8 +287,9 @@ def main():
                        "swaps_per_step": plan.info["nswaps"], "parallelism": f"state sharded over {world} GPU(s)",
                        "l2": "state (16 GiB) >> L2 (126 MB); no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                         "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "tile_pass_kernel", "bytes_per_launch": bytes_per_launch,
+                         "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "traffic_source": "profiles/r01_traffic_cfg3_30q.json (ncu dram__bytes_read+write per launch)",
+                         "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
             "gpu_launches": args.steps * npass,
