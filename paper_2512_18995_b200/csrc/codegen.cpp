@@ -419,9 +419,38 @@ struct Gen {
         const int G = static_cast<int>(ph.groups.size());
         const bool permuted = !ph.out_perm.empty();
         const bool any_e = next_max > 0;
-        o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
-        o << "  (void)tile;\n";
+        // prefetch mode: two shared tiles; while tile t is transformed, the
+        // cp.async copies of tile t + gridDim stream into the other buffer and
+        // the first group reads shared memory instead of HBM
+        const bool pf = prefetch;
+        if (pf) {
+            o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
+            o << "    const int row = (int)(t >> " << tpr_log << ");\n";
+            o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
+            o << "    const " << V << " *src = (const " << V << " *)a.state + (u64)row * a.row_stride;\n";
+            o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
+            o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
+            o << "      const int u = ch * " << apu << ";\n";
+            o << "      const u64 g = tb | (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") | (u & "
+              << ((1 << L) - 1) << ");\n";
+            o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[swz(u)]);\n";
+            o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&src[g]) : "
+                 "\"memory\");\n";
+            o << "    }\n  };\n";
+            o << "  int cur = 0;\n";
+            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
+            o << "  asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
+        } else {
+            o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
+            o << "  (void)tile;\n";
+        }
         o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        if (pf) {
+            o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
+            o << "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" << V << " *)smem_raw + ((cur ^ 1) << "
+              << K << "));\n";
+            o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
+        }
         o << "    const int row = (int)(t >> " << tpr_log << ");\n";
         o << "    (void)row;\n";
         o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
@@ -446,11 +475,14 @@ struct Gen {
                 }
             }
         }
-        if (any_e) o << "    __syncthreads();\n";
+        if (pf) {
+            o << "    asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
+            o << "    __syncthreads();\n";
+        } else if (any_e) o << "    __syncthreads();\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
             cur_group = static_cast<int>(gi);
-            const bool from_hbm = gi == 0, to_hbm = static_cast<int>(gi) == G - 1 && !permuted;
+            const bool from_hbm = gi == 0 && !pf, to_hbm = static_cast<int>(gi) == G - 1 && !permuted;
             o << "    // ---- group " << gi << "\n";
             std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
@@ -509,12 +541,15 @@ struct Gen {
             o << "      }\n    }\n";
         }
         // the next tile's first group rewrites the shared tile / E
-        if (G >= 2 || any_e || permuted) o << "    __syncthreads();\n";
+        if (G >= 2 || any_e || permuted || pf) o << "    __syncthreads();\n";
+        if (pf) o << "    cur ^= 1;\n";
         o << "  }\n";
+        if (pf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
         o << "}\n";
         return o.str();
     }
     bool double_buffer = true;
+    bool prefetch = false;
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
     std::map<int, int> stab_off; // global table offset -> shared-memory offset
@@ -524,7 +559,8 @@ struct Gen {
 
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf) {
     Gen g(ph, dtype);
-    g.double_buffer = dbuf;
+    g.double_buffer = false;
+    g.prefetch = dbuf;
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const int nchunks = (1 << ph.K) / (16 / amp);

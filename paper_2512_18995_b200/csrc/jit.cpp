@@ -167,7 +167,13 @@ struct JitKernel {
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     const std::string name = "qsv_pass";
     int threads = 256;
-    const bool dbuf = double_buffer_enabled();
+    // prefetch (two shared tiles, cp.async of the next tile in flight) when
+    // both buffers fit in 64 KiB: K <= 11 for complex128, K <= 12 for complex64
+    const int amp0 = dtype == QSV_C64 ? 8 : 16;
+    const char *pe = std::getenv("QSV_PREFETCH");
+    const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
+                      (1 << ph.K) * amp0 >= 16 * 32;
+    (void)double_buffer_enabled;
     std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf);
     char key[32];
     std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
@@ -193,7 +199,8 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     dp.threads = threads;
     // groups between the first (loads from HBM) and the last (stores to HBM)
     // exchange amplitudes through a shared tile; a one-group pass needs none
-    dp.smem = (ph.groups.size() >= 2 || !ph.out_perm.empty()) ? (static_cast<size_t>(amp) << ph.K) : 0;
+    dp.smem = dbuf ? 2 * (static_cast<size_t>(amp) << ph.K)
+                   : (ph.groups.size() >= 2 || !ph.out_perm.empty()) ? (static_cast<size_t>(amp) << ph.K) : 0;
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
@@ -210,7 +217,11 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
 // Source of a pass's specialised kernel (diagnostics / tests).
 std::string jit_source(const PassHost &ph, int dtype) {
     int threads = 0;
-    return generate_pass_source(ph, dtype, "qsv_pass", &threads, double_buffer_enabled());
+    const int amp0 = dtype == QSV_C64 ? 8 : 16;
+    const char *pe = std::getenv("QSV_PREFETCH");
+    const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
+                      (1 << ph.K) * amp0 >= 16 * 32;
+    return generate_pass_source(ph, dtype, "qsv_pass", &threads, dbuf);
 }
 
 void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s) {
