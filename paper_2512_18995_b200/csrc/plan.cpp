@@ -208,7 +208,7 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.phase_flush = p->opts.no_phase_flush == 0;
     // complex128: 3-qubit register groups (8 amplitudes = 32 registers) keep a
     // 512-thread CTA under 64 registers, i.e. 32 warps per SM at 2 CTAs/SM
-    cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : (dtype == QSV_C128 ? 3 : 4);
+    cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : 0; // 0: per pass (planner.cpp)
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
     if (ctx->world == 1) {

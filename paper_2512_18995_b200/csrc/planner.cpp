@@ -33,7 +33,9 @@
 namespace qsv {
 
 int default_tile_bits(int dtype, int nlocal) {
-    const int k = dtype == QSV_C64 ? 13 : 12; // 64 KiB tiles: 2-3 CTAs per SM
+    // complex128: 32 KiB tiles, double-buffered (prefetch) -> 64 KiB per CTA;
+    // complex64: 64 KiB single-buffered tiles (r01 sweep, scripts/sweep2.py)
+    const int k = dtype == QSV_C64 ? 13 : 11;
     return std::min(k, nlocal);
 }
 int default_low_bits(int dtype, int nlocal) {
@@ -625,7 +627,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
     const int nl = cfg.nlocal;
     const int K = std::min(cfg.K, nl);
     const int L = std::min(cfg.L, K);
-    const int R = std::min(cfg.R, K);
+    int R = cfg.R > 0 ? std::min(cfg.R, K) : std::min(3, K); // cfg.R <= 0: chosen per pass below
     require(K >= 1, "planner: empty local state");
     const uint64_t localmask = nl >= 64 ? ~0ull : ((1ull << nl) - 1);
     const std::vector<GateRec> fused = cfg.fuse_1q ? fuse_single_qubit_runs(gates_in) : gates_in;
@@ -661,6 +663,21 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
         }
         require(!took.empty(), "planner: no progress");
         size_t first_encs = encs.size();
+        if (cfg.R <= 0) { // auto: 4-qubit groups unless complex dense math dominates (register pressure)
+            bool heavy = false;
+            for (int i : took) {
+                const GateRec &g = gates[i];
+                if (g.diag) continue;
+                const int d = 1 << g.k;
+                bool complex_m = g.encoded;
+                for (int q = 0; q < d * d && !complex_m; ++q) complex_m = g.m[q].imag() != 0.0;
+                bool perm = !g.encoded;
+                for (int q = 0; q < d * d && perm; ++q)
+                    perm = g.m[q] == cplx(0, 0) || g.m[q] == cplx(1, 0);
+                if (complex_m || (g.k == 2 && !perm)) heavy = true;
+            }
+            R = std::min(heavy ? 3 : 4, K);
+        }
         PassHost ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         // keep the program within the shared-memory budget: give the tail of
         // the admitted gates back (they commute with everything skipped before
