@@ -56,31 +56,47 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
     std::vector<int> phys = p.perm_in;
     std::vector<int> wire_at(n);
     for (int w = 0; w < n; ++w) wire_at[phys[w]] = w;
-    size_t i = 0;
-    const size_t G = p.gates.size();
-    auto next_use = [&](int wire, size_t from) -> size_t {
-        for (size_t j = from; j < G; ++j) {
-            const GateRec &g = p.gates[j];
+    // Gates still to schedule, in order. Each round runs the maximal
+    // commutation-closed front that needs no communication (a gate joins when
+    // it commutes with every earlier blocked gate and has no non-diagonal
+    // target on a rank bit), then swaps in the rank-bit qubits the blocked
+    // frontier needs.
+    std::vector<int> rem(p.gates.size());
+    for (size_t i = 0; i < rem.size(); ++i) rem[i] = static_cast<int>(i);
+    auto next_use = [&](int wire, size_t from) -> size_t { // position in rem
+        for (size_t j = from; j < rem.size(); ++j) {
+            const GateRec &g = p.gates[rem[j]];
             if (g.diag) continue;
             for (int t = 0; t < g.k; ++t)
                 if (g.wires[t] == wire) return j;
         }
-        return G + 1;
+        return rem.size() + 1;
     };
-    while (i < G) {
-        // maximal local segment
-        size_t j = i;
-        while (j < G) {
-            const GateRec &g = p.gates[j];
-            bool ok = true;
-            if (!g.diag)
-                for (int t = 0; t < g.k; ++t)
-                    if (phys[g.wires[t]] >= nl) ok = false;
-            if (!ok) break;
-            ++j;
+    while (!rem.empty()) {
+        std::vector<int> front, blocked;
+        uint64_t bN = 0, bD = 0; // wires (logical) blocked non-diagonally / diagonally
+        for (int gi : rem) {
+            const GateRec &g = p.gates[gi];
+            uint64_t nm = 0, dm = 0;
+            bool global_n = false;
+            for (int t = 0; t < g.k; ++t) {
+                if (g.diag) dm |= 1ull << g.wires[t];
+                else {
+                    nm |= 1ull << g.wires[t];
+                    if (phys[g.wires[t]] >= nl) global_n = true;
+                }
+            }
+            for (int c : g.ctls) dm |= 1ull << c;
+            const bool conflict = (nm & (bN | bD)) || (dm & bN);
+            if (conflict || global_n) {
+                bN |= nm;
+                bD |= dm;
+                blocked.push_back(gi);
+            } else front.push_back(gi);
         }
-        if (j > i) {
-            std::vector<GateRec> seg(p.gates.begin() + i, p.gates.begin() + j);
+        if (!front.empty()) {
+            std::vector<GateRec> seg;
+            for (int gi : front) seg.push_back(p.gates[gi]);
             auto passes = plan_passes(seg, phys, cfg, p.encs);
             for (auto &ph : passes) {
                 Step s;
@@ -89,26 +105,45 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
                 p.passes.push_back(std::move(ph));
                 p.steps.push_back(std::move(s));
             }
-            i = j;
-            continue;
         }
-        // gate i needs a swap
-        const GateRec &g = p.gates[i];
+        rem.swap(blocked);
+        if (rem.empty()) break;
+        // swap in the rank-bit targets of the first blocked gate (it is blocked
+        // only by them: everything before it has run), plus those of the next
+        // blocked gates (look-ahead) while rank bits remain, in one step
         Step s;
         s.kind = 1;
-        std::vector<int> keep; // local bits that must stay (this gate's local targets)
-        for (int t = 0; t < g.k; ++t)
-            if (phys[g.wires[t]] < nl) keep.push_back(phys[g.wires[t]]);
-        for (int t = 0; t < g.k; ++t) {
-            const int gb = phys[g.wires[t]];
+        std::vector<int> keep, want; // local bits that must stay / rank-bit wires to bring in
+        {
+            const size_t look = std::min<size_t>(rem.size(), 64);
+            for (size_t j = 0; j < look && static_cast<int>(want.size()) < p.ctx->gbits; ++j) {
+                const GateRec &h = p.gates[rem[j]];
+                if (h.diag) continue;
+                for (int t = 0; t < h.k; ++t) {
+                    const int b = phys[h.wires[t]];
+                    if (b < nl) {
+                        if (j == 0) keep.push_back(b);
+                    } else if (std::find(want.begin(), want.end(), h.wires[t]) == want.end() &&
+                               (j == 0 || static_cast<int>(want.size()) < p.ctx->gbits))
+                        want.push_back(h.wires[t]);
+                }
+            }
+        }
+        for (int w : want) {
+            const int gb = phys[w];
             if (gb < nl) continue;
+            // victim: the local wire needed furthest in the future; among
+            // equally distant ones (or ones not needed before the next few
+            // gates) the highest bit, whose halves are contiguous runs
             int best = -1;
             size_t best_use = 0;
-            for (int lb = nl - 1; lb >= 0; --lb) {
+            for (int lb = nl - 1; lb >= 0; --lb) { // Belady; ties -> the highest bit
                 if (std::find(keep.begin(), keep.end(), lb) != keep.end()) continue;
-                const size_t u = next_use(wire_at[lb], i);
-                if (best < 0 || u > best_use) best = lb, best_use = u;
-                if (u == G + 1) break;
+                bool wanted = false;
+                for (int w : want) wanted = wanted || wire_at[lb] == w;
+                if (wanted) continue;
+                const size_t score = next_use(wire_at[lb], 0);
+                if (best < 0 || score > best_use) best = lb, best_use = score;
             }
             require(best >= 0, "dist: no local qubit available for a swap");
             keep.push_back(best);
