@@ -191,6 +191,17 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
 /* marginal_probabilities on row `row`: out has 2^k entries. */
 int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
 
+/* ---- gradients (quasar::qubit::adjoint_gradients, adjoint.hpp:52-110) ---- */
+/* Gradient of sum_i <O_i> by the adjoint method: param_grads gets one entry
+ * per parameter of each trainable, non-encoded gate (circuit order; *nparams
+ * receives the count, at most param_cap are written), data_grads one per
+ * encode slot (data order; `slots` must equal the circuit's encode slots).
+ * init: 2^n interleaved (re,im) amplitudes of the initial state, or NULL for
+ * |0...0>. Pure states, one data row per call, like the reference. */
+int qsv_adjoint_gradients(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, int nobs,
+                          const qsv_obs *obs, const double *init, const double *data, int slots,
+                          double *param_grads, int param_cap, int *nparams, double *data_grads);
+
 /* Plans on the host only (no device, no upload): fills info as
  * qsv_plan_info_get would for a context of `world` ranks, and, when src is
  * non-null, the generated CUDA source of pass `pass_index`. For tests and

@@ -21,6 +21,9 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots);
 void profile_plan(Plan &p, State &st, double *launch_ms);
 int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads);
+void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates, int nobs, const qsv_obs *obs,
+                       const double *init, const double *data, int slots, std::vector<double> &pg,
+                       std::vector<double> &dg);
 } // namespace qsv
 
 using namespace qsv;
@@ -492,6 +495,24 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
             bits.push_back(st->perm[wires[i]]);
         }
         reduce_marginal(*st, row, bits, out);
+    });
+}
+
+int qsv_adjoint_gradients(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, int nobs,
+                          const qsv_obs *obs, const double *init, const double *data, int slots,
+                          double *param_grads, int param_cap, int *nparams, double *data_grads) {
+    return guard([&] {
+        require(ctx != nullptr, "null ctx");
+        require(nqubit >= 1 && nqubit <= kMaxQubits, "adjoint_gradients: nqubit out of range");
+        require(dtype == QSV_C64 || dtype == QSV_C128, "adjoint_gradients: bad dtype");
+        require(slots == 0 || data, "adjoint_gradients: data missing");
+        std::vector<double> pg, dg;
+        adjoint_gradients(ctx, nqubit, dtype, gates, ngates, nobs, obs, init, data, slots, pg, dg);
+        if (nparams) *nparams = static_cast<int>(pg.size());
+        if (param_grads)
+            for (int i = 0; i < std::min<int>(param_cap, static_cast<int>(pg.size())); ++i) param_grads[i] = pg[i];
+        if (data_grads)
+            for (size_t i = 0; i < dg.size(); ++i) data_grads[i] = dg[i];
     });
 }
 

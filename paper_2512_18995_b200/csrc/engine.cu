@@ -8,6 +8,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "qsv_internal.hpp"
 
@@ -290,10 +292,44 @@ void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, ui
 }
 
 namespace {
+// Small reduction buffers come from a per-device cache (cudaMalloc/cudaFree
+// synchronise the device and cost milliseconds; the reductions run every step
+// of a batched workload). Blocks are returned after the host has synchronised
+// with the stream that used them, so reuse is ordered.
+struct BufCache {
+    std::mutex mu;
+    std::multimap<size_t, std::pair<int, void *>> free_blocks; // size -> (device, ptr)
+};
+BufCache &buf_cache() {
+    static BufCache *c = new BufCache(); // intentionally leaked: outlives static destruction
+    return *c;
+}
 struct DevBuf {
     void *p = nullptr;
-    explicit DevBuf(size_t bytes) { QSV_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
-    ~DevBuf() { cudaFree(p); }
+    size_t cap = 0;
+    int dev = 0;
+    explicit DevBuf(size_t bytes) {
+        bytes = std::max<size_t>(bytes, 256);
+        QSV_CUDA(cudaGetDevice(&dev));
+        BufCache &c = buf_cache();
+        {
+            std::lock_guard<std::mutex> lk(c.mu);
+            for (auto it = c.free_blocks.lower_bound(bytes); it != c.free_blocks.end() && it->first <= 4 * bytes; ++it)
+                if (it->second.first == dev) {
+                    p = it->second.second;
+                    cap = it->first;
+                    c.free_blocks.erase(it);
+                    return;
+                }
+        }
+        QSV_CUDA(cudaMalloc(&p, bytes));
+        cap = bytes;
+    }
+    ~DevBuf() {
+        BufCache &c = buf_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        c.free_blocks.emplace(cap, std::make_pair(dev, p));
+    }
     template <typename X> X *as() { return static_cast<X *>(p); }
 };
 } // namespace

@@ -128,6 +128,9 @@ _SIGS = {
     "qsv_expect_pauli": (C.c_int, [_P, C.c_int, C.POINTER(qsv_obs), C.c_void_p]),
     "qsv_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
     "qsv_rng_fill": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int]),
+    "qsv_adjoint_gradients": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.c_int,
+                                        C.POINTER(qsv_obs), C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                        C.POINTER(C.c_int), C.c_void_p]),
     "qsv_plan_dry": (C.c_int, [C.c_int, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.POINTER(qsv_opts),
                                C.POINTER(qsv_plan_info), C.c_int, C.c_char_p, C.c_size_t]),
 }
@@ -619,6 +622,44 @@ def marginal_probabilities(state: QubitState, wires, batch_index: int = 0) -> np
     out = np.zeros(1 << k)
     check(lib().qsv_marginal_probs(state.h, batch_index, k, w, _ptr(out)))
     return out
+
+
+@dataclass
+class AdjointGradients:
+    """adjoint.hpp:25-28."""
+    param_grads: list
+    data_grads: list
+
+
+def adjoint_gradients(cir: Circuit, init: "QubitState | None" = None, data=(), dtype: int = C128,
+                      ctx: Context | None = None) -> AdjointGradients:
+    """quasar::qubit::adjoint_gradients (adjoint.hpp:52-110) on the GPU:
+    gradient of the summed expectation of the circuit's observables."""
+    ctx = ctx or default_context()
+    arr, keep = gate_array(cir.gates())
+    obs = cir.observables()
+    oarr = (qsv_obs * max(1, len(obs)))()
+    for i, o in enumerate(obs):
+        w = (C.c_int32 * max(1, len(o.wires)))(*o.wires)
+        b = o.basis.encode()
+        keep += [w, b]
+        oarr[i].nwires = len(o.wires)
+        oarr[i].wires = C.cast(w, C.POINTER(C.c_int32))
+        oarr[i].basis = b
+    d = np.ascontiguousarray(np.asarray(list(data), dtype=np.float64))
+    ini = None
+    if init is not None:
+        if init.batch() != 1:
+            raise InvalidInput("adjoint_gradients: one batch row at a time")
+        ini = np.ascontiguousarray(init.amplitudes(0)).view(np.float64)
+    cap = sum(g.num_params() for g in cir.gates())
+    pg = np.zeros(max(1, cap))
+    dg = np.zeros(max(1, len(d)))
+    npar = C.c_int()
+    check(lib().qsv_adjoint_gradients(ctx.h, cir.nqubit(), dtype, arr, len(cir.gates()), len(obs), oarr,
+                                      _ptr(ini) if ini is not None else None, _ptr(d) if d.size else None, len(d),
+                                      _ptr(pg), cap, C.byref(npar), _ptr(dg)))
+    return AdjointGradients(list(pg[: npar.value]), list(dg[: len(d)]))
 
 
 def bits_to_string(outcome: int, k: int) -> str:
