@@ -67,10 +67,17 @@ std::string scatter(const std::string &x, const std::vector<int> &pos, bool wide
 // One register set per thread per group (up to 512 threads: 2 CTAs x 16 warps
 // per SM), at least one 16-byte chunk per thread for the tile copies.
 int kernel_threads(const PassHost &ph, int dtype) {
-    const int nsets = 1 << (ph.K - ph.R);
-    const int nchunks = (1 << ph.K) / (dtype == QSV_C64 ? 2 : 1);
-    const int th = std::max(32, std::min(512, std::max(nsets, std::min(nchunks, 256))));
+    (void)dtype;
+    const int nsets = 1 << (ph.K - ph.R); // exactly one register set per thread per group
+    const int th = std::max(32, std::min(512, nsets));
     return (th + 31) / 32 * 32;
+}
+
+// CTAs per SM the register budget is sized for: 2^R amplitudes per thread
+// (R = 4 -> up to 128 registers, R <= 3 -> 64).
+int kernel_min_blocks(const PassHost &ph, int threads) {
+    const int regcap = ph.R >= 4 ? 128 : 64;
+    return std::max(1, std::min(8, 65536 / (threads * regcap)));
 }
 
 struct Gen {
@@ -370,8 +377,8 @@ struct Gen {
         // the cp.async copies of tile t + gridDim are already in flight into
         // the other (one CTA per SM, 2 x 2^K amplitudes).
         const bool dbuf = double_buffer;
-        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", " << (dbuf ? 1 : 2) << ") " << name
-          << "(const Args a) {\n";
+        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
+          << (dbuf ? 1 : kernel_min_blocks(ph, threads)) << ") " << name << "(const Args a) {\n";
         o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
         // per-tile external phase factors of ALL groups get distinct slots
         ebase.assign(ph.groups.size(), 0);
@@ -470,7 +477,10 @@ struct Gen {
                     const int thr = (k % nwarps) * 32 + (k / nwarps) % 32;
                     ++k;
                     o << "    if (threadIdx.x == " << thr << ") {\n      " << V << " f = mk(1, 0);\n";
-                    for (int q = t.ext_begin; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", "      ");
+                    for (int c = 0; c < t.ext_chunks; ++c)
+                        o << "      f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
+                          << ") & 255)]);\n";
+                    for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", "      ");
                     o << "      E[" << ebase[gi] + t.eidx << "] = f;\n    }\n";
                 }
             }

@@ -199,8 +199,52 @@ struct GroupLowering {
             mix.insert(mix.end(), ext.begin(), ext.end());
             ext.clear();
         }
-        t.ext_begin = static_cast<int>(ph.recs.size());
-        ph.recs.insert(ph.recs.end(), ext.begin(), ext.end());
+        // per-tile records over the tile index bits (ext_pos) that stay inside
+        // one 8-bit chunk of the tile index become chunk tables
+        t.ext_tab = -1;
+        t.ext_chunks = 0;
+        std::vector<DiagRec> rest;
+        {
+            const int ne = static_cast<int>(ph.ext_pos.size());
+            const int nch = (ne + 7) / 8;
+            std::vector<std::vector<DiagRec>> by_chunk(nch);
+            for (const DiagRec &r : ext) {
+                const uint64_t d = rec_deps(r);
+                int chunk = -1;
+                bool ok = d != 0;
+                for (int b = 0; b < 64 && ok; ++b) {
+                    if (!((d >> b) & 1)) continue;
+                    const auto it = std::find(ph.ext_pos.begin(), ph.ext_pos.end(), b);
+                    if (it == ph.ext_pos.end()) ok = false; // a rank bit
+                    else {
+                        const int c = static_cast<int>(it - ph.ext_pos.begin()) / 8;
+                        if (chunk >= 0 && c != chunk) ok = false;
+                        chunk = c;
+                    }
+                }
+                if (ok) by_chunk[chunk].push_back(r);
+                else rest.push_back(r);
+            }
+            bool any = false;
+            for (auto &v : by_chunk) any = any || !v.empty();
+            if (any) {
+                t.ext_tab = static_cast<int>(ph.tables.size());
+                t.ext_chunks = nch;
+                for (int c = 0; c < nch; ++c)
+                    for (int j = 0; j < 256; ++j) {
+                        uint64_t pb = 0;
+                        for (int i = 0; i < 8 && 8 * c + i < ne; ++i)
+                            if ((j >> i) & 1) pb |= 1ull << ph.ext_pos[8 * c + i];
+                        cplx f(1, 0);
+                        for (const DiagRec &r : by_chunk[c]) f *= eval_rec(r, pb);
+                        ph.tables.push_back(f);
+                    }
+            }
+        }
+        // records evaluated per tile: [ext_rest, ext_end) (all of them without tables)
+        t.ext_begin = t.ext_rest = static_cast<int>(ph.recs.size());
+        if (t.ext_tab >= 0) ph.recs.insert(ph.recs.end(), rest.begin(), rest.end());
+        else ph.recs.insert(ph.recs.end(), ext.begin(), ext.end());
         t.ext_end = static_cast<int>(ph.recs.size());
         if (!ext.empty()) t.eidx = n_ext++;
         t.mix_begin = static_cast<int>(ph.recs.size());

@@ -96,7 +96,10 @@ struct alignas(16) FlushTarget {
     int32_t eidx;           // index into the CTA's shared E array, or -1
     // separable part of the tile records: table_lo[s & lo_mask] * table_hi[s >> lo_bits]
     int32_t table_lo, table_hi, lo_bits;
-    int32_t pad[2];
+    // separable part of the per-tile (EXT) records: prod_c ext_tab[c * 256 + ((tile >> 8c) & 255)];
+    // the records in [ext_rest, ext_end) span chunks or read rank bits and are evaluated per tile
+    int32_t ext_tab, ext_chunks, ext_rest;
+    int32_t pad[3];
 };
 
 struct alignas(16) GroupDesc {

@@ -339,7 +339,9 @@ __global__ void __launch_bounds__(256, 2) tile_pass_kernel(const PassArgs a) {
                     const FlushTarget &ft = c.targets[ti];
                     if (ft.eidx < 0) continue;
                     V f{1, 0};
-                    for (int k = ft.ext_begin; k < ft.ext_end; ++k) f = cmul(f, eval_rec<V>(c.recs[k], pbase));
+                    for (int k = ft.ext_rest; k < ft.ext_end; ++k) f = cmul(f, eval_rec<V>(c.recs[k], pbase));
+                    for (int ch = 0; ch < ft.ext_chunks; ++ch)
+                        f = cmul(f, __ldg(c.tables + ft.ext_tab + ch * 256 + ((tid_in_row >> (8 * ch)) & 255)));
                     E[ft.eidx] = f;
                 }
             }
