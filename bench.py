@@ -187,10 +187,18 @@ def main():
     qsv.set_default_context(ctx)
     n = args.n
     cir = W.cfg3_circuit(n)
-    psi = W.cfg3_input(n)  # full logical state on the host (16 GiB at n = 30)
     g = int(np.log2(world))
     nl = n - g
-    mine = psi[rank << nl:(rank + 1) << nl]
+    # this rank's slice of the seeded input (counter-based stream: no rank
+    # generates more than its own 2^(n-g) amplitudes), normalised globally
+    mine = W.cfg3_slice(rank << nl, 1 << nl)
+    ss = float(np.dot(mine.view(np.float64), mine.view(np.float64)))
+    if world > 1:
+        t = torch.tensor([ss], dtype=torch.float64)
+        torch.distributed.all_reduce(t)
+        ss = float(t.item())
+    mine /= np.sqrt(ss)
+    psi = mine  # full state when world == 1 (the CPU baseline samples it)
     plan = qsv.Plan(n, cir.gates(), dtype=qsv.C128, ctx=ctx)
     st = qsv.QubitState(n, dtype=qsv.C128, ctx=ctx)
     st.upload(mine)
@@ -227,7 +235,8 @@ def main():
     value = args.steps * ngates / (t_ms / 1e3)
 
     # ---- roofline of the dominant kernel (tile_pass_kernel) ----
-    lm = np.array(launch_ms)[:, :npass]  # steps x passes (swap steps excluded when world == 1)
+    kinds = plan.step_kinds()
+    lm = np.array(launch_ms)[:, kinds == 0]  # steps x passes (qubit-swap steps excluded)
     amp_bytes = 16
     bytes_per_launch = 2.0 * amp_bytes * (1 << nl)  # read + write of every local amplitude
     avg_launch_ms = float(lm.mean())
@@ -292,7 +301,10 @@ def main():
                          "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
-            "gpu_launches": args.steps * npass,
+            # pass kernels + per swapped bit pair one gather and one scatter
+            # kernel per 256 MiB chunk of the moving half (dist.cu)
+            "gpu_launches": args.steps * (npass + plan.info["nswaps"] * 2 *
+                                          -(-((1 << nl) // 2 * amp_bytes) // (256 << 20))),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),

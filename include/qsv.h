@@ -215,6 +215,13 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
  * so it runs on nthreads host threads and still reproduces the sequential
  * stream exactly. */
 int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads);
+/* The same stream starting `offset` draws in (even for normals): a rank fills
+ * only its slice of a seeded input. */
+int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset, uint64_t count, void *out,
+                    int nthreads);
+/* Step kinds of a plan in execution order (0 = local pass, 1 = qubit swap);
+ * returns the step count (fills at most cap entries). */
+int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap);
 
 #ifdef __cplusplus
 }

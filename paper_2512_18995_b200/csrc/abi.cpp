@@ -20,7 +20,7 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
                          const qsv_opts *opts);
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots);
 void profile_plan(Plan &p, State &st, double *launch_ms);
-int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads);
+int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads, uint64_t offset);
 void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates, int nobs, const qsv_obs *obs,
                        const double *init, const double *data, int slots, std::vector<double> &pg,
                        std::vector<double> &dg);
@@ -597,8 +597,23 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
 int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads) {
     return guard([&] {
         require(out != nullptr || count == 0, "null out");
-        rng_fill(seed, label, kind, count, out, nthreads);
+        rng_fill(seed, label, kind, count, out, nthreads, 0);
     });
+}
+
+int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset, uint64_t count, void *out,
+                    int nthreads) {
+    return guard([&] {
+        require(out != nullptr || count == 0, "null out");
+        rng_fill(seed, label, kind, count, out, nthreads, offset);
+    });
+}
+
+int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
+    if (!plan) return -QSV_ERR_INVALID;
+    const int n = static_cast<int>(plan->steps.size());
+    for (int i = 0; i < n && i < cap && kinds; ++i) kinds[i] = plan->steps[i].kind;
+    return n;
 }
 
 } // extern "C"

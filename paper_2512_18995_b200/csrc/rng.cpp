@@ -58,23 +58,27 @@ struct Seq { // sequential reference semantics (used on the rejection path)
 };
 } // namespace
 
-int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads) {
+int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads,
+             uint64_t offset) {
     require(kind >= 0 && kind <= 2, "rng_fill: kind must be 0 (u64), 1 (uniform) or 2 (normal)");
+    require(kind != 2 || offset % 2 == 0, "rng_fill: normal draws start at an even offset (Box-Muller pairs)");
     if (label) seed ^= fnv1a(label);
     const uint64_t key = mix(seed ^ kPhi); // Rng(uint64_t) constructor
     unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     unsigned T = nthreads > 0 ? static_cast<unsigned>(nthreads) : hw;
     T = std::max(1u, std::min<unsigned>(T, static_cast<unsigned>(std::max<uint64_t>(1, count >> 16))));
     std::atomic<bool> rejected{false};
-    // work unit: one draw (kinds 0/1) or one normal pair (kind 2)
+    // work unit: one draw (kinds 0/1) or one normal pair (kind 2); the
+    // stream starts `offset` draws in (counter-based: no sequential skip)
     const uint64_t units = kind == 2 ? (count + 1) / 2 : count;
+    const uint64_t c0 = offset;
     auto work = [&](uint64_t b, uint64_t e) {
         for (uint64_t j = b; j < e; ++j) {
-            if (kind == 0) static_cast<uint64_t *>(out)[j] = mix(key + kPhi * (j + 1));
-            else if (kind == 1) static_cast<double *>(out)[j] = to_unit(mix(key + kPhi * (j + 1)));
+            if (kind == 0) static_cast<uint64_t *>(out)[j] = mix(key + kPhi * (c0 + j + 1));
+            else if (kind == 1) static_cast<double *>(out)[j] = to_unit(mix(key + kPhi * (c0 + j + 1)));
             else {
-                const double u1 = to_unit(mix(key + kPhi * (2 * j + 1)));
-                const double u2 = to_unit(mix(key + kPhi * (2 * j + 2)));
+                const double u1 = to_unit(mix(key + kPhi * (c0 + 2 * j + 1)));
+                const double u2 = to_unit(mix(key + kPhi * (c0 + 2 * j + 2)));
                 if (u1 == 0.0) {
                     rejected = true;
                     return;
@@ -96,9 +100,10 @@ int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *o
         }
         for (auto &th : pool) th.join();
     }
-    if (rejected) {
+    if (rejected) { // p ~ 2^-53 per pair: replay the sequential stream exactly
         Seq s{key};
         double *o = static_cast<double *>(out);
+        for (uint64_t i = 0; i < offset; ++i) s.normal();
         for (uint64_t i = 0; i < count; ++i) o[i] = s.normal();
     }
     return 0;

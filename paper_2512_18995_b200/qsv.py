@@ -128,6 +128,8 @@ _SIGS = {
     "qsv_expect_pauli": (C.c_int, [_P, C.c_int, C.POINTER(qsv_obs), C.c_void_p]),
     "qsv_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
     "qsv_rng_fill": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int]),
+    "qsv_rng_fill_at": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_int]),
+    "qsv_plan_steps": (C.c_int, [_P, C.c_void_p, C.c_int]),
     "qsv_adjoint_gradients": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.c_int,
                                         C.POINTER(qsv_obs), C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
                                         C.POINTER(C.c_int), C.c_void_p]),
@@ -559,10 +561,19 @@ class Plan:
             d = np.ascontiguousarray(data, dtype=np.float64)
             check(lib().qsv_plan_execute(self.h, state.h, _ptr(d), d.shape[0], d.shape[1]))
 
+    def step_kinds(self) -> np.ndarray:
+        """0 = local pass, 1 = global<->local qubit swap, in execution order."""
+        n = lib().qsv_plan_steps(self.h, None, 0)
+        k = np.zeros(max(1, n), dtype=np.int32)
+        lib().qsv_plan_steps(self.h, _ptr(k), n)
+        return k[:n]
+
     def profile(self, state: QubitState) -> np.ndarray:
-        out = np.zeros(self.info["npasses"] + self.info["nswaps"] + 1)
+        """One execution with CUDA events around every step; per-step ms."""
+        n = lib().qsv_plan_steps(self.h, None, 0)
+        out = np.zeros(max(1, n))
         check(lib().qsv_plan_profile(self.h, state.h, _ptr(out)))
-        return out
+        return out[:n]
 
     def close(self):
         if getattr(self, "h", None):
@@ -749,10 +760,12 @@ class Rng:
         return self.next_u64() % n if n else 0
 
 
-def rng_fill(seed: int, label: str | None, kind: str, count: int, nthreads: int = 0) -> np.ndarray:
+def rng_fill(seed: int, label: str | None, kind: str, count: int, nthreads: int = 0, offset: int = 0) -> np.ndarray:
     """Bulk stream Rng(seed, label) draws through the library (multi-threaded,
-    bit-identical to the sequential stream). kind: 'u64' | 'uniform' | 'normal'."""
+    bit-identical to the sequential stream), starting `offset` draws in.
+    kind: 'u64' | 'uniform' | 'normal'."""
     k = {"u64": 0, "uniform": 1, "normal": 2}[kind]
     out = np.empty(count, dtype=np.uint64 if k == 0 else np.float64)
-    check(lib().qsv_rng_fill(seed, label.encode() if label is not None else None, k, count, _ptr(out), nthreads))
+    check(lib().qsv_rng_fill_at(seed, label.encode() if label is not None else None, k, offset, count, _ptr(out),
+                                nthreads))
     return out

@@ -93,6 +93,13 @@ def cfg3_input(n: int = 30, nthreads: int = 0) -> np.ndarray:
     return z
 
 
+def cfg3_slice(lo: int, count: int, nthreads: int = 0) -> np.ndarray:
+    """Amplitudes [lo, lo + count) of cfg3_input BEFORE normalisation (a rank's
+    slice; the counter-based stream starts at draw 2 * lo). Divide by the
+    square root of the all-reduced sum of |a|^2."""
+    return rng_fill(0, "cfg3", "normal", 2 * count, nthreads, offset=2 * lo).view(np.complex128)
+
+
 def cfg4_circuit(n: int = 34, layers: int = 20) -> Circuit:
     """`layers` x (U3 with U[0,2pi) angles on every qubit, brickwork CNOTs:
     even layers cnot(2i, 2i+1), odd layers cnot(2i+1, 2i+2))."""
