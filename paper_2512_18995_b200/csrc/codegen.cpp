@@ -16,6 +16,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
+#include <functional>
 #include <map>
 #include <sstream>
 #include <string>
@@ -314,24 +316,80 @@ struct Gen {
         o << ind << "}\n";
     }
 
+    // A FLUSH multiplies register slot r by the product of the factors of its
+    // targets (slot -1: every slot; slot b: slots with bit b set). The
+    // factors of one slot class are merged first (g_all, g_b), then the
+    // per-slot products are built down a binary tree over the bits
+    // (ph[r | 1<<b] = ph[r] * g_b, depth-first so at most R + 1 are live)
+    // and applied once per slot: 2^R - 1 + 2^R complex multiplies at most,
+    // against 2^(R-1) per single-bit target + 2^R per all-slot target when
+    // every target is applied on its own. A uniform real register scale
+    // (the deferred 1/sqrt(2)^h of the butterflies) rides on the root.
     void emit_flush(const HostOp &op, const std::string &ind) {
         const int NR = 1 << R;
+        o << ind << "{\n";
+        const std::string in = ind + "  ";
+        std::vector<int> nfac(R + 1, 0); // index R: the all-slot class
         for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti) {
             const FlushTarget &t = ph.targets[ti];
-            o << ind << "{ " << V << " f = "
-              << (t.eidx >= 0 ? "E[" + std::to_string(ebase[cur_group] + t.eidx) + "]" : "mk(1, 0)") << ";\n";
-            if (t.table >= 0) o << ind << "  f = cmulv(f, tab" << ti << ");\n";
+            const int cls = t.slot < 0 ? R : t.slot;
+            const std::string g = "g" + std::to_string(cls);
+            const std::string f = "f" + std::to_string(ti);
+            o << in << V << " " << f << " = "
+              << (t.eidx >= 0 ? "E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]" : "mk(1, 0)") << ";\n";
+            if (t.table >= 0) o << in << f << " = cmulv(" << f << ", tab" << ti << ");\n";
             if (t.table_lo >= 0)
-                o << ind << "  f = cmulv(f, stab[" << stab_off.at(t.table_lo) << " + (s & " << ((1 << t.lo_bits) - 1)
-                  << ")]);\n";
+                o << in << f << " = cmulv(" << f << ", stab[" << stab_off.at(t.table_lo) << " + (s & "
+                  << ((1 << t.lo_bits) - 1) << ")]);\n";
             if (t.table_hi >= 0)
-                o << ind << "  f = cmulv(f, stab[" << stab_off.at(t.table_hi) << " + (s >> " << t.lo_bits << ")]);\n";
-            for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", "f", ind + "  ");
-            for (int r = 0; r < NR; ++r)
-                if (t.slot < 0 || ((r >> t.slot) & 1)) o << ind << "  v" << r << " = cmulv(v" << r << ", f);\n";
-            o << ind << "}\n";
+                o << in << f << " = cmulv(" << f << ", stab[" << stab_off.at(t.table_hi) << " + (s >> " << t.lo_bits
+                  << ")]);\n";
+            for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", f, in);
+            if (nfac[cls]++ == 0) o << in << V << " " << g << " = " << f << ";\n";
+            else o << in << g << " = cmulv(" << g << ", " << f << ");\n";
         }
-        if (op.flush.regmask)
+        bool uniform = op.flush.regmask == (NR >= 32 ? 0xffffffffu : ((1u << NR) - 1)) &&
+                       static_cast<int>(op.regtab.size()) >= NR && op.regtab[0].imag() == 0.0;
+        for (int r = 1; uniform && r < NR; ++r) uniform = op.regtab[r] == op.regtab[0];
+        // root: "" (identity), a real constant, or the all-slot factor
+        std::string root;
+        double rc = 1.0;
+        if (uniform) rc = op.regtab[0].real();
+        if (nfac[R]) {
+            root = "g" + std::to_string(R);
+            if (rc != 1.0) o << in << root << " = mk(" << c(rc) << "*" << root << ".x, " << c(rc) << "*" << root
+                             << ".y);\n";
+        }
+        int nph = 0;
+        // ph: variable holding the product for slot r ("" = identity), or the
+        // real constant rc when the slot carries only the scale
+        std::function<void(int, const std::string &, bool)> visit = [&](int r, const std::string &p, bool scaled) {
+            if (!p.empty()) o << in << "v" << r << " = cmulv(v" << r << ", " << p << ");\n";
+            else if (scaled && rc != 1.0)
+                o << in << "v" << r << " = mk(" << c(rc) << "*v" << r << ".x, " << c(rc) << "*v" << r << ".y);\n";
+            const int top = r ? 64 - __builtin_clzll(static_cast<unsigned long long>(r)) : 0;
+            for (int b = top; b < R; ++b) {
+                const int ch = r | (1 << b);
+                if (!nfac[b]) {
+                    visit(ch, p, scaled);
+                    continue;
+                }
+                const std::string gb = "g" + std::to_string(b);
+                std::string q;
+                if (!p.empty()) {
+                    q = "p" + std::to_string(nph++);
+                    o << in << V << " " << q << " = cmulv(" << p << ", " << gb << ");\n";
+                } else if (scaled && rc != 1.0) {
+                    q = "p" + std::to_string(nph++);
+                    o << in << V << " " << q << " = mk(" << c(rc) << "*" << gb << ".x, " << c(rc) << "*" << gb
+                      << ".y);\n";
+                } else q = gb;
+                visit(ch, q, false);
+            }
+        };
+        visit(0, root, root.empty() && uniform);
+        o << ind << "}\n";
+        if (op.flush.regmask && !uniform)
             for (int r = 0; r < NR; ++r)
                 if ((op.flush.regmask >> r) & 1) cmul_const(r, op.regtab[r], ind);
     }
@@ -391,7 +449,12 @@ struct Gen {
             ebase[gi] = next_max;
             next_max += ne;
         }
-        if (next_max) o << "  __shared__ " << V << " E[" << next_max << "];\n";
+        const bool pf = prefetch;
+        late = pf && late_issue;
+        // late-issue prefetch rewrites E while other warps may still read the
+        // previous tile's factors: one E set per shared tile
+        if (next_max) o << "  __shared__ " << V << " E[" << (late ? 2 * next_max : next_max) << "];\n";
+        e_stride = next_max;
         // separable phase tables (low / high set-index bits) live in shared memory
         {
             std::vector<std::pair<int, int>> ranges; // (global offset, length)
@@ -429,7 +492,6 @@ struct Gen {
         // prefetch mode: two shared tiles; while tile t is transformed, the
         // cp.async copies of tile t + gridDim stream into the other buffer and
         // the first group reads shared memory instead of HBM
-        const bool pf = prefetch;
         if (pf) {
             o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
             o << "    const int row = (int)(t >> " << tpr_log << ");\n";
@@ -452,11 +514,12 @@ struct Gen {
             o << "  (void)tile;\n";
         }
         o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        const std::string issue_next = "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" + std::string(V) +
+                                       " *)smem_raw + ((cur ^ 1) << " + std::to_string(K) +
+                                       "));\n    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
         if (pf) {
             o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
-            o << "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" << V << " *)smem_raw + ((cur ^ 1) << "
-              << K << "));\n";
-            o << "    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
+            if (!late) o << issue_next;
         }
         o << "    const int row = (int)(t >> " << tpr_log << ");\n";
         o << "    (void)row;\n";
@@ -481,13 +544,18 @@ struct Gen {
                         o << "      f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
                           << ") & 255)]);\n";
                     for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", "      ");
-                    o << "      E[" << ebase[gi] + t.eidx << "] = f;\n    }\n";
+                    o << "      E[" << eoff() << ebase[gi] + t.eidx << "] = f;\n    }\n";
                 }
             }
         }
         if (pf) {
-            o << "    asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
+            // early issue: tile t + gridDim is already in flight, wait for the
+            // older group only. Late issue: this barrier also retires every
+            // read of the other buffer (the previous tile), so the next copy
+            // goes out now and no end-of-tile barrier is needed.
+            o << "    asm volatile(\"cp.async.wait_group " << (late ? 0 : 1) << ";\\n\" ::: \"memory\");\n";
             o << "    __syncthreads();\n";
+            if (late) o << issue_next;
         } else if (any_e) o << "    __syncthreads();\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
             const HostGroup &g = ph.groups[gi];
@@ -551,7 +619,7 @@ struct Gen {
             o << "      }\n    }\n";
         }
         // the next tile's first group rewrites the shared tile / E
-        if (G >= 2 || any_e || permuted || pf) o << "    __syncthreads();\n";
+        if (!late && (G >= 2 || any_e || permuted || pf)) o << "    __syncthreads();\n";
         if (pf) o << "    cur ^= 1;\n";
         o << "  }\n";
         if (pf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
@@ -560,6 +628,10 @@ struct Gen {
     }
     bool double_buffer = true;
     bool prefetch = false;
+    bool late_issue = true; // prefetch: issue tile t + gridDim after tile t's barrier
+    bool late = false;
+    int e_stride = 0;
+    std::string eoff() const { return late ? "(cur * " + std::to_string(e_stride) + ") + " : ""; }
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
     std::map<int, int> stab_off; // global table offset -> shared-memory offset
@@ -571,6 +643,8 @@ std::string generate_pass_source(const PassHost &ph, int dtype, const std::strin
     Gen g(ph, dtype);
     g.double_buffer = false;
     g.prefetch = dbuf;
+    const char *pe = std::getenv("QSV_PF_EARLY");
+    g.late_issue = !(pe && pe[0] == '1');
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const int nchunks = (1 << ph.K) / (16 / amp);

@@ -493,12 +493,30 @@ struct GroupLowering {
 
 PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg, const std::vector<int> &took,
                     uint64_t active, const std::vector<int> &phys, const PlanConfig &cfg, int K, int L, int R,
-                    std::vector<EncDesc> &encs) {
+                    std::vector<EncDesc> &encs, const std::vector<int> *out_perm = nullptr) {
     const int nl = cfg.nlocal;
     PassHost ph;
     ph.K = K;
     ph.L = L;
     ph.R = R;
+    if (out_perm) {
+        // permuted pass: the tile is read in runs of 2^(lowest contiguous input
+        // bits) amplitudes and written in runs of 2^(lowest contiguous output
+        // bits); pad by lengthening the shorter run
+        std::vector<int> src(nl, -1);
+        for (int b = 0; b < nl; ++b) src[(*out_perm)[b]] = b;
+        while (std::popcount(active) < K) {
+            int in_run = 0, out_run = 0;
+            while (in_run < nl && (active >> in_run & 1)) ++in_run;
+            while (out_run < nl && (active >> src[out_run] & 1)) ++out_run;
+            int b = -1;
+            if (out_run < in_run && out_run < nl) b = src[out_run];
+            else if (in_run < nl) b = in_run;
+            else if (out_run < nl) b = src[out_run];
+            if (b < 0) break;
+            active |= 1ull << b;
+        }
+    }
     for (int b = 0; b < nl && std::popcount(active) < K; ++b) active |= 1ull << b; // lengthen contiguous runs
     for (int b = 0; b < nl; ++b)
         if (active & (1ull << b)) ph.tile_pos.push_back(b);
@@ -754,7 +772,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
         if (!passes.empty() && std::popcount(last_active | need) <= K) {
             const size_t first_encs = encs.size();
             (void)first_encs;
-            PassHost ph = lower_pass(gates, pg, last_took, last_active | need, phys, cfg, K, L, R, encs);
+            PassHost ph = lower_pass(gates, pg, last_took, last_active | need, phys, cfg, K, L, R, encs, &out_perm);
             // the re-lowered pass re-registered its encoded gates: drop the old ones
             if (pass_program_bytes(ph, cfg.dtype) <= static_cast<size_t>(kProgramBudget)) {
                 ph.out_perm = out_perm;
@@ -763,7 +781,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             }
         }
         if (!done) {
-            PassHost ph = lower_pass(gates, pg, {}, lowmask | need, phys, cfg, K, L, R, encs);
+            PassHost ph = lower_pass(gates, pg, {}, lowmask | need, phys, cfg, K, L, R, encs, &out_perm);
             ph.out_perm = out_perm;
             passes.push_back(std::move(ph));
         }
