@@ -28,6 +28,28 @@ namespace qsv {
 
 namespace {
 
+// Matrix / phase entries within 1e-15 of 0 or +-1 become exact (sin/cos of
+// multiples of pi/2 leave ~6e-17 residues): the folded term costs no FLOPs and
+// the change is far below the 1e-12 (complex128) parity bound.
+double snap(double v) {
+    if (std::fabs(v) < 1e-15) return 0.0;
+    if (std::fabs(v - 1.0) < 1e-15) return 1.0;
+    if (std::fabs(v + 1.0) < 1e-15) return -1.0;
+    return v;
+}
+
+// The shared-tile swizzle (same formula as the generated swz()); it is
+// linear over GF(2), so swz(a | b) = swz(a) ^ swz(b) for disjoint a, b.
+int swz_host(int u, bool f32) {
+    if (f32) {
+        const int w = u >> 1;
+        const int f = (w >> 3) ^ (w >> 6) ^ (w >> 9) ^ (w >> 12);
+        return ((w ^ (f & 7)) << 1) | (u & 1);
+    }
+    const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ (u >> 12);
+    return u ^ (f & 7);
+}
+
 std::string lit(double v, bool f32) {
     char buf[64];
     if (f32) {
@@ -99,7 +121,7 @@ struct Gen {
     // dst = coefficient * x (complex), with constant folding; returns terms
     // for the real and imaginary parts (appended to re/im lists)
     void term(const cplx &m, const std::string &x, std::vector<std::string> &re, std::vector<std::string> &im) {
-        const double a = m.real(), b = m.imag();
+        const double a = snap(m.real()), b = snap(m.imag());
         auto mulstr = [&](double k, const std::string &v) -> std::string {
             if (k == 1.0) return "+" + v;
             if (k == -1.0) return "-" + v;
@@ -140,7 +162,7 @@ struct Gen {
     }
 
     void cmul_const(int r, const cplx &f, const std::string &ind) {
-        if (f == cplx(1, 0)) return;
+        if (snap(f.real()) == 1.0 && snap(f.imag()) == 0.0) return;
         std::vector<std::string> re, im;
         term(f, "v" + std::to_string(r), re, im);
         o << ind << "v" << r << " = mk(" << sum(re) << ", " << sum(im) << ");\n";
@@ -492,43 +514,16 @@ struct Gen {
         // prefetch mode: two shared tiles; while tile t is transformed, the
         // cp.async copies of tile t + gridDim stream into the other buffer and
         // the first group reads shared memory instead of HBM
-        if (pf) {
-            o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
-            o << "    const int row = (int)(t >> " << tpr_log << ");\n";
-            o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
-            o << "    const " << V << " *src = (const " << V << " *)a.state + (u64)row * a.row_stride;\n";
-            o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
-            o << "    for (int ch = threadIdx.x; ch < " << nchunks << "; ch += " << threads << ") {\n";
-            o << "      const int u = ch * " << apu << ";\n";
-            o << "      const u64 g = tb | (" << scatter("(u >> " + std::to_string(L) + ")", hi, true) << ") | (u & "
-              << ((1 << L) - 1) << ");\n";
-            o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[swz(u)]);\n";
-            o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&src[g]) : "
-                 "\"memory\");\n";
-            o << "    }\n  };\n";
-            o << "  int cur = 0;\n";
-            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
-            o << "  asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
-        } else {
-            o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
-            o << "  (void)tile;\n";
-        }
-        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
-        const std::string issue_next = "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" + std::string(V) +
-                                       " *)smem_raw + ((cur ^ 1) << " + std::to_string(K) +
-                                       "));\n    asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
-        if (pf) {
-            o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
-            if (!late) o << issue_next;
-        }
-        o << "    const int row = (int)(t >> " << tpr_log << ");\n";
-        o << "    (void)row;\n";
-        o << "    const u64 tl = t & " << ((1ull << tpr_log) - 1) << "ull;\n";
-        o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
-        o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
-        o << "    const u64 pbase = a.rank_base | tb;\n";
-        // external phase factors of every group, one per thread spread over
-        // the warps, while the tile copies are in flight
+        // Per-tile external phase factors E (one per FlushTarget with eidx >= 0),
+        // each owned by one thread spread over the warps. Pipelined (prefetch +
+        // late issue): the owner cp.asyncs the table entries of tile t + gridDim
+        // together with that tile's data and multiplies them out at the end of
+        // tile t, so no L2 round trip sits in front of a tile's first barrier.
+        struct ETask {
+            int thr, slot, ti, raw;
+        };
+        std::vector<ETask> etasks;
+        int nraw = 0;
         {
             int k = 0;
             const int nwarps = threads / 32;
@@ -539,15 +534,117 @@ struct Gen {
                     if (t.eidx < 0) continue;
                     const int thr = (k % nwarps) * 32 + (k / nwarps) % 32;
                     ++k;
-                    o << "    if (threadIdx.x == " << thr << ") {\n      " << V << " f = mk(1, 0);\n";
-                    for (int c = 0; c < t.ext_chunks; ++c)
-                        o << "      f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
-                          << ") & 255)]);\n";
-                    for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", "      ");
-                    o << "      E[" << eoff() << ebase[gi] + t.eidx << "] = f;\n    }\n";
+                    etasks.push_back({thr, ebase[gi] + t.eidx, ti, nraw});
+                    nraw += t.ext_chunks;
                 }
             }
         }
+        const bool epipe = pf && late && any_e;
+        const std::string tmask = std::to_string((1ull << tpr_log) - 1) + "ull";
+        auto emit_e_direct = [&](const std::string &ind) {
+            for (const ETask &e : etasks) {
+                const FlushTarget &t = ph.targets[e.ti];
+                o << ind << "if (threadIdx.x == " << e.thr << ") {\n" << ind << "  " << V << " f = mk(1, 0);\n";
+                for (int c = 0; c < t.ext_chunks; ++c)
+                    o << ind << "  f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
+                      << ") & 255)]);\n";
+                for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", ind + "  ");
+                o << ind << "  E[" << eoff() << e.slot << "] = f;\n" << ind << "}\n";
+            }
+        };
+        auto emit_e_issue = [&](const std::string &tv, const std::string &nb, const std::string &ind) {
+            if (!nraw) return;
+            o << ind << "{ const u64 tlx = (" << tv << ") & " << tmask << ";\n";
+            for (const ETask &e : etasks) {
+                const FlushTarget &t = ph.targets[e.ti];
+                if (!t.ext_chunks) continue;
+                o << ind << "  if (threadIdx.x == " << e.thr << ") {\n";
+                for (int c = 0; c < t.ext_chunks; ++c) {
+                    o << ind << "    asm volatile(\"cp.async." << (f32 ? "ca" : "cg") << ".shared.global [%0], [%1], "
+                      << (f32 ? 8 : 16) << ";\\n\" :: \"r\"((unsigned)__cvta_generic_to_shared(&Eraw[(" << nb << ") * "
+                      << nraw << " + " << e.raw + c << "])), \"l\"(&a.tables[" << t.ext_tab + c * 256
+                      << " + ((tlx >> " << 8 * c << ") & 255)]) : \"memory\");\n";
+                }
+                o << ind << "  }\n";
+            }
+            o << ind << "}\n";
+        };
+        auto emit_e_compute = [&](const std::string &tv, const std::string &nb, const std::string &ind) {
+            o << ind << "{ const u64 tlx = (" << tv << ") & " << tmask << ";\n";
+            o << ind << "  const u64 pbx = a.rank_base | " << scatter("tlx", ph.ext_pos, true) << ";\n";
+            o << ind << "  (void)pbx;\n";
+            for (const ETask &e : etasks) {
+                const FlushTarget &t = ph.targets[e.ti];
+                o << ind << "  if (threadIdx.x == " << e.thr << ") {\n" << ind << "    " << V << " f = mk(1, 0);\n";
+                for (int c = 0; c < t.ext_chunks; ++c)
+                    o << ind << "    f = " << (c ? "cmulv(f, " : "(") << "Eraw[(" << nb << ") * " << nraw << " + "
+                      << e.raw + c << "]);\n";
+                for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbx", "f", ind + "    ");
+                o << ind << "    E[(" << nb << ") * " << e_stride << " + " << e.slot << "] = f;\n" << ind << "  }\n";
+            }
+            o << ind << "}\n";
+        };
+        const std::string commit = "asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
+        if (epipe && nraw) o << "  __shared__ " << V << " Eraw[" << 2 * nraw << "];\n";
+        if (pf) {
+            o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
+            o << "    const int row = (int)(t >> " << tpr_log << ");\n";
+            o << "    const u64 tl = t & " << tmask << ";\n";
+            o << "    const " << V << " *src = (const " << V << " *)a.state + (u64)row * a.row_stride;\n";
+            o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
+            // chunk u = tid * apu + k * threads * apu: bit scatter and swizzle are
+            // linear, so the per-thread parts are computed once
+            const int step = threads * apu;
+            o << "    const int u0 = threadIdx.x * " << apu << ";\n";
+            o << "    const u64 g0 = tb | (" << scatter("(u0 >> " + std::to_string(L) + ")", hi, true) << ") | (u0 & "
+              << ((1 << L) - 1) << ");\n";
+            o << "    const int s0 = swz(u0);\n";
+            if (nchunks % threads == 0) {
+                o << "#pragma unroll\n";
+                o << "    for (int k = 0; k < " << nchunks / threads << "; ++k) {\n";
+            } else {
+                o << "    for (int k = 0; k * " << threads << " + threadIdx.x < " << nchunks << "; ++k) {\n";
+            }
+            // k * step has bits only at or above log2(step) (a power of two)
+            o << "      const int uk = k * " << step << ";\n";
+            o << "      const u64 g = g0 | (" << scatter("(uk >> " + std::to_string(L) + ")", hi, true) << ") | (uk & "
+              << ((1 << L) - 1) << ");\n";
+            o << "      const unsigned sa = (unsigned)__cvta_generic_to_shared(&buf[s0 ^ swz(uk)]);\n";
+            o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&src[g]) : "
+                 "\"memory\");\n";
+            o << "    }\n  };\n";
+            o << "  int cur = 0;\n";
+            if (epipe) {
+                o << "  if (blockIdx.x < a.total_tiles) {\n";
+                emit_e_issue("blockIdx.x", "0", "    ");
+                o << "  }\n  " << commit;
+            }
+            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
+            o << "  " << commit;
+            if (epipe) {
+                o << "  asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
+                o << "  if (blockIdx.x < a.total_tiles) {\n";
+                emit_e_compute("blockIdx.x", "0", "    ");
+                o << "  }\n";
+            }
+        } else {
+            o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
+            o << "  (void)tile;\n";
+        }
+        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
+        const std::string issue_next = "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" + std::string(V) +
+                                       " *)smem_raw + ((cur ^ 1) << " + std::to_string(K) + "));\n    " + commit;
+        if (pf) {
+            o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
+            if (!late) o << issue_next;
+        }
+        o << "    const int row = (int)(t >> " << tpr_log << ");\n";
+        o << "    (void)row;\n";
+        o << "    const u64 tl = t & " << tmask << ";\n";
+        o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
+        o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
+        o << "    const u64 pbase = a.rank_base | tb;\n";
+        if (!epipe) emit_e_direct("    ");
         if (pf) {
             // early issue: tile t + gridDim is already in flight, wait for the
             // older group only. Late issue: this barrier also retires every
@@ -555,6 +652,11 @@ struct Gen {
             // goes out now and no end-of-tile barrier is needed.
             o << "    asm volatile(\"cp.async.wait_group " << (late ? 0 : 1) << ";\\n\" ::: \"memory\");\n";
             o << "    __syncthreads();\n";
+            if (epipe) {
+                o << "    if (t + gridDim.x < a.total_tiles) {\n";
+                emit_e_issue("t + gridDim.x", "cur ^ 1", "      ");
+                o << "    }\n    " << commit;
+            }
             if (late) o << issue_next;
         } else if (any_e) o << "    __syncthreads();\n";
         for (size_t gi = 0; gi < ph.groups.size(); ++gi) {
@@ -566,10 +668,11 @@ struct Gen {
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
             o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
             o << "      const int ub = " << scatter("s", ngt, false) << ";\n";
+            o << "      const int sb = swz(ub);\n";
             o << "      const u64 ls = " << scatter("s", ngp, true) << ";\n";
             o << "      const u64 pb = pbase | ls;\n";
             o << "      const u64 gb = tb | ls;\n";
-            o << "      (void)ub; (void)gb;\n";
+            o << "      (void)ub; (void)sb; (void)gb;\n";
             // phase tables: issue the (L2-resident) loads before the gate math
             for (int oi = g.op_begin; oi < g.op_end; ++oi) {
                 const HostOp &op = ph.ops[oi];
@@ -590,12 +693,19 @@ struct Gen {
             for (int r = 0; r < NR; ++r) {
                 if (from_hbm)
                     o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
-                else o << "      " << V << " v" << r << " = tile[swz(ub | " << uoff[r] << ")];\n";
+                else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_host(uoff[r], f32) << "];\n";
             }
-            for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
+            // QSV_DEBUG_NOCOMPUTE=1 (diagnostics only): the pass moves data without
+            // applying its gates -- the memory-structure ceiling of its geometry
+            static const bool nocompute = [] {
+                const char *e = std::getenv("QSV_DEBUG_NOCOMPUTE");
+                return e && e[0] == '1';
+            }();
+            if (!nocompute)
+                for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
             for (int r = 0; r < NR; ++r) {
                 if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
-                else o << "      tile[swz(ub | " << uoff[r] << ")] = v" << r << ";\n";
+                else o << "      tile[sb ^ " << swz_host(uoff[r], f32) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
             if (!to_hbm) o << "    __syncthreads();\n";
@@ -620,6 +730,12 @@ struct Gen {
         }
         // the next tile's first group rewrites the shared tile / E
         if (!late && (G >= 2 || any_e || permuted || pf)) o << "    __syncthreads();\n";
+        if (epipe) {
+            o << "    asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
+            o << "    if (t + gridDim.x < a.total_tiles) {\n";
+            emit_e_compute("t + gridDim.x", "cur ^ 1", "      ");
+            o << "    }\n";
+        }
         if (pf) o << "    cur ^= 1;\n";
         o << "  }\n";
         if (pf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";

@@ -243,7 +243,17 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     a.tables = dp.args.tables;
     a.enc_table = dp.args.enc_table;
     a.batch = dp.args.batch;
-    const uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(dp.grid, 1)));
+    uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(dp.grid, 1)));
+    // A few tiles per CTA rather than one persistent wave: CTAs that start
+    // and retire at different times keep HBM reads and writes interleaved,
+    // where a persistent grid moves in lock-step read / compute / write
+    // phases (measured on cfg3 30q: 29.7 -> 23.1 ms for 4 passes; 128-byte
+    // runs at large strides suffer most, scripts/micro/runs.cu).
+    static const int tpc = [] {
+        const char *e = std::getenv("QSV_TILES_PER_CTA");
+        return e ? std::atoi(e) : 4;
+    }();
+    if (tpc > 0) grid = std::min<uint64_t>(a.total_tiles, std::max<uint64_t>(grid, (a.total_tiles + tpc - 1) / tpc));
     void *args[] = {&a};
     QSV_CUDA(cudaLaunchKernel(dp.jit, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
 }
