@@ -452,7 +452,7 @@ struct Gen {
             o << "static __device__ __forceinline__ int swz(int u) { const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ "
                  "(u >> 12); return u ^ (f & 7); }\n";
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
-          << " *tables; const " << T << " *enc_table; int batch; int pad; void *out; };\n";
+          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; };\n";
         // Double buffering: while tile t is transformed in one shared buffer,
         // the cp.async copies of tile t + gridDim are already in flight into
         // the other (one CTA per SM, 2 x 2^K amplitudes).
@@ -586,6 +586,11 @@ struct Gen {
         };
         const std::string commit = "asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
         if (epipe && nraw) o << "  __shared__ " << V << " Eraw[" << 2 * nraw << "];\n";
+        // tiles of this CTA: a block of a.tpc consecutive tiles (neighbouring
+        // DRAM runs back to back) or, with a.tpc == 0, a grid-strided sequence
+        o << "  const u64 t0 = a.tpc > 0 ? (u64)blockIdx.x * a.tpc : (u64)blockIdx.x;\n";
+        o << "  const u64 tend = a.tpc > 0 ? (t0 + a.tpc < a.total_tiles ? t0 + a.tpc : a.total_tiles) : a.total_tiles;\n";
+        o << "  const u64 tstep = a.tpc > 0 ? 1ull : (u64)gridDim.x;\n";
         if (pf) {
             o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
             o << "    const int row = (int)(t >> " << tpr_log << ");\n";
@@ -613,27 +618,43 @@ struct Gen {
             o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&src[g]) : "
                  "\"memory\");\n";
             o << "    }\n  };\n";
-            o << "  int cur = 0;\n";
+            // S-stage ring (late issue): tile t + (S-1) steps is issued at the
+            // top of tile t; per iteration the commit groups are [Eraw of the
+            // next tile] (epipe only) and [tile data], so tile t is complete
+            // once at most (S-2) * gpi younger groups are pending
+            const int S = late ? stages : 2;
+            const int gpi = epipe ? 2 : 1;  // commit groups per iteration
+            o << "  int cur = 0, ec = 0;\n";
             if (epipe) {
-                o << "  if (blockIdx.x < a.total_tiles) {\n";
-                emit_e_issue("blockIdx.x", "0", "    ");
+                o << "  if (t0 < tend) {\n";
+                emit_e_issue("t0", "0", "    ");
                 o << "  }\n  " << commit;
             }
-            o << "  if (blockIdx.x < a.total_tiles) issue(blockIdx.x, (" << V << " *)smem_raw);\n";
+            o << "  if (t0 < tend) issue(t0, (" << V << " *)smem_raw);\n";
             o << "  " << commit;
+            for (int j = 1; j + 1 < S; ++j) {
+                if (epipe) o << "  " << commit;  // (empty) Eraw slot keeps the group count uniform
+                o << "  if (t0 + " << j << " * tstep < tend) issue(t0 + " << j << " * tstep, (" << V
+                  << " *)smem_raw + (" << j << " << " << K << "));\n";
+                o << "  " << commit;
+            }
             if (epipe) {
-                o << "  asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
-                o << "  if (blockIdx.x < a.total_tiles) {\n";
-                emit_e_compute("blockIdx.x", "0", "    ");
+                o << "  asm volatile(\"cp.async.wait_group " << 1 + (S - 2) * gpi << ";\\n\" ::: \"memory\");\n";
+                o << "  if (t0 < tend) {\n";
+                emit_e_compute("t0", "0", "    ");
                 o << "  }\n";
             }
         } else {
             o << "  " << V << " *tile = (" << V << " *)smem_raw;\n";
             o << "  (void)tile;\n";
         }
-        o << "  for (u64 t = blockIdx.x; t < a.total_tiles; t += gridDim.x) {\n";
-        const std::string issue_next = "    if (t + gridDim.x < a.total_tiles) issue(t + gridDim.x, (" + std::string(V) +
-                                       " *)smem_raw + ((cur ^ 1) << " + std::to_string(K) + "));\n    " + commit;
+        const int S = (pf && late) ? stages : 2;
+        const int gpi = epipe ? 2 : 1;
+        o << "  for (u64 t = t0; t < tend; t += tstep) {\n";
+        const std::string nb = S == 2 ? "(cur ^ 1)" : "((cur + " + std::to_string(S - 1) + ") % " + std::to_string(S) + ")";
+        const std::string issue_next = "    if (t + " + std::to_string(S - 1) + " * tstep < tend) issue(t + " +
+                                       std::to_string(S - 1) + " * tstep, (" + std::string(V) + " *)smem_raw + (" + nb +
+                                       " << " + std::to_string(K) + "));\n    " + commit;
         if (pf) {
             o << "    " << V << " *tile = (" << V << " *)smem_raw + (cur << " << K << ");\n";
             if (!late) o << issue_next;
@@ -648,13 +669,13 @@ struct Gen {
         if (pf) {
             // early issue: tile t + gridDim is already in flight, wait for the
             // older group only. Late issue: this barrier also retires every
-            // read of the other buffer (the previous tile), so the next copy
-            // goes out now and no end-of-tile barrier is needed.
-            o << "    asm volatile(\"cp.async.wait_group " << (late ? 0 : 1) << ";\\n\" ::: \"memory\");\n";
+            // read of the buffer about to be refilled (the previous tile), so
+            // the next copy goes out now and no end-of-tile barrier is needed.
+            o << "    asm volatile(\"cp.async.wait_group " << (late ? (S - 2) * gpi : 1) << ";\\n\" ::: \"memory\");\n";
             o << "    __syncthreads();\n";
             if (epipe) {
-                o << "    if (t + gridDim.x < a.total_tiles) {\n";
-                emit_e_issue("t + gridDim.x", "cur ^ 1", "      ");
+                o << "    if (t + tstep < tend) {\n";
+                emit_e_issue("t + tstep", "ec ^ 1", "      ");
                 o << "    }\n    " << commit;
             }
             if (late) o << issue_next;
@@ -732,11 +753,15 @@ struct Gen {
         if (!late && (G >= 2 || any_e || permuted || pf)) o << "    __syncthreads();\n";
         if (epipe) {
             o << "    asm volatile(\"cp.async.wait_group 1;\\n\" ::: \"memory\");\n";
-            o << "    if (t + gridDim.x < a.total_tiles) {\n";
-            emit_e_compute("t + gridDim.x", "cur ^ 1", "      ");
+            o << "    if (t + tstep < tend) {\n";
+            emit_e_compute("t + tstep", "ec ^ 1", "      ");
             o << "    }\n";
         }
-        if (pf) o << "    cur ^= 1;\n";
+        if (pf) {
+            if (S == 2) o << "    cur ^= 1;\n";
+            else o << "    cur = cur + 1 == " << S << " ? 0 : cur + 1;\n";
+            o << "    ec ^= 1;\n";
+        }
         o << "  }\n";
         if (pf) o << "  asm volatile(\"cp.async.wait_group 0;\\n\" ::: \"memory\");\n";
         o << "}\n";
@@ -747,7 +772,8 @@ struct Gen {
     bool late_issue = true; // prefetch: issue tile t + gridDim after tile t's barrier
     bool late = false;
     int e_stride = 0;
-    std::string eoff() const { return late ? "(cur * " + std::to_string(e_stride) + ") + " : ""; }
+    std::string eoff() const { return late ? "(ec * " + std::to_string(e_stride) + ") + " : ""; }
+    int stages = 2;  // shared tile buffers in prefetch mode (late issue)
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
     std::map<int, int> stab_off; // global table offset -> shared-memory offset
@@ -755,12 +781,26 @@ struct Gen {
 
 } // namespace
 
+// Shared tile buffers of a prefetching pass: QSV_STAGES (default 2), capped
+// so the ring stays within 160 KiB.
+int dbuf_stages(const PassHost &ph, int dtype) {
+    static const int env = [] {
+        const char *e = std::getenv("QSV_STAGES");
+        return e ? std::atoi(e) : 2;
+    }();
+    const size_t tile = static_cast<size_t>(dtype == QSV_C64 ? 8 : 16) << ph.K;
+    int s = std::max(2, std::min(4, env));
+    while (s > 2 && s * tile > (160u << 10)) --s;
+    return s;
+}
+
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf) {
     Gen g(ph, dtype);
     g.double_buffer = false;
     g.prefetch = dbuf;
     const char *pe = std::getenv("QSV_PF_EARLY");
     g.late_issue = !(pe && pe[0] == '1');
+    g.stages = dbuf_stages(ph, dtype);
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const int nchunks = (1 << ph.K) / (16 / amp);

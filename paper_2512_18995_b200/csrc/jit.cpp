@@ -24,6 +24,7 @@
 namespace qsv {
 
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf);
+int dbuf_stages(const PassHost &ph, int dtype);
 bool double_buffer_enabled() {
     const char *e = std::getenv("QSV_DBUF");
     return e && e[0] == '1'; // measured slower than 2 single-buffered CTAs per SM (r01)
@@ -199,7 +200,7 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     dp.threads = threads;
     // groups between the first (loads from HBM) and the last (stores to HBM)
     // exchange amplitudes through a shared tile; a one-group pass needs none
-    dp.smem = dbuf ? 2 * (static_cast<size_t>(amp) << ph.K)
+    dp.smem = dbuf ? dbuf_stages(ph, dtype) * (static_cast<size_t>(amp) << ph.K)
                    : (ph.groups.size() >= 2 || !ph.out_perm.empty()) ? (static_cast<size_t>(amp) << ph.K) : 0;
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
@@ -231,7 +232,7 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
         const void *tables;
         const void *enc_table;
         int batch;
-        int pad;
+        int tpc;  // > 0: each CTA runs a block of tpc consecutive tiles
         void *out;
     } a{};
     a.state = state;
@@ -253,7 +254,14 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
         const char *e = std::getenv("QSV_TILES_PER_CTA");
         return e ? std::atoi(e) : 4;
     }();
-    if (tpc > 0) grid = std::min<uint64_t>(a.total_tiles, std::max<uint64_t>(grid, (a.total_tiles + tpc - 1) / tpc));
+    static const bool blocked = [] {
+        const char *e = std::getenv("QSV_TILE_ORDER");
+        return !(e && e[0] == 's');
+    }();
+    if (tpc > 0) {
+        grid = std::min<uint64_t>(a.total_tiles, std::max<uint64_t>(grid, (a.total_tiles + tpc - 1) / tpc));
+        if (blocked) a.tpc = static_cast<int>((a.total_tiles + grid - 1) / grid);
+    }
     void *args[] = {&a};
     QSV_CUDA(cudaLaunchKernel(dp.jit, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
 }

@@ -18,7 +18,13 @@ for cfg in cfgs:
     opts = json.loads(os.environ.get("QSV_OPTS", "{}")) or None
     p = qsv.Plan(n, cir.gates(), dtype=dt, opts=opts)
     st = qsv.QubitState(n, dtype=dt)
-    runs = [p.profile(st)[: p.info["npasses"]] for _ in range(5)]
+    # random (seeded Gaussian) amplitudes: DRAM power, and so clocks and
+    # times, depend on the data -- a basis state reads as faster than it is
+    psi = W.cfg3_slice(0, 1 << n)
+    psi /= np.sqrt(float(np.vdot(psi, psi).real))
+    st.upload(psi.astype(np.complex64) if dt == qsv.C64 else psi)
+    runs = [p.profile(st)[: p.info["npasses"]] for _ in range(8)]
+    runs = runs[3:]
     best = min(runs, key=lambda m: m.sum())
     amp = 8 if dt == qsv.C64 else 16
     gbs = 2 * amp * (1 << n) / (best.mean() / 1e3) / 1e9

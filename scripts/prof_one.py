@@ -16,6 +16,10 @@ else:
     cir, dt = W.cfg1_circuit(n), qsv.C128
 p = qsv.Plan(n, cir.gates(), dtype=dt)
 st = qsv.QubitState(n, dtype=dt)
+import numpy as np
+psi = W.cfg3_slice(0, 1 << n)
+psi /= np.sqrt(float(np.vdot(psi, psi).real))
+st.upload(psi.astype(np.complex64) if dt == qsv.C64 else psi)
 for _ in range(reps):
     p.execute(st)
 p.ctx.sync()
