@@ -118,6 +118,57 @@ struct Gen {
 
     std::string c(double x) const { return lit(x, f32); }
 
+    // complex128 tile swizzle: the 16-byte slot of amplitude u is u with its
+    // low 3 bits XORed with parities of the high bits (swm[i] = the high bits
+    // folded into bit i). Any such map is linear over GF(2). It is chosen per
+    // pass so that every 8-thread phase of the pass's shared-memory accesses
+    // (each group's set -> slot mapping, the permuted copy-out) hits 8
+    // distinct 16-byte bank groups; the default folds bits 3+i, 6+i, 9+i, 12+i.
+    int swm[3] = {0, 0, 0};
+    int swz_of(int u) const {
+        if (f32) return swz_host(u, true);
+        int f = 0;
+        for (int i = 0; i < 3; ++i) f |= (__builtin_popcount(u & swm[i]) & 1) << i;
+        return u ^ f;
+    }
+    void choose_swizzle(const std::vector<std::vector<int>> &patterns) {
+        const int K = ph.K;
+        auto ok = [&](const int m[3], const std::vector<int> &b) {
+            // the three phase-varying tile bits must map to independent low-bit vectors
+            int v[3];
+            for (int j = 0; j < 3; ++j) {
+                if (b[j] < 3) v[j] = 1 << b[j];
+                else {
+                    v[j] = 0;
+                    for (int i = 0; i < 3; ++i) v[j] |= ((m[i] >> b[j]) & 1) << i;
+                }
+            }
+            return v[0] && v[1] && v[2] && v[0] != v[1] && v[0] != v[2] && v[1] != v[2] && (v[0] ^ v[1]) != v[2];
+        };
+        auto score = [&](const int m[3]) {
+            int n = 0;
+            for (const auto &b : patterns) n += ok(m, b);
+            return n;
+        };
+        int best[3];
+        for (int i = 0; i < 3; ++i) {
+            best[i] = 0;
+            for (int k = 3 + i; k < K; k += 3) best[i] |= 1 << k;
+        }
+        int bs = score(best);
+        uint64_t x = 0x9e3779b97f4a7c15ull;
+        for (int it = 0; it < 4000 && bs < static_cast<int>(patterns.size()); ++it) {
+            int m[3];
+            for (int i = 0; i < 3; ++i) {
+                x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+                m[i] = static_cast<int>(x) & (((1 << K) - 1) & ~7);
+            }
+            const int sc = score(m);
+            if (sc > bs) bs = sc, std::copy(m, m + 3, best);
+        }
+        std::copy(best, best + 3, swm);
+    }
+
     // dst = coefficient * x (complex), with constant folding; returns terms
     // for the real and imaginary parts (appended to re/im lists)
     void term(const cplx &m, const std::string &x, std::vector<std::string> &re, std::vector<std::string> &im) {
@@ -448,9 +499,22 @@ struct Gen {
         if (f32)
             o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; const int f = (w >> 3) ^ "
                  "(w >> 6) ^ (w >> 9) ^ (w >> 12); return ((w ^ (f & 7)) << 1) | (u & 1); }\n";
-        else
-            o << "static __device__ __forceinline__ int swz(int u) { const int f = (u >> 3) ^ (u >> 6) ^ (u >> 9) ^ "
-                 "(u >> 12); return u ^ (f & 7); }\n";
+        else {
+            // patterns of this pass: each group's first three set bits, the
+            // copy-out's first three input bits
+            std::vector<std::vector<int>> pats;
+            for (const HostGroup &g : ph.groups)
+                if (ph.K - ph.R >= 3) pats.push_back({g.ng_bit[0], g.ng_bit[1], g.ng_bit[2]});
+            if (!ph.out_perm.empty()) {
+                std::vector<std::pair<int, int>> q;
+                for (int i = 0; i < ph.K; ++i) q.emplace_back(ph.out_perm[ph.tile_pos[i]], i);
+                std::sort(q.begin(), q.end());
+                pats.push_back({q[0].second, q[1].second, q[2].second});
+            }
+            choose_swizzle(pats);
+            o << "static __device__ __forceinline__ int swz(int u) { return u ^ ((__popc(u & " << swm[0]
+              << ") & 1) | ((__popc(u & " << swm[1] << ") & 1) << 1) | ((__popc(u & " << swm[2] << ") & 1) << 2)); }\n";
+        }
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
           << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; };\n";
         // Double buffering: while tile t is transformed in one shared buffer,
@@ -714,7 +778,7 @@ struct Gen {
             for (int r = 0; r < NR; ++r) {
                 if (from_hbm)
                     o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
-                else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_host(uoff[r], f32) << "];\n";
+                else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_of(uoff[r]) << "];\n";
             }
             // QSV_DEBUG_NOCOMPUTE=1 (diagnostics only): the pass moves data without
             // applying its gates -- the memory-structure ceiling of its geometry
@@ -726,7 +790,7 @@ struct Gen {
                 for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
             for (int r = 0; r < NR; ++r) {
                 if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
-                else o << "      tile[sb ^ " << swz_host(uoff[r], f32) << "] = v" << r << ";\n";
+                else o << "      tile[sb ^ " << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
             if (!to_hbm) o << "    __syncthreads();\n";
