@@ -408,15 +408,24 @@ struct Gen {
             const int cls = t.slot < 0 ? R : t.slot;
             const std::string g = "g" + std::to_string(cls);
             const std::string f = "f" + std::to_string(ti);
-            o << in << V << " " << f << " = "
-              << (t.eidx >= 0 ? "E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]" : "mk(1, 0)") << ";\n";
-            if (t.table >= 0) o << in << f << " = cmulv(" << f << ", tab" << ti << ");\n";
+            // the factor's terms (no multiplication by a constant 1: without
+            // fast-math 0 * x does not fold, so it would cost FP64 work)
+            std::vector<std::string> terms;
+            const bool eh = t.eidx >= 0 && t.table_hi >= 0 && ehoff.count(ti);
+            if (eh)  // per-tile E x hi-table product (computed with E)
+                terms.push_back("EH[" + ehoff_str() + std::to_string(ehoff.at(ti)) + " + (s >> " +
+                                std::to_string(t.lo_bits) + ")]");
+            else if (t.eidx >= 0) terms.push_back("E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]");
+            if (t.table >= 0) terms.push_back("tab" + std::to_string(ti));
             if (t.table_lo >= 0)
-                o << in << f << " = cmulv(" << f << ", stab[" << stab_off.at(t.table_lo) << " + (s & "
-                  << ((1 << t.lo_bits) - 1) << ")]);\n";
-            if (t.table_hi >= 0)
-                o << in << f << " = cmulv(" << f << ", stab[" << stab_off.at(t.table_hi) << " + (s >> " << t.lo_bits
-                  << ")]);\n";
+                terms.push_back("stab[" + std::to_string(stab_off.at(t.table_lo)) + " + (s & " +
+                                std::to_string((1 << t.lo_bits) - 1) + ")]");
+            if (t.table_hi >= 0 && !eh)
+                terms.push_back("stab[" + std::to_string(stab_off.at(t.table_hi)) + " + (s >> " +
+                                std::to_string(t.lo_bits) + ")]");
+            if (terms.empty()) terms.push_back("mk(1, 0)");
+            o << in << V << " " << f << " = " << terms[0] << ";\n";
+            for (size_t k = 1; k < terms.size(); ++k) o << in << f << " = cmulv(" << f << ", " << terms[k] << ");\n";
             for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_factor(ph.recs[k], "pb", f, in);
             if (nfac[cls]++ == 0) o << in << V << " " << g << " = " << f << ";\n";
             else o << in << g << " = cmulv(" << g << ", " << f << ");\n";
@@ -603,6 +612,32 @@ struct Gen {
                 }
             }
         }
+        // E x hi-table rows: a target with both a per-tile factor and a
+        // high-set-bit table gets 2^hi entries per tile, so its flush factor is
+        // one product (EH[s >> lo] * lo[s & mask]) instead of two
+        ehoff.clear();
+        eh_total = 0;
+        // Measured slower (cfg3 30q, interleaved A/B: 27.0 vs 26.3 ms median):
+        // the extra per-tile products sit on the owner threads' path to the
+        // next barrier. Kept behind QSV_X_EH=1 for further experiments.
+        const char *xeh = std::getenv("QSV_X_EH");
+        for (const ETask &e : etasks) {
+            const FlushTarget &t = ph.targets[e.ti];
+            if (t.table_hi < 0 || !(xeh && xeh[0] == '1')) continue;
+            ehoff[e.ti] = eh_total;
+            eh_total += 1 << ((K - R) - t.lo_bits);
+        }
+        if (eh_total) o << "  __shared__ " << V << " EH[" << (late ? 2 * eh_total : eh_total) << "];\n";
+        auto emit_e_store = [&](const ETask &e, const std::string &ehofs, const std::string &eofs,
+                                const std::string &ind) {
+            const FlushTarget &t = ph.targets[e.ti];
+            if (ehoff.count(e.ti)) {
+                const int nh = 1 << ((K - R) - t.lo_bits);
+                for (int j = 0; j < nh; ++j)
+                    o << ind << "EH[" << ehofs << ehoff.at(e.ti) + j << "] = cmulv(f, stab["
+                      << stab_off.at(t.table_hi) + j << "]);\n";
+            } else o << ind << "E[" << eofs << e.slot << "] = f;\n";
+        };
         const bool epipe = pf && late && any_e;
         const std::string tmask = std::to_string((1ull << tpr_log) - 1) + "ull";
         auto emit_e_direct = [&](const std::string &ind) {
@@ -613,7 +648,8 @@ struct Gen {
                     o << ind << "  f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
                       << ") & 255)]);\n";
                 for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", ind + "  ");
-                o << ind << "  E[" << eoff() << e.slot << "] = f;\n" << ind << "}\n";
+                emit_e_store(e, ehoff_str(), eoff(), ind + "  ");
+                o << ind << "}\n";
             }
         };
         auto emit_e_issue = [&](const std::string &tv, const std::string &nb, const std::string &ind) {
@@ -644,7 +680,9 @@ struct Gen {
                     o << ind << "    f = " << (c ? "cmulv(f, " : "(") << "Eraw[(" << nb << ") * " << nraw << " + "
                       << e.raw + c << "]);\n";
                 for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbx", "f", ind + "    ");
-                o << ind << "    E[(" << nb << ") * " << e_stride << " + " << e.slot << "] = f;\n" << ind << "  }\n";
+                emit_e_store(e, "(" + nb + ") * " + std::to_string(eh_total) + " + ",
+                             "(" + nb + ") * " + std::to_string(e_stride) + " + ", ind + "    ");
+                o << ind << "  }\n";
             }
             o << ind << "}\n";
         };
@@ -668,6 +706,22 @@ struct Gen {
             o << "    const u64 g0 = tb | (" << scatter("(u0 >> " + std::to_string(L) + ")", hi, true) << ") | (u0 & "
               << ((1 << L) - 1) << ");\n";
             o << "    const int s0 = swz(u0);\n";
+            const char *xold = std::getenv("QSV_X_OLDISSUE");
+            if (nchunks % threads == 0 && !(xold && xold[0] == '1')) {
+                // unrolled: per chunk one constant global offset (its tile bits
+                // are disjoint from g0's, so OR = ADD) and one constant XOR
+                o << "    const " << V << " *p0 = src + g0;\n";
+                for (int k = 0; k < nchunks / threads; ++k) {
+                    const int uk = k * step;
+                    uint64_t gk = static_cast<uint64_t>(uk & ((1 << L) - 1));
+                    for (size_t i = 0; i < hi.size(); ++i)
+                        if (((uk >> L) >> i) & 1) gk |= 1ull << hi[i];
+                    o << "    asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"((unsigned)"
+                         "__cvta_generic_to_shared(&buf[s0 ^ "
+                      << swz_of(uk) << "])), \"l\"(p0 + " << gk << "ull) : \"memory\");\n";
+                }
+                o << "  };\n";
+            } else {
             if (nchunks % threads == 0) {
                 o << "#pragma unroll\n";
                 o << "    for (int k = 0; k < " << nchunks / threads << "; ++k) {\n";
@@ -682,6 +736,7 @@ struct Gen {
             o << "      asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"(sa), \"l\"(&src[g]) : "
                  "\"memory\");\n";
             o << "    }\n  };\n";
+            }
             // S-stage ring (late issue): tile t + (S-1) steps is issued at the
             // top of tile t; per iteration the commit groups are [Eraw of the
             // next tile] (epipe only) and [tile data], so tile t is complete
@@ -837,6 +892,9 @@ struct Gen {
     bool late = false;
     int e_stride = 0;
     std::string eoff() const { return late ? "(ec * " + std::to_string(e_stride) + ") + " : ""; }
+    std::map<int, int> ehoff;  // FlushTarget index -> first EH entry
+    int eh_total = 0;
+    std::string ehoff_str() const { return late ? "(ec * " + std::to_string(eh_total) + ") + " : ""; }
     int stages = 2;  // shared tile buffers in prefetch mode (late issue)
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
