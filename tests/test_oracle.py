@@ -201,3 +201,21 @@ def test_golden_circuits_port():
     for case in load_circuit_cases():
         got = O.port_forward(case["n"], case["gates"], init=case.get("init"), data=case.get("data"))
         assert np.max(np.abs(got - case["out"])) <= 1e-14, case["name"]
+
+
+@pytest.mark.parametrize("k", [1, 5, 37])
+def test_qft_closed_form_convention(k):
+    """QFT|k> = (1/sqrt N) sum_j exp(+2 pi i j k / N)|j> for the reference's
+    qft_circuit (circuit.hpp:167-178) plus the final swaps (the cfg3 circuit):
+    pins the closed form test_gpu_fullsize.py checks at 30 qubits."""
+    from paper_2512_18995_b200 import workloads as W
+
+    n = 6
+    N = 1 << n
+    psi = np.zeros(N, complex)
+    psi[k] = 1
+    gates = W.cfg3_circuit(n).gates()
+    got = O.ref_forward(n, gates, init=psi)[0] if O.REF_LIB.exists() else O.port_forward(n, gates, init=psi)[0]
+    j = np.arange(N)
+    want = np.exp(2j * np.pi * j * k / N) / np.sqrt(N)
+    assert np.max(np.abs(got - want)) <= 1e-14
