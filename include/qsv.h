@@ -191,6 +191,22 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
 /* marginal_probabilities on row `row`: out has 2^k entries. */
 int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
 
+/* ---- mixed states (density matrices, channels) --------------------------
+ * A batch of m-qubit density matrices is an engine state of 2m qubits holding
+ * vec(rho)[r * 2^m + c] per row (row wires = engine wires 0..m-1, column
+ * wires = m..2m-1). A gate U on wires W acts as U on W and conj(U) on m + W
+ * (state.hpp:159-172: U rho U^dagger); a single-qubit channel is the 4x4
+ * superoperator sum_i K_i (x) conj(K_i) on wires {w, m + w}
+ * (channel.hpp:73-100); both go through qsv_apply_matrix. The reductions read
+ * rho's diagonal (or one flip-diagonal) only. */
+/* Tr[rho P] per observable: out[b * nobs + i]; imaginary residue >= 1e-10
+ * fails like circuit.hpp:280. Replaces expectation_one's mixed branch
+ * (circuit.hpp:264-281). */
+int qsv_density_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
+/* marginal_probabilities' mixed branch (circuit.hpp:199-203): Re rho[i, i]
+ * binned by the outcome bits of `wires` (1..12 wires). */
+int qsv_density_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
+
 /* ---- gradients (quasar::qubit::adjoint_gradients, adjoint.hpp:52-110) ---- */
 /* Gradient of sum_i <O_i> by the adjoint method: param_grads gets one entry
  * per parameter of each trainable, non-encoded gate (circuit order; *nparams

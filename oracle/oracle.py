@@ -320,3 +320,122 @@ def port_gate_matrix(g):
         raise OracleError(k, "qo_gate_matrix failed")
     d = 1 << k
     return out[: 2 * d * d].view(np.complex128).reshape(d, d)
+
+
+# ------------------------------------------------- mixed states (channels) ---
+# Ops of a mixed-state run: a qsv Gate, or (channel_name, wire, parameter)
+# with channel_name in CHANNEL_KINDS (channel.hpp:40-69).
+CHANNEL_KINDS = {"bit_flip": 1, "phase_flip": 2, "depolarizing": 3, "amplitude_damping": 4, "phase_damping": 5}
+
+
+def ref_mixed_run(n, ops, init=None):
+    """to_mixed + apply_gate / apply_channel in order (reference library)."""
+    L = ref()
+    gates = [op for op in ops if not isinstance(op, tuple)]
+    arr, keep = gate_structs(gates)
+    kinds = (C.c_int32 * max(1, len(ops)))(*[0 if not isinstance(op, tuple) else CHANNEL_KINDS[op[0]] for op in ops])
+    wires = (C.c_int32 * max(1, len(ops)))(*[op[1] if isinstance(op, tuple) else 0 for op in ops])
+    params = np.array([op[2] if isinstance(op, tuple) else 0.0 for op in ops] or [0.0])
+    dim = 1 << n
+    out = np.zeros((dim, dim), dtype=np.complex128)
+    ini = None if init is None else np.ascontiguousarray(init, dtype=np.complex128)
+    rc = L.ref_mixed_run(n, None if ini is None else _p(ini), len(ops), kinds, wires, _p(params), arr, _p(out))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return out
+
+
+def ref_density_expectation(n, rho, obs):
+    L = ref()
+    r = np.ascontiguousarray(rho, dtype=np.complex128)
+    arr, keep = _obs_array(obs)
+    out = np.zeros(max(1, len(obs)))
+    rc = L.ref_density_expectation(n, _p(r), len(obs), arr, _p(out))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return out[: len(obs)]
+
+
+def ref_density_marginal(n, rho, wires):
+    L = ref()
+    r = np.ascontiguousarray(rho, dtype=np.complex128)
+    w = (C.c_int32 * len(wires))(*wires)
+    out = np.zeros(1 << len(wires))
+    rc = L.ref_density_marginal(n, _p(r), len(wires), w, _p(out))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return out
+
+
+_SQ = np.sqrt
+_KX = np.array([[0, 1], [1, 0]], complex)
+_KY = np.array([[0, -1j], [1j, 0]], complex)
+_KZ = np.array([[1, 0], [0, -1]], complex)
+
+
+def port_kraus(name, p):
+    """channel.hpp:40-69 restated."""
+    i2 = np.eye(2, dtype=complex)
+    if name == "bit_flip":
+        return [_SQ(1 - p) * i2, _SQ(p) * _KX]
+    if name == "phase_flip":
+        return [_SQ(1 - p) * i2, _SQ(p) * _KZ]
+    if name == "depolarizing":
+        return [_SQ(1 - 3 * p / 4) * i2, _SQ(p / 4) * _KX, _SQ(p / 4) * _KY, _SQ(p / 4) * _KZ]
+    if name == "amplitude_damping":
+        return [np.array([[1, 0], [0, _SQ(1 - p)]], complex), np.array([[0, _SQ(p)], [0, 0]], complex)]
+    if name == "phase_damping":
+        return [np.array([[1, 0], [0, _SQ(1 - p)]], complex), np.array([[0, 0], [0, _SQ(p)]], complex)]
+    raise ValueError(name)
+
+
+def _conjugate_columns_rows(rho, n, m, wires, controls=()):
+    """state.hpp:159-172 / channel.hpp:80-92: M on every column, conj(M) on
+    every row, with the strided kernel restatement."""
+    t = rho.copy()
+    for c in range(t.shape[1]):
+        t[:, c] = port_apply_matrix(t[:, c], n, m, wires, controls)
+    mc = np.conj(m)
+    for r in range(t.shape[0]):
+        t[r, :] = port_apply_matrix(t[r, :], n, mc, wires, controls)
+    return t
+
+
+def port_mixed_run(n, ops, init=None):
+    """Restatement of to_mixed + apply_gate (mixed) + apply_channel."""
+    dim = 1 << n
+    psi = np.zeros(dim, complex) if init is None else np.asarray(init, complex)
+    if init is None:
+        psi[0] = 1
+    rho = np.outer(psi, psi.conj())
+    for op in ops:
+        if isinstance(op, tuple):
+            name, w, p = op
+            rho = sum(_conjugate_columns_rows(rho, n, k, [w]) for k in port_kraus(name, p))
+        else:
+            rho = _conjugate_columns_rows(rho, n, port_gate_matrix(op), op.wires, op.controls)
+    return rho
+
+
+def port_density_expectation(n, rho, wires, basis):
+    """circuit.hpp:264-281 restated: Paulis on every column, then the trace."""
+    t = np.asarray(rho, complex).copy()
+    pm = {"x": _KX, "y": _KY, "z": _KZ}
+    for c in range(t.shape[1]):
+        v = t[:, c]
+        for w, b in zip(wires, basis):
+            v = port_apply_matrix(v, n, pm[b], [w])
+        t[:, c] = v
+    return np.trace(t)
+
+
+def port_density_marginal(n, rho, wires):
+    """circuit.hpp:199-203 restated."""
+    out = np.zeros(1 << len(wires))
+    d = np.real(np.diag(rho))
+    for idx in range(1 << n):
+        o = 0
+        for w in wires:
+            o = (o << 1) | ((idx >> (n - 1 - w)) & 1)
+        out[o] += d[idx]
+    return out

@@ -20,6 +20,10 @@
 //   adjoint_gradients           adjoint.hpp:52-110
 //   qft_circuit                 circuit.hpp:167-178
 //   Rng                         rng.hpp:29-103
+//   to_mixed / apply_gate (mixed) / apply_channel and the channel factories
+//                               state.hpp:73-80,159-172; channel.hpp:22-100
+//   expectation_one / marginal_probabilities on density matrices
+//                               circuit.hpp:199-203,264-281
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -28,6 +32,7 @@
 #include <vector>
 
 #include "quasar/qubit/adjoint.hpp"
+#include "quasar/qubit/channel.hpp"
 #include "quasar/qubit/circuit.hpp"
 #include "quasar/rng.hpp"
 
@@ -254,6 +259,63 @@ int ref_time_apply(int n, const RefGate *gates, int ngates, double *amps, int sk
         const auto t1 = std::chrono::steady_clock::now();
         *seconds = std::chrono::duration<double>(t1 - t0).count();
         from_cvec(s.amplitudes(0), amps);
+    });
+}
+
+/// Mixed-state run: |init> (or |0..0>) promoted with to_mixed(), then ops
+/// in order: kind 0 = apply_gate(gates[next]), kind 1..5 = apply_channel of
+/// bit_flip / phase_flip / depolarizing / amplitude_damping / phase_damping
+/// on wires[i] with parameter params[i]. out = rho (2^n x 2^n row-major).
+int ref_mixed_run(int n, const double *init, int nops, const int32_t *kinds, const int32_t *wires,
+                  const double *params, const RefGate *gates, double *out) {
+    return guard([&] {
+        const std::size_t dim = std::size_t(1) << n;
+        QubitState s = init ? QubitState::from_amplitudes(n, to_cvec(init, dim)) : QubitState::basis(n);
+        s = s.to_mixed();
+        int gi = 0;
+        for (int i = 0; i < nops; ++i) {
+            switch (kinds[i]) {
+            case 0: s = apply_gate(s, to_gate(gates[gi++])); break;
+            case 1: s = apply_channel(s, bit_flip(wires[i], params[i])); break;
+            case 2: s = apply_channel(s, phase_flip(wires[i], params[i])); break;
+            case 3: s = apply_channel(s, depolarizing(wires[i], params[i])); break;
+            case 4: s = apply_channel(s, amplitude_damping(wires[i], params[i])); break;
+            case 5: s = apply_channel(s, phase_damping(wires[i], params[i])); break;
+            default: throw invalid_input("ref_mixed_run: bad op kind");
+            }
+        }
+        const cmat &rho = s.density(0);
+        for (std::size_t r = 0; r < dim; ++r)
+            for (std::size_t c = 0; c < dim; ++c) {
+                out[2 * (r * dim + c)] = rho(r, c).real();
+                out[2 * (r * dim + c) + 1] = rho(r, c).imag();
+            }
+    });
+}
+
+static QubitState density_of(int n, const double *rho) {
+    const std::size_t dim = std::size_t(1) << n;
+    cmat m(dim, dim);
+    for (std::size_t r = 0; r < dim; ++r)
+        for (std::size_t c = 0; c < dim; ++c) m(r, c) = cdouble(rho[2 * (r * dim + c)], rho[2 * (r * dim + c) + 1]);
+    return QubitState::from_density(n, m);
+}
+
+int ref_density_expectation(int n, const double *rho, int nobs, const RefObs *obs, double *out) {
+    return guard([&] {
+        QubitState s = density_of(n, rho);
+        for (int i = 0; i < nobs; ++i) {
+            Observable o{std::vector<int>(obs[i].wires, obs[i].wires + obs[i].nwires), std::string(obs[i].basis)};
+            out[i] = expectation_one(s, o);
+        }
+    });
+}
+
+int ref_density_marginal(int n, const double *rho, int k, const int32_t *wires, double *out) {
+    return guard([&] {
+        QubitState s = density_of(n, rho);
+        auto p = marginal_probabilities(s, std::vector<int>(wires, wires + k));
+        std::memcpy(out, p.data(), p.size() * sizeof(double));
     });
 }
 

@@ -498,6 +498,76 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
     });
 }
 
+namespace {
+void require_canonical_density(const qsv_state *st) {
+    require(st->n % 2 == 0 && st->n >= 2, "density: a mixed state of m qubits is held on 2m engine qubits");
+    require(st->nlocal == st->n, "density: mixed states run on one GPU");
+    for (int w = 0; w < st->n; ++w)
+        require(st->perm[w] == st->n - 1 - w, "density: state layout is not canonical");
+}
+} // namespace
+
+int qsv_density_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
+    return guard([&] {
+        require(st && (nobs == 0 || (obs && out)), "null argument");
+        require_canonical_density(st);
+        const int m = st->n / 2;
+        for (int i = 0; i < nobs; ++i) {
+            const qsv_obs &o = obs[i];
+            require(o.nwires >= 0 && (o.nwires == 0 || (o.wires && o.basis)), "observable: bad wires");
+            require(static_cast<int>(std::strlen(o.basis ? o.basis : "")) == o.nwires,
+                    "observable: one basis letter per wire"); // circuit.hpp:97
+            uint64_t flip = 0, zy = 0;
+            int ny = 0;
+            std::vector<int> seen;
+            for (int j = 0; j < o.nwires; ++j) {
+                const char c = o.basis[j];
+                require(c == 'x' || c == 'y' || c == 'z', "observable: basis letter outside {x,y,z}");
+                const int w = o.wires[j];
+                require(w >= 0 && w < m, "target wire out of range");
+                if (std::find(seen.begin(), seen.end(), w) != seen.end())
+                    fail(QSV_ERR_INVALID, "observable: repeated wire not supported");
+                seen.push_back(w);
+                const uint64_t bit = 1ull << (m - 1 - w);
+                if (c == 'x') flip |= bit;
+                if (c == 'y') flip |= bit, zy |= bit, ++ny;
+                if (c == 'z') zy |= bit;
+            }
+            std::vector<double> v(static_cast<size_t>(st->batch) * 2);
+            reduce_dm_pauli(*st, m, flip, zy, v.data());
+            // Tr[rho P] = i^ny * sum_r rho[r, r ^ flip] (-1)^popc(r & zy)
+            const int q = ny & 3;
+            for (int b = 0; b < st->batch; ++b) {
+                double re = v[2 * b], im = v[2 * b + 1];
+                for (int t = 0; t < q; ++t) {
+                    const double nre = -im, nim = re; // multiply by i
+                    re = nre, im = nim;
+                }
+                // circuit.hpp:280 (1e-10 in double; a complex64 rho is Hermitian to ~1e-7)
+                if (std::abs(im) >= (st->dtype == QSV_C64 ? 1e-5 : 1e-10))
+                    fail(QSV_ERR_INVALID, "expectation: imaginary residue");
+                out[static_cast<size_t>(b) * nobs + i] = re;
+            }
+        }
+    });
+}
+
+int qsv_density_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out) {
+    return guard([&] {
+        require(st && out, "null argument");
+        require(k >= 1 && wires, "measure: empty wire list"); // circuit.hpp:185
+        require(row >= 0 && row < st->batch, "batch index out of range");
+        require_canonical_density(st);
+        const int m = st->n / 2;
+        std::vector<int> bits;
+        for (int i = 0; i < k; ++i) {
+            require(wires[i] >= 0 && wires[i] < m, "target wire out of range");
+            bits.push_back(m - 1 - wires[i]);
+        }
+        reduce_dm_marginal(*st, m, row, bits, out);
+    });
+}
+
 int qsv_adjoint_gradients(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, int nobs,
                           const qsv_obs *obs, const double *init, const double *data, int slots,
                           double *param_grads, int param_cap, int *nparams, double *data_grads) {

@@ -244,6 +244,60 @@ __global__ void __launch_bounds__(256) marginal_kernel(const typename Vec2<T>::t
         out_partial[static_cast<size_t>(blockIdx.x) * nb + j] = hist[j];
 }
 
+// Mixed states: the engine holds rho (2^m x 2^m, row-major) as the 2m-qubit
+// vector vec(rho)[r * 2^m + c] (row wires = the high m bits). Tr[rho P] for a
+// Pauli string P is sum_r rho[r, r ^ flip] * (-1)^popc(r & zy) times i^#Y
+// (applied by the caller): only the 2^m entries of one "diagonal" are read.
+template <typename T>
+__global__ void __launch_bounds__(256) dm_pauli_kernel(const typename Vec2<T>::type *__restrict__ st,
+                                                       uint64_t row_stride, int m, uint64_t flip, uint64_t zy,
+                                                       double *__restrict__ partial) {
+    using V = typename Vec2<T>::type;
+    const int row = blockIdx.y;
+    const V *p = st + static_cast<size_t>(row) * row_stride;
+    const uint64_t dim = 1ull << m;
+    double re = 0.0, im = 0.0;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < dim;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const V a = p[(r << m) | (r ^ flip)];
+        const double sgn = (__popcll(r & zy) & 1) ? -1.0 : 1.0;
+        re += sgn * static_cast<double>(a.x);
+        im += sgn * static_cast<double>(a.y);
+    }
+    __shared__ double red[2][8];
+    re = warp_sum(re);
+    im = warp_sum(im);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) red[0][wid] = re, red[1][wid] = im;
+    __syncthreads();
+    if (threadIdx.x < 2) {
+        double s = 0.0;
+        for (int w = 0; w < (blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
+        partial[(static_cast<size_t>(row) * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = s;
+    }
+}
+
+// marginal_probabilities of a mixed state: bins of Re rho[r, r] (circuit.hpp:199-203).
+template <typename T>
+__global__ void __launch_bounds__(256) dm_marginal_kernel(const typename Vec2<T>::type *__restrict__ p, int m,
+                                                          const int *__restrict__ bits, int k,
+                                                          double *__restrict__ out_partial) {
+    extern __shared__ double hist[];
+    const int nb = 1 << k;
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) hist[j] = 0.0;
+    __syncthreads();
+    const uint64_t dim = 1ull << m;
+    for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < dim;
+         r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double w = static_cast<double>(p[(r << m) | r].x);
+        int o = 0;
+        for (int j = 0; j < k; ++j) o = (o << 1) | static_cast<int>((r >> bits[j]) & 1ull);
+        atomicAdd(&hist[o], w);
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < nb; j += blockDim.x) out_partial[static_cast<size_t>(blockIdx.x) * nb + j] = hist[j];
+}
+
 int grid_for(uint64_t work, int threads, int sm_count) {
     const uint64_t want = (work + threads - 1) / threads;
     const uint64_t cap = static_cast<uint64_t>(sm_count) * 8;
@@ -378,6 +432,51 @@ void reduce_pauli(State &st, uint64_t flip, uint64_t zy, double *host_out) {
     if (st.ctx->world > 1) dist_allreduce_sum(*st.ctx, out.as<double>(), static_cast<size_t>(rows) * 2);
     QSV_CUDA(cudaMemcpyAsync(host_out, out.p, sizeof(double) * rows * 2, cudaMemcpyDeviceToHost, s));
     QSV_CUDA(cudaStreamSynchronize(s));
+}
+
+void reduce_dm_pauli(State &st, int m, uint64_t flip, uint64_t zy, double *host_out) {
+    require(2 * m == st.n && st.nlocal == st.n, "density: state is not a single-GPU vectorised density matrix");
+    const int rows = st.batch;
+    const uint64_t dim = 1ull << m;
+    const int per_row = std::max(1, std::min<int>(static_cast<int>((dim + 255) / 256), st.ctx->sm_count * 4));
+    DevBuf partial(sizeof(double) * rows * per_row * 2), out(sizeof(double) * rows * 2);
+    const dim3 grid(per_row, rows);
+    cudaStream_t s = st.ctx->stream;
+    if (st.dtype == QSV_C64)
+        dm_pauli_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float2 *>(st.d), st.local_amps, m, flip, zy, partial.as<double>());
+    else
+        dm_pauli_kernel<double><<<grid, 256, 0, s>>>(static_cast<const double2 *>(st.d), st.local_amps, m, flip, zy, partial.as<double>());
+    QSV_CUDA(cudaGetLastError());
+    reduce_partials_kernel<<<rows, 64, 0, s>>>(partial.as<double>(), per_row, 2, out.as<double>());
+    QSV_CUDA(cudaGetLastError());
+    QSV_CUDA(cudaMemcpyAsync(host_out, out.p, sizeof(double) * rows * 2, cudaMemcpyDeviceToHost, s));
+    QSV_CUDA(cudaStreamSynchronize(s));
+}
+
+void reduce_dm_marginal(State &st, int m, int row, const std::vector<int> &bits_r, double *host_out) {
+    require(2 * m == st.n && st.nlocal == st.n, "density: state is not a single-GPU vectorised density matrix");
+    const int k = static_cast<int>(bits_r.size());
+    require(k >= 1 && k <= 12, "marginal_probs: 1..12 wires supported for density matrices");
+    const int nb = 1 << k;
+    const uint64_t dim = 1ull << m;
+    const int blocks = std::max(1, std::min<int>(static_cast<int>((dim + 255) / 256), st.ctx->sm_count * 2));
+    DevBuf bits(sizeof(int) * k), partial(sizeof(double) * static_cast<size_t>(blocks) * nb);
+    cudaStream_t s = st.ctx->stream;
+    QSV_CUDA(cudaMemcpyAsync(bits.p, bits_r.data(), sizeof(int) * k, cudaMemcpyHostToDevice, s));
+    const size_t smem = sizeof(double) * nb;
+    if (st.dtype == QSV_C64)
+        dm_marginal_kernel<float><<<blocks, 256, smem, s>>>(static_cast<const float2 *>(st.d) + static_cast<size_t>(row) * st.local_amps, m, bits.as<int>(), k, partial.as<double>());
+    else
+        dm_marginal_kernel<double><<<blocks, 256, smem, s>>>(static_cast<const double2 *>(st.d) + static_cast<size_t>(row) * st.local_amps, m, bits.as<int>(), k, partial.as<double>());
+    QSV_CUDA(cudaGetLastError());
+    std::vector<double> host(static_cast<size_t>(blocks) * nb);
+    QSV_CUDA(cudaMemcpyAsync(host.data(), partial.p, sizeof(double) * host.size(), cudaMemcpyDeviceToHost, s));
+    QSV_CUDA(cudaStreamSynchronize(s));
+    for (int j = 0; j < nb; ++j) {
+        double acc = 0.0;
+        for (int b = 0; b < blocks; ++b) acc += host[static_cast<size_t>(b) * nb + j];
+        host_out[j] = acc;
+    }
 }
 
 void reduce_norm2(State &st, double *host_out) {

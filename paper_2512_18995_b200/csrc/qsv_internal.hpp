@@ -316,6 +316,10 @@ void reduce_norm2(State &st, double *host_out);
 void reduce_z_all(State &st, double *host_out /* batch x kZ: [total, S_bit0..] */);
 void reduce_pauli(State &st, uint64_t flip, uint64_t zy, double *host_out /* batch x 2 */);
 void reduce_marginal(State &st, int row, const std::vector<int> &phys_bits, double *host_out);
+// Mixed states held as vec(rho) on 2m qubits (row wires high): Tr-type sums
+// along the flip-diagonal, and diagonal marginals (bits are positions in r).
+void reduce_dm_pauli(State &st, int m, uint64_t flip, uint64_t zy, double *host_out /* batch x 2 */);
+void reduce_dm_marginal(State &st, int m, int row, const std::vector<int> &bits_r, double *host_out);
 
 // ---- distributed (dist.cu) -------------------------------------------------
 void nccl_unique_id(void *out128);

@@ -127,6 +127,8 @@ _SIGS = {
     "qsv_expect_z_all": (C.c_int, [_P, C.c_void_p]),
     "qsv_expect_pauli": (C.c_int, [_P, C.c_int, C.POINTER(qsv_obs), C.c_void_p]),
     "qsv_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
+    "qsv_density_expect_pauli": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_void_p]),
+    "qsv_density_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
     "qsv_rng_fill": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int]),
     "qsv_rng_fill_at": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p, C.c_int]),
     "qsv_plan_steps": (C.c_int, [_P, C.c_void_p, C.c_int]),
@@ -346,6 +348,7 @@ class QubitState:
         n, b, d, g, la = C.c_int(), C.c_int(), C.c_int(), C.c_int(), C.c_uint64()
         check(lib().qsv_state_info(self.h, C.byref(n), C.byref(b), C.byref(d), C.byref(g), C.byref(la)))
         self._n, self._batch, self.dtype, self.global_bits, self.local_amps = n.value, b.value, d.value, g.value, la.value
+        self._mixed = None  # m when this engine state holds vec(rho) of m-qubit density matrices
 
     # reference constructors
     @staticmethod
@@ -369,7 +372,50 @@ class QubitState:
         return s
 
     def nqubit(self) -> int:
-        return self._n
+        return self._mixed if self._mixed is not None else self._n
+
+    def is_mixed(self) -> bool:
+        return self._mixed is not None
+
+    # ---- mixed states (state.hpp:53-62, 73-80; channel.hpp) ----
+    @staticmethod
+    def from_density(nqubit: int, rho, dtype: int = C128, ctx: Context | None = None) -> "QubitState":
+        """state.hpp:53-62: shape, Hermitian within 1e-9, unit trace within 1e-10."""
+        r = np.ascontiguousarray(rho, dtype=np.complex128)
+        dim = 1 << nqubit
+        if r.shape != (dim, dim):
+            raise InvalidInput("QubitState: density shape mismatch")
+        if np.max(np.abs(r - r.conj().T)) >= 1e-9:
+            raise InvalidInput("QubitState: rho not Hermitian")
+        if abs(np.trace(r).real - 1.0) >= 1e-10:
+            raise InvalidInput("QubitState: trace != 1")
+        s = QubitState(2 * nqubit, dtype=dtype, ctx=ctx)
+        s.upload(r.reshape(-1))
+        s._mixed = nqubit
+        return s
+
+    def to_mixed(self) -> "QubitState":
+        """state.hpp:73-80: rows become |psi><psi| (vec(rho) on 2m engine
+        qubits, built on the host: O(4^m) host memory)."""
+        if self._mixed is not None:
+            return self.clone()
+        m = self._n
+        if 2 * m > 34:
+            raise InvalidInput("to_mixed: 2n engine qubits exceed one GPU")
+        s = QubitState(2 * m, batch=self._batch, dtype=self.dtype, ctx=self.ctx)
+        for b in range(self._batch):
+            a = self.amplitudes(b)
+            s.upload(np.outer(a, a.conj()).reshape(-1), b)
+        s._mixed = m
+        return s
+
+    def density(self, b: int = 0) -> np.ndarray:
+        if self._mixed is None:
+            raise InvalidInput("QubitState: not a mixed state")
+        out = np.empty(self.local_amps, dtype=np.complex128)
+        check(lib().qsv_state_download(self.h, b, _ptr(out.view(np.float64)), self.local_amps))
+        d = 1 << self._mixed
+        return out.reshape(d, d)
 
     def batch(self) -> int:
         return self._batch
@@ -379,6 +425,8 @@ class QubitState:
         check(lib().qsv_state_upload(self.h, row, _ptr(a.view(np.float64)), a.size))
 
     def amplitudes(self, b: int = 0) -> np.ndarray:
+        if self._mixed is not None:
+            raise InvalidInput("QubitState: mixed state has no amplitudes (use density)")
         out = np.empty(self.local_amps, dtype=np.complex128)
         check(lib().qsv_state_download(self.h, b, _ptr(out.view(np.float64)), self.local_amps))
         return out
@@ -386,7 +434,9 @@ class QubitState:
     def clone(self) -> "QubitState":
         h = C.c_void_p()
         check(lib().qsv_state_clone(self.h, C.byref(h)))
-        return QubitState(self._n, ctx=self.ctx, _handle=h)
+        out = QubitState(self._n, ctx=self.ctx, _handle=h)
+        out._mixed = self._mixed
+        return out
 
     def norm2(self) -> np.ndarray:
         out = np.zeros(self._batch)
@@ -421,8 +471,123 @@ class QubitState:
             pass
 
 
+def approx_unitary(u, tol: float = 1e-8) -> bool:
+    """core.hpp:53-57."""
+    u = np.asarray(u, dtype=np.complex128)
+    if u.ndim != 2 or u.shape[0] != u.shape[1]:
+        return False
+    return float(np.max(np.abs(u.conj().T @ u - np.eye(u.shape[0])))) < tol
+
+
+# --------------------------------------------------------------- channels ---
+@dataclass
+class Channel:
+    """channel.hpp:22-27: a single-qubit channel as a Kraus set."""
+    name: str
+    wire: int
+    kraus: list
+
+
+def make_channel(name: str, wire: int, kraus) -> Channel:
+    """channel.hpp:29-38: 2x2 Kraus operators, sum K^dagger K = I within 1e-10."""
+    ks = [np.asarray(k, dtype=np.complex128) for k in kraus]
+    acc = np.zeros((2, 2), dtype=np.complex128)
+    for k in ks:
+        if k.shape != (2, 2):
+            raise InvalidInput("channel: Kraus operators must be 2x2")
+        acc += k.conj().T @ k
+    if np.max(np.abs(acc - np.eye(2))) >= 1e-10:
+        raise InvalidInput("channel: Kraus set not trace preserving")
+    return Channel(str(name), int(wire), ks)
+
+
+_PX = np.array([[0, 1], [1, 0]], dtype=np.complex128)
+_PY = np.array([[0, -1j], [1j, 0]], dtype=np.complex128)
+_PZ = np.array([[1, 0], [0, -1]], dtype=np.complex128)
+_I2 = np.eye(2, dtype=np.complex128)
+
+
+def bit_flip(wire: int, p: float) -> Channel:  # channel.hpp:40-43
+    return make_channel("bit_flip", wire, [math.sqrt(1 - p) * _I2, math.sqrt(p) * _PX])
+
+
+def phase_flip(wire: int, p: float) -> Channel:  # channel.hpp:45-48
+    return make_channel("phase_flip", wire, [math.sqrt(1 - p) * _I2, math.sqrt(p) * _PZ])
+
+
+def depolarizing(wire: int, p: float) -> Channel:  # channel.hpp:50-55
+    return make_channel("depolarizing", wire, [math.sqrt(1 - 3.0 * p / 4.0) * _I2, math.sqrt(p / 4.0) * _PX,
+                                               math.sqrt(p / 4.0) * _PY, math.sqrt(p / 4.0) * _PZ])
+
+
+def amplitude_damping(wire: int, gamma: float) -> Channel:  # channel.hpp:57-62
+    return make_channel("amplitude_damping", wire, [np.array([[1, 0], [0, math.sqrt(1 - gamma)]]),
+                                                    np.array([[0, math.sqrt(gamma)], [0, 0]])])
+
+
+def phase_damping(wire: int, lam: float) -> Channel:  # channel.hpp:64-69
+    return make_channel("phase_damping", wire, [np.array([[1, 0], [0, math.sqrt(1 - lam)]]),
+                                                np.array([[0, 0], [0, math.sqrt(lam)]])])
+
+
+def density_trace(state: QubitState) -> np.ndarray:
+    """Tr rho per batch row (the identity observable on the device)."""
+    arr = (qsv_obs * 1)()
+    arr[0].nwires = 0
+    arr[0].wires = None
+    arr[0].basis = b""
+    out = np.zeros(state.batch())
+    check(lib().qsv_density_expect_pauli(state.h, 1, arr, _ptr(out)))
+    return out
+
+
+def apply_channel(state: QubitState, ch: Channel) -> QubitState:
+    """channel.hpp:73-100: rho' = sum_i K_i rho K_i^dagger, pure states
+    promoted first. On the device this is ONE pass: the 4x4 superoperator
+    sum_i K_i (x) conj(K_i) on the (row, column) wire pair of vec(rho)."""
+    out = state.to_mixed()
+    m = out.nqubit()
+    if not 0 <= ch.wire < m:
+        raise InvalidInput("target wire out of range")
+    sop = sum(np.kron(k, k.conj()) for k in ch.kraus)
+    out.apply_matrix(sop, [ch.wire, ch.wire + m])
+    tr = density_trace(out)
+    # channel.hpp:96 checks 1e-10 in double; a complex64 state carries ~1e-7
+    if np.any(np.abs(tr - 1.0) >= (1e-10 if out.dtype == C128 else 1e-5)):
+        raise InvalidInput("channel: trace not preserved")
+    return out
+
+
+def _conj_gate(g: Gate, m: int) -> Gate:
+    """conj(U) of gate g acting on the column wires m + w of vec(rho)."""
+    return Gate("custom", [w + m for w in g.wires], [c + m for c in g.controls], [], False, False,
+                np.conj(gate_matrix(g)))
+
+
+def _mixed_gates(gates, m: int) -> list:
+    """The 2m-qubit circuit of U rho U^dagger (state.hpp:159-172): each gate on
+    the row wires, then its conjugate on the column wires."""
+    out = []
+    for g in gates:
+        if g.encode:
+            raise InvalidInput("encoded batch runs expect a pure initial state")  # circuit.hpp:131
+        out += [g, _conj_gate(g, m)]
+    return out
+
+
 def apply_gate(state: QubitState, g: Gate) -> QubitState:
-    """Value semantics like state.hpp:149-157: returns a new state."""
+    """Value semantics like state.hpp:149-157: returns a new state. A mixed
+    state gets U on its row wires and conj(U) on its column wires."""
+    if state.is_mixed():
+        m = state.nqubit()
+        if not approx_unitary(gate_matrix(g), 1e-10):
+            raise InvalidInput(f"gate {g.name}: matrix not unitary")
+        out = state.clone()
+        for h in (g, _conj_gate(g, m)):
+            keep: list = []
+            cg = _to_c_gate(h, keep)
+            check(lib().qsv_apply_gate(out.h, C.byref(cg)))
+        return out
     out = state.clone()
     keep: list = []
     cg = _to_c_gate(g, keep)
@@ -511,12 +676,18 @@ class Circuit:
             if slots != 0:
                 raise InvalidInput("circuit has encode slots but no data given")
             s = init.clone() if init is not None else QubitState.basis(self._n, dtype=dtype, ctx=ctx)
+            if s.is_mixed():  # the same fused passes on the 2m-qubit vec(rho)
+                arr, keep = gate_array(_mixed_gates(self._gates, self._n))
+                check(lib().qsv_run_circuit(s.h, arr, 2 * len(self._gates), None, 0, 0, C.byref(o)))
+                return s
             check(lib().qsv_run_circuit(s.h, arr, len(self._gates), None, 0, 0, C.byref(o)))
             return s
         rows = [list(map(float, r)) for r in data]
         for r in rows:
             if len(r) != slots:
                 raise InvalidInput(f"data length {len(r)} != encode slots {slots}")
+        if init is not None and init.is_mixed():
+            raise InvalidInput("encoded batch runs expect a pure initial state")  # circuit.hpp:131
         if init is not None and init.batch() != 1:
             raise InvalidInput("encoded runs broadcast a single initial state")
         dt = init.dtype if init is not None else dtype
@@ -615,7 +786,8 @@ def expectation_many(state: QubitState, obs: Sequence[Observable]) -> np.ndarray
         arr[i].wires = C.cast(w, C.POINTER(C.c_int32))
         arr[i].basis = b
     out = np.zeros(state.batch() * max(1, len(obs)))
-    check(lib().qsv_expect_pauli(state.h, len(obs), arr, _ptr(out)))
+    fn = lib().qsv_density_expect_pauli if state.is_mixed() else lib().qsv_expect_pauli
+    check(fn(state.h, len(obs), arr, _ptr(out)))
     return out.reshape(state.batch(), max(1, len(obs)))[:, : len(obs)]
 
 
@@ -631,6 +803,9 @@ def marginal_probabilities(state: QubitState, wires, batch_index: int = 0) -> np
     k = len(wires)
     w = (C.c_int32 * k)(*wires)
     out = np.zeros(1 << k)
+    if state.is_mixed():
+        check(lib().qsv_density_marginal_probs(state.h, batch_index, k, w, _ptr(out)))
+        return out
     check(lib().qsv_marginal_probs(state.h, batch_index, k, w, _ptr(out)))
     return out
 
@@ -660,6 +835,8 @@ def adjoint_gradients(cir: Circuit, init: "QubitState | None" = None, data=(), d
     d = np.ascontiguousarray(np.asarray(list(data), dtype=np.float64))
     ini = None
     if init is not None:
+        if init.is_mixed():
+            raise InvalidInput("adjoint_gradients: pure states only")  # adjoint.hpp:54
         if init.batch() != 1:
             raise InvalidInput("adjoint_gradients: one batch row at a time")
         ini = np.ascontiguousarray(init.amplitudes(0)).view(np.float64)

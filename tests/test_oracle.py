@@ -219,3 +219,30 @@ def test_qft_closed_form_convention(k):
     j = np.arange(N)
     want = np.exp(2j * np.pi * j * k / N) / np.sqrt(N)
     assert np.max(np.abs(got - want)) <= 1e-14
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="reference headers/library absent")
+def test_mixed_state_port_matches_reference():
+    """The density-matrix restatement (oracle.port_mixed_run & co.) equals the
+    reference's to_mixed / apply_gate / apply_channel / expectation /
+    marginals on seeded circuits with every channel kind (test_qubit.cpp:376-420
+    exercises the same functions)."""
+    from paper_2512_18995_b200.qsv import make_gate
+
+    rng = np.random.default_rng(5)
+    n = 3
+    ops = [make_gate("h", [0]), make_gate("x", [1], [0]), ("depolarizing", 0, 0.3),
+           make_gate("ry", [2], [], [0.7]), ("amplitude_damping", 2, 0.4), make_gate("rzz", [0, 2], [], [0.5]),
+           ("bit_flip", 1, 0.2), ("phase_flip", 0, 0.1), ("phase_damping", 1, 0.6),
+           make_gate("u3", [1], [2], [0.3, 0.2, 0.1])]
+    psi = rng.normal(size=8) + 1j * rng.normal(size=8)
+    psi /= np.linalg.norm(psi)
+    for init in (None, psi):
+        want = O.ref_mixed_run(n, ops, init)
+        got = O.port_mixed_run(n, ops, init)
+        assert np.max(np.abs(got - want)) <= 1e-14
+        for wires, basis in (([0], "z"), ([1, 2], "xy"), ([0, 1, 2], "zzx")):
+            e = O.ref_density_expectation(n, want, [(wires, basis)])[0]
+            assert abs(O.port_density_expectation(n, want, wires, basis) - e) <= 1e-14
+        assert np.allclose(O.port_density_marginal(n, want, [2, 0]), O.ref_density_marginal(n, want, [2, 0]),
+                           atol=1e-15, rtol=0)
