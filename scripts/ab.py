@@ -18,12 +18,17 @@ psi /= np.sqrt(float(np.vdot(psi, psi).real))
 st.upload(psi.astype(np.complex64) if dt == qsv.C64 else psi)
 plans = []
 for v in variants:
+    opts = {}
     for kv in filter(None, v.split(",")):
         k, val = kv.split("=")
-        os.environ[k] = val
-    plans.append(qsv.Plan(n, cir.gates(), dtype=dt))
+        if k.startswith("OPT_"):
+            opts[k[4:]] = int(val)
+        else:
+            os.environ[k] = val
+    plans.append(qsv.Plan(n, cir.gates(), dtype=dt, opts=opts or None))
     for kv in filter(None, v.split(",")):
-        os.environ.pop(kv.split("=")[0])
+        if not kv.startswith("OPT_"):
+            os.environ.pop(kv.split("=")[0])
 res = {v: [] for v in variants}
 for rep in range(int(os.environ.get("AB_REPS", "20"))):
     for v, p in zip(variants, plans):
