@@ -177,6 +177,12 @@ int qsv_plan_create(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, 
 int qsv_plan_destroy(qsv_plan *plan);
 int qsv_plan_info_get(const qsv_plan *plan, qsv_plan_info *info);
 int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots);
+/* Circuit::forward(data) followed by expectation() of the n single-qubit Z
+ * observables (circuit.hpp:121-157, 248-282): out[b * n + w] = <Z_w> for every
+ * batch row. When the plan's last pass holds a whole row per tile (batched
+ * small circuits) the |a|^2 sums are fused into that pass (no second read of
+ * the state); otherwise one extra reduction pass runs. */
+int qsv_plan_execute_expect_z(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots, double *out);
 /* Execute once with a CUDA event pair around every launch; launch_ms gets
  * npasses durations (ms). */
 int qsv_plan_profile(qsv_plan *plan, qsv_state *st, double *launch_ms);

@@ -18,7 +18,6 @@ namespace qsv {
 void build_plan(Plan &p, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts);
 void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates,
                          const qsv_opts *opts);
-void execute_plan(Plan &p, State &st, const double *data, int rows, int slots);
 void profile_plan(Plan &p, State &st, double *launch_ms);
 int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads, uint64_t offset);
 void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates, int nobs, const qsv_obs *obs,
@@ -407,6 +406,13 @@ int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows
     return guard([&] {
         require(plan && st, "null argument");
         execute_plan(*plan, *st, data, rows, slots);
+    });
+}
+
+int qsv_plan_execute_expect_z(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots, double *out) {
+    return guard([&] {
+        require(plan && st && out, "null argument");
+        execute_plan_z(*plan, *st, data, rows, slots, out);
     });
 }
 

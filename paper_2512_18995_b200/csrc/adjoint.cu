@@ -20,7 +20,6 @@
 namespace qsv {
 
 void build_plan(Plan &p, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts);
-void execute_plan(Plan &p, State &st, const double *data, int rows, int slots);
 
 namespace {
 

@@ -525,7 +525,7 @@ struct Gen {
               << ") & 1) | ((__popc(u & " << swm[1] << ") & 1) << 1) | ((__popc(u & " << swm[2] << ") & 1) << 2)); }\n";
         }
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
-          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; };\n";
+          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; };\n";
         // Double buffering: while tile t is transformed in one shared buffer,
         // the cp.async copies of tile t + gridDim are already in flight into
         // the other (one CTA per SM, 2 x 2^K amplitudes).
@@ -806,6 +806,13 @@ struct Gen {
             o << "    // ---- group " << gi << "\n";
             std::vector<int> ngt(g.ng_bit, g.ng_bit + (K - R)), ngp;
             for (int b : ngt) ngp.push_back(ph.tile_pos[b]);
+            const bool zhere = zsum && to_hbm;
+            if (zhere) {
+                // fused <Z> epilogue (one tile = one whole row): per-thread sums of
+                // |a|^2 in total and per physical bit, FP64
+                o << "    double zacc[" << K + 1 << "];\n";
+                o << "#pragma unroll\n    for (int j = 0; j < " << K + 1 << "; ++j) zacc[j] = 0.0;\n";
+            }
             o << "    for (int s = threadIdx.x; s < " << nsets << "; s += " << threads << ") {\n";
             o << "      const int ub = " << scatter("s", ngt, false) << ";\n";
             o << "      const int sb = swz(ub);\n";
@@ -843,11 +850,42 @@ struct Gen {
             }();
             if (!nocompute)
                 for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
+            if (zhere) {
+                o << "      { double zt = 0.0";
+                for (int j = 0; j < R; ++j) o << ", zs" << j << " = 0.0";
+                o << ";\n";
+                for (int r = 0; r < NR; ++r) {
+                    o << "        { const double q = (double)v" << r << ".x * v" << r << ".x + (double)v" << r << ".y * v" << r
+                      << ".y; zt += q;";
+                    for (int j = 0; j < R; ++j)
+                        if ((r >> j) & 1) o << " zs" << j << " += q;";
+                    o << " }\n";
+                }
+                o << "        zacc[0] += zt;\n";
+                for (int j = 0; j < R; ++j) o << "        zacc[" << 1 + ph.tile_pos[g.slot_bit[j]] << "] += zs" << j << ";\n";
+                for (size_t i = 0; i < ngt.size(); ++i)
+                    o << "        if ((s >> " << i << ") & 1) zacc[" << 1 + ph.tile_pos[ngt[i]] << "] += zt;\n";
+                o << "      }\n";
+            }
             for (int r = 0; r < NR; ++r) {
                 if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
                 else o << "      tile[sb ^ " << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
+            if (zhere) {
+                // block reduction: warp shuffles, then one partial per warp
+                const int nw = threads / 32;
+                o << "    {\n      __shared__ double zred[" << nw << "][" << K + 1 << "];\n";
+                o << "#pragma unroll\n      for (int j = 0; j < " << K + 1 << "; ++j) {\n";
+                o << "        double x = zacc[j];\n";
+                o << "        for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);\n";
+                o << "        if ((threadIdx.x & 31) == 0) zred[threadIdx.x >> 5][j] = x;\n      }\n";
+                o << "      __syncthreads();\n";
+                o << "      if (threadIdx.x < " << K + 1 << ") {\n        double x = 0.0;\n";
+                o << "        for (int w = 0; w < " << nw << "; ++w) x += zred[w][threadIdx.x];\n";
+                o << "        a.zout[(u64)row * " << K + 1 << " + threadIdx.x] = x;\n      }\n";
+                o << "      __syncthreads();\n    }\n";
+            }
             if (!to_hbm) o << "    __syncthreads();\n";
         }
         if (permuted) {
@@ -896,6 +934,7 @@ struct Gen {
     int eh_total = 0;
     std::string ehoff_str() const { return late ? "(ec * " + std::to_string(eh_total) + ") + " : ""; }
     int stages = 2;  // shared tile buffers in prefetch mode (late issue)
+    bool zsum = false; // fused <Z> epilogue in the last group (whole-row tiles)
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
     std::map<int, int> stab_off; // global table offset -> shared-memory offset
@@ -916,8 +955,10 @@ int dbuf_stages(const PassHost &ph, int dtype) {
     return s;
 }
 
-std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf) {
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
+                                 bool zsum) {
     Gen g(ph, dtype);
+    g.zsum = zsum;
     g.double_buffer = false;
     g.prefetch = dbuf;
     const char *pe = std::getenv("QSV_PF_EARLY");

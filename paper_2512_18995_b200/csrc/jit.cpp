@@ -23,7 +23,8 @@
 
 namespace qsv {
 
-std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf);
+std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
+                                 bool zsum = false);
 int dbuf_stages(const PassHost &ph, int dtype);
 bool double_buffer_enabled() {
     const char *e = std::getenv("QSV_DBUF");
@@ -164,8 +165,9 @@ struct JitKernel {
     cudaKernel_t kernel = nullptr;
 };
 
-// Compiles (or fetches) the specialised kernel of one pass and fills dp.
-void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
+// Compiles (or fetches) the specialised kernel of one pass and fills dp
+// (zsum: the variant with the fused <Z> epilogue, dp.jit_z / dp.grid_z).
+static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, bool zsum) {
     const std::string name = "qsv_pass";
     int threads = 256;
     // prefetch (two shared tiles, cp.async of the next tile in flight) when
@@ -175,7 +177,7 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
     const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
                       (1 << ph.K) * amp0 >= 16 * 32;
     (void)double_buffer_enabled;
-    std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf);
+    std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf, zsum);
     char key[32];
     std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
     std::vector<char> cubin = compile(src, key);
@@ -196,7 +198,22 @@ void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
         }
     }
     const int amp = dtype == QSV_C64 ? 8 : 16;
-    dp.jit = reinterpret_cast<const void *>(jk.kernel);
+    const void *kern = reinterpret_cast<const void *>(jk.kernel);
+    if (zsum) {
+        require(threads == dp.threads, "jit: <Z> variant changed the CTA shape");
+        int optin = 0;
+        QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        cudaFuncAttributes fa{};
+        QSV_CUDA(cudaFuncGetAttributes(&fa, kern));
+        QSV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      optin - static_cast<int>(fa.sharedSizeBytes)));
+        int blocks = 0;
+        QSV_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, kern, dp.threads, dp.smem));
+        dp.jit_z = kern;
+        dp.grid_z = std::max(1, blocks) * sm_count;
+        return;
+    }
+    dp.jit = kern;
     dp.threads = threads;
     // groups between the first (loads from HBM) and the last (stores to HBM)
     // exchange amplitudes through a shared tile; a one-group pass needs none
@@ -225,7 +242,10 @@ std::string jit_source(const PassHost &ph, int dtype) {
     return generate_pass_source(ph, dtype, "qsv_pass", &threads, dbuf);
 }
 
-void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s) {
+void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) { jit_build(dp, ph, dtype, sm_count, false); }
+void jit_prepare_z(DevPass &dp, const PassHost &ph, int dtype, int sm_count) { jit_build(dp, ph, dtype, sm_count, true); }
+
+void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout) {
     struct JArgs {
         void *state;
         uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
@@ -234,6 +254,7 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
         int batch;
         int tpc;  // > 0: each CTA runs a block of tpc consecutive tiles
         void *out;
+        double *zout;  // fused <Z> epilogue: batch x (K + 1) sums
     } a{};
     a.state = state;
     a.out = out;
@@ -244,7 +265,10 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     a.tables = dp.args.tables;
     a.enc_table = dp.args.enc_table;
     a.batch = dp.args.batch;
-    uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(dp.grid, 1)));
+    a.zout = zout;
+    const void *kern = zout ? dp.jit_z : dp.jit;
+    require(kern != nullptr, "jit: kernel variant not prepared");
+    uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(zout ? dp.grid_z : dp.grid, 1)));
     // A few tiles per CTA rather than one persistent wave: CTAs that start
     // and retire at different times keep HBM reads and writes interleaved,
     // where a persistent grid moves in lock-step read / compute / write
@@ -263,7 +287,7 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
         if (blocked) a.tpc = static_cast<int>((a.total_tiles + grid - 1) / grid);
     }
     void *args[] = {&a};
-    QSV_CUDA(cudaLaunchKernel(dp.jit, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
+    QSV_CUDA(cudaLaunchKernel(kern, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
 }
 
 } // namespace qsv

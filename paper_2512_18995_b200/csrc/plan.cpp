@@ -37,6 +37,7 @@ Plan::~Plan() {
     cudaFree(d_encs);
     cudaFree(d_enc_table);
     cudaFree(d_data);
+    cudaFree(d_z);
 }
 
 namespace {
@@ -288,11 +289,12 @@ bool plan_uses_jit(const Plan &p) {
     return p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
 }
 
-void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s) {
+void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *zout) {
     if (!dp.out_of_place) {
-        launch_pass(dp, dtype, st.d, st.batch, s);
+        launch_pass(dp, dtype, st.d, st.batch, s, zout);
         return;
     }
+    require(zout == nullptr, "fused <Z>: not on a permuting pass");
     if (!st.scratch) {
         const size_t bytes = st.local_amps * st.amp_bytes() * static_cast<size_t>(st.batch);
         if (cudaMalloc(&st.scratch, bytes) != cudaSuccess) {
@@ -388,7 +390,7 @@ void upload_plan(Plan &p) {
     }
 }
 
-void execute_plan(Plan &p, State &st, const double *data, int rows, int slots) {
+void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout) {
     require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
     require(st.ctx == p.ctx, "plan/state belong to different contexts");
     if (rows == 0) {
@@ -418,16 +420,63 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots) {
         launch_bind(p, static_cast<const double *>(p.d_data), rows, slots, s);
         enc_table = p.d_enc_table;
     }
-    for (const Step &stp : p.steps) {
+    for (size_t i = 0; i < p.steps.size(); ++i) {
+        const Step &stp = p.steps[i];
         if (stp.kind == 0) {
             DevPass dp = p.dev[stp.pass];
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
-            run_pass(dp, p.dtype, st, s);
+            run_pass(dp, p.dtype, st, s, i + 1 == p.steps.size() ? zout : nullptr);
         } else {
             dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         }
     }
+}
+
+namespace {
+// The last step can carry the fused <Z> epilogue: a specialised, in-place
+// pass whose tile is the whole (single-GPU) row.
+bool z_fusable(Plan &p) {
+    if (p.steps.empty() || p.steps.back().kind != 0 || p.ctx->world != 1) return false;
+    const int pi = p.steps.back().pass;
+    const PassHost &ph = p.passes[pi];
+    const DevPass &dp = p.dev[pi];
+    return dp.jit != nullptr && !dp.out_of_place && ph.ext_pos.empty() && ph.out_perm.empty() && ph.K == p.nlocal;
+}
+} // namespace
+
+void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots, double *host_out) {
+    const int n = st.n, K1 = p.nlocal + 1;
+    if (!z_fusable(p)) {
+        execute_plan(p, st, data, rows, slots);
+        std::vector<double> z(static_cast<size_t>(st.batch) * 41);
+        reduce_z_all(st, z.data());
+        for (int b = 0; b < st.batch; ++b)
+            for (int w = 0; w < n; ++w)
+                host_out[static_cast<size_t>(b) * n + w] = z[b * 41] - 2.0 * z[b * 41 + 1 + st.perm[w]];
+        return;
+    }
+    DevPass &last = p.dev[p.steps.back().pass];
+    if (!last.jit_z) {
+        QSV_CUDA(cudaSetDevice(p.ctx->device));
+        jit_prepare_z(last, p.passes[p.steps.back().pass], p.dtype, p.ctx->sm_count);
+    }
+    const size_t zbytes = sizeof(double) * static_cast<size_t>(st.batch) * K1;
+    if (zbytes > p.d_z_cap) {
+        cudaFree(p.d_z);
+        p.d_z = nullptr;
+        QSV_CUDA(cudaMalloc(&p.d_z, zbytes));
+        p.d_z_cap = zbytes;
+    }
+    execute_plan(p, st, data, rows, slots, static_cast<double *>(p.d_z));
+    std::vector<double> z(static_cast<size_t>(st.batch) * K1);
+    cudaStream_t s = p.ctx->stream;
+    QSV_CUDA(cudaMemcpyAsync(z.data(), p.d_z, zbytes, cudaMemcpyDeviceToHost, s));
+    QSV_CUDA(cudaStreamSynchronize(s));
+    for (int b = 0; b < st.batch; ++b)
+        for (int w = 0; w < n; ++w)
+            host_out[static_cast<size_t>(b) * n + w] =
+                z[static_cast<size_t>(b) * K1] - 2.0 * z[static_cast<size_t>(b) * K1 + 1 + st.perm[w]];
 }
 
 void profile_plan(Plan &p, State &st, double *launch_ms) {

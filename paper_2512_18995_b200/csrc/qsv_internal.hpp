@@ -242,6 +242,8 @@ struct DevPass {
     const void *jit = nullptr;  // specialised kernel (cudaKernel_t), else the interpreter
     bool out_of_place = false;  // writes State::scratch (bit-permuting pass)
     int jit_regs = 0, jit_spill = 0;
+    const void *jit_z = nullptr;  // variant with the fused <Z> epilogue (prepared on first use)
+    int grid_z = 0;
     double bytes = 0;
     int ngates = 0;
 };
@@ -269,6 +271,8 @@ struct Plan {
     size_t enc_table_rows = 0;
     void *d_data = nullptr;
     size_t d_data_cap = 0;
+    void *d_z = nullptr;       // fused <Z> sums: batch x (nlocal + 1)
+    size_t d_z_cap = 0;
     std::vector<DevPass> dev;
     qsv_opts opts{};
     ~Plan();
@@ -300,16 +304,23 @@ int default_low_bits(int dtype, int nlocal);
 
 // ---- device launchers (engine.cu) -----------------------------------------
 void upload_plan(Plan &p);
-void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s);
+void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s, double *zout = nullptr);
 // Runs one pass on `st`; an out-of-place pass writes State::scratch and swaps it in.
-void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s);
+void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *zout = nullptr);
+// Circuit::forward + expectation() of every single-Z observable in one call:
+// out[b * n + w] = <Z_w>. The <Z> sums are fused into the last pass when its
+// tile is the whole row (batched small circuits, cfg2), else one extra
+// reduction pass.
+void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots, double *host_out);
+void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout = nullptr);
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
 int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
 // ---- pass specialisation (codegen.cpp, jit.cpp) ----------------------------
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
-void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s);
+void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout = nullptr);
+void jit_prepare_z(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
 std::string jit_source(const PassHost &ph, int dtype);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);

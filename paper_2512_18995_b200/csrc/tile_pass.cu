@@ -413,11 +413,12 @@ int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem) {
     return blocks;
 }
 
-void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s) {
+void launch_pass(const DevPass &dp, int dtype, void *state, int rows, cudaStream_t s, double *zout) {
     if (dp.jit) {
-        launch_jit(dp, state, state, rows, s);
+        launch_jit(dp, state, state, rows, s, zout);
         return;
     }
+    require(zout == nullptr, "fused <Z> needs a specialised pass kernel");
     PassArgs a = dp.args;
     a.state = state;
     a.total_tiles = a.tiles_per_row * static_cast<uint64_t>(rows);

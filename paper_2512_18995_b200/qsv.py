@@ -127,6 +127,7 @@ _SIGS = {
     "qsv_expect_z_all": (C.c_int, [_P, C.c_void_p]),
     "qsv_expect_pauli": (C.c_int, [_P, C.c_int, C.POINTER(qsv_obs), C.c_void_p]),
     "qsv_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
+    "qsv_plan_execute_expect_z": (C.c_int, [_P, _P, C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
     "qsv_density_expect_pauli": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_void_p]),
     "qsv_density_marginal_probs": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_void_p]),
     "qsv_rng_fill": (C.c_int, [C.c_uint64, C.c_char_p, C.c_int, C.c_uint64, C.c_void_p, C.c_int]),
@@ -731,6 +732,16 @@ class Plan:
         else:
             d = np.ascontiguousarray(data, dtype=np.float64)
             check(lib().qsv_plan_execute(self.h, state.h, _ptr(d), d.shape[0], d.shape[1]))
+
+    def execute_expect_z(self, state: QubitState, data=None) -> np.ndarray:
+        """forward + every <Z_w>: batch x n (qsv_plan_execute_expect_z)."""
+        out = np.zeros(state.batch() * state.nqubit())
+        if data is None:
+            check(lib().qsv_plan_execute_expect_z(self.h, state.h, None, 0, 0, _ptr(out)))
+        else:
+            d = np.ascontiguousarray(data, dtype=np.float64)
+            check(lib().qsv_plan_execute_expect_z(self.h, state.h, _ptr(d), d.shape[0], d.shape[1], _ptr(out)))
+        return out.reshape(state.batch(), state.nqubit())
 
     def step_kinds(self) -> np.ndarray:
         """0 = local pass, 1 = global<->local qubit swap, in execution order."""

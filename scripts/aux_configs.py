@@ -42,6 +42,11 @@ def f2():
     qsv.check(L.qsv_state_set_basis(st.h, 0)); p.execute(st, data)
 ms = timed(f2)
 ms_z = timed(lambda: (f2(), st.expect_z_all()), reps=10)
+def f2z():
+    qsv.check(L.qsv_state_set_basis(st.h, 0)); return p.execute_expect_z(st, data)
+ms_fz = timed(f2z, reps=10)
+print(f"cfg2 fused forward + <Z_i> (qsv_plan_execute_expect_z, host sync) {ms_fz:.3f} ms "
+      f"({4096 / ms_fz * 1e3:.0f} circuits/s)", flush=True)
 print(f"cfg2 4096x12q c64 {p.info['ngates']} gates passes={p.info['npasses']}: forward {ms:.3f} ms "
       f"({4096 / ms * 1e3:.0f} circuits/s); forward + <Z_i> (host sync) {ms_z:.3f} ms "
       f"({4096 / ms_z * 1e3:.0f} circuits/s)", flush=True)

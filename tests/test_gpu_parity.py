@@ -311,3 +311,26 @@ def test_cfg5_family_c64_vs_reference():
     assert np.max(np.abs(s.amplitudes() - want)) <= 1e-5
     e = qsv.expectation(s, cir)[0]
     assert abs(e - O.port_expectation(16, want, [0, 15], "zz")[0]) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol", [(C64, 1e-5), (C128, 1e-12)])
+def test_execute_expect_z_fused_and_fallback(dtype, tol):
+    """qsv_plan_execute_expect_z: the fused <Z> epilogue (whole-row tiles,
+    cfg2's batched circuits) and the fallback (multi-pass state) equal
+    forward + expectation() of every Z_w."""
+    cir, data = W.cfg2_circuit(10, layers=3, rows=257)
+    p = qsv.Plan(10, cir.gates(), dtype=dtype)
+    st = QubitState(10, batch=257, dtype=dtype)
+    z = p.execute_expect_z(st, data)
+    ref = cir.forward(data=data, dtype=dtype).expect_z_all()
+    assert np.max(np.abs(z - ref)) <= tol
+    w = ref_or_port_forward(10, cir.gates(), data=data[:3])
+    for r in range(3):
+        want = [O.port_expectation(10, w[r], [q], "z")[0] for q in range(10)]
+        assert np.max(np.abs(z[r] - want)) <= tol
+    big = W.cfg4_circuit(16, layers=2)
+    p2 = qsv.Plan(16, big.gates(), dtype=dtype)
+    s2 = QubitState(16, dtype=dtype)
+    z2 = p2.execute_expect_z(s2)
+    want2 = big.forward(dtype=dtype).expect_z_all()
+    assert np.max(np.abs(z2 - want2)) <= tol
