@@ -101,6 +101,10 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # diagnostics only: every rank on device 0 (the multi-rank path through
+    # tests/fake_nccl on a one-GPU box); never set for a measurement
+    if os.environ.get("QSV_BENCH_SHARE_GPU") == "1":
+        local = 0
     return rank, world, local
 
 
@@ -159,7 +163,7 @@ def main():
     ap.add_argument("--impl", default="qsv")
     ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--n", type=int, default=N_QUBITS, help="(diagnostics only) qubit count")
+    ap.add_argument("--qubits", type=int, default=N_QUBITS, help="(diagnostics only) qubit count")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -185,7 +189,7 @@ def main():
     else:
         ctx = qsv.Context(local)
     qsv.set_default_context(ctx)
-    n = args.n
+    n = args.qubits
     cir = W.cfg3_circuit(n)
     g = int(np.log2(world))
     nl = n - g

@@ -1,0 +1,141 @@
+"""The engine's REAL multi-rank path (dist.cu qubit swaps, all-reduced
+reductions, the distributed schedule, bench.py's N > 1 code) on ONE GPU.
+
+Every rank is a separate process with its own qsv context on device 0;
+NCCL is replaced by tests/fake_nccl (QSV_NCCL_LIB), a host-driven stand-in:
+at each group end the ranks synchronise their streams, exchange CUDA IPC
+handles through POSIX shared memory and copy with cudaMemcpy -- no kernel
+ever waits on another process (B200_PROFILING.md: ranks whose kernels wait on
+one another must not share a GPU). What runs on the device is exactly the
+production code: pass kernels with rank bits, gather/scatter of the swapped
+half-slices, FP64 partial sums. Results are gathered and compared with the
+single-rank reference, as the reference's own dist tests do
+(tests/test_dist.cpp:59-62, 128-205).
+"""
+import multiprocessing as mp
+import os
+import subprocess
+import sys
+import traceback
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2512_18995_b200 import qsv
+from paper_2512_18995_b200 import workloads as W
+from tests.helpers import random_circuit, random_state
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+SHIM = ROOT / "tests" / "fake_nccl" / "_build" / "libnccl_fake.so"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _shim():
+    if qsv.lib().qsv_device_count() < 1:
+        pytest.fail("no CUDA device: the -m gpu suite needs a B200")
+    if not SHIM.exists():
+        subprocess.run(["make", "-C", str(SHIM.parent.parent)], check=True, capture_output=True)
+    from paper_2512_18995_b200 import build
+
+    build.build()
+    os.environ["QSV_NCCL_LIB"] = str(SHIM)
+    yield
+
+
+def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q):
+    try:
+        os.environ["QSV_NCCL_LIB"] = str(SHIM)
+        from paper_2512_18995_b200 import qsv as Q
+
+        ctx = Q.Context(0, rank, world, uid)
+        g = int(np.log2(world))
+        nl = n - g
+        st = Q.QubitState(n, dtype=dtype, ctx=ctx)
+        if init is not None:
+            st.upload(init[rank << nl:(rank + 1) << nl])
+        plan = Q.Plan(n, gates, dtype=dtype, ctx=ctx)
+        plan.execute(st)
+        local = st.amplitudes()
+        z = st.expect_z_all()[0]
+        nrm = float(st.norm2()[0])
+        ex = Q.expectation_many(st, [Q.Observable(w, b) for w, b in obs])[0] if obs else []
+        q.put((rank, local, z, nrm, list(ex), plan.info["nswaps"]))
+        del plan, st
+        ctx.close()
+    except Exception:
+        q.put((rank, traceback.format_exc(), None, None, None, None))
+
+
+def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=()):
+    uid = qsv.Context.nccl_unique_id()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    procs = [ctxm.Process(target=_rank_main, args=(r, world, uid, n, gates, init, dtype, list(obs), q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, local, z, nrm, ex, nsw = q.get(timeout=180)
+            if z is None:
+                raise AssertionError(f"rank {r} failed:\n{local}")
+            res[r] = (local, z, nrm, ex, nsw)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    full = np.concatenate([res[r][0] for r in range(world)])
+    return full, res[0][1], res[0][2], res[0][3], res[0][4]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_random_circuits_match_single_rank(world):  # test_dist.cpp:128-145
+    rng = qsv.Rng(7, f"shim-{world}")
+    n = 10
+    for trial in range(2):
+        cir = random_circuit(rng, n, 60)
+        psi = random_state(rng, n)
+        got, z, nrm, _, nsw = run_ranks(n, cir.gates(), world, init=psi)
+        want = O.port_forward(n, cir.gates(), init=psi)[0]
+        assert np.max(np.abs(got - want)) <= 1e-12, (world, trial)
+        zw = [O.port_expectation(n, want, [w], "z")[0] for w in range(n)]
+        assert np.max(np.abs(z - zw)) <= 1e-12
+        assert abs(nrm - 1.0) <= 1e-12
+
+
+def test_cfg4_family_swaps_4_ranks():
+    """Non-diagonal gates on global wires force qubit swaps (dist_swap_bits)."""
+    n = 14
+    cir = W.cfg4_circuit(n, layers=4)
+    got, z, nrm, _, nsw = run_ranks(n, cir.gates(), 4)
+    want = O.port_forward(n, cir.gates())[0]
+    assert nsw > 0
+    assert np.max(np.abs(got - want)) <= 1e-12
+    assert abs(nrm - 1.0) <= 1e-12
+
+
+def test_cfg5_family_c64_and_global_pauli_2_ranks():
+    n = 12
+    cir = W.cfg5_circuit(n, layers=3)
+    obs = [([0, n - 1], "zz"), ([n - 1], "x"), ([2, n - 2], "yz")]  # wire 0 is a rank bit
+    got, z, nrm, ex, nsw = run_ranks(n, cir.gates(), 2, dtype=qsv.C64, obs=obs)
+    want = O.port_forward(n, cir.gates())[0]
+    assert np.max(np.abs(got - want)) <= 1e-5
+    for (w, b), e in zip(obs, ex):
+        assert abs(e - O.port_expectation(n, want, w, b)[0]) <= 1e-5
+
+
+def test_qft_2_ranks_bench_path():
+    n = 16
+    cir = W.cfg3_circuit(n)
+    psi = W.cfg3_input(n)
+    got, _, nrm, _, _ = run_ranks(n, cir.gates(), 2, init=psi)
+    want = O.port_forward(n, cir.gates(), init=psi)[0]
+    assert np.max(np.abs(got - want)) <= 1e-12
+    assert abs(nrm - 1.0) <= 1e-12
