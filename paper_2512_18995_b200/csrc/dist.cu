@@ -7,8 +7,13 @@
 // (test_dist.cpp:112-126); here a global qubit is instead SWAPPED with a local
 // one: each rank keeps the half of its slice whose local bit already matches
 // and exchanges the other half with the partner rank, so every later gate on
-// that qubit is local. The exchange is chunked through a bounded staging
-// buffer and is in place (no second copy of the state).
+// that qubit is local. Several pairs swap at once as ONE all-to-all: with m
+// pairs the local index space splits into 2^m blocks by the values v of the
+// m local bits; block v of rank r belongs to the peer whose m rank bits are v
+// and that peer's block holding r's rank bits comes back into the same
+// positions, so each rank sends (1 - 2^-m) of its slice once (m sequential
+// pairwise swaps would send m/2 of it). The exchange is chunked through
+// persistent staging and is in place (no second copy of the state).
 //
 // NCCL is dlopen'ed (libnccl.so.2, the one torch bundles) so the library
 // loads and single-GPU runs need no NCCL at all.
@@ -73,29 +78,34 @@ void nccl_ok(const Nccl &n, ncclResult_t r, const char *what) {
     if (r != 0) fail(QSV_ERR_TRANSPORT, std::string("NCCL ") + what + ": " + n.GetErrorString(r));
 }
 
-// element e of the half-slice where local bit `lb` == val  <->  local index
-__global__ void gather_half_kernel(const unsigned char *__restrict__ src, unsigned char *__restrict__ dst,
-                                   uint64_t e0, uint64_t count, int lb, int val, int amp_bytes) {
-    const uint64_t lowmask = (1ull << lb) - 1;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t e = e0 + i;
-        const uint64_t idx = ((e & ~lowmask) << 1) | (static_cast<uint64_t>(val) << lb) | (e & lowmask);
-        if (amp_bytes == 16)
-            reinterpret_cast<double2 *>(dst)[i] = reinterpret_cast<const double2 *>(src)[idx];
-        else reinterpret_cast<float2 *>(dst)[i] = reinterpret_cast<const float2 *>(src)[idx];
+// The m local bits of a swap step (ascending positions) and one block's
+// values: element e of block v <-> the local index with v's bits deposited
+// at those positions.
+struct BlockBits {
+    int m;
+    int pos[8];
+};
+__device__ __forceinline__ uint64_t deposit(uint64_t e, const BlockBits &bb, unsigned v) {
+    uint64_t x = e;
+    for (int i = 0; i < bb.m; ++i) {
+        const int p = bb.pos[i];
+        x = ((x >> p) << (p + 1)) | (static_cast<uint64_t>((v >> i) & 1u) << p) | (x & ((1ull << p) - 1));
     }
+    return x;
 }
-__global__ void scatter_half_kernel(const unsigned char *__restrict__ src, unsigned char *__restrict__ dst,
-                                    uint64_t e0, uint64_t count, int lb, int val, int amp_bytes) {
-    const uint64_t lowmask = (1ull << lb) - 1;
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+// gather (dir 0: state -> staging) or scatter (dir 1) of `count` elements
+// starting at e0 of every block listed in vs[0..nv) (slot j <-> vs[j])
+template <typename V>
+__global__ void block_copy_kernel(V *__restrict__ state, V *__restrict__ stage, BlockBits bb, uint64_t e0,
+                                  uint64_t count, const unsigned *__restrict__ vs, int nv, int dir) {
+    const uint64_t total = count * static_cast<uint64_t>(nv);
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t e = e0 + i;
-        const uint64_t idx = ((e & ~lowmask) << 1) | (static_cast<uint64_t>(val) << lb) | (e & lowmask);
-        if (amp_bytes == 16)
-            reinterpret_cast<double2 *>(dst)[idx] = reinterpret_cast<const double2 *>(src)[i];
-        else reinterpret_cast<float2 *>(dst)[idx] = reinterpret_cast<const float2 *>(src)[i];
+        const int j = static_cast<int>(i / count);
+        const uint64_t e = e0 + (i - static_cast<uint64_t>(j) * count);
+        const uint64_t idx = deposit(e, bb, vs[j]);
+        if (dir == 0) stage[i] = state[idx];
+        else state[idx] = stage[i];
     }
 }
 
@@ -120,6 +130,12 @@ void nccl_init(Ctx &ctx, const void *uid) {
 }
 
 void nccl_destroy(Ctx &ctx) {
+    if (ctx.stage) {
+        cudaStreamSynchronize(ctx.stream);
+        cudaFree(ctx.stage);
+        ctx.stage = nullptr;
+        ctx.stage_bytes = 0;
+    }
     if (ctx.comm && ctx.nccl) ctx.nccl->CommDestroy(static_cast<ncclComm_t>(ctx.comm));
     ctx.comm = nullptr;
     delete ctx.nccl;
@@ -133,42 +149,110 @@ void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count) {
             "AllReduce");
 }
 
+namespace {
+void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs);
+}
+
+// A step's pairs apply in order (a later pair may reuse a bit of an earlier
+// one, e.g. when the layout is restored); maximal runs of pairwise-disjoint
+// pairs commute and go as one all-to-all each.
 void dist_swap_bits(State &st, const std::vector<std::pair<int, int>> &pairs, void *, size_t) {
+    std::vector<std::pair<int, int>> run;
+    for (const auto &p : pairs) {
+        bool clash = false;
+        for (const auto &q : run) clash = clash || q.first == p.first || q.second == p.second;
+        if (clash) {
+            swap_disjoint(st, run);
+            run.clear();
+        }
+        run.push_back(p);
+    }
+    if (!run.empty()) swap_disjoint(st, run);
+}
+
+namespace {
+void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
     Ctx &ctx = *st.ctx;
     require(ctx.world > 1 && ctx.comm, "swap on a non-distributed state");
     const Nccl &n = *ctx.nccl;
+    const int m = static_cast<int>(pairs.size());
+    require(m >= 1 && m <= 6, "swap: 1..6 bit pairs per step");
     const int amp = static_cast<int>(st.amp_bytes());
-    const uint64_t half = st.local_amps / 2;
-    const uint64_t chunk = std::min<uint64_t>(half, (256ull << 20) / amp); // 256 MiB staging per direction
-    unsigned char *stage = nullptr;
-    QSV_CUDA(cudaMalloc(&stage, 2 * chunk * amp));
-    unsigned char *sbuf = stage, *rbuf = stage + chunk * amp;
-    for (const auto &[gb, lb] : pairs) {
+    // local bits ascending, each with its rank bit
+    std::vector<std::pair<int, int>> pr(pairs.begin(), pairs.end());
+    for (const auto &[gb, lb] : pr)
         require(gb >= st.nlocal && gb < st.n && lb >= 0 && lb < st.nlocal, "swap: bad bit pair");
-        const int r = gb - st.nlocal;
-        const int peer = ctx.rank ^ (1 << r);
-        const int my = (ctx.rank >> r) & 1;
-        const int val = 1 - my; // the half whose local bit disagrees with my rank bit moves
-        for (int row = 0; row < st.batch; ++row) {
-            unsigned char *base = static_cast<unsigned char *>(st.d) + static_cast<size_t>(row) * st.local_amps * amp;
-            for (uint64_t e0 = 0; e0 < half; e0 += chunk) {
-                const uint64_t c = std::min(chunk, half - e0);
-                const int blocks = static_cast<int>(std::min<uint64_t>((c + 255) / 256, 148 * 8));
-                gather_half_kernel<<<blocks, 256, 0, ctx.stream>>>(base, sbuf, e0, c, lb, val, amp);
-                QSV_CUDA(cudaGetLastError());
-                nccl_ok(n, n.GroupStart(), "GroupStart");
-                nccl_ok(n, n.Send(sbuf, c * amp, ncclUint8, peer, static_cast<ncclComm_t>(ctx.comm), ctx.stream),
-                        "Send");
-                nccl_ok(n, n.Recv(rbuf, c * amp, ncclUint8, peer, static_cast<ncclComm_t>(ctx.comm), ctx.stream),
-                        "Recv");
-                nccl_ok(n, n.GroupEnd(), "GroupEnd");
-                scatter_half_kernel<<<blocks, 256, 0, ctx.stream>>>(rbuf, base, e0, c, lb, val, amp);
-                QSV_CUDA(cudaGetLastError());
+    std::sort(pr.begin(), pr.end(), [](auto &a, auto &b) { return a.second < b.second; });
+    BlockBits bb{};
+    bb.m = m;
+    unsigned own = 0;
+    for (int i = 0; i < m; ++i) {
+        bb.pos[i] = pr[i].second;
+        own |= static_cast<unsigned>((ctx.rank >> (pr[i].first - st.nlocal)) & 1) << i;
+    }
+    // peers: block v goes to the rank whose swapped rank bits equal v
+    std::vector<unsigned> vs;
+    std::vector<int> peers;
+    for (unsigned v = 0; v < (1u << m); ++v) {
+        if (v == own) continue;
+        int peer = ctx.rank;
+        for (int i = 0; i < m; ++i) {
+            const int rb = pr[i].first - st.nlocal;
+            peer = (peer & ~(1 << rb)) | static_cast<int>(((v >> i) & 1u) << rb);
+        }
+        vs.push_back(v);
+        peers.push_back(peer);
+    }
+    const int nv = static_cast<int>(vs.size());
+    const uint64_t block = st.local_amps >> m;
+    // persistent staging: send + receive halves, up to 512 MiB each
+    const uint64_t want = std::min<uint64_t>(block * nv, (512ull << 20) / amp);
+    const uint64_t chunk = std::max<uint64_t>(1, want / nv);  // elements per block per round
+    const size_t need = 2 * chunk * nv * static_cast<size_t>(amp);
+    if (ctx.stage_bytes < need) {
+        QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+        cudaFree(ctx.stage);
+        ctx.stage = nullptr;
+        ctx.stage_bytes = 0;
+        QSV_CUDA(cudaMalloc(&ctx.stage, need));
+        ctx.stage_bytes = need;
+    }
+    unsigned char *sbuf = static_cast<unsigned char *>(ctx.stage);
+    unsigned char *rbuf = sbuf + chunk * nv * amp;
+    unsigned *d_vs = nullptr;
+    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_vs), sizeof(unsigned) * nv, ctx.stream));
+    QSV_CUDA(cudaMemcpyAsync(d_vs, vs.data(), sizeof(unsigned) * nv, cudaMemcpyHostToDevice, ctx.stream));
+    for (int row = 0; row < st.batch; ++row) {
+        unsigned char *base = static_cast<unsigned char *>(st.d) + static_cast<size_t>(row) * st.local_amps * amp;
+        for (uint64_t e0 = 0; e0 < block; e0 += chunk) {
+            const uint64_t c = std::min(chunk, block - e0);
+            const int blocks = static_cast<int>(std::min<uint64_t>((c * nv + 255) / 256, 148 * 8));
+            if (amp == 16)
+                block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
+                    reinterpret_cast<double2 *>(sbuf), bb, e0, c, d_vs, nv, 0);
+            else
+                block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
+                    reinterpret_cast<float2 *>(sbuf), bb, e0, c, d_vs, nv, 0);
+            QSV_CUDA(cudaGetLastError());
+            nccl_ok(n, n.GroupStart(), "GroupStart");
+            for (int j = 0; j < nv; ++j) {
+                nccl_ok(n, n.Send(sbuf + static_cast<size_t>(j) * c * amp, c * amp, ncclUint8, peers[j],
+                                  static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Send");
+                nccl_ok(n, n.Recv(rbuf + static_cast<size_t>(j) * c * amp, c * amp, ncclUint8, peers[j],
+                                  static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Recv");
             }
+            nccl_ok(n, n.GroupEnd(), "GroupEnd");
+            if (amp == 16)
+                block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
+                    reinterpret_cast<double2 *>(rbuf), bb, e0, c, d_vs, nv, 1);
+            else
+                block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
+                    reinterpret_cast<float2 *>(rbuf), bb, e0, c, d_vs, nv, 1);
+            QSV_CUDA(cudaGetLastError());
         }
     }
-    QSV_CUDA(cudaStreamSynchronize(ctx.stream));
-    cudaFree(stage);
+    QSV_CUDA(cudaFreeAsync(d_vs, ctx.stream));
 }
+} // namespace
 
 } // namespace qsv

@@ -219,6 +219,8 @@ struct Ctx {
     size_t smem_optin = 0;
     void *comm = nullptr;       // ncclComm_t
     Nccl *nccl = nullptr;       // owned; freed by nccl_destroy
+    void *stage = nullptr;      // qubit-swap staging (send + receive), persistent
+    size_t stage_bytes = 0;
     ~Ctx();
 };
 
@@ -336,8 +338,9 @@ void reduce_dm_marginal(State &st, int m, int row, const std::vector<int> &bits_
 void nccl_unique_id(void *out128);
 void nccl_init(Ctx &ctx, const void *uid);
 void nccl_destroy(Ctx &ctx);
-// Exchange: swap physical rank bit `gbit` (>= nlocal) with local bit `lbit`
-// for every batch row, in place, chunked.
+// Exchange: swap every physical rank bit `gbit` (>= nlocal) with its local
+// bit `lbit` at once -- one in-place all-to-all over the 2^m - 1 peer ranks
+// (m = pairs), for every batch row, chunked through persistent staging.
 void dist_swap_bits(State &st, const std::vector<std::pair<int, int>> &pairs, void *staging, size_t staging_bytes);
 void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count);
 

@@ -34,9 +34,9 @@
 namespace {
 constexpr int kMaxRanks = 16;
 constexpr size_t kRedDoubles = 1 << 17;
+constexpr size_t kArea = 8u << 20;
 
 struct Slot {
-    CUipcMemHandle h;
     uint64_t off, bytes;
     int valid;
 };
@@ -46,6 +46,7 @@ struct Ctl {
     std::atomic<int> gen;
     Slot send[kMaxRanks][kMaxRanks];  // [src][dst]
     double red[kMaxRanks][kRedDoubles];
+    unsigned char area[kMaxRanks][kArea];
 };
 struct Comm {
     Ctl *ctl = nullptr;
@@ -84,21 +85,35 @@ void barrier(Comm *c) {
     }
 }
 
+bool cu_ok(CUresult r, const char *what) {
+    if (r == CUDA_SUCCESS) return true;
+    const char *name = nullptr;
+    cuGetErrorName(r, &name);
+    std::fprintf(stderr, "fake nccl: %s failed: %s\n", what, name ? name : "?");
+    return false;
+}
+
 int run_group(std::vector<Op> &ops) {
     if (ops.empty()) return 0;
     Comm *c = ops[0].comm;
     for (const Op &o : ops)
-        if (cuCtxSynchronize() != CUDA_SUCCESS || cuStreamSynchronize(o.stream) != CUDA_SUCCESS) return 1;
+        if (!cu_ok(cuCtxSynchronize(), "cuCtxSynchronize") || !cu_ok(cuStreamSynchronize(o.stream), "cuStreamSynchronize"))
+            return 1;
+    uint64_t used = 0;
     for (const Op &o : ops) {
         if (!o.send) continue;
-        CUdeviceptr base = 0;
-        size_t sz = 0;
-        if (cuMemGetAddressRange(&base, &sz, reinterpret_cast<CUdeviceptr>(o.buf)) != CUDA_SUCCESS) return 1;
+        if (used + o.bytes > kArea) {
+            std::fprintf(stderr, "fake nccl: more than %zu bytes sent per rank per group\n", kArea);
+            return 4;
+        }
+        if (!cu_ok(cuMemcpyDtoH(c->ctl->area[c->rank] + used, reinterpret_cast<CUdeviceptr>(o.buf), o.bytes),
+                   "cuMemcpyDtoH"))
+            return 1;
         Slot &s = c->ctl->send[c->rank][o.peer];
-        if (cuIpcGetMemHandle(&s.h, base) != CUDA_SUCCESS) return 1;
-        s.off = reinterpret_cast<uint64_t>(o.buf) - base;
+        s.off = used;
         s.bytes = o.bytes;
         s.valid = 1;
+        used += (o.bytes + 255) & ~uint64_t(255);
     }
     barrier(c);
     int rc = 0;
@@ -106,16 +121,13 @@ int run_group(std::vector<Op> &ops) {
         if (o.send) continue;
         Slot &s = c->ctl->send[o.peer][c->rank];
         if (!s.valid || s.bytes != o.bytes) {
-            rc = 1;
+            std::fprintf(stderr, "fake nccl: unmatched receive from rank %d\n", o.peer);
+            rc = 4;
             continue;
         }
-        CUdeviceptr p = 0;
-        if (cuIpcOpenMemHandle(&p, s.h, CU_IPC_MEM_LAZY_ENABLE_PEER_ACCESS) != CUDA_SUCCESS) {
+        if (!cu_ok(cuMemcpyHtoD(reinterpret_cast<CUdeviceptr>(o.buf), c->ctl->area[o.peer] + s.off, o.bytes),
+                   "cuMemcpyHtoD"))
             rc = 1;
-            continue;
-        }
-        if (cuMemcpyDtoD(reinterpret_cast<CUdeviceptr>(o.buf), p + s.off, o.bytes) != CUDA_SUCCESS) rc = 1;
-        cuIpcCloseMemHandle(p);
     }
     if (cuCtxSynchronize() != CUDA_SUCCESS) rc = 1;  // the copies land before the caller's stream goes on
     barrier(c);

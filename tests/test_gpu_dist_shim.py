@@ -139,3 +139,16 @@ def test_qft_2_ranks_bench_path():
     want = O.port_forward(n, cir.gates(), init=psi)[0]
     assert np.max(np.abs(got - want)) <= 1e-12
     assert abs(nrm - 1.0) <= 1e-12
+
+
+def test_cfg4_family_8_ranks_multi_bit_all_to_all():
+    """8 ranks: swap steps carry up to 3 bit pairs -> one in-place all-to-all
+    over 7 peers (dist.cu block exchange)."""
+    n = 14
+    cir = W.cfg4_circuit(n, layers=3)
+    sched = qsv.plan_schedule(n, cir.gates(), world=8)
+    assert max(len(s["pairs"]) for s in sched["steps"] if s["kind"] == "swap") >= 2
+    got, z, nrm, _, nsw = run_ranks(n, cir.gates(), 8)
+    want = O.port_forward(n, cir.gates())[0]
+    assert np.max(np.abs(got - want)) <= 1e-12
+    assert abs(nrm - 1.0) <= 1e-12
