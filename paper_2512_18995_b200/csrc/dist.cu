@@ -136,6 +136,11 @@ void nccl_destroy(Ctx &ctx) {
         ctx.stage = nullptr;
         ctx.stage_bytes = 0;
     }
+    if (ctx.comm_stream) {
+        cudaStreamSynchronize(ctx.comm_stream);
+        cudaStreamDestroy(ctx.comm_stream);
+        ctx.comm_stream = nullptr;
+    }
     if (ctx.comm && ctx.nccl) ctx.nccl->CommDestroy(static_cast<ncclComm_t>(ctx.comm));
     ctx.comm = nullptr;
     delete ctx.nccl;
@@ -205,51 +210,90 @@ void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
     }
     const int nv = static_cast<int>(vs.size());
     const uint64_t block = st.local_amps >> m;
-    // persistent staging: send + receive halves, up to 512 MiB each
-    const uint64_t want = std::min<uint64_t>(block * nv, (512ull << 20) / amp);
+    // persistent staging: two sets (send + receive each), a set <= 2 x 256 MiB
+    // QSV_SWAP_STAGE_BYTES (tests): a small per-set payload forces many
+    // pipelined rounds on small states
+    static const uint64_t set_cap = [] {
+        const char *e = std::getenv("QSV_SWAP_STAGE_BYTES");
+        return e ? std::max<uint64_t>(256, std::strtoull(e, nullptr, 10)) : (256ull << 20);
+    }();
+    const uint64_t want = std::min<uint64_t>(block * nv, set_cap / amp);
     const uint64_t chunk = std::max<uint64_t>(1, want / nv);  // elements per block per round
-    const size_t need = 2 * chunk * nv * static_cast<size_t>(amp);
-    if (ctx.stage_bytes < need) {
+    const size_t set_bytes = 2 * chunk * nv * static_cast<size_t>(amp);
+    if (ctx.stage_bytes < 2 * set_bytes) {
         QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (ctx.comm_stream) QSV_CUDA(cudaStreamSynchronize(ctx.comm_stream));
         cudaFree(ctx.stage);
         ctx.stage = nullptr;
         ctx.stage_bytes = 0;
-        QSV_CUDA(cudaMalloc(&ctx.stage, need));
-        ctx.stage_bytes = need;
+        QSV_CUDA(cudaMalloc(&ctx.stage, 2 * set_bytes));
+        ctx.stage_bytes = 2 * set_bytes;
     }
-    unsigned char *sbuf = static_cast<unsigned char *>(ctx.stage);
-    unsigned char *rbuf = sbuf + chunk * nv * amp;
+    if (!ctx.comm_stream) QSV_CUDA(cudaStreamCreateWithFlags(&ctx.comm_stream, cudaStreamNonBlocking));
     unsigned *d_vs = nullptr;
     QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_vs), sizeof(unsigned) * nv, ctx.stream));
     QSV_CUDA(cudaMemcpyAsync(d_vs, vs.data(), sizeof(unsigned) * nv, cudaMemcpyHostToDevice, ctx.stream));
-    for (int row = 0; row < st.batch; ++row) {
-        unsigned char *base = static_cast<unsigned char *>(st.d) + static_cast<size_t>(row) * st.local_amps * amp;
-        for (uint64_t e0 = 0; e0 < block; e0 += chunk) {
-            const uint64_t c = std::min(chunk, block - e0);
-            const int blocks = static_cast<int>(std::min<uint64_t>((c * nv + 255) / 256, 148 * 8));
-            if (amp == 16)
-                block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
-                    reinterpret_cast<double2 *>(sbuf), bb, e0, c, d_vs, nv, 0);
-            else
-                block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
-                    reinterpret_cast<float2 *>(sbuf), bb, e0, c, d_vs, nv, 0);
-            QSV_CUDA(cudaGetLastError());
-            nccl_ok(n, n.GroupStart(), "GroupStart");
-            for (int j = 0; j < nv; ++j) {
-                nccl_ok(n, n.Send(sbuf + static_cast<size_t>(j) * c * amp, c * amp, ncclUint8, peers[j],
-                                  static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Send");
-                nccl_ok(n, n.Recv(rbuf + static_cast<size_t>(j) * c * amp, c * amp, ncclUint8, peers[j],
-                                  static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Recv");
-            }
-            nccl_ok(n, n.GroupEnd(), "GroupEnd");
-            if (amp == 16)
-                block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
-                    reinterpret_cast<double2 *>(rbuf), bb, e0, c, d_vs, nv, 1);
-            else
-                block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
-                    reinterpret_cast<float2 *>(rbuf), bb, e0, c, d_vs, nv, 1);
-            QSV_CUDA(cudaGetLastError());
+    // rounds (row, chunk) in order; round k uses staging set k % 2. The copy
+    // stream issues gather(k + 1) before scatter(k), so the next chunk is
+    // gathered while chunk k is on the wire; scatter(k - 1) precedes
+    // gather(k + 1) on the copy stream, which frees set (k + 1) % 2.
+    struct Round {
+        int row;
+        uint64_t e0, c;
+    };
+    std::vector<Round> rounds;
+    for (int row = 0; row < st.batch; ++row)
+        for (uint64_t e0 = 0; e0 < block; e0 += chunk) rounds.push_back({row, e0, std::min(chunk, block - e0)});
+    const size_t K = rounds.size();
+    std::vector<cudaEvent_t> ev_g(K), ev_c(K);
+    for (size_t k = 0; k < K; ++k) {
+        QSV_CUDA(cudaEventCreateWithFlags(&ev_g[k], cudaEventDisableTiming));
+        QSV_CUDA(cudaEventCreateWithFlags(&ev_c[k], cudaEventDisableTiming));
+    }
+    auto set_ptr = [&](size_t k, int recv) {
+        return static_cast<unsigned char *>(ctx.stage) + (k % 2) * set_bytes + (recv ? set_bytes / 2 : 0);
+    };
+    auto copy = [&](size_t k, int dir) {
+        const Round &r = rounds[k];
+        unsigned char *base = static_cast<unsigned char *>(st.d) + static_cast<size_t>(r.row) * st.local_amps * amp;
+        const int blocks = static_cast<int>(std::min<uint64_t>((r.c * nv + 255) / 256, 148 * 8));
+        unsigned char *buf = set_ptr(k, dir);
+        if (amp == 16)
+            block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
+                reinterpret_cast<double2 *>(buf), bb, r.e0, r.c, d_vs, nv, dir);
+        else
+            block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
+                reinterpret_cast<float2 *>(buf), bb, r.e0, r.c, d_vs, nv, dir);
+        QSV_CUDA(cudaGetLastError());
+    };
+    auto transfer = [&](size_t k) {
+        const Round &r = rounds[k];
+        QSV_CUDA(cudaStreamWaitEvent(ctx.comm_stream, ev_g[k], 0));
+        unsigned char *sb = set_ptr(k, 0), *rb = set_ptr(k, 1);
+        nccl_ok(n, n.GroupStart(), "GroupStart");
+        for (int j = 0; j < nv; ++j) {
+            nccl_ok(n, n.Send(sb + static_cast<size_t>(j) * r.c * amp, r.c * amp, ncclUint8, peers[j],
+                              static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream), "Send");
+            nccl_ok(n, n.Recv(rb + static_cast<size_t>(j) * r.c * amp, r.c * amp, ncclUint8, peers[j],
+                              static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream), "Recv");
         }
+        nccl_ok(n, n.GroupEnd(), "GroupEnd");
+        QSV_CUDA(cudaEventRecord(ev_c[k], ctx.comm_stream));
+    };
+    copy(0, 0);
+    QSV_CUDA(cudaEventRecord(ev_g[0], ctx.stream));
+    for (size_t k = 0; k < K; ++k) {
+        transfer(k);
+        if (k + 1 < K) {
+            copy(k + 1, 0);
+            QSV_CUDA(cudaEventRecord(ev_g[k + 1], ctx.stream));
+        }
+        QSV_CUDA(cudaStreamWaitEvent(ctx.stream, ev_c[k], 0));
+        copy(k, 1);
+    }
+    for (size_t k = 0; k < K; ++k) {
+        cudaEventDestroy(ev_g[k]);
+        cudaEventDestroy(ev_c[k]);
     }
     QSV_CUDA(cudaFreeAsync(d_vs, ctx.stream));
 }

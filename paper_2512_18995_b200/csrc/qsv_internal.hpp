@@ -219,8 +219,9 @@ struct Ctx {
     size_t smem_optin = 0;
     void *comm = nullptr;       // ncclComm_t
     Nccl *nccl = nullptr;       // owned; freed by nccl_destroy
-    void *stage = nullptr;      // qubit-swap staging (send + receive), persistent
+    void *stage = nullptr;      // qubit-swap staging (2 sets of send + receive), persistent
     size_t stage_bytes = 0;
+    cudaStream_t comm_stream = nullptr;  // NCCL transfers of a swap, overlapped with its copies
     ~Ctx();
 };
 

@@ -46,9 +46,10 @@ def _shim():
     yield
 
 
-def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q):
+def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q, env=None):
     try:
         os.environ["QSV_NCCL_LIB"] = str(SHIM)
+        os.environ.update(env or {})
         from paper_2512_18995_b200 import qsv as Q
 
         ctx = Q.Context(0, rank, world, uid)
@@ -70,11 +71,11 @@ def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q):
         q.put((rank, traceback.format_exc(), None, None, None, None))
 
 
-def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=()):
+def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=(), env=None):
     uid = qsv.Context.nccl_unique_id()
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
-    procs = [ctxm.Process(target=_rank_main, args=(r, world, uid, n, gates, init, dtype, list(obs), q))
+    procs = [ctxm.Process(target=_rank_main, args=(r, world, uid, n, gates, init, dtype, list(obs), q, env))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -152,3 +153,14 @@ def test_cfg4_family_8_ranks_multi_bit_all_to_all():
     want = O.port_forward(n, cir.gates())[0]
     assert np.max(np.abs(got - want)) <= 1e-12
     assert abs(nrm - 1.0) <= 1e-12
+
+
+def test_pipelined_swap_rounds_4_ranks():
+    """A 1 KiB staging set forces many chunk rounds per swap: gather(k + 1)
+    overlaps transfer(k) on the two streams, scatter(k) waits for it."""
+    n = 14
+    cir = W.cfg4_circuit(n, layers=2)
+    got, z, nrm, _, nsw = run_ranks(n, cir.gates(), 4, env={"QSV_SWAP_STAGE_BYTES": "1024"})
+    want = O.port_forward(n, cir.gates())[0]
+    assert nsw > 0
+    assert np.max(np.abs(got - want)) <= 1e-12
