@@ -525,7 +525,7 @@ struct Gen {
               << ") & 1) | ((__popc(u & " << swm[1] << ") & 1) << 1) | ((__popc(u & " << swm[2] << ") & 1) << 2)); }\n";
         }
         o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
-          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; };\n";
+          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; const " << V << " *prefix; };\n";
         // Double buffering: while tile t is transformed in one shared buffer,
         // the cp.async copies of tile t + gridDim are already in flight into
         // the other (one CTA per SM, 2 x 2^K amplitudes).
@@ -837,11 +837,37 @@ struct Gen {
                         uoff[r] |= 1 << g.slot_bit[j];
                         poff[r] |= 1ull << ph.tile_pos[g.slot_bit[j]];
                     }
-            for (int r = 0; r < NR; ++r) {
-                if (from_hbm)
-                    o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
-                else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_of(uoff[r]) << "];\n";
-            }
+            if (from_hbm && ph.synth) {
+                // product state M_k..M_1|0> per wire: the set's factor over its
+                // non-slot bits, then a binary tree over the R slot bits
+                const int nl = K + static_cast<int>(ph.ext_pos.size());
+                o << "      const " << V << " *U = a.prefix + (u64)row * " << 2 * nl << ";\n";
+                o << "      " << V << " f = mk(1, 0);\n";
+                for (size_t i = 0; i < ngt.size(); ++i)
+                    o << "      f = cmulv(f, U[" << 2 * ph.tile_pos[ngt[i]] << " + ((s >> " << i << ") & 1)]);\n";
+                for (int e : ph.ext_pos)
+                    o << "      f = cmulv(f, U[" << 2 * e << " + (int)((tb >> " << e << ") & 1ull)]);\n";
+                std::vector<std::string> cur{"f"};
+                for (int j = 0; j < R; ++j) {
+                    const int pj = ph.tile_pos[g.slot_bit[j]];
+                    std::vector<std::string> nxt(cur.size() * 2);
+                    for (size_t r = 0; r < cur.size(); ++r)
+                        for (int b = 0; b < 2; ++b) {
+                            const size_t idx = r | (static_cast<size_t>(b) << j);
+                            const std::string nm = j + 1 == R ? "v" + std::to_string(idx)
+                                                              : "t" + std::to_string(j) + "_" + std::to_string(idx);
+                            o << "      " << V << " " << nm << " = cmulv(" << cur[r] << ", U[" << 2 * pj + b << "]);\n";
+                            nxt[idx] = nm;
+                        }
+                    cur.swap(nxt);
+                }
+                if (R == 0) o << "      " << V << " v0 = f;\n";
+            } else
+                for (int r = 0; r < NR; ++r) {
+                    if (from_hbm)
+                        o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
+                    else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_of(uoff[r]) << "];\n";
+                }
             // QSV_DEBUG_NOCOMPUTE=1 (diagnostics only): the pass moves data without
             // applying its gates -- the memory-structure ceiling of its geometry
             static const bool nocompute = [] {

@@ -306,6 +306,52 @@ int grid_for(uint64_t work, int threads, int sm_count) {
 
 } // namespace
 
+// Product-state prefix of a from-|0> plan: u_w = M_k ... M_1 |0> per (row,
+// wire), written as out[(row * n + p) * 2 + b] = u_w[b] with p = n - 1 - w
+// (the canonical physical bit of wire w).
+template <typename T>
+__global__ void prefix_kernel(const int *__restrict__ prog, const double *__restrict__ mats,
+                              const T *__restrict__ enc_table, int rows, int n, typename Vec2<T>::type *out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= rows * n) return;
+    const int row = i / n, w = i % n;
+    double a0 = 1.0, a1 = 0.0, b0 = 0.0, b1 = 0.0;  // (a0 + i a1, b0 + i b1)
+    for (int k = prog[w]; k < prog[w + 1]; ++k) {
+        const int e = prog[k];
+        double m[8];
+        if (e >= 0) {
+            const T *t = enc_table + (static_cast<size_t>(e) * rows + row) * 32;
+            for (int q = 0; q < 8; ++q) m[q] = static_cast<double>(t[q]);
+        } else {
+            const double *t = mats + static_cast<size_t>(-1 - e) * 8;
+            for (int q = 0; q < 8; ++q) m[q] = t[q];
+        }
+        const double na0 = m[0] * a0 - m[1] * a1 + m[2] * b0 - m[3] * b1;
+        const double na1 = m[0] * a1 + m[1] * a0 + m[2] * b1 + m[3] * b0;
+        const double nb0 = m[4] * a0 - m[5] * a1 + m[6] * b0 - m[7] * b1;
+        const double nb1 = m[4] * a1 + m[5] * a0 + m[6] * b1 + m[7] * b0;
+        a0 = na0, a1 = na1, b0 = nb0, b1 = nb1;
+    }
+    using V = typename Vec2<T>::type;
+    V *o = out + (static_cast<size_t>(row) * n + (n - 1 - w)) * 2;
+    o[0] = V{static_cast<T>(a0), static_cast<T>(a1)};
+    o[1] = V{static_cast<T>(b0), static_cast<T>(b1)};
+}
+
+void launch_prefix(const Plan &p, int rows, cudaStream_t s) {
+    const int work = rows * p.nlocal;
+    const int threads = 128, blocks = (work + threads - 1) / threads;
+    if (p.dtype == QSV_C64)
+        prefix_kernel<float><<<blocks, threads, 0, s>>>(static_cast<const int *>(p.d_prefix_prog),
+            static_cast<const double *>(p.d_prefix_mats), static_cast<const float *>(p.d_enc_table), rows, p.nlocal,
+            static_cast<float2 *>(p.d_prefix));
+    else
+        prefix_kernel<double><<<blocks, threads, 0, s>>>(static_cast<const int *>(p.d_prefix_prog),
+            static_cast<const double *>(p.d_prefix_mats), static_cast<const double *>(p.d_enc_table), rows, p.nlocal,
+            static_cast<double2 *>(p.d_prefix));
+    QSV_CUDA(cudaGetLastError());
+}
+
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s) {
     const int nenc = static_cast<int>(p.encs.size());
     if (nenc == 0) return;

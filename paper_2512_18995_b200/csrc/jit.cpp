@@ -175,7 +175,7 @@ static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, 
     const int amp0 = dtype == QSV_C64 ? 8 : 16;
     const char *pe = std::getenv("QSV_PREFETCH");
     const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
-                      (1 << ph.K) * amp0 >= 16 * 32;
+                      (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
     (void)double_buffer_enabled;
     std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf, zsum);
     char key[32];
@@ -238,7 +238,7 @@ std::string jit_source(const PassHost &ph, int dtype) {
     const int amp0 = dtype == QSV_C64 ? 8 : 16;
     const char *pe = std::getenv("QSV_PREFETCH");
     const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
-                      (1 << ph.K) * amp0 >= 16 * 32;
+                      (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
     return generate_pass_source(ph, dtype, "qsv_pass", &threads, dbuf);
 }
 
@@ -255,6 +255,7 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
         int tpc;  // > 0: each CTA runs a block of tpc consecutive tiles
         void *out;
         double *zout;  // fused <Z> epilogue: batch x (K + 1) sums
+        const void *prefix;  // synthesising pass: product-state vectors
     } a{};
     a.state = state;
     a.out = out;
@@ -266,6 +267,7 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     a.enc_table = dp.args.enc_table;
     a.batch = dp.args.batch;
     a.zout = zout;
+    a.prefix = dp.args.prefix;
     const void *kern = zout ? dp.jit_z : dp.jit;
     require(kern != nullptr, "jit: kernel variant not prepared");
     uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(zout ? dp.grid_z : dp.grid, 1)));

@@ -38,6 +38,9 @@ Plan::~Plan() {
     cudaFree(d_enc_table);
     cudaFree(d_data);
     cudaFree(d_z);
+    cudaFree(d_prefix_prog);
+    cudaFree(d_prefix_mats);
+    cudaFree(d_prefix);
 }
 
 namespace {
@@ -218,6 +221,59 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
 
 } // namespace
 
+namespace {
+// From |0...0>, the gates a wire sees before any multi-qubit gate, control
+// or swap touches it leave it in a product state: per wire a 2-vector
+// M_k ... M_1 |0>, evaluated per row on the device (encoded gates included)
+// and synthesised inside the first pass instead of loading the state
+// (cfg2: the encoding layer and the first U3 layer never run as gates).
+void extract_prefix(Plan &p) {
+    const int n = p.n;
+    std::vector<std::vector<const GateRec *>> pre(n);
+    std::vector<char> open(n, 1);
+    std::vector<GateRec> rest;
+    for (const GateRec &g : p.gates) {
+        const bool single = g.k == 1 && g.ctls.empty() && g.flags == 0 && g.kind != GK_SWAP;
+        if (single && open[g.wires[0]]) {
+            pre[g.wires[0]].push_back(&g);
+            continue;
+        }
+        for (int t = 0; t < g.k; ++t) open[g.wires[t]] = 0;
+        for (int c : g.ctls) open[c] = 0;
+        rest.push_back(g);
+    }
+    bool any = false;
+    for (const auto &v : pre) any = any || !v.empty();
+    if (!any || rest.empty()) return;
+    std::vector<int> prog(n + 1, 0), entries;
+    for (int w = 0; w < n; ++w) {
+        prog[w] = static_cast<int>(entries.size());
+        for (const GateRec *g : pre[w]) {
+            if (g->encoded) {
+                EncDesc e{};
+                e.kind = g->kind;
+                e.slot = g->enc_slot;
+                e.nparams = g->nparams;
+                e.diag = 0;  // the full 2x2 matrix
+                entries.push_back(static_cast<int>(p.encs.size()));
+                p.encs.push_back(e);
+            } else {
+                entries.push_back(-1 - static_cast<int>(p.prefix_mats.size() / 4));
+                p.prefix_mats.insert(p.prefix_mats.end(), g->m, g->m + 4);
+            }
+        }
+    }
+    prog[n] = static_cast<int>(entries.size());
+    for (int &o : prog) o += n + 1;  // entries follow the offset table
+    prog.insert(prog.end(), entries.begin(), entries.end());
+    p.prefix_prog = std::move(prog);
+    std::vector<GateRec> keep;
+    keep.swap(rest);
+    p.gates = std::move(keep);
+    p.synth = true;
+}
+} // namespace
+
 void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts) {
     require(n >= 1 && n <= kMaxQubits, "plan: nqubit out of range");
     require(dtype == QSV_C64 || dtype == QSV_C128, "plan: bad dtype");
@@ -247,6 +303,7 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : 0; // 0: per pass (planner.cpp)
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
+    if (p->opts.from_zero && ctx->world == 1 && cfg.fuse && plan_uses_jit(*p)) extract_prefix(*p);
     if (ctx->world == 1) {
         // swaps as relabelings, the final layout folded into the last pass
         const bool relabel = cfg.fuse && p->opts.no_relabel == 0 && plan_uses_jit(*p) && p->nslots == 0;
@@ -261,6 +318,10 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
         }
         if (!p->gates.empty()) {
             auto passes = plan_passes(gl, phys, cfg, p->encs, out_perm);
+            if (p->synth) {
+                require(!passes.empty(), "plan: product-state prefix without a pass");
+                passes.front().synth = true;
+            }
             for (auto &ph : passes) {
                 Step s;
                 s.pass = static_cast<int>(p->passes.size());
@@ -348,6 +409,10 @@ void upload_plan(Plan &p) {
     up(&p.d_blob, blob.data(), blob.size());
     up(&p.d_tables, tables.data(), tables.size());
     if (!p.encs.empty()) up(&p.d_encs, p.encs.data(), p.encs.size() * sizeof(EncDesc));
+    if (p.synth) {
+        up(&p.d_prefix_prog, p.prefix_prog.data(), p.prefix_prog.size() * sizeof(int));
+        up(&p.d_prefix_mats, p.prefix_mats.data(), p.prefix_mats.size() * sizeof(cplx));
+    }
     const size_t amp = p.dtype == QSV_C64 ? 8 : 16;
     p.dev.clear();
     for (size_t i = 0; i < p.passes.size(); ++i) {
@@ -381,6 +446,7 @@ void upload_plan(Plan &p) {
                 "plan: pass program does not fit in shared memory");
         dp.grid = std::max(1, tile_kernel_blocks_per_sm(p.dtype, dp.R, dp.threads, dp.smem)) * p.ctx->sm_count;
         const bool use_jit = plan_uses_jit(p);
+        require(!ph.synth || use_jit, "plan: a synthesising pass needs the specialised kernels");
         dp.out_of_place = !ph.out_perm.empty();
         require(!dp.out_of_place || use_jit, "plan: permuting passes need the specialised kernels");
         if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
@@ -420,12 +486,24 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
         launch_bind(p, static_cast<const double *>(p.d_data), rows, slots, s);
         enc_table = p.d_enc_table;
     }
+    const int brows = rows > 0 ? rows : st.batch;
+    if (p.synth) {
+        const size_t need = static_cast<size_t>(brows) * p.nlocal * 2 * (p.dtype == QSV_C64 ? 8 : 16);
+        if (static_cast<size_t>(brows) > p.prefix_rows) {
+            cudaFree(p.d_prefix);
+            p.d_prefix = nullptr;
+            QSV_CUDA(cudaMalloc(&p.d_prefix, need));
+            p.prefix_rows = brows;
+        }
+        launch_prefix(p, brows, s);
+    }
     for (size_t i = 0; i < p.steps.size(); ++i) {
         const Step &stp = p.steps[i];
         if (stp.kind == 0) {
             DevPass dp = p.dev[stp.pass];
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
+            dp.args.prefix = p.passes[stp.pass].synth ? p.d_prefix : nullptr;
             run_pass(dp, p.dtype, st, s, i + 1 == p.steps.size() ? zout : nullptr);
         } else {
             dist_swap_bits(st, stp.swap_bits, nullptr, 0);

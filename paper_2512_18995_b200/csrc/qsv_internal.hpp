@@ -137,6 +137,7 @@ struct PassArgs {
     int32_t nlocal, K, L, ngroups, next;
     int32_t tile_pos[kMaxTileBits];  // physical position of tile-local bit i
     int32_t ext_pos[kMaxQubits];     // physical positions of non-tile local bits
+    const void *prefix;              // synthesising first pass: [row][phys bit][0/1] complex T
 };
 
 // Shared-memory layout of a tile CTA: [tile 2^K amps][hi_off 2^(K-L) u64][program]
@@ -199,6 +200,9 @@ struct PassHost {
     // Output bit permutation (input physical bit -> output physical bit);
     // empty = identity. A permuting pass writes out of place (State::scratch).
     std::vector<int> out_perm;
+    // First pass of a from-|0> plan: the register sets are synthesised from
+    // the per-row, per-bit product-state vectors instead of loaded.
+    bool synth = false;
     // The pass's gates in execution order, wires mapped to physical bits
     // (schedule export for host-side verification, qsv_plan_dry).
     std::vector<GateRec> exec_gates;
@@ -275,6 +279,14 @@ struct Plan {
     void *d_data = nullptr;
     size_t d_data_cap = 0;
     void *d_z = nullptr;       // fused <Z> sums: batch x (nlocal + 1)
+    // product-state prefix of a from-|0> plan: per wire, its leading
+    // single-qubit gates (prog: n + 1 offsets, then entries enc index >= 0 or
+    // -(1 + constant matrix index)); d_prefix: [row][phys bit][2] complex T
+    bool synth = false;
+    std::vector<int> prefix_prog;
+    std::vector<cplx> prefix_mats;
+    void *d_prefix_prog = nullptr, *d_prefix_mats = nullptr, *d_prefix = nullptr;
+    size_t prefix_rows = 0;
     size_t d_z_cap = 0;
     std::vector<DevPass> dev;
     qsv_opts opts{};
@@ -317,6 +329,8 @@ void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *z
 void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots, double *host_out);
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout = nullptr);
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
+// per-row, per-bit product-state vectors of a from-|0> plan into p.d_prefix
+void launch_prefix(const Plan &p, int rows, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);
 int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);

@@ -79,7 +79,8 @@ class qsv_obs(C.Structure):
 class qsv_opts(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_bits", C.c_int32), ("low_bits", C.c_int32), ("use_graph", C.c_int32),
                 ("no_fuse_1q", C.c_int32), ("no_phase_flush", C.c_int32), ("jit", C.c_int32), ("reg_slots", C.c_int32),
-                ("no_relabel", C.c_int32), ("reserved", C.c_int32 * 3)]
+                ("no_relabel", C.c_int32), ("from_zero", C.c_int32),
+                ("reserved", C.c_int32 * 2)]
 
 
 class qsv_plan_info(C.Structure):
@@ -673,6 +674,8 @@ class Circuit:
         data = [] if data is None else data
         arr, keep = gate_array(self._gates)
         o = make_opts(opts)
+        if init is None and "from_zero" not in (opts or {}):
+            o.from_zero = 1  # starts from |0...0>: leading 1q gates become a synthesised product state
         if len(data) == 0:
             if slots != 0:
                 raise InvalidInput("circuit has encode slots but no data given")

@@ -47,6 +47,12 @@ def f2z():
 ms_fz = timed(f2z, reps=10)
 print(f"cfg2 fused forward + <Z_i> (qsv_plan_execute_expect_z, host sync) {ms_fz:.3f} ms "
       f"({4096 / ms_fz * 1e3:.0f} circuits/s)", flush=True)
+pz = qsv.Plan(12, cir.gates(), dtype=qsv.C64, opts={"from_zero": 1})
+ms_pz = timed(lambda: pz.execute(st, data))
+ms_pzz = timed(lambda: pz.execute_expect_z(st, data), reps=10)
+print(f"cfg2 from-|0> plan (product-state prefix synthesised in the pass): forward {ms_pz:.3f} ms "
+      f"({4096 / ms_pz * 1e3:.0f} circuits/s); forward + <Z_i> {ms_pzz:.3f} ms ({4096 / ms_pzz * 1e3:.0f} circuits/s)",
+      flush=True)
 print(f"cfg2 4096x12q c64 {p.info['ngates']} gates passes={p.info['npasses']}: forward {ms:.3f} ms "
       f"({4096 / ms * 1e3:.0f} circuits/s); forward + <Z_i> (host sync) {ms_z:.3f} ms "
       f"({4096 / ms_z * 1e3:.0f} circuits/s)", flush=True)

@@ -334,3 +334,26 @@ def test_execute_expect_z_fused_and_fallback(dtype, tol):
     z2 = p2.execute_expect_z(s2)
     want2 = big.forward(dtype=dtype).expect_z_all()
     assert np.max(np.abs(z2 - want2)) <= tol
+
+
+@pytest.mark.parametrize("dtype,tol", [(C64, 1e-5), (C128, 1e-12)])
+def test_from_zero_product_state_prefix(dtype, tol):
+    """opts.from_zero: each wire's leading 1q gates (encoded ones included)
+    become a product state synthesised in the first pass; the state's old
+    content is ignored. Equal to the plain plan run on |0...0>."""
+    cir, data = W.cfg2_circuit(10, layers=3, rows=129)
+    fast = qsv.Plan(10, cir.gates(), dtype=dtype, opts={"from_zero": 1})
+    plain = qsv.Plan(10, cir.gates(), dtype=dtype)
+    st = QubitState(10, batch=129, dtype=dtype)
+    st.upload(random_state(Rng(3, "junk"), 10), 0)  # ignored by the from-zero plan
+    z1 = fast.execute_expect_z(st, data)
+    a1 = st.amplitudes(5)
+    s0 = QubitState(10, batch=129, dtype=dtype)
+    z0 = plain.execute_expect_z(s0, data)
+    assert np.max(np.abs(z1 - z0)) <= tol
+    assert np.max(np.abs(a1 - s0.amplitudes(5))) <= tol
+    for cirx, n in ((W.cfg4_circuit(12, layers=3), 12), (W.cfg1_circuit(12, layers=2), 12),
+                    (random_circuit(Rng(5, "fz"), 9, 80), 9)):
+        got = cirx.forward(dtype=dtype).amplitudes()  # forward() plans from zero
+        want = ref_or_port_forward(n, cirx.gates())[0]
+        assert np.max(np.abs(got - want)) <= tol
