@@ -444,11 +444,62 @@ int qsv_expect_z_all(qsv_state *st, double *out) {
     });
 }
 
+namespace {
+// X/Y of an observable on a global (rank) qubit: swap that qubit with a local
+// bit the observable does not use -- the same exchange a gate on the wire
+// triggers (dist.cu) -- so the Pauli kernel sees it locally; swapping the
+// same pairs again restores the layout (tests/test_dist.cpp:189-204 measures
+// X on a rank wire).
+std::vector<std::pair<int, int>> localise_xy(qsv_state *st, const qsv_obs &o) {
+    std::vector<std::pair<int, int>> pairs;
+    if (st->nlocal == st->n) return pairs;
+    std::vector<char> used(st->n, 0);
+    for (int j = 0; j < o.nwires; ++j)
+        if (o.wires[j] >= 0 && o.wires[j] < st->n) used[st->perm[o.wires[j]]] = 1;
+    int next_lb = 0;
+    for (int j = 0; j < o.nwires; ++j) {
+        const char c = o.basis[j];
+        if (c == 'z' || o.wires[j] < 0 || o.wires[j] >= st->n) continue;
+        const int gb = st->perm[o.wires[j]];
+        if (gb < st->nlocal) continue;
+        while (next_lb < st->nlocal && used[next_lb]) ++next_lb;
+        require(next_lb < st->nlocal, "observable: no free local qubit to localise a global x/y");
+        used[next_lb] = 1;
+        pairs.emplace_back(gb, next_lb);
+    }
+    return pairs;
+}
+void apply_swaps(qsv_state *st, const std::vector<std::pair<int, int>> &pairs) {
+    if (pairs.empty()) return;
+    dist_swap_bits(*st, pairs, nullptr, 0);
+    for (const auto &[gb, lb] : pairs) {
+        int wa = -1, wb = -1;
+        for (int w = 0; w < st->n; ++w) {
+            if (st->perm[w] == gb) wa = w;
+            if (st->perm[w] == lb) wb = w;
+        }
+        std::swap(st->perm[wa], st->perm[wb]);
+    }
+}
+} // namespace
+
 int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
     return guard([&] {
         require(st && (nobs == 0 || (obs && out)), "null argument");
         for (int i = 0; i < nobs; ++i) {
             const qsv_obs &o = obs[i];
+            const auto moved = localise_xy(st, o);
+            apply_swaps(st, moved);
+            struct Restore {  // the layout comes back even when the observable fails
+                qsv_state *st;
+                std::vector<std::pair<int, int>> pairs;
+                ~Restore() {
+                    try {
+                        apply_swaps(st, pairs);
+                    } catch (...) {
+                    }
+                }
+            } restore{st, std::vector<std::pair<int, int>>(moved.rbegin(), moved.rend())};
             require(o.nwires >= 0 && (o.nwires == 0 || (o.wires && o.basis)), "observable: bad wires");
             require(static_cast<int>(std::strlen(o.basis ? o.basis : "")) == o.nwires,
                     "observable: one basis letter per wire"); // circuit.hpp:97
@@ -467,7 +518,7 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
                     fail(QSV_ERR_INVALID, "observable: repeated wire not supported");
                 seen.push_back(w);
                 const int pb = st->perm[w];
-                require(pb < st->nlocal || c == 'z', "observable: x/y on a global qubit not supported");
+                require(pb < st->nlocal || c == 'z', "observable: internal: x/y on a global qubit after localisation");
                 const uint64_t bit = 1ull << pb;
                 if (c == 'x') flip |= bit;
                 if (c == 'y') flip |= bit, zy |= bit, ++ny;

@@ -46,7 +46,7 @@ def _shim():
     yield
 
 
-def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q, env=None):
+def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q, env=None, data=None):
     try:
         os.environ["QSV_NCCL_LIB"] = str(SHIM)
         os.environ.update(env or {})
@@ -59,23 +59,25 @@ def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q, env=None):
         if init is not None:
             st.upload(init[rank << nl:(rank + 1) << nl])
         plan = Q.Plan(n, gates, dtype=dtype, ctx=ctx)
-        plan.execute(st)
+        plan.execute(st, data)
         local = st.amplitudes()
         z = st.expect_z_all()[0]
         nrm = float(st.norm2()[0])
         ex = Q.expectation_many(st, [Q.Observable(w, b) for w, b in obs])[0] if obs else []
-        q.put((rank, local, z, nrm, list(ex), plan.info["nswaps"]))
+        local = st.amplitudes()  # again: expectations must leave the layout as they found it
+        counts = Q.measure(st, 1000, [0, n - 1], Q.Rng(3, "shim-measure"), True)  # measure_dist
+        q.put((rank, local, z, nrm, list(ex) + [counts], plan.info["nswaps"]))
         del plan, st
         ctx.close()
     except Exception:
         q.put((rank, traceback.format_exc(), None, None, None, None))
 
 
-def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=(), env=None):
+def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=(), env=None, data=None):
     uid = qsv.Context.nccl_unique_id()
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
-    procs = [ctxm.Process(target=_rank_main, args=(r, world, uid, n, gates, init, dtype, list(obs), q, env))
+    procs = [ctxm.Process(target=_rank_main, args=(r, world, uid, n, gates, init, dtype, list(obs), q, env, data))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -164,3 +166,44 @@ def test_pipelined_swap_rounds_4_ranks():
     want = O.port_forward(n, cir.gates())[0]
     assert nsw > 0
     assert np.max(np.abs(got - want)) <= 1e-12
+
+
+def test_reference_dist_expectation_case_and_global_xy():
+    """tests/test_dist.cpp:189-204: 4 qubits on 4 ranks, encoded Ry layer +
+    cnot ring, <Z_0> and <X_1> -- X on a RANK wire (localised by a swap and
+    swapped back); plus Y/X on rank wires of a larger cfg5-family state."""
+    cir = qsv.Circuit(4)
+    cir.rylayer(encode=True)
+    cir.cnot_ring()
+    data = [[0.0, 1.0, 2.0, 3.0]]
+    full = O.port_forward(4, cir.gates(), data=data)[0]
+    got, z, nrm, ex, _ = run_ranks(4, cir.gates(), 4, obs=[([0], "z"), ([1], "x")], data=data)
+    assert np.max(np.abs(got - full)) <= 1e-12
+    assert abs(ex[0] - O.port_expectation(4, full, [0], "z")[0]) <= 1e-12
+    assert abs(ex[1] - O.port_expectation(4, full, [1], "x")[0]) <= 1e-12
+    n = 10
+    c5 = W.cfg5_circuit(n, layers=2)
+    obs = [([0], "x"), ([1, 0], "yz"), ([0, 1, 5], "xyz"), ([1], "y")]
+    got, z, nrm, ex, _ = run_ranks(n, c5.gates(), 4, obs=obs)
+    want = O.port_forward(n, c5.gates())[0]
+    assert np.max(np.abs(got - want)) <= 1e-12  # the layout was restored
+    for (w, b), e in zip(obs, ex):
+        assert abs(e - O.port_expectation(n, want, w, b)[0]) <= 1e-12
+
+
+def test_measure_dist_equals_single_rank_histogram():  # tests/test_dist.cpp:176-187
+    n = 10
+    cir = W.cfg4_circuit(n, layers=2)
+    got, z, nrm, ex, _ = run_ranks(n, cir.gates(), 4)
+    counts = ex[-1]
+    want = O.port_forward(n, cir.gates())[0]
+    if O.REF_LIB.exists():
+        ref = O.ref_measure(n, want, 1000, [0, n - 1], 3, "shim-measure")
+        for i, c in enumerate(ref):
+            key = format(i, "02b")
+            assert counts.get(key, {"count": 0})["count"] == int(c), key
+    probs = O.port_marginal(n, want, [0, n - 1])
+    for i, pr in enumerate(probs):
+        key = format(i, "02b")
+        if pr > 0:
+            assert abs(counts[key]["probability"] - pr) <= 1e-12
