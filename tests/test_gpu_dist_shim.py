@@ -207,3 +207,70 @@ def test_measure_dist_equals_single_rank_histogram():  # tests/test_dist.cpp:176
         key = format(i, "02b")
         if pr > 0:
             assert abs(counts[key]["probability"] - pr) <= 1e-12
+
+
+def _adjoint_rank(rank, world, uid, cir, data, q):
+    try:
+        os.environ["QSV_NCCL_LIB"] = str(SHIM)
+        from paper_2512_18995_b200 import qsv as Q
+
+        ctx = Q.Context(0, rank, world, uid)
+        g = Q.adjoint_gradients(cir, None, data, ctx=ctx)
+        q.put((rank, list(g.param_grads), list(g.data_grads)))
+        ctx.close()
+    except Exception:
+        q.put((rank, traceback.format_exc(), None))
+
+
+def run_adjoint(cir, world, data=()):
+    uid = qsv.Context.nccl_unique_id()
+    ctxm = mp.get_context("spawn")
+    q = ctxm.Queue()
+    procs = [ctxm.Process(target=_adjoint_rank, args=(r, world, uid, cir, list(data), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, pg, dg = q.get(timeout=180)
+            if dg is None:
+                raise AssertionError(f"rank {r} failed:\n{pg}")
+            res[r] = (pg, dg)
+    finally:
+        for p in procs:
+            p.join(timeout=60)
+            if p.is_alive():
+                p.kill()
+    return res
+
+
+def test_adjoint_dist_matches_single_rank():  # tests/test_dist.cpp:224-276
+    # (the reference's 1-qubit-on-2-ranks case leaves no local qubit; this
+    # engine needs n >= log2(ranks) + 1 and says so: "more ranks than amplitudes")
+    cir = qsv.Circuit(2)
+    cir.ry(0, 1.1, trainable=True)
+    cir.observable([0], "z")
+    res = run_adjoint(cir, 2)  # wire 0 is the rank qubit
+    for r in res:
+        assert abs(res[r][0][0] + np.sin(1.1)) <= 1e-10
+    rng = qsv.Rng(13, "shim-adj")
+    for world in (2, 4):
+        c = random_circuit(rng, 6, 14)
+        for g in c.gates():
+            g.trainable = bool(g.params)
+        c.observable([0], "z")
+        c.observable([2], "x")
+        want = qsv.adjoint_gradients(c)
+        res = run_adjoint(c, world)
+        for r in res:
+            assert np.max(np.abs(np.asarray(res[r][0]) - want.param_grads)) <= 1e-10
+    c = qsv.Circuit(4)
+    c.rylayer(encode=True)
+    c.cnot_ring()
+    c.observable([0], "z")
+    c.observable([1], "x")
+    data = [0.0, 1.0, 2.0, 3.0]
+    want = qsv.adjoint_gradients(c, None, data)
+    res = run_adjoint(c, 4, data)
+    for r in res:
+        assert np.max(np.abs(np.asarray(res[r][1]) - want.data_grads)) <= 1e-10
