@@ -411,16 +411,12 @@ struct Gen {
             // the factor's terms (no multiplication by a constant 1: without
             // fast-math 0 * x does not fold, so it would cost FP64 work)
             std::vector<std::string> terms;
-            const bool eh = t.eidx >= 0 && t.table_hi >= 0 && ehoff.count(ti);
-            if (eh)  // per-tile E x hi-table product (computed with E)
-                terms.push_back("EH[" + ehoff_str() + std::to_string(ehoff.at(ti)) + " + (s >> " +
-                                std::to_string(t.lo_bits) + ")]");
-            else if (t.eidx >= 0) terms.push_back("E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]");
+            if (t.eidx >= 0) terms.push_back("E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]");
             if (t.table >= 0) terms.push_back("tab" + std::to_string(ti));
             if (t.table_lo >= 0)
                 terms.push_back("stab[" + std::to_string(stab_off.at(t.table_lo)) + " + (s & " +
                                 std::to_string((1 << t.lo_bits) - 1) + ")]");
-            if (t.table_hi >= 0 && !eh)
+            if (t.table_hi >= 0)
                 terms.push_back("stab[" + std::to_string(stab_off.at(t.table_hi)) + " + (s >> " +
                                 std::to_string(t.lo_bits) + ")]");
             if (terms.empty()) terms.push_back("mk(1, 0)");
@@ -545,7 +541,7 @@ struct Gen {
             next_max += ne;
         }
         const bool pf = prefetch;
-        late = pf && late_issue;
+        late = pf;  // prefetching passes issue tile t + 1 after tile t's first barrier
         // late-issue prefetch rewrites E while other warps may still read the
         // previous tile's factors: one E set per shared tile
         if (next_max) o << "  __shared__ " << V << " E[" << (late ? 2 * next_max : next_max) << "];\n";
@@ -612,31 +608,8 @@ struct Gen {
                 }
             }
         }
-        // E x hi-table rows: a target with both a per-tile factor and a
-        // high-set-bit table gets 2^hi entries per tile, so its flush factor is
-        // one product (EH[s >> lo] * lo[s & mask]) instead of two
-        ehoff.clear();
-        eh_total = 0;
-        // Measured slower (cfg3 30q, interleaved A/B: 27.0 vs 26.3 ms median):
-        // the extra per-tile products sit on the owner threads' path to the
-        // next barrier. Kept behind QSV_X_EH=1 for further experiments.
-        const char *xeh = std::getenv("QSV_X_EH");
-        for (const ETask &e : etasks) {
-            const FlushTarget &t = ph.targets[e.ti];
-            if (t.table_hi < 0 || !(xeh && xeh[0] == '1')) continue;
-            ehoff[e.ti] = eh_total;
-            eh_total += 1 << ((K - R) - t.lo_bits);
-        }
-        if (eh_total) o << "  __shared__ " << V << " EH[" << (late ? 2 * eh_total : eh_total) << "];\n";
-        auto emit_e_store = [&](const ETask &e, const std::string &ehofs, const std::string &eofs,
-                                const std::string &ind) {
-            const FlushTarget &t = ph.targets[e.ti];
-            if (ehoff.count(e.ti)) {
-                const int nh = 1 << ((K - R) - t.lo_bits);
-                for (int j = 0; j < nh; ++j)
-                    o << ind << "EH[" << ehofs << ehoff.at(e.ti) + j << "] = cmulv(f, stab["
-                      << stab_off.at(t.table_hi) + j << "]);\n";
-            } else o << ind << "E[" << eofs << e.slot << "] = f;\n";
+        auto emit_e_store = [&](const ETask &e, const std::string &eofs, const std::string &ind) {
+            o << ind << "E[" << eofs << e.slot << "] = f;\n";
         };
         const bool epipe = pf && late && any_e;
         const std::string tmask = std::to_string((1ull << tpr_log) - 1) + "ull";
@@ -648,7 +621,7 @@ struct Gen {
                     o << ind << "  f = cmulv(f, a.tables[" << t.ext_tab + c * 256 << " + ((tl >> " << 8 * c
                       << ") & 255)]);\n";
                 for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbase", "f", ind + "  ");
-                emit_e_store(e, ehoff_str(), eoff(), ind + "  ");
+                emit_e_store(e, eoff(), ind + "  ");
                 o << ind << "}\n";
             }
         };
@@ -680,8 +653,7 @@ struct Gen {
                     o << ind << "    f = " << (c ? "cmulv(f, " : "(") << "Eraw[(" << nb << ") * " << nraw << " + "
                       << e.raw + c << "]);\n";
                 for (int q = t.ext_rest; q < t.ext_end; ++q) emit_rec_factor(ph.recs[q], "pbx", "f", ind + "    ");
-                emit_e_store(e, "(" + nb + ") * " + std::to_string(eh_total) + " + ",
-                             "(" + nb + ") * " + std::to_string(e_stride) + " + ", ind + "    ");
+                emit_e_store(e, "(" + nb + ") * " + std::to_string(e_stride) + " + ", ind + "    ");
                 o << ind << "  }\n";
             }
             o << ind << "}\n";
@@ -706,8 +678,7 @@ struct Gen {
             o << "    const u64 g0 = tb | (" << scatter("(u0 >> " + std::to_string(L) + ")", hi, true) << ") | (u0 & "
               << ((1 << L) - 1) << ");\n";
             o << "    const int s0 = swz(u0);\n";
-            const char *xold = std::getenv("QSV_X_OLDISSUE");
-            if (nchunks % threads == 0 && !(xold && xold[0] == '1')) {
+            if (nchunks % threads == 0) {
                 // unrolled: per chunk one constant global offset (its tile bits
                 // are disjoint from g0's, so OR = ADD) and one constant XOR
                 o << "    const " << V << " *p0 = src + g0;\n";
@@ -722,12 +693,7 @@ struct Gen {
                 }
                 o << "  };\n";
             } else {
-            if (nchunks % threads == 0) {
-                o << "#pragma unroll\n";
-                o << "    for (int k = 0; k < " << nchunks / threads << "; ++k) {\n";
-            } else {
                 o << "    for (int k = 0; k * " << threads << " + threadIdx.x < " << nchunks << "; ++k) {\n";
-            }
             // k * step has bits only at or above log2(step) (a power of two)
             o << "      const int uk = k * " << step << ";\n";
             o << "      const u64 g = g0 | (" << scatter("(uk >> " + std::to_string(L) + ")", hi, true) << ") | (uk & "
@@ -952,13 +918,9 @@ struct Gen {
     }
     bool double_buffer = true;
     bool prefetch = false;
-    bool late_issue = true; // prefetch: issue tile t + gridDim after tile t's barrier
     bool late = false;
     int e_stride = 0;
     std::string eoff() const { return late ? "(ec * " + std::to_string(e_stride) + ") + " : ""; }
-    std::map<int, int> ehoff;  // FlushTarget index -> first EH entry
-    int eh_total = 0;
-    std::string ehoff_str() const { return late ? "(ec * " + std::to_string(eh_total) + ") + " : ""; }
     int stages = 2;  // shared tile buffers in prefetch mode (late issue)
     bool zsum = false; // fused <Z> epilogue in the last group (whole-row tiles)
     std::vector<int> ebase; // first E slot of each group
@@ -987,8 +949,6 @@ std::string generate_pass_source(const PassHost &ph, int dtype, const std::strin
     g.zsum = zsum;
     g.double_buffer = false;
     g.prefetch = dbuf;
-    const char *pe = std::getenv("QSV_PF_EARLY");
-    g.late_issue = !(pe && pe[0] == '1');
     g.stages = dbuf_stages(ph, dtype);
     const int nsets = 1 << (ph.K - ph.R);
     const int amp = dtype == QSV_C64 ? 8 : 16;

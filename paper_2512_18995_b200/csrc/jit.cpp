@@ -26,10 +26,6 @@ namespace qsv {
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
                                  bool zsum = false);
 int dbuf_stages(const PassHost &ph, int dtype);
-bool double_buffer_enabled() {
-    const char *e = std::getenv("QSV_DBUF");
-    return e && e[0] == '1'; // measured slower than 2 single-buffered CTAs per SM (r01)
-}
 
 namespace {
 
@@ -176,7 +172,6 @@ static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, 
     const char *pe = std::getenv("QSV_PREFETCH");
     const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
                       (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
-    (void)double_buffer_enabled;
     std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf, zsum);
     char key[32];
     std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
