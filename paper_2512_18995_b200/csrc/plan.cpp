@@ -15,6 +15,8 @@
 #include <bit>
 #include <cstring>
 
+#include <cmath>
+
 #include "qsv_internal.hpp"
 
 namespace qsv {
@@ -306,7 +308,18 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     if (p->opts.from_zero && ctx->world == 1 && cfg.fuse && plan_uses_jit(*p)) extract_prefix(*p);
     if (ctx->world == 1) {
         // swaps as relabelings, the final layout folded into the last pass
-        const bool relabel = cfg.fuse && p->opts.no_relabel == 0 && plan_uses_jit(*p) && p->nslots == 0;
+        bool relabel = cfg.fuse && p->opts.no_relabel == 0 && plan_uses_jit(*p) && p->nslots == 0;
+        // relabelled swaps end in an out-of-place pass (a second state-sized
+        // buffer); when two states do not fit, swaps move data in place
+        if (relabel && ctx->stream) {
+            size_t free_b = 0, total_b = 0;
+            if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+                const double state = std::ldexp(static_cast<double>(dtype == QSV_C64 ? 8 : 16), p->nlocal);
+                if (2.0 * state > 0.92 * static_cast<double>(total_b)) relabel = false;
+            } else {
+                cudaGetLastError();
+            }
+        }
         std::vector<GateRec> gl = p->gates;
         std::vector<int> phys = p->perm_in, out_perm;
         if (relabel) {
