@@ -125,6 +125,7 @@ struct Gen {
     // (each group's set -> slot mapping, the permuted copy-out) hits 8
     // distinct 16-byte bank groups; the default folds bits 3+i, 6+i, 9+i, 12+i.
     int swm[3] = {0, 0, 0};
+    bool noswz() const { return !f32 && swm[0] == 0 && swm[1] == 0 && swm[2] == 0; }
     int swz_of(int u) const {
         if (f32) return swz_host(u, true);
         int f = 0;
@@ -150,6 +151,14 @@ struct Gen {
             for (const auto &b : patterns) n += ok(m, b);
             return n;
         };
+        // no swizzle at all when every pattern's phase-varying bits are the 3
+        // lowest tile bits (the usual case: they are the contiguous-run bits):
+        // then a register slot's offset is a plain immediate on the set's base
+        const int zero[3] = {0, 0, 0};
+        if (score(zero) == static_cast<int>(patterns.size())) {
+            swm[0] = swm[1] = swm[2] = 0;
+            return;
+        }
         int best[3];
         for (int i = 0; i < 3; ++i) {
             best[i] = 0;
@@ -688,8 +697,8 @@ struct Gen {
                     for (size_t i = 0; i < hi.size(); ++i)
                         if (((uk >> L) >> i) & 1) gk |= 1ull << hi[i];
                     o << "    asm volatile(\"cp.async.cg.shared.global [%0], [%1], 16;\\n\" :: \"r\"((unsigned)"
-                         "__cvta_generic_to_shared(&buf[s0 ^ "
-                      << swz_of(uk) << "])), \"l\"(p0 + " << gk << "ull) : \"memory\");\n";
+                         "__cvta_generic_to_shared(&buf[s0 "
+                      << (noswz() ? "+ " : "^ ") << swz_of(uk) << "])), \"l\"(p0 + " << gk << "ull) : \"memory\");\n";
                 }
                 o << "  };\n";
             } else {
@@ -832,7 +841,8 @@ struct Gen {
                 for (int r = 0; r < NR; ++r) {
                     if (from_hbm)
                         o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
-                    else o << "      " << V << " v" << r << " = tile[sb ^ " << swz_of(uoff[r]) << "];\n";
+                    else o << "      " << V << " v" << r << " = tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r])
+                           << "];\n";
                 }
             // QSV_DEBUG_NOCOMPUTE=1 (diagnostics only): the pass moves data without
             // applying its gates -- the memory-structure ceiling of its geometry
@@ -861,7 +871,7 @@ struct Gen {
             }
             for (int r = 0; r < NR; ++r) {
                 if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
-                else o << "      tile[sb ^ " << swz_of(uoff[r]) << "] = v" << r << ";\n";
+                else o << "      tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
             if (zhere) {
