@@ -123,6 +123,35 @@ def cpu_reference_sample(cir, n, psi, gates_per_step, steps):
     return times
 
 
+def swap_kernels(n, cir, world, nl, amp_bytes):
+    """Kernels one execute launches for its qubit swaps (dist.cu): per run of
+    disjoint bit pairs (m pairs) one gather and one scatter per chunk round,
+    a round moving up to 256 MiB over the 2^m - 1 peers."""
+    if world == 1:
+        return 0
+    from paper_2512_18995_b200 import qsv
+
+    sched = qsv.plan_schedule(n, cir.gates(), world=world)
+    total = 0
+    for step in sched["steps"]:
+        if step["kind"] != "swap":
+            continue
+        runs, cur = [], []
+        for gb, lb in step["pairs"]:
+            if any(gb == g or lb == l for g, l in cur):
+                runs.append(cur)
+                cur = []
+            cur.append((gb, lb))
+        runs.append(cur)
+        for r in runs:
+            m = len(r)
+            nv = (1 << m) - 1
+            block = (1 << nl) >> m
+            chunk = max(1, min(block * nv, (256 << 20) // amp_bytes) // nv)
+            total += 2 * -(-block // chunk)
+    return total
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -332,10 +361,7 @@ def main():
                          "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
-            # pass kernels + per swapped bit pair one gather and one scatter
-            # kernel per 256 MiB chunk of the moving half (dist.cu)
-            "gpu_launches": args.steps * (npass + plan.info["nswaps"] * 2 *
-                                          -(-((1 << nl) // 2 * amp_bytes) // (256 << 20))),
+            "gpu_launches": args.steps * (npass + swap_kernels(n, cir, world, nl, amp_bytes)),
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
