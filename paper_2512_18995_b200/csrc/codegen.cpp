@@ -903,10 +903,27 @@ struct Gen {
             for (int e : ph.ext_pos) ext_out.push_back(ph.out_perm[e]);
             o << "    {\n      " << V << " *dst = (" << V << " *)a.out + (u64)row * a.row_stride;\n";
             o << "      const u64 tbo = " << scatter("tl", ext_out, true) << ";\n";
-            o << "      for (int w = threadIdx.x; w < " << (1 << K) << "; w += " << threads << ") {\n";
-            o << "        const int u = " << scatter("w", w2u, false) << ";\n";
-            o << "        stcs(&dst[tbo | " << scatter("w", w2out, true) << "], tile[swz(u)]);\n";
-            o << "      }\n    }\n";
+            if ((1 << K) % threads == 0 && (threads & (threads - 1)) == 0) {
+                // w = tid + k * threads: both bit scatters and the swizzle are
+                // linear, so the per-thread parts are computed once and every
+                // k adds constants (the unrolled loop needs no index math)
+                o << "      const int su0 = swz(" << scatter("threadIdx.x", w2u, false) << ");\n";
+                o << "      " << V << " *d0 = dst + (tbo | " << scatter("threadIdx.x", w2out, true) << ");\n";
+                for (int k = 0; k < (1 << K) / threads; ++k) {
+                    const int wk = k * threads;
+                    int uk = 0;
+                    uint64_t ok = 0;
+                    for (size_t i = 0; i < w2u.size(); ++i)
+                        if ((wk >> i) & 1) uk |= 1 << w2u[i], ok |= 1ull << w2out[i];
+                    o << "      stcs(d0 + " << ok << "ull, tile[su0 ^ " << swz_of(uk) << "]);\n";
+                }
+                o << "    }\n";
+            } else {
+                o << "      for (int w = threadIdx.x; w < " << (1 << K) << "; w += " << threads << ") {\n";
+                o << "        const int u = " << scatter("w", w2u, false) << ";\n";
+                o << "        stcs(&dst[tbo | " << scatter("w", w2out, true) << "], tile[swz(u)]);\n";
+                o << "      }\n    }\n";
+            }
         }
         // the next tile's first group rewrites the shared tile / E
         if (!late && (G >= 2 || any_e || permuted || pf)) o << "    __syncthreads();\n";
