@@ -152,6 +152,28 @@ def swap_kernels(n, cir, world, nl, amp_bytes):
     return total
 
 
+def swap_bytes(n, cir, world, nl, amp_bytes):
+    """Bytes one GPU sends per execute in its qubit swaps: a run of m disjoint
+    bit pairs moves (1 - 2^-m) of the local slice (dist.cu all-to-all)."""
+    from paper_2512_18995_b200 import qsv
+
+    sched = qsv.plan_schedule(n, cir.gates(), world=world)
+    total = 0
+    for step in sched["steps"]:
+        if step["kind"] != "swap":
+            continue
+        runs, cur = [], []
+        for gb, lb in step["pairs"]:
+            if any(gb == g or lb == l for g, l in cur):
+                runs.append(cur)
+                cur = []
+            cur.append((gb, lb))
+        runs.append(cur)
+        for r in runs:
+            total += (amp_bytes << nl) * (1.0 - 2.0 ** -len(r))
+    return total
+
+
 def run_reference(args):
     rank, world, local = dist_env()
     if rank != 0:
@@ -271,6 +293,16 @@ def main():
     kinds = plan.step_kinds()
     lm = np.array(launch_ms)[:, kinds == 0]  # steps x passes (qubit-swap steps excluded)
     amp_bytes = 16
+    # qubit swaps (N > 1): bytes each GPU sends per execute over the swap
+    # steps' time, against the measured 770 GB/s per-direction peer copy and
+    # the nominal 900 GB/s (B200_PROFILING.md)
+    nvlink = None
+    if world > 1 and (kinds == 1).any():
+        sw_ms = float(np.array(launch_ms)[:, kinds == 1].sum(axis=1).mean())
+        sent = swap_bytes(n, cir, world, nl, amp_bytes)
+        gbs = sent / (sw_ms / 1e3) / 1e9
+        nvlink = {"bytes_sent_per_gpu_per_step": sent, "swap_ms_per_step": sw_ms, "achieved_GBps": gbs,
+                  "frac_of_measured_770": gbs / 770.0, "frac_of_nominal_900": gbs / 900.0}
     bytes_per_launch = 2.0 * amp_bytes * (1 << nl)  # read + write of every local amplitude
     avg_launch_ms = float(lm.mean())
     hbm_peak, peak_kind = peaks()
@@ -362,6 +394,7 @@ def main():
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
             "gpu_launches": args.steps * (npass + swap_kernels(n, cir, world, nl, amp_bytes)),
+            "nvlink": nvlink,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
