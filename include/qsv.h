@@ -106,17 +106,23 @@ typedef struct qsv_opts {
                                (Circuit::forward without init); the leading
                                single-qubit gates of every wire then become a
                                product state synthesised inside the first pass */
-    int32_t reserved[2];
+    int32_t super_bits;     /* L2 super-passes: pairs of passes whose tiles span at
+                               most this many qubits run as one launch, chunk by
+                               chunk through L2 (> 0 = on with this chunk size;
+                               0 = $QSV_SUPER_BITS, default off; -1 = off) */
+    int32_t reserved[1];
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */
 typedef struct qsv_plan_info {
     int32_t ngates;          /* source gates */
-    int32_t npasses;         /* state passes (kernel launches) per execute */
+    int32_t npasses;         /* pass launches per execute (an L2 super-pass is one) */
     int32_t nswaps;          /* global<->local qubit swaps (multi-GPU) */
     int32_t max_tile_bits;
     double bytes_per_exec;   /* algorithmic HBM bytes per execute (all passes) */
     double comm_bytes_per_exec; /* bytes sent per rank per execute */
+    int32_t ntile_passes;    /* tile passes per execute (>= npasses: super-passes run two) */
+    int32_t reserved;
 } qsv_plan_info;
 
 /* ---- library --------------------------------------------------------- */
@@ -245,7 +251,9 @@ int qsv_rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, voi
  * only its slice of a seeded input. */
 int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset, uint64_t count, void *out,
                     int nthreads);
-/* Step kinds of a plan in execution order (0 = local pass, 1 = qubit swap);
+/* Step kinds of a plan in execution order (0 = local pass launch, 1 = qubit
+ * swap, 2 = local pass run inside the previous step's launch: the second half
+ * of an L2 super-pass, whose profiled time is 0);
  * returns the step count (fills at most cap entries). */
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap);
 

@@ -390,6 +390,8 @@ int qsv_plan_info_get(const qsv_plan *p, qsv_plan_info *info) {
         info->ngates = p->ngates;
         for (const Step &s : p->steps) {
             if (s.kind == 0) {
+                info->ntile_passes += 1;
+                if (p->passes[s.pass].pair == 2) continue;  // inside its head's launch
                 info->npasses += 1;
                 info->bytes_per_exec += p->dev[s.pass].bytes;
                 info->max_tile_bits = std::max(info->max_tile_bits, p->passes[s.pass].K);
@@ -659,6 +661,8 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
             const double amp = dtype == QSV_C64 ? 8 : 16;
             for (const Step &s : p.steps) {
                 if (s.kind == 0) {
+                    info->ntile_passes += 1;
+                    if (p.passes[s.pass].pair == 2) continue;
                     info->npasses += 1;
                     info->bytes_per_exec += 2.0 * amp * std::ldexp(1.0, p.nlocal);
                     info->max_tile_bits = std::max(info->max_tile_bits, p.passes[s.pass].K);
@@ -688,7 +692,7 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
                     continue;
                 }
                 const PassHost &ph = p.passes[s.pass];
-                js += "{\"kind\":\"pass\",\"tile\":[";
+                js += "{\"kind\":\"pass\",\"pair\":" + std::to_string(ph.pair) + ",\"tile\":[";
                 for (size_t k = 0; k < ph.tile_pos.size(); ++k) js += (k ? "," : "") + std::to_string(ph.tile_pos[k]);
                 js += "],\"out_perm\":[";
                 for (size_t k = 0; k < ph.out_perm.size(); ++k) js += (k ? "," : "") + std::to_string(ph.out_perm[k]);
@@ -713,7 +717,9 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
         } else if (src && cap) {
             src[0] = 0;
             if (pass_index >= 0 && pass_index < static_cast<int>(p.passes.size())) {
-                const std::string s = jit_source(p.passes[pass_index], dtype);
+                const PassHost &ph = p.passes[pass_index];
+                const std::string s = ph.pair == 1 ? jit_pair_source(ph, p.passes[pass_index + 1], dtype)
+                                                   : jit_source(ph, dtype);
                 std::snprintf(src, cap, "%s", s.c_str());
             }
         }
@@ -739,7 +745,10 @@ int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset,
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
     if (!plan) return -QSV_ERR_INVALID;
     const int n = static_cast<int>(plan->steps.size());
-    for (int i = 0; i < n && i < cap && kinds; ++i) kinds[i] = plan->steps[i].kind;
+    for (int i = 0; i < n && i < cap && kinds; ++i) {
+        const Step &s = plan->steps[i];
+        kinds[i] = s.kind == 0 && plan->passes[s.pass].pair == 2 ? 2 : s.kind;
+    }
     return n;
 }
 

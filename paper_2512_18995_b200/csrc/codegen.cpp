@@ -481,35 +481,67 @@ struct Gen {
                 if ((op.flush.regmask >> r) & 1) cmul_const(r, op.regtab[r], ind);
     }
 
+    // Types and helpers shared by every pass body of one source.
+    std::string common() const {
+        std::ostringstream c;
+        c << "typedef unsigned long long u64;\n";
+        c << "struct __align__(" << (f32 ? 8 : 16) << ") " << V << " { " << T << " x, y; };\n";
+        c << "static __device__ __forceinline__ " << V << " mk(" << T << " x, " << T << " y) { " << V
+          << " r; r.x = x; r.y = y; return r; }\n";
+        c << "static __device__ __forceinline__ " << V << " cmulv(" << V << " a, " << V
+          << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
+        c << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
+          << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
+        // streaming (evict-first) 8/16-byte amplitude loads and stores; stwb:
+        // a plain write-back store (the first pass of an L2 super-pass keeps
+        // its output in L2 for the second)
+        const char *sfx = f32 ? "v2.f32" : "v2.f64";
+        const char *rc = f32 ? "f" : "d";
+        c << "static __device__ __forceinline__ " << V << " ldcs(const " << V << " *p) { " << V
+          << " r; asm volatile(\"ld.global.cs." << sfx << " {%0,%1}, [%2];\" : \"=" << rc << "\"(r.x), \"=" << rc
+          << "\"(r.y) : \"l\"(p)); return r; }\n";
+        c << "static __device__ __forceinline__ " << V << " ldcg(const " << V << " *p) { " << V
+          << " r; asm volatile(\"ld.global.cg." << sfx << " {%0,%1}, [%2];\" : \"=" << rc << "\"(r.x), \"=" << rc
+          << "\"(r.y) : \"l\"(p) : \"memory\"); return r; }\n";
+        c << "static __device__ __forceinline__ void stcs(" << V << " *p, " << V << " v) { asm volatile(\"st.global.cs."
+          << sfx << " [%0], {%1,%2};\" :: \"l\"(p), \"" << rc << "\"(v.x), \"" << rc << "\"(v.y) : \"memory\"); }\n";
+        c << "static __device__ __forceinline__ void stwb(" << V << " *p, " << V << " v) { asm volatile(\"st.global."
+          << sfx << " [%0], {%1,%2};\" :: \"l\"(p), \"" << rc << "\"(v.x), \"" << rc << "\"(v.y) : \"memory\"); }\n";
+        c << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
+          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; const " << V
+          << " *prefix; };\n";
+        return c.str();
+    }
+
+    int threads_of() const { return (kernel_threads(ph, f32 ? QSV_C64 : QSV_C128) + 31) / 32 * 32; }
+
+    // A whole single-pass kernel: the pass body over this CTA's tiles (a
+    // block of a.tpc consecutive tiles, or with a.tpc == 0 a grid-strided
+    // sequence).
     std::string source(const std::string &name) {
+        const int threads = threads_of();
+        const std::string body = body_fn("pass_body");
+        std::ostringstream k;
+        k << "// generated by qsv codegen.cpp: one fused tile pass\n" << common() << body;
+        k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
+          << (double_buffer ? 1 : kernel_min_blocks(ph, threads)) << ") " << name << "(const Args a) {\n";
+        k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+        k << "  const u64 t0 = a.tpc > 0 ? (u64)blockIdx.x * a.tpc : (u64)blockIdx.x;\n";
+        k << "  const u64 tend = a.tpc > 0 ? (t0 + a.tpc < a.total_tiles ? t0 + a.tpc : a.total_tiles) : a.total_tiles;\n";
+        k << "  const u64 tstep = a.tpc > 0 ? 1ull : (u64)gridDim.x;\n";
+        k << "  pass_body(a, t0, tend, tstep, smem_raw);\n}\n";
+        return k.str();
+    }
+
+    // The pass as a device function over tiles t0, t0 + tstep, ... < tend.
+    std::string body_fn(const std::string &fname) {
         const int K = ph.K, L = ph.L, NR = 1 << R;
         const int amp = f32 ? 8 : 16;
         const int apu = 16 / amp;
         const int nchunks = (1 << K) / apu;
         const int nsets = 1 << (K - R);
-        int threads = kernel_threads(ph, f32 ? QSV_C64 : QSV_C128);
-        threads = (threads + 31) / 32 * 32;
-        o << "// generated by qsv codegen.cpp: one fused tile pass\n";
-        o << "typedef unsigned long long u64;\n";
-        o << "struct __align__(" << (f32 ? 8 : 16) << ") " << V << " { " << T << " x, y; };\n";
-        o << "static __device__ __forceinline__ " << V << " mk(" << T << " x, " << T << " y) { " << V
-          << " r; r.x = x; r.y = y; return r; }\n";
-        o << "static __device__ __forceinline__ " << V << " cmulv(" << V << " a, " << V
-          << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
-        o << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
-          << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
-        // streaming (evict-first) 8/16-byte amplitude loads and stores
-        if (f32) {
-            o << "static __device__ __forceinline__ cf ldcs(const cf *p) { cf r; asm volatile(\"ld.global.cs.v2.f32 "
-                 "{%0,%1}, [%2];\" : \"=f\"(r.x), \"=f\"(r.y) : \"l\"(p)); return r; }\n";
-            o << "static __device__ __forceinline__ void stcs(cf *p, cf v) { asm volatile(\"st.global.cs.v2.f32 "
-                 "[%0], {%1,%2};\" :: \"l\"(p), \"f\"(v.x), \"f\"(v.y) : \"memory\"); }\n";
-        } else {
-            o << "static __device__ __forceinline__ cd ldcs(const cd *p) { cd r; asm volatile(\"ld.global.cs.v2.f64 "
-                 "{%0,%1}, [%2];\" : \"=d\"(r.x), \"=d\"(r.y) : \"l\"(p)); return r; }\n";
-            o << "static __device__ __forceinline__ void stcs(cd *p, cd v) { asm volatile(\"st.global.cs.v2.f64 "
-                 "[%0], {%1,%2};\" :: \"l\"(p), \"d\"(v.x), \"d\"(v.y) : \"memory\"); }\n";
-        }
+        const int threads = threads_of();
+        const bool dbuf = double_buffer;
         if (f32)
             o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; const int f = (w >> 3) ^ "
                  "(w >> 6) ^ (w >> 9) ^ (w >> 12); return ((w ^ (f & 7)) << 1) | (u & 1); }\n";
@@ -529,15 +561,8 @@ struct Gen {
             o << "static __device__ __forceinline__ int swz(int u) { return u ^ ((__popc(u & " << swm[0]
               << ") & 1) | ((__popc(u & " << swm[1] << ") & 1) << 1) | ((__popc(u & " << swm[2] << ") & 1) << 2)); }\n";
         }
-        o << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
-          << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; const " << V << " *prefix; };\n";
-        // Double buffering: while tile t is transformed in one shared buffer,
-        // the cp.async copies of tile t + gridDim are already in flight into
-        // the other (one CTA per SM, 2 x 2^K amplitudes).
-        const bool dbuf = double_buffer;
-        o << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
-          << (dbuf ? 1 : kernel_min_blocks(ph, threads)) << ") " << name << "(const Args a) {\n";
-        o << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+        o << "static __device__ __forceinline__ void " << fname
+          << "(const Args &a, const u64 t0, const u64 tend, const u64 tstep, unsigned char *smem_raw) {\n";
         // per-tile external phase factors of ALL groups get distinct slots
         ebase.assign(ph.groups.size(), 0);
         int next_max = 0;
@@ -553,7 +578,16 @@ struct Gen {
         late = pf;  // prefetching passes issue tile t + 1 after tile t's first barrier
         // late-issue prefetch rewrites E while other warps may still read the
         // previous tile's factors: one E set per shared tile
-        if (next_max) o << "  __shared__ " << V << " E[" << (late ? 2 * next_max : next_max) << "];\n";
+        // dynamic shared memory: the tile ring first, then this pass's E /
+        // stab / Eraw arrays (not static __shared__: the two passes of a
+        // super-pass share one launch and must not add up)
+        {
+            const size_t tile = static_cast<size_t>(amp) << K;
+            const bool shared_tile = ph.groups.size() >= 2 || !ph.out_perm.empty();
+            dyn_base = pf ? static_cast<size_t>(stages) * tile : shared_tile ? tile : 0;
+            dyn_extra = 0;
+        }
+        if (next_max) salloc("E", late ? 2 * next_max : next_max);
         e_stride = next_max;
         // separable phase tables (low / high set-index bits) live in shared memory
         {
@@ -569,7 +603,7 @@ struct Gen {
                 total += r.second;
             }
             if (total) {
-                o << "  __shared__ " << V << " stab[" << total << "];\n";
+                salloc("stab", total);
                 for (auto &r : ranges)
                     o << "  for (int i = threadIdx.x; i < " << r.second << "; i += " << threads << ") stab["
                       << stab_off[r.first] << " + i] = a.tables[" << r.first << " + i];\n";
@@ -668,12 +702,9 @@ struct Gen {
             o << ind << "}\n";
         };
         const std::string commit = "asm volatile(\"cp.async.commit_group;\\n\" ::: \"memory\");\n";
-        if (epipe && nraw) o << "  __shared__ " << V << " Eraw[" << 2 * nraw << "];\n";
+        if (epipe && nraw) salloc("Eraw", 2 * nraw);
         // tiles of this CTA: a block of a.tpc consecutive tiles (neighbouring
         // DRAM runs back to back) or, with a.tpc == 0, a grid-strided sequence
-        o << "  const u64 t0 = a.tpc > 0 ? (u64)blockIdx.x * a.tpc : (u64)blockIdx.x;\n";
-        o << "  const u64 tend = a.tpc > 0 ? (t0 + a.tpc < a.total_tiles ? t0 + a.tpc : a.total_tiles) : a.total_tiles;\n";
-        o << "  const u64 tstep = a.tpc > 0 ? 1ull : (u64)gridDim.x;\n";
         if (pf) {
             o << "  auto issue = [&](u64 t, " << V << " *buf) {\n";
             o << "    const int row = (int)(t >> " << tpr_log << ");\n";
@@ -840,7 +871,7 @@ struct Gen {
             } else
                 for (int r = 0; r < NR; ++r) {
                     if (from_hbm)
-                        o << "      " << V << " v" << r << " = ldcs(&st[gb + " << poff[r] << "ull]);\n";
+                        o << "      " << V << " v" << r << " = " << ld_in << "(&st[gb + " << poff[r] << "ull]);\n";
                     else o << "      " << V << " v" << r << " = tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r])
                            << "];\n";
                 }
@@ -870,7 +901,7 @@ struct Gen {
                 o << "      }\n";
             }
             for (int r = 0; r < NR; ++r) {
-                if (to_hbm) o << "      stcs(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
+                if (to_hbm) o << "      " << st_out << "(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
                 else o << "      tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
@@ -950,6 +981,14 @@ struct Gen {
     std::string eoff() const { return late ? "(ec * " + std::to_string(e_stride) + ") + " : ""; }
     int stages = 2;  // shared tile buffers in prefetch mode (late issue)
     bool zsum = false; // fused <Z> epilogue in the last group (whole-row tiles)
+    std::string st_out = "stcs"; // the last group's stores (stwb: keep the output in L2)
+    std::string ld_in = "ldcs";  // the first group's direct loads (ldcg: L2 only, data written in this launch)
+    size_t dyn_base = 0, dyn_extra = 0; // dynamic shared memory: tile ring, then salloc'ed arrays
+    size_t dyn_bytes() const { return dyn_base + dyn_extra; }
+    void salloc(const char *name, int count) {
+        o << "  " << V << " *const " << name << " = (" << V << " *)(smem_raw + " << dyn_base + dyn_extra << ");\n";
+        dyn_extra += (static_cast<size_t>(count) * (f32 ? 8 : 16) + 15) / 16 * 16;
+    }
     std::vector<int> ebase; // first E slot of each group
     int cur_group = 0;
     std::map<int, int> stab_off; // global table offset -> shared-memory offset
@@ -970,21 +1009,79 @@ int dbuf_stages(const PassHost &ph, int dtype) {
     return s;
 }
 
+// L2 super-pass: passes A (pair = 1) and B (pair = 2) as one kernel. Each
+// CTA takes one item -- tpi consecutive tiles of one pass inside one chunk --
+// from an atomic ticket; tickets run A(0 .. D-1), then per chunk m the items
+// of A(m + D) followed by those of B(m). A's items store with plain
+// write-back stores and signal a per-chunk counter; a B item waits for all of
+// its chunk's A items and reads through L2 (cp.async.cg / ld.global.cg), so
+// B finds A's output in L2 and the state crosses HBM once for both passes.
+// Tickets are taken in order by running CTAs, so every A item a B item waits
+// for is held by a running CTA that never waits: no deadlock, whatever else
+// shares the GPU.
+std::string generate_pair_source(const PassHost &A, const PassHost &B, int dtype, const std::string &name,
+                                 int *threads, bool dbuf, size_t *smem) {
+    Gen ga(A, dtype), gb(B, dtype);
+    for (Gen *g : {&ga, &gb}) {
+        g->double_buffer = false;
+        g->prefetch = dbuf;
+        g->stages = dbuf_stages(g->ph, dtype);
+    }
+    ga.st_out = "stwb";
+    gb.ld_in = "ldcg";
+    const int th = ga.threads_of();
+    require(th == gb.threads_of(), "codegen: super-pass halves differ in CTA shape");
+    *threads = th;
+    std::ostringstream k;
+    k << "// generated by qsv codegen.cpp: an L2 super-pass (two tile passes, chunk by chunk)\n" << ga.common();
+    k << "namespace pa {\n" << ga.body_fn("body") << "}\n";
+    k << "namespace pb {\n" << gb.body_fn("body") << "}\n";
+    if (smem) *smem = std::max(ga.dyn_bytes(), gb.dyn_bytes());
+    k << "struct Pair { unsigned *sync; u64 nchunks; int chunk_tiles_log; int tpi; int lookahead; };\n";
+    k << "extern \"C\" __global__ void __launch_bounds__(" << th << ", " << kernel_min_blocks(A, th) << ") " << name
+      << "(const Args a, const Args b, const Pair q) {\n";
+    k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+    k << "  __shared__ unsigned tk;\n";
+    k << "  if (threadIdx.x == 0) tk = atomicAdd(q.sync + q.nchunks, 1u);\n";
+    k << "  __syncthreads();\n";
+    k << "  const u64 ipc = (1ull << q.chunk_tiles_log) / (u64)q.tpi;\n";
+    k << "  const u64 m = tk / (2 * ipc), r = tk % (2 * ipc);\n";
+    k << "  if (r < ipc) {\n";
+    k << "    if (m >= q.nchunks) return;\n";
+    k << "    const u64 t0 = (m << q.chunk_tiles_log) + r * q.tpi;\n";
+    k << "    pa::body(a, t0, t0 + q.tpi, 1, smem_raw);\n";
+    k << "    __syncthreads();\n";
+    k << "    if (threadIdx.x == 0) { __threadfence(); atomicAdd(q.sync + m, 1u); }\n";
+    k << "  } else {\n";
+    k << "    if (m < (u64)q.lookahead) return;\n";
+    k << "    const u64 c = m - q.lookahead;\n";
+    k << "    if (c >= q.nchunks) return;\n";
+    k << "    if (threadIdx.x == 0) {\n";
+    k << "      unsigned v;\n";
+    k << "      for (;;) {\n";
+    k << "        asm volatile(\"ld.acquire.gpu.global.u32 %0, [%1];\" : \"=r\"(v) : \"l\"(q.sync + c) : \"memory\");\n";
+    k << "        if ((u64)v >= ipc) break;\n";
+    k << "        __nanosleep(64);\n";
+    k << "      }\n";
+    k << "    }\n";
+    k << "    __syncthreads();\n";
+    k << "    const u64 t0 = (c << q.chunk_tiles_log) + (r - ipc) * q.tpi;\n";
+    k << "    pb::body(b, t0, t0 + q.tpi, 1, smem_raw);\n";
+    k << "  }\n}\n";
+    return k.str();
+}
+
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
-                                 bool zsum) {
+                                 bool zsum, size_t *smem) {
     Gen g(ph, dtype);
     g.zsum = zsum;
     g.double_buffer = false;
     g.prefetch = dbuf;
     g.stages = dbuf_stages(ph, dtype);
-    const int nsets = 1 << (ph.K - ph.R);
-    const int amp = dtype == QSV_C64 ? 8 : 16;
-    const int nchunks = (1 << ph.K) / (16 / amp);
-    int th = kernel_threads(ph, dtype);
-    (void)nsets;
-    (void)nchunks;
-    *threads = (th + 31) / 32 * 32;
-    return g.source(name);
+    *threads = g.threads_of();
+    std::string src = g.source(name);
+    if (smem) *smem = g.dyn_bytes();
+    return src;
 }
 
 } // namespace qsv

@@ -24,8 +24,10 @@
 namespace qsv {
 
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
-                                 bool zsum = false);
+                                 bool zsum = false, size_t *smem = nullptr);
 int dbuf_stages(const PassHost &ph, int dtype);
+std::string generate_pair_source(const PassHost &A, const PassHost &B, int dtype, const std::string &name,
+                                 int *threads, bool dbuf, size_t *smem = nullptr);
 
 namespace {
 
@@ -161,18 +163,8 @@ struct JitKernel {
     cudaKernel_t kernel = nullptr;
 };
 
-// Compiles (or fetches) the specialised kernel of one pass and fills dp
-// (zsum: the variant with the fused <Z> epilogue, dp.jit_z / dp.grid_z).
-static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, bool zsum) {
-    const std::string name = "qsv_pass";
-    int threads = 256;
-    // prefetch (two shared tiles, cp.async of the next tile in flight) when
-    // both buffers fit in 64 KiB: K <= 11 for complex128, K <= 12 for complex64
-    const int amp0 = dtype == QSV_C64 ? 8 : 16;
-    const char *pe = std::getenv("QSV_PREFETCH");
-    const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
-                      (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
-    std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf, zsum);
+namespace {
+JitKernel load_kernel(const std::string &src, const std::string &name) {
     char key[32];
     std::snprintf(key, sizeof key, "p%016llx%08zx", static_cast<unsigned long long>(fnv64(src)), src.size());
     std::vector<char> cubin = compile(src, key);
@@ -182,16 +174,60 @@ static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, 
     int dev = 0;
     QSV_CUDA(cudaGetDevice(&dev));
     const std::string lkey = std::string(key) + ":" + std::to_string(dev);
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        auto it = loaded.find(lkey);
-        if (it != loaded.end()) jk = it->second;
-        else {
-            QSV_CUDA(cudaLibraryLoadData(&jk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
-            QSV_CUDA(cudaLibraryGetKernel(&jk.kernel, jk.lib, name.c_str()));
-            loaded[lkey] = jk;
-        }
-    }
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = loaded.find(lkey);
+    if (it != loaded.end()) return it->second;
+    QSV_CUDA(cudaLibraryLoadData(&jk.lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+    QSV_CUDA(cudaLibraryGetKernel(&jk.kernel, jk.lib, name.c_str()));
+    loaded[lkey] = jk;
+    return jk;
+}
+
+bool use_prefetch(const PassHost &ph, int dtype) {
+    const int amp0 = dtype == QSV_C64 ? 8 : 16;
+    const char *pe = std::getenv("QSV_PREFETCH");
+    return (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
+           (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
+}
+} // namespace
+
+void jit_prepare_pair(DevPass &head, const PassHost &a, const PassHost &b, int dtype, int sm_count) {
+    (void)sm_count;
+    const bool dbuf = use_prefetch(a, dtype);
+    require(dbuf == use_prefetch(b, dtype), "jit: super-pass halves differ in staging");
+    int threads = 0;
+    size_t smem = 0;
+    const std::string src = generate_pair_source(a, b, dtype, "qsv_pair", &threads, dbuf, &smem);
+    const JitKernel jk = load_kernel(src, "qsv_pair");
+    head.jit_pair = reinterpret_cast<const void *>(jk.kernel);
+    head.threads = threads;
+    head.smem = smem;
+    head.pair = 1;
+    head.chunk_tiles_log = a.chunk_bits - a.K;
+    int dev = 0, optin = 0;
+    QSV_CUDA(cudaGetDevice(&dev));
+    QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    QSV_CUDA(cudaFuncGetAttributes(&fa, head.jit_pair));
+    QSV_CUDA(cudaFuncSetAttribute(head.jit_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+    head.jit_regs = fa.numRegs;
+    head.jit_spill = static_cast<int>(fa.localSizeBytes);
+}
+
+// Compiles (or fetches) the specialised kernel of one pass and fills dp
+// (zsum: the variant with the fused <Z> epilogue, dp.jit_z / dp.grid_z).
+static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, bool zsum) {
+    const std::string name = "qsv_pass";
+    int threads = 256;
+    // prefetch (two shared tiles, cp.async of the next tile in flight) when
+    // both buffers fit in 64 KiB: K <= 11 for complex128, K <= 12 for complex64
+    const bool dbuf = use_prefetch(ph, dtype);
+    size_t smem = 0;
+    std::string src = generate_pass_source(ph, dtype, name, &threads, dbuf, zsum, &smem);
+    const JitKernel jk = load_kernel(src, name);
+    int dev = 0;
+    QSV_CUDA(cudaGetDevice(&dev));
     const int amp = dtype == QSV_C64 ? 8 : 16;
     const void *kern = reinterpret_cast<const void *>(jk.kernel);
     if (zsum) {
@@ -212,8 +248,7 @@ static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, 
     dp.threads = threads;
     // groups between the first (loads from HBM) and the last (stores to HBM)
     // exchange amplitudes through a shared tile; a one-group pass needs none
-    dp.smem = dbuf ? dbuf_stages(ph, dtype) * (static_cast<size_t>(amp) << ph.K)
-                   : (ph.groups.size() >= 2 || !ph.out_perm.empty()) ? (static_cast<size_t>(amp) << ph.K) : 0;
+    dp.smem = smem;
     int optin = 0;
     QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
     cudaFuncAttributes fa{};
@@ -230,11 +265,12 @@ static void jit_build(DevPass &dp, const PassHost &ph, int dtype, int sm_count, 
 // Source of a pass's specialised kernel (diagnostics / tests).
 std::string jit_source(const PassHost &ph, int dtype) {
     int threads = 0;
-    const int amp0 = dtype == QSV_C64 ? 8 : 16;
-    const char *pe = std::getenv("QSV_PREFETCH");
-    const bool dbuf = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
-                      (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
-    return generate_pass_source(ph, dtype, "qsv_pass", &threads, dbuf);
+    return generate_pass_source(ph, dtype, "qsv_pass", &threads, use_prefetch(ph, dtype));
+}
+
+std::string jit_pair_source(const PassHost &a, const PassHost &b, int dtype) {
+    int threads = 0;
+    return generate_pair_source(a, b, dtype, "qsv_pair", &threads, use_prefetch(a, dtype));
 }
 
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) { jit_build(dp, ph, dtype, sm_count, false); }
@@ -287,4 +323,61 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     QSV_CUDA(cudaLaunchKernel(kern, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
 }
 
+} // namespace qsv
+
+namespace qsv {
+void launch_pair(const DevPass &head, const DevPass &tail, void *state, void *out, int rows, unsigned *sync,
+                 uint64_t nchunks, cudaStream_t s) {
+    struct JArgs {
+        void *state;
+        uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
+        const void *tables;
+        const void *enc_table;
+        int batch;
+        int tpc;
+        void *out;
+        double *zout;
+        const void *prefix;
+    } a{}, b{};
+    struct Pair {
+        unsigned *sync;
+        uint64_t nchunks;
+        int chunk_tiles_log;
+        int tpi;
+        int lookahead;
+    } q{};
+    const DevPass *dps[2] = {&head, &tail};
+    JArgs *as[2] = {&a, &b};
+    for (int i = 0; i < 2; ++i) {
+        JArgs &x = *as[i];
+        const DevPass &dp = *dps[i];
+        x.state = state;
+        x.out = i == 0 ? state : out;
+        x.row_stride = dp.args.row_stride;
+        x.rank_base = dp.args.rank_base;
+        x.tiles_per_row = dp.args.tiles_per_row;
+        x.total_tiles = dp.args.tiles_per_row * static_cast<uint64_t>(rows);
+        x.tables = dp.args.tables;
+        x.batch = rows;
+    }
+    static const int look = [] {
+        const char *e = std::getenv("QSV_SUPER_LOOKAHEAD");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    q.sync = sync;
+    q.nchunks = nchunks;
+    q.chunk_tiles_log = head.chunk_tiles_log;
+    static const int tpi = [] {
+        const char *e = std::getenv("QSV_SUPER_TPI");
+        return e ? std::max(1, std::atoi(e)) : 4;
+    }();
+    q.tpi = std::min(tpi, 1 << head.chunk_tiles_log);
+    q.lookahead = look;
+    const uint64_t ipc = (1ull << head.chunk_tiles_log) / static_cast<uint64_t>(q.tpi);
+    const uint64_t items = (nchunks + static_cast<uint64_t>(look)) * 2 * ipc;
+    require(items < (1ull << 32), "super-pass: too many items");
+    void *args[] = {&a, &b, &q};
+    QSV_CUDA(cudaLaunchKernel(head.jit_pair, dim3(static_cast<unsigned>(items)), dim3(head.threads), args, head.smem,
+                              s));
+}
 } // namespace qsv

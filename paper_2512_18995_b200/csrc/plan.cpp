@@ -43,6 +43,7 @@ Plan::~Plan() {
     cudaFree(d_prefix_prog);
     cudaFree(d_prefix_mats);
     cudaFree(d_prefix);
+    cudaFree(d_sync);
 }
 
 namespace {
@@ -306,6 +307,20 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
     if (p->opts.from_zero && ctx->world == 1 && cfg.fuse && plan_uses_jit(*p)) extract_prefix(*p);
+    // L2 super-passes (planner.cpp), opt-in: opts.super_bits (or
+    // QSV_SUPER_BITS) = the largest chunk, e.g. 19 (C128) / 20 (C64) = 8 MiB.
+    // Off by default: measured slower on B200 (DESIGN.md 4.1 -- a pass is
+    // already co-limited by its shared-memory exchanges and latency, so two
+    // passes' SM work in one launch costs what the saved HBM sweep gains).
+    {
+        static const int env = [] {
+            const char *e = std::getenv("QSV_SUPER_BITS");
+            return e ? std::atoi(e) : 0;
+        }();
+        int sb = p->opts.super_bits != 0 ? p->opts.super_bits : env;
+        if (sb < 0 || !cfg.fuse || !plan_uses_jit(*p) || p->synth) sb = 0;
+        cfg.super_bits = sb;
+    }
     if (ctx->world == 1) {
         // swaps as relabelings, the final layout folded into the last pass
         bool relabel = cfg.fuse && p->opts.no_relabel == 0 && plan_uses_jit(*p) && p->nslots == 0;
@@ -363,12 +378,8 @@ bool plan_uses_jit(const Plan &p) {
     return p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
 }
 
-void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *zout) {
-    if (!dp.out_of_place) {
-        launch_pass(dp, dtype, st.d, st.batch, s, zout);
-        return;
-    }
-    require(zout == nullptr, "fused <Z>: not on a permuting pass");
+namespace {
+void ensure_scratch(State &st) {
     if (!st.scratch) {
         const size_t bytes = st.local_amps * st.amp_bytes() * static_cast<size_t>(st.batch);
         if (cudaMalloc(&st.scratch, bytes) != cudaSuccess) {
@@ -378,6 +389,39 @@ void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *z
                                        " bytes); plan with opts.no_relabel = 1");
         }
     }
+}
+
+// One L2 super-pass launch: pass pi in place, then pass pi + 1 (in place or
+// into the scratch state), chunk by chunk.
+void run_pair(Plan &p, int pi, State &st, cudaStream_t s) {
+    const DevPass &head = p.dev[pi], &tail = p.dev[pi + 1];
+    const PassHost &ph = p.passes[pi];
+    const uint64_t nchunks = static_cast<uint64_t>(st.batch) << (p.nlocal - ph.chunk_bits);
+    const size_t bytes = (nchunks + 1) * sizeof(unsigned);
+    if (bytes > p.d_sync_cap) {
+        cudaFree(p.d_sync);
+        p.d_sync = nullptr;
+        QSV_CUDA(cudaMalloc(&p.d_sync, bytes));
+        p.d_sync_cap = bytes;
+    }
+    QSV_CUDA(cudaMemsetAsync(p.d_sync, 0, bytes, s));
+    void *out = st.d;
+    if (tail.out_of_place) {
+        ensure_scratch(st);
+        out = st.scratch;
+    }
+    launch_pair(head, tail, st.d, out, st.batch, static_cast<unsigned *>(p.d_sync), nchunks, s);
+    if (tail.out_of_place) std::swap(st.d, st.scratch);
+}
+} // namespace
+
+void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *zout) {
+    if (!dp.out_of_place) {
+        launch_pass(dp, dtype, st.d, st.batch, s, zout);
+        return;
+    }
+    require(zout == nullptr, "fused <Z>: not on a permuting pass");
+    ensure_scratch(st);
     launch_jit(dp, st.d, st.scratch, st.batch, s);
     std::swap(st.d, st.scratch);
 }
@@ -462,7 +506,9 @@ void upload_plan(Plan &p) {
         require(!ph.synth || use_jit, "plan: a synthesising pass needs the specialised kernels");
         dp.out_of_place = !ph.out_perm.empty();
         require(!dp.out_of_place || use_jit, "plan: permuting passes need the specialised kernels");
-        if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
+        if (use_jit && ph.pair == 1) jit_prepare_pair(dp, ph, p.passes[i + 1], p.dtype, p.ctx->sm_count);
+        else if (use_jit && ph.pair == 2) dp.pair = 2;  // runs inside its head's launch
+        else if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
         dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
         dp.ngates = ph.ngates;
         p.dev.push_back(dp);
@@ -512,7 +558,10 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     }
     for (size_t i = 0; i < p.steps.size(); ++i) {
         const Step &stp = p.steps[i];
-        if (stp.kind == 0) {
+        if (stp.kind == 0 && p.dev[stp.pass].pair) {
+            require(!zout || i + 1 < p.steps.size(), "fused <Z>: not on a super-pass");
+            if (p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
+        } else if (stp.kind == 0) {
             DevPass dp = p.dev[stp.pass];
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
@@ -579,7 +628,9 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
     size_t k = 0;
     for (const Step &stp : p.steps) {
         QSV_CUDA(cudaEventRecord(ev[2 * k], s));
-        if (stp.kind == 0) run_pass(p.dev[stp.pass], p.dtype, st, s);
+        if (stp.kind == 0 && p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
+        else if (stp.kind == 0 && p.dev[stp.pass].pair == 2) {
+        } else if (stp.kind == 0) run_pass(p.dev[stp.pass], p.dtype, st, s);
         else dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         QSV_CUDA(cudaEventRecord(ev[2 * k + 1], s));
         ++k;

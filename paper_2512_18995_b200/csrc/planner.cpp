@@ -493,7 +493,8 @@ struct GroupLowering {
 
 PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg, const std::vector<int> &took,
                     uint64_t active, const std::vector<int> &phys, const PlanConfig &cfg, int K, int L, int R,
-                    std::vector<EncDesc> &encs, const std::vector<int> *out_perm = nullptr) {
+                    std::vector<EncDesc> &encs, const std::vector<int> *out_perm = nullptr,
+                    uint64_t ext_first = 0) {
     const int nl = cfg.nlocal;
     PassHost ph;
     ph.K = K;
@@ -520,7 +521,11 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
     for (int b = 0; b < nl && std::popcount(active) < K; ++b) active |= 1ull << b; // lengthen contiguous runs
     for (int b = 0; b < nl; ++b)
         if (active & (1ull << b)) ph.tile_pos.push_back(b);
-        else ph.ext_pos.push_back(b);
+    // tile index bits: the ext bits in ext_first (an L2 super-pass chunk)
+    // are the low ones, so a chunk's tiles are one contiguous index range
+    for (int pass = 0; pass < 2; ++pass)
+        for (int b = 0; b < nl; ++b)
+            if (!(active & (1ull << b)) && (((ext_first >> b) & 1) != 0) == (pass == 0)) ph.ext_pos.push_back(b);
     require(static_cast<int>(ph.tile_pos.size()) == K, "planner: tile size");
     int tile_of_phys[64];
     for (int &x : tile_of_phys) x = -1;
@@ -798,6 +803,12 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
     }
 
     std::vector<PassHost> passes;
+    struct Lowering {
+        std::vector<int> took;
+        uint64_t active;
+        bool permuted;
+    };
+    std::vector<Lowering> how; // per pass: what lower_pass was given (re-lowered for super-passes)
     std::vector<int> order(gates.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = static_cast<int>(i);
     const uint64_t lowmask = (1ull << L) - 1;
@@ -848,6 +859,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         }
         passes.push_back(std::move(ph));
+        how.push_back({took, active, false});
         last_took = took;
         last_active = active;
     }
@@ -869,6 +881,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             if (pass_program_bytes(ph, cfg.dtype) <= static_cast<size_t>(kProgramBudget)) {
                 ph.out_perm = out_perm;
                 passes.back() = std::move(ph);
+                how.back() = {last_took, last_active | need, true};
                 done = true;
             }
         }
@@ -876,6 +889,41 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             PassHost ph = lower_pass(gates, pg, {}, lowmask | need, phys, cfg, K, L, R, encs, &out_perm);
             ph.out_perm = out_perm;
             passes.push_back(std::move(ph));
+            how.push_back({{}, lowmask | need, true});
+        }
+    }
+    // L2 super-passes: pair consecutive passes whose two tiles span at most
+    // cfg.super_bits bits. The pair runs as one launch over chunks (the
+    // 2^chunk_bits amplitudes of fixed values of every other bit): the first
+    // pass's tiles of a chunk, then -- a few chunks later, while they are
+    // still in L2 -- the second pass's tiles of it, so the state crosses HBM
+    // once for both passes (codegen.cpp generate_pair_source).
+    bool any_enc = false;
+    for (const GateRec &g : gates) any_enc = any_enc || g.encoded;
+    if (cfg.super_bits > 0 && !any_enc) {
+        for (size_t i = 0; i + 1 < passes.size();) {
+            const PassHost &A = passes[i], &B = passes[i + 1];
+            uint64_t cm = 0;
+            for (int b : A.tile_pos) cm |= 1ull << b;
+            for (int b : B.tile_pos) cm |= 1ull << b;
+            const int cb = std::popcount(cm);
+            const bool ok = A.K == B.K && A.R == B.R && !A.synth && !B.synth && A.out_perm.empty() &&
+                            cb <= cfg.super_bits && cb >= A.K + 2 && cb < nl;
+            if (!ok) {
+                ++i;
+                continue;
+            }
+            for (int j = 0; j < 2; ++j) {
+                const Lowering &h = how[i + j];
+                const int Rj = passes[i + j].R;
+                PassHost ph = lower_pass(gates, pg, h.took, h.active, phys, cfg, K, L, Rj, encs,
+                                         h.permuted ? &out_perm : nullptr, cm);
+                if (h.permuted) ph.out_perm = out_perm;
+                ph.pair = j + 1;
+                ph.chunk_bits = cb;
+                passes[i + j] = std::move(ph);
+            }
+            i += 2;
         }
     }
     if (gphase != cplx(1, 0)) {

@@ -203,6 +203,11 @@ struct PassHost {
     // First pass of a from-|0> plan: the register sets are synthesised from
     // the per-row, per-bit product-state vectors instead of loaded.
     bool synth = false;
+    // L2 super-pass: 1 = first pass of a pair (its launch runs both), 2 =
+    // second; chunk_bits = bits spanned by the pair's two tiles (the ext bits
+    // inside the chunk come first in ext_pos, so a chunk is a tile range)
+    int pair = 0;
+    int chunk_bits = 0;
     // The pass's gates in execution order, wires mapped to physical bits
     // (schedule export for host-side verification, qsv_plan_dry).
     std::vector<GateRec> exec_gates;
@@ -251,6 +256,9 @@ struct DevPass {
     int jit_regs = 0, jit_spill = 0;
     const void *jit_z = nullptr;  // variant with the fused <Z> epilogue (prepared on first use)
     int grid_z = 0;
+    int pair = 0;                 // L2 super-pass: 1 = head (jit_pair runs it and the next pass), 2 = tail
+    const void *jit_pair = nullptr;
+    int chunk_tiles_log = 0;      // log2 tiles per chunk (head)
     double bytes = 0;
     int ngates = 0;
 };
@@ -288,6 +296,8 @@ struct Plan {
     void *d_prefix_prog = nullptr, *d_prefix_mats = nullptr, *d_prefix = nullptr;
     size_t prefix_rows = 0;
     size_t d_z_cap = 0;
+    void *d_sync = nullptr;    // L2 super-passes: per-chunk counters + the item ticket
+    size_t d_sync_cap = 0;
     std::vector<DevPass> dev;
     qsv_opts opts{};
     ~Plan();
@@ -300,6 +310,9 @@ struct PlanConfig {
     bool fuse_1q = true;      // pre-multiply runs of single-qubit gates
     bool phase_flush = true;  // lazy phase factors for diagonal gates
     int dtype = QSV_C128;
+    // L2 super-passes: consecutive passes whose tiles together span at most
+    // this many bits run as one launch, chunk by chunk (0: off)
+    int super_bits = 0;
 };
 // Swap gates as qubit relabelings: rewrites `gates` onto physical bits (the
 // returned gates' wires ARE physical bits), dropping uncontrolled swaps and
@@ -337,8 +350,14 @@ int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
 // ---- pass specialisation (codegen.cpp, jit.cpp) ----------------------------
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
 void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout = nullptr);
+// L2 super-pass (PassHost::pair): compiles the pair kernel into head; the
+// launch runs head's pass in place on state and the tail's into out.
+void jit_prepare_pair(DevPass &head, const PassHost &a, const PassHost &b, int dtype, int sm_count);
+void launch_pair(const DevPass &head, const DevPass &tail, void *state, void *out, int rows, unsigned *sync,
+                 uint64_t nchunks, cudaStream_t s);
 void jit_prepare_z(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
 std::string jit_source(const PassHost &ph, int dtype);
+std::string jit_pair_source(const PassHost &a, const PassHost &b, int dtype);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);
 void reduce_z_all(State &st, double *host_out /* batch x kZ: [total, S_bit0..] */);

@@ -89,3 +89,22 @@ def test_rng_fill_matches_reference_stream():
             got = qsv.rng_fill(0, "cfg3", kind, cnt, nthreads=4)
             want = O.port_rng(0, "cfg3", k, cnt)
             assert np.array_equal(got, want), (kind, cnt)
+
+
+def test_super_pass_planning_is_opt_in():
+    # L2 super-passes pair consecutive passes only when asked (opts.super_bits)
+    # and only when both tiles fit one chunk; the schedule marks head / tail
+    from paper_2512_18995_b200 import workloads as W
+
+    cir = W.cfg3_circuit(30)
+    off, _ = qsv.plan_dry(30, cir.gates())
+    assert off["npasses"] == off["ntile_passes"] == 4
+    on, _ = qsv.plan_dry(30, cir.gates(), opts={"super_bits": 19})
+    assert on["npasses"] == 2 and on["ntile_passes"] == 4
+    assert on["bytes_per_exec"] == off["bytes_per_exec"] / 2
+    sch = qsv.plan_schedule(30, cir.gates(), opts={"super_bits": 19})
+    assert [s["pair"] for s in sch["steps"]] == [1, 2, 1, 2]
+    small, _ = qsv.plan_dry(30, cir.gates(), opts={"super_bits": 15})  # no two tiles fit 2^15
+    assert small["npasses"] == 4
+    _, src = qsv.plan_dry(30, cir.gates(), opts={"super_bits": 19}, source_of_pass=0)
+    assert "qsv_pair" in src and "ld.acquire.gpu" in src and "namespace pb" in src

@@ -357,3 +357,38 @@ def test_from_zero_product_state_prefix(dtype, tol):
         got = cirx.forward(dtype=dtype).amplitudes()  # forward() plans from zero
         want = ref_or_port_forward(n, cirx.gates())[0]
         assert np.max(np.abs(got - want)) <= tol
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_l2_super_passes_match_reference(dtype):
+    # opt-in L2 super-passes (pairs of passes in one launch, chunk by chunk,
+    # the second reading the first's output through L2; the second may be the
+    # permuting out-of-place pass): same results as the reference, batched
+    # rows included, whatever the lookahead / items per ticket
+    rng = Rng(41, "super")
+    cases = ((18, 17), (20, 19)) if dtype == C128 else ((20, 19),)
+    for n, sb in cases:
+        cir = W.cfg3_circuit(n)
+        psi = random_state(rng, n)
+        info, _ = qsv.plan_dry(n, cir.gates(), dtype=dtype, opts={"jit": 1, "super_bits": sb})
+        assert info["npasses"] < info["ntile_passes"], info
+        got, _ = run(n, cir.gates(), init=psi, dtype=dtype, opts={"jit": 1, "super_bits": sb})
+        want = ref_or_port_forward(n, cir.gates(), init=psi)[0]
+        assert np.max(np.abs(got[0] - want)) <= TOL[dtype], (n, sb)
+        gates = [random_gate(rng, n) for _ in range(150)]
+        got, _ = run(n, gates, init=psi, dtype=dtype, opts={"jit": 1, "super_bits": sb})
+        want = O.port_forward(n, gates, init=psi)[0]
+        assert np.max(np.abs(got[0] - want)) <= TOL[dtype], (n, sb, "random")
+    # two batch rows: chunks of both rows in one launch
+    n, sb = cases[0]
+    cir = W.cfg3_circuit(n)
+    rows = np.stack([random_state(rng, n), random_state(rng, n)])
+    st = QubitState(n, 2, dtype)
+    for b in range(2):
+        st.upload(rows[b], b)
+    p = qsv.Plan(n, cir.gates(), dtype=dtype, opts={"jit": 1, "super_bits": sb})
+    assert p.info["npasses"] < p.info["ntile_passes"]
+    p.execute(st)
+    for b in range(2):
+        want = O.port_forward(n, cir.gates(), init=rows[b])[0]
+        assert np.max(np.abs(st.amplitudes(b) - want)) <= TOL[dtype], b
