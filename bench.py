@@ -123,19 +123,37 @@ def cpu_reference_sample(cir, n, psi, gates_per_step, steps):
     return times
 
 
-def swap_kernels(n, cir, world, nl, amp_bytes):
-    """Kernels one execute launches for its qubit swaps (dist.cu): per run of
-    disjoint bit pairs (m pairs) one gather and one scatter per chunk round,
-    a round moving up to 256 MiB over the 2^m - 1 peers."""
+def swap_accounting(n, cir, world, nl, amp_bytes, fused):
+    """Per execute on one GPU: (bytes sent by NCCL swap all-to-alls, bytes
+    stored into peers by passes with swaps fused into them, our kernels
+    launched for the NCCL swaps, step indices of the fusing passes).
+
+    An NCCL swap step: per run of m disjoint bit pairs (dist.cu) (1 - 2^-m)
+    of the local slice leaves, with one gather and one scatter kernel per
+    chunk round of up to 256 MiB. A fusing pass (fused=True: the state has
+    peer memory) sends the amplitudes whose destination rank -- set by the
+    m local bits its global permutation maps to rank bits -- is another one:
+    (1 - 2^-m) of the slice, with no extra kernel."""
     if world == 1:
-        return 0
+        return 0.0, 0.0, 0, []
     from paper_2512_18995_b200 import qsv
 
     sched = qsv.plan_schedule(n, cir.gates(), world=world)
-    total = 0
-    for step in sched["steps"]:
-        if step["kind"] != "swap":
+    nccl = peer = 0.0
+    kernels = 0
+    fusing = []
+    fused_done = False
+    for i, step in enumerate(sched["steps"]):
+        if step["kind"] == "pass":
+            fused_done = fused and bool(step["gperm"])
+            if fused_done:
+                m = sum(1 for b in range(nl) if step["gperm"][b] >= nl)
+                peer += (amp_bytes << nl) * (1.0 - 2.0 ** -m)
+                fusing.append(i)
             continue
+        if step["fused"] and fused_done:
+            continue
+        fused_done = False
         runs, cur = [], []
         for gb, lb in step["pairs"]:
             if any(gb == g or lb == l for g, l in cur):
@@ -145,33 +163,12 @@ def swap_kernels(n, cir, world, nl, amp_bytes):
         runs.append(cur)
         for r in runs:
             m = len(r)
+            nccl += (amp_bytes << nl) * (1.0 - 2.0 ** -m)
             nv = (1 << m) - 1
             block = (1 << nl) >> m
             chunk = max(1, min(block * nv, (256 << 20) // amp_bytes) // nv)
-            total += 2 * -(-block // chunk)
-    return total
-
-
-def swap_bytes(n, cir, world, nl, amp_bytes):
-    """Bytes one GPU sends per execute in its qubit swaps: a run of m disjoint
-    bit pairs moves (1 - 2^-m) of the local slice (dist.cu all-to-all)."""
-    from paper_2512_18995_b200 import qsv
-
-    sched = qsv.plan_schedule(n, cir.gates(), world=world)
-    total = 0
-    for step in sched["steps"]:
-        if step["kind"] != "swap":
-            continue
-        runs, cur = [], []
-        for gb, lb in step["pairs"]:
-            if any(gb == g or lb == l for g, l in cur):
-                runs.append(cur)
-                cur = []
-            cur.append((gb, lb))
-        runs.append(cur)
-        for r in runs:
-            total += (amp_bytes << nl) * (1.0 - 2.0 ** -len(r))
-    return total
+            kernels += 2 * -(-block // chunk)
+    return nccl, peer, kernels, fusing
 
 
 def run_reference(args):
@@ -297,12 +294,21 @@ def main():
     # steps' time, against the measured 770 GB/s per-direction peer copy and
     # the nominal 900 GB/s (B200_PROFILING.md)
     nvlink = None
-    if world > 1 and (kinds == 1).any():
-        sw_ms = float(np.array(launch_ms)[:, kinds == 1].sum(axis=1).mean())
-        sent = swap_bytes(n, cir, world, nl, amp_bytes)
-        gbs = sent / (sw_ms / 1e3) / 1e9
-        nvlink = {"bytes_sent_per_gpu_per_step": sent, "swap_ms_per_step": sw_ms, "achieved_GBps": gbs,
-                  "frac_of_measured_770": gbs / 770.0, "frac_of_nominal_900": gbs / 900.0}
+    fused = world > 1 and st.peer_memory() == 1
+    nccl_sent, peer_sent, swap_kern, fusing = swap_accounting(n, cir, world, nl, amp_bytes, fused)
+    if world > 1 and (nccl_sent or peer_sent):
+        lmall = np.array(launch_ms)
+        sw_ms = float(lmall[:, kinds == 1].sum(axis=1).mean()) if (kinds == 1).any() else 0.0
+        fz_ms = float(lmall[:, fusing].sum(axis=1).mean()) if fusing else 0.0
+        sent = nccl_sent + peer_sent
+        t = sw_ms + fz_ms
+        gbs = sent / (t / 1e3) / 1e9 if t > 0 else None
+        nvlink = {"bytes_sent_per_gpu_per_step": sent, "nccl_swap_bytes": nccl_sent, "peer_store_bytes": peer_sent,
+                  "swaps": "fused into the passes (peer-memory stores)" if fused else "NCCL all-to-all",
+                  "swap_ms_per_step": sw_ms, "fusing_pass_ms_per_step": fz_ms,
+                  # the fusing passes also do their gate math: a lower bound of the link rate
+                  "achieved_GBps": gbs, "frac_of_measured_770": gbs / 770.0 if gbs else None,
+                  "frac_of_nominal_900": gbs / 900.0 if gbs else None}
     bytes_per_launch = 2.0 * amp_bytes * (1 << nl)  # read + write of every local amplitude
     avg_launch_ms = float(lm.mean())
     hbm_peak, peak_kind = peaks()
@@ -393,7 +399,7 @@ def main():
                          "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
-            "gpu_launches": args.steps * (npass + swap_kernels(n, cir, world, nl, amp_bytes)),
+            "gpu_launches": args.steps * (npass + swap_kern),
             "nvlink": nvlink,
             "e2e": e2e,
             "cpu_baseline": cpu,

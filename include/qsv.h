@@ -165,6 +165,10 @@ int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count);
 int qsv_state_clone(const qsv_state *st, qsv_state **out);
 /* Device pointer of row `row` in the engine's PHYSICAL order (tests). */
 int qsv_state_device_ptr(qsv_state *st, int row, void **ptr);
+/* Multi-GPU: whether this state's qubit swaps run fused into the passes
+ * through peer memory (1), as NCCL all-to-alls (-1: peer memory unavailable
+ * or QSV_P2P_SWAP=0), or not decided yet (0: set up on the first swap). */
+int qsv_state_peer_memory(const qsv_state *st, int *out);
 
 /* ---- gates ------------------------------------------------------------- */
 /* gate_matrix() with reference semantics; out is 2^k x 2^k (re,im). */
@@ -253,7 +257,9 @@ int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset,
                     int nthreads);
 /* Step kinds of a plan in execution order (0 = local pass launch, 1 = qubit
  * swap, 2 = local pass run inside the previous step's launch: the second half
- * of an L2 super-pass, whose profiled time is 0);
+ * of an L2 super-pass, whose profiled time is 0; 3 = qubit swap fused into
+ * the preceding pass, which stores its tiles through peer memory when every
+ * rank has it -- profiled time 0 -- else an NCCL swap like kind 1);
  * returns the step count (fills at most cap entries). */
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap);
 

@@ -301,6 +301,13 @@ int qsv_state_device_ptr(qsv_state *st, int row, void **ptr) {
     });
 }
 
+int qsv_state_peer_memory(const qsv_state *st, int *out) {
+    return guard([&] {
+        require(st && out, "null argument");
+        *out = st->p2p;
+    });
+}
+
 int qsv_gate_matrix(const qsv_gate *g, double *out, int *k) {
     return guard([&] {
         require(g && out, "null argument");
@@ -684,7 +691,7 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
                 const Step &s = p.steps[si];
                 if (si) js += ",";
                 if (s.kind == 1) {
-                    js += "{\"kind\":\"swap\",\"pairs\":[";
+                    js += std::string("{\"kind\":\"swap\",\"fused\":") + (s.fused ? "true" : "false") + ",\"pairs\":[";
                     for (size_t k = 0; k < s.swap_bits.size(); ++k)
                         js += (k ? ",[" : "[") + std::to_string(s.swap_bits[k].first) + "," +
                               std::to_string(s.swap_bits[k].second) + "]";
@@ -694,6 +701,8 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
                 const PassHost &ph = p.passes[s.pass];
                 js += "{\"kind\":\"pass\",\"pair\":" + std::to_string(ph.pair) + ",\"tile\":[";
                 for (size_t k = 0; k < ph.tile_pos.size(); ++k) js += (k ? "," : "") + std::to_string(ph.tile_pos[k]);
+                js += "],\"gperm\":[";
+                for (size_t k = 0; k < ph.gperm.size(); ++k) js += (k ? "," : "") + std::to_string(ph.gperm[k]);
                 js += "],\"out_perm\":[";
                 for (size_t k = 0; k < ph.out_perm.size(); ++k) js += (k ? "," : "") + std::to_string(ph.out_perm[k]);
                 js += "],\"gates\":[";
@@ -714,6 +723,11 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
             js += "]}";
             require(js.size() + 1 <= cap, "plan_dry: schedule buffer too small");
             std::memcpy(src, js.c_str(), js.size() + 1);
+        } else if (src && cap && pass_index <= -3) { // the peer-memory variant of pass -3 - index
+            src[0] = 0;
+            const int pi = -3 - pass_index;
+            if (pi < static_cast<int>(p.passes.size()) && !p.passes[pi].gperm.empty())
+                std::snprintf(src, cap, "%s", jit_gout_source(p.passes[pi], dtype).c_str());
         } else if (src && cap) {
             src[0] = 0;
             if (pass_index >= 0 && pass_index < static_cast<int>(p.passes.size())) {
@@ -747,7 +761,7 @@ int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
     const int n = static_cast<int>(plan->steps.size());
     for (int i = 0; i < n && i < cap && kinds; ++i) {
         const Step &s = plan->steps[i];
-        kinds[i] = s.kind == 0 && plan->passes[s.pass].pair == 2 ? 2 : s.kind;
+        kinds[i] = s.kind == 0 && plan->passes[s.pass].pair == 2 ? 2 : s.kind == 1 && s.fused ? 3 : s.kind;
     }
     return n;
 }

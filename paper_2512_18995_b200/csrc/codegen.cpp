@@ -74,6 +74,24 @@ std::vector<Run> runs_of(const std::vector<int> &pos) {
     }
     return rs;
 }
+// Scatter of selected source bits: (source bit, destination bit) pairs.
+std::string scatter_sel(const std::string &x, const std::vector<std::pair<int, int>> &sd) {
+    if (sd.empty()) return "0ull";
+    std::ostringstream o;
+    size_t k = 0;
+    bool first = true;
+    while (k < sd.size()) {
+        size_t e = k + 1;
+        while (e < sd.size() && sd[e].first == sd[e - 1].first + 1 && sd[e].second == sd[e - 1].second + 1) ++e;
+        const int len = static_cast<int>(e - k);
+        if (!first) o << " | ";
+        first = false;
+        o << "(((((unsigned long long)(" << x << ")) >> " << sd[k].first << ") & " << ((1ull << len) - 1) << "ull) << "
+          << sd[k].second << ")";
+        k = e;
+    }
+    return o.str();
+}
 std::string scatter(const std::string &x, const std::vector<int> &pos, bool wide) {
     auto rs = runs_of(pos);
     if (rs.empty()) return wide ? "0ull" : "0";
@@ -509,7 +527,7 @@ struct Gen {
           << sfx << " [%0], {%1,%2};\" :: \"l\"(p), \"" << rc << "\"(v.x), \"" << rc << "\"(v.y) : \"memory\"); }\n";
         c << "struct Args { void *state; u64 row_stride, rank_base, tiles_per_row, total_tiles; const " << V
           << " *tables; const " << T << " *enc_table; int batch; int tpc; void *out; double *zout; const " << V
-          << " *prefix; };\n";
+          << " *prefix; void *const *peers; u64 out_lconst; int out_rconst; };\n";
         return c.str();
     }
 
@@ -529,7 +547,10 @@ struct Gen {
         k << "  const u64 t0 = a.tpc > 0 ? (u64)blockIdx.x * a.tpc : (u64)blockIdx.x;\n";
         k << "  const u64 tend = a.tpc > 0 ? (t0 + a.tpc < a.total_tiles ? t0 + a.tpc : a.total_tiles) : a.total_tiles;\n";
         k << "  const u64 tstep = a.tpc > 0 ? 1ull : (u64)gridDim.x;\n";
-        k << "  pass_body(a, t0, tend, tstep, smem_raw);\n}\n";
+        k << "  pass_body(a, t0, tend, tstep, smem_raw);\n";
+        // peer-memory stores: performed system-wide before the CTA retires
+        if (gout) k << "  __threadfence_system();\n";
+        k << "}\n";
         return k.str();
     }
 
@@ -790,6 +811,20 @@ struct Gen {
         o << "    " << V << " *st = (" << V << " *)a.state + (u64)row * a.row_stride;\n";
         o << "    const u64 tb = " << scatter("tl", ph.ext_pos, true) << ";\n";
         o << "    const u64 pbase = a.rank_base | tb;\n";
+        if (gout) {
+            // stores go to the destination rank's buffer: the ext bits map to
+            // local output bits or to rank bits (tile bits map to themselves)
+            const int nl = K + static_cast<int>(ph.ext_pos.size());
+            std::vector<std::pair<int, int>> lp, rp;
+            for (size_t i = 0; i < ph.ext_pos.size(); ++i) {
+                const int q = ph.gperm[ph.ext_pos[i]];
+                if (q < nl) lp.emplace_back(static_cast<int>(i), q);
+                else rp.emplace_back(static_cast<int>(i), q - nl);
+            }
+            o << "    const u64 tbo = " << scatter_sel("tl", lp) << ";\n";
+            o << "    const int drk = a.out_rconst | (int)(" << scatter_sel("tl", rp) << ");\n";
+            o << "    const u64 rowoff = (u64)row * a.row_stride + a.out_lconst;\n";
+        }
         if (!epipe) emit_e_direct("    ");
         if (pf) {
             // early issue: tile t + gridDim is already in flight, wait for the
@@ -825,6 +860,37 @@ struct Gen {
             o << "      const u64 ls = " << scatter("s", ngp, true) << ";\n";
             o << "      const u64 pb = pbase | ls;\n";
             o << "      const u64 gb = tb | ls;\n";
+            // peer-memory stores (last group): the set's bits and each
+            // register's slot bits map to output local bits or rank bits
+            std::vector<uint64_t> poffo(NR, 0);
+            std::vector<int> rkr(NR, 0);
+            if (gout && to_hbm) {
+                const int nl = K + static_cast<int>(ph.ext_pos.size());
+                std::vector<std::pair<int, int>> lsp, rsp;
+                for (size_t i = 0; i < ngt.size(); ++i) {
+                    const int q = ph.gperm[ph.tile_pos[ngt[i]]];
+                    if (q < nl) lsp.emplace_back(static_cast<int>(i), q);
+                    else rsp.emplace_back(static_cast<int>(i), q - nl);
+                }
+                o << "      const u64 lso = " << scatter_sel("s", lsp) << ";\n";
+                o << "      const int rks = drk | (int)(" << scatter_sel("s", rsp) << ");\n";
+                std::map<int, int> ptrs;
+                for (int r = 0; r < NR; ++r) {
+                    for (int j = 0; j < R; ++j)
+                        if ((r >> j) & 1) {
+                            const int q = ph.gperm[ph.tile_pos[g.slot_bit[j]]];
+                            if (q < nl) poffo[r] |= 1ull << q;
+                            else rkr[r] |= 1 << (q - nl);
+                        }
+                    if (!ptrs.count(rkr[r])) {
+                        const int id = static_cast<int>(ptrs.size());
+                        ptrs[rkr[r]] = id;
+                        o << "      " << V << " *const pd" << id << " = (" << V << " *)a.peers[rks | " << rkr[r]
+                          << "] + rowoff + lso;\n";
+                    }
+                    rkr[r] = ptrs[rkr[r]];
+                }
+            }
             o << "      (void)ub; (void)sb; (void)gb;\n";
             // phase tables: issue the (L2-resident) loads before the gate math
             for (int oi = g.op_begin; oi < g.op_end; ++oi) {
@@ -901,7 +967,8 @@ struct Gen {
                 o << "      }\n";
             }
             for (int r = 0; r < NR; ++r) {
-                if (to_hbm) o << "      " << st_out << "(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
+                if (to_hbm && gout) o << "      " << st_out << "(&pd" << rkr[r] << "[tbo + " << poffo[r] << "ull], v" << r << ");\n";
+                else if (to_hbm) o << "      " << st_out << "(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
                 else o << "      tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
@@ -983,6 +1050,7 @@ struct Gen {
     bool zsum = false; // fused <Z> epilogue in the last group (whole-row tiles)
     std::string st_out = "stcs"; // the last group's stores (stwb: keep the output in L2)
     std::string ld_in = "ldcs";  // the first group's direct loads (ldcg: L2 only, data written in this launch)
+    bool gout = false;           // last group stores through peer memory (PassHost::gperm)
     size_t dyn_base = 0, dyn_extra = 0; // dynamic shared memory: tile ring, then salloc'ed arrays
     size_t dyn_bytes() const { return dyn_base + dyn_extra; }
     void salloc(const char *name, int count) {
@@ -1072,9 +1140,12 @@ std::string generate_pair_source(const PassHost &A, const PassHost &B, int dtype
 }
 
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
-                                 bool zsum, size_t *smem) {
+                                 bool zsum, size_t *smem, bool gout) {
     Gen g(ph, dtype);
     g.zsum = zsum;
+    g.gout = gout;
+    require(!gout || !ph.gperm.empty(), "codegen: peer-memory pass without a global permutation");
+    require(!gout || (!zsum && ph.out_perm.empty()), "codegen: peer-memory stores on a permuting / <Z> pass");
     g.double_buffer = false;
     g.prefetch = dbuf;
     g.stages = dbuf_stages(ph, dtype);

@@ -23,6 +23,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "qsv_internal.hpp"
 
@@ -156,6 +157,131 @@ void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count) {
 
 namespace {
 void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs);
+
+// every rank's flag summed (a float all-reduce on the state's stream, then
+// read back): agreement on whether the peer-memory path is usable
+int agree_failures(State &st, int mine) {
+    Ctx &ctx = *st.ctx;
+    const Nccl &n = *ctx.nccl;
+    if (!st.d_barrier) QSV_CUDA(cudaMalloc(&st.d_barrier, sizeof(double)));
+    const double f = static_cast<double>(mine);
+    QSV_CUDA(cudaMemcpyAsync(st.d_barrier, &f, sizeof f, cudaMemcpyHostToDevice, ctx.stream));
+    nccl_ok(n, n.AllReduce(st.d_barrier, st.d_barrier, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx.comm),
+                           ctx.stream), "AllReduce");
+    double tot = 0;
+    QSV_CUDA(cudaMemcpyAsync(&tot, st.d_barrier, sizeof tot, cudaMemcpyDeviceToHost, ctx.stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+    return static_cast<int>(tot + 0.5);
+}
+} // namespace
+
+// Peer memory for qubit swaps fused into passes (plan.cpp run_gout): both
+// state buffers of every rank are mapped into every rank with CUDA IPC
+// (handles exchanged over NCCL send / recv), so a pass can store each tile
+// straight into its destination rank's scratch state over NVLink. Collective:
+// all ranks reach it at the same step of the same plan, and they agree on
+// the outcome (a failure anywhere -- no room for the scratch state, no peer
+// access -- leaves every rank on the NCCL swaps). QSV_P2P_SWAP=0 disables it.
+bool dist_p2p_ready(State &st) {
+    if (st.p2p != 0) return st.p2p > 0;
+    Ctx &ctx = *st.ctx;
+    require(ctx.world > 1 && ctx.comm, "peer memory on a non-distributed state");
+    const Nccl &n = *ctx.nccl;
+    const char *env = std::getenv("QSV_P2P_SWAP");
+    int bad = env && env[0] == '0' ? 1 : 0;
+    const size_t bytes = st.local_amps * st.amp_bytes() * static_cast<size_t>(st.batch);
+    if (!bad && !st.scratch && cudaMalloc(&st.scratch, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        st.scratch = nullptr;
+        bad = 1;
+    }
+    cudaIpcMemHandle_t mine[2];
+    std::memset(mine, 0, sizeof mine);
+    if (!bad) {
+        st.p2p_buf[0] = st.d;
+        st.p2p_buf[1] = st.scratch;
+        for (int i = 0; i < 2 && !bad; ++i)
+            if (cudaIpcGetMemHandle(&mine[i], st.p2p_buf[i]) != cudaSuccess) {
+                cudaGetLastError();
+                bad = 1;
+            }
+    }
+    if (agree_failures(st, bad) > 0) {
+        st.p2p = -1;
+        return false;
+    }
+    // exchange: rank r's two handles land in slot r on every rank
+    const int W = ctx.world;
+    const size_t hb = sizeof mine;
+    unsigned char *d_h = nullptr;
+    QSV_CUDA(cudaMalloc(&d_h, hb * W));
+    QSV_CUDA(cudaMemcpyAsync(d_h + hb * ctx.rank, mine, hb, cudaMemcpyHostToDevice, ctx.stream));
+    nccl_ok(n, n.GroupStart(), "GroupStart");
+    for (int r = 0; r < W; ++r) {
+        if (r == ctx.rank) continue;
+        nccl_ok(n, n.Send(d_h + hb * ctx.rank, hb, ncclUint8, r, static_cast<ncclComm_t>(ctx.comm), ctx.stream),
+                "Send");
+        nccl_ok(n, n.Recv(d_h + hb * r, hb, ncclUint8, r, static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Recv");
+    }
+    nccl_ok(n, n.GroupEnd(), "GroupEnd");
+    std::vector<cudaIpcMemHandle_t> all(2 * static_cast<size_t>(W));
+    QSV_CUDA(cudaMemcpyAsync(all.data(), d_h, hb * W, cudaMemcpyDeviceToHost, ctx.stream));
+    QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaFree(d_h);
+    std::vector<void *> table(2 * static_cast<size_t>(W), nullptr);
+    for (int r = 0; r < W && !bad; ++r)
+        for (int i = 0; i < 2 && !bad; ++i) {
+            if (r == ctx.rank) {
+                table[static_cast<size_t>(i) * W + r] = st.p2p_buf[i];
+                continue;
+            }
+            void *ptr = nullptr;
+            if (cudaIpcOpenMemHandle(&ptr, all[2 * static_cast<size_t>(r) + i], cudaIpcMemLazyEnablePeerAccess) !=
+                cudaSuccess) {
+                cudaGetLastError();
+                bad = 1;
+                break;
+            }
+            st.p2p_opened.push_back(ptr);
+            table[static_cast<size_t>(i) * W + r] = ptr;
+        }
+    if (!bad) {
+        if (cudaMalloc(reinterpret_cast<void **>(&st.d_peers), table.size() * sizeof(void *)) != cudaSuccess) {
+            cudaGetLastError();
+            st.d_peers = nullptr;
+            bad = 1;
+        } else {
+            QSV_CUDA(cudaMemcpy(st.d_peers, table.data(), table.size() * sizeof(void *), cudaMemcpyHostToDevice));
+        }
+    }
+    if (agree_failures(st, bad) > 0) {
+        dist_p2p_release(st);
+        st.p2p = -1;
+        return false;
+    }
+    st.p2p_cur = 0;
+    st.p2p = 1;
+    return true;
+}
+
+// Orders a fused pass's peer stores before anything that reads them: every
+// rank's pass kernel has completed once this all-reduce (on the same
+// stream) completes anywhere.
+void dist_p2p_barrier(State &st) {
+    Ctx &ctx = *st.ctx;
+    const Nccl &n = *ctx.nccl;
+    nccl_ok(n, n.AllReduce(st.d_barrier, st.d_barrier, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx.comm),
+                           ctx.stream), "AllReduce");
+}
+
+void dist_p2p_release(State &st) {
+    for (void *p : st.p2p_opened) cudaIpcCloseMemHandle(p);
+    st.p2p_opened.clear();
+    if (st.d_peers) cudaFree(st.d_peers);
+    st.d_peers = nullptr;
+    if (st.d_barrier) cudaFree(st.d_barrier);
+    st.d_barrier = nullptr;
+    st.p2p = 0;
 }
 
 // A step's pairs apply in order (a later pair may reuse a bit of an earlier

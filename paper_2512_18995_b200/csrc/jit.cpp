@@ -24,7 +24,7 @@
 namespace qsv {
 
 std::string generate_pass_source(const PassHost &ph, int dtype, const std::string &name, int *threads, bool dbuf,
-                                 bool zsum = false, size_t *smem = nullptr);
+                                 bool zsum = false, size_t *smem = nullptr, bool gout = false);
 int dbuf_stages(const PassHost &ph, int dtype);
 std::string generate_pair_source(const PassHost &A, const PassHost &B, int dtype, const std::string &name,
                                  int *threads, bool dbuf, size_t *smem = nullptr);
@@ -268,26 +268,57 @@ std::string jit_source(const PassHost &ph, int dtype) {
     return generate_pass_source(ph, dtype, "qsv_pass", &threads, use_prefetch(ph, dtype));
 }
 
+std::string jit_gout_source(const PassHost &ph, int dtype) {
+    int threads = 0;
+    return generate_pass_source(ph, dtype, "qsv_pass", &threads, use_prefetch(ph, dtype), false, nullptr, true);
+}
+
 std::string jit_pair_source(const PassHost &a, const PassHost &b, int dtype) {
     int threads = 0;
     return generate_pair_source(a, b, dtype, "qsv_pair", &threads, use_prefetch(a, dtype));
 }
 
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count) { jit_build(dp, ph, dtype, sm_count, false); }
+
+void jit_prepare_gout(DevPass &dp, const PassHost &ph, int dtype, int sm_count) {
+    (void)sm_count;
+    int threads = 0;
+    size_t smem = 0;
+    const std::string src =
+        generate_pass_source(ph, dtype, "qsv_pass", &threads, use_prefetch(ph, dtype), false, &smem, true);
+    require(threads == dp.threads && smem == dp.smem, "jit: peer-memory variant changed the CTA shape");
+    const JitKernel jk = load_kernel(src, "qsv_pass");
+    const void *kern = reinterpret_cast<const void *>(jk.kernel);
+    int dev = 0, optin = 0;
+    QSV_CUDA(cudaGetDevice(&dev));
+    QSV_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    cudaFuncAttributes fa{};
+    QSV_CUDA(cudaFuncGetAttributes(&fa, kern));
+    QSV_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(fa.sharedSizeBytes)));
+    dp.jit_gout = kern;
+}
 void jit_prepare_z(DevPass &dp, const PassHost &ph, int dtype, int sm_count) { jit_build(dp, ph, dtype, sm_count, true); }
 
-void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout) {
-    struct JArgs {
-        void *state;
-        uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
-        const void *tables;
-        const void *enc_table;
-        int batch;
-        int tpc;  // > 0: each CTA runs a block of tpc consecutive tiles
-        void *out;
-        double *zout;  // fused <Z> epilogue: batch x (K + 1) sums
-        const void *prefix;  // synthesising pass: product-state vectors
-    } a{};
+namespace {
+// Kernel parameters of a generated pass (codegen.cpp Args, same layout).
+struct JArgs {
+    void *state;
+    uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
+    const void *tables;
+    const void *enc_table;
+    int batch;
+    int tpc;             // > 0: each CTA runs a block of tpc consecutive tiles
+    void *out;
+    double *zout;        // fused <Z> epilogue: batch x (K + 1) sums
+    const void *prefix;  // synthesising pass: product-state vectors
+    void *const *peers;  // peer-memory stores: destination buffer per rank
+    uint64_t out_lconst;
+    int out_rconst;
+};
+
+JArgs make_args(const DevPass &dp, void *state, void *out, int rows) {
+    JArgs a{};
     a.state = state;
     a.out = out;
     a.row_stride = dp.args.row_stride;
@@ -297,16 +328,18 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     a.tables = dp.args.tables;
     a.enc_table = dp.args.enc_table;
     a.batch = dp.args.batch;
-    a.zout = zout;
     a.prefix = dp.args.prefix;
-    const void *kern = zout ? dp.jit_z : dp.jit;
+    return a;
+}
+
+// A few tiles per CTA rather than one persistent wave: CTAs that start and
+// retire at different times keep HBM reads and writes interleaved, where a
+// persistent grid moves in lock-step read / compute / write phases (measured
+// on cfg3 30q: 29.7 -> 23.1 ms for 4 passes; 128-byte runs at large strides
+// suffer most, scripts/micro/runs.cu).
+void launch_tiles(const void *kern, const DevPass &dp, JArgs &a, int grid_cap, cudaStream_t s) {
     require(kern != nullptr, "jit: kernel variant not prepared");
-    uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(zout ? dp.grid_z : dp.grid, 1)));
-    // A few tiles per CTA rather than one persistent wave: CTAs that start
-    // and retire at different times keep HBM reads and writes interleaved,
-    // where a persistent grid moves in lock-step read / compute / write
-    // phases (measured on cfg3 30q: 29.7 -> 23.1 ms for 4 passes; 128-byte
-    // runs at large strides suffer most, scripts/micro/runs.cu).
+    uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(grid_cap, 1)));
     static const int tpc = [] {
         const char *e = std::getenv("QSV_TILES_PER_CTA");
         return e ? std::atoi(e) : 4;
@@ -322,23 +355,29 @@ void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_
     void *args[] = {&a};
     QSV_CUDA(cudaLaunchKernel(kern, dim3(static_cast<unsigned>(grid)), dim3(dp.threads), args, dp.smem, s));
 }
+} // namespace
+
+void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout) {
+    JArgs a = make_args(dp, state, out, rows);
+    a.zout = zout;
+    launch_tiles(zout ? dp.jit_z : dp.jit, dp, a, zout ? dp.grid_z : dp.grid, s);
+}
+
+void launch_gout(const DevPass &dp, void *state, int rows, void *const *peers, uint64_t out_lconst, int out_rconst,
+                 cudaStream_t s) {
+    JArgs a = make_args(dp, state, state, rows);
+    a.peers = peers;
+    a.out_lconst = out_lconst;
+    a.out_rconst = out_rconst;
+    launch_tiles(dp.jit_gout, dp, a, dp.grid, s);
+}
 
 } // namespace qsv
 
 namespace qsv {
 void launch_pair(const DevPass &head, const DevPass &tail, void *state, void *out, int rows, unsigned *sync,
                  uint64_t nchunks, cudaStream_t s) {
-    struct JArgs {
-        void *state;
-        uint64_t row_stride, rank_base, tiles_per_row, total_tiles;
-        const void *tables;
-        const void *enc_table;
-        int batch;
-        int tpc;
-        void *out;
-        double *zout;
-        const void *prefix;
-    } a{}, b{};
+    JArgs a{}, b{};
     struct Pair {
         unsigned *sync;
         uint64_t nchunks;

@@ -27,6 +27,7 @@ Ctx::~Ctx() {
 }
 
 State::~State() {
+    if (p2p_opened.size() || d_peers || d_barrier) dist_p2p_release(*this);
     if (d) cudaFree(d);
     if (scratch) cudaFree(scratch);
 }
@@ -52,6 +53,32 @@ std::vector<int> canonical_perm(int n) {
     std::vector<int> p(n);
     for (int w = 0; w < n; ++w) p[w] = n - 1 - w; // wire 0 = MSB (state.hpp:21-24)
     return p;
+}
+
+// Qubit swaps fused into the pass before them (used when every rank has peer
+// memory, dist.cu dist_p2p_ready): a run of swap steps is one permutation of
+// the global index bits, and the pass writes every tile straight to where the
+// permutation puts it -- the destination rank's scratch state, over NVLink --
+// instead of writing in place and exchanging halves through NCCL afterwards.
+// Needs a specialised kernel and no output permutation of its own. The swap
+// steps stay in the plan: without peer memory they run as NCCL all-to-alls.
+void fuse_swaps_into_passes(Plan &p) {
+    const int n = p.n, nl = p.nlocal;
+    if (!plan_uses_jit(p)) return;
+    for (size_t i = 1; i < p.steps.size(); ++i) {
+        if (p.steps[i].kind != 1 || p.steps[i - 1].kind != 0) continue;
+        PassHost &ph = p.passes[p.steps[i - 1].pass];
+        if (!ph.out_perm.empty() || ph.synth || ph.pair || !ph.gperm.empty()) continue;
+        std::vector<int> where(n); // input bit -> its position after the swaps
+        for (int b = 0; b < n; ++b) where[b] = b;
+        size_t j = i;
+        for (; j < p.steps.size() && p.steps[j].kind == 1; ++j)
+            for (const auto &[a, b] : p.steps[j].swap_bits)
+                for (int &w : where) w = w == a ? b : w == b ? a : w;
+        ph.gperm = where;
+        for (size_t k = i; k < j; ++k) p.steps[k].fused = true;
+        i = j - 1;
+    }
 }
 
 // Distributed schedule: split the gate list into local segments separated by
@@ -142,15 +169,37 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
             // victim: the local wire needed furthest in the future; among
             // equally distant ones (or ones not needed before the next few
             // gates) the highest bit, whose halves are contiguous runs
+            // ties -> a bit outside the tile of the pass just before the
+            // swap (the swap can then be fused into that pass, see
+            // fuse_swaps_into_passes), then the highest bit
+            uint64_t prev_tile = 0;
+            if (!p.steps.empty() && p.steps.back().kind == 0)
+                for (int t : p.passes[p.steps.back().pass].tile_pos) prev_tile |= 1ull << t;
+            const char *slack_env = std::getenv("QSV_SWAP_SLACK");
+            const size_t slack = slack_env ? std::strtoull(slack_env, nullptr, 10) : 0;
+            size_t far = 0; // Belady: the furthest next use among the candidates
+            auto candidate = [&](int lb) {
+                if (std::find(keep.begin(), keep.end(), lb) != keep.end()) return false;
+                for (int w : want)
+                    if (wire_at[lb] == w) return false;
+                return true;
+            };
+            for (int lb = nl - 1; lb >= 0; --lb)
+                if (candidate(lb)) far = std::max(far, next_use(wire_at[lb], 0));
+            // within `slack` gates of it (QSV_SWAP_SLACK, default 0: ties
+            // only -- a one-layer slack measured more passes and swaps on the
+            // cfg4 family), a bit outside the previous pass's tile wins (its
+            // fused stores keep whole tiles together), then the furthest,
+            // then the highest bit
             int best = -1;
             size_t best_use = 0;
-            for (int lb = nl - 1; lb >= 0; --lb) { // Belady; ties -> the highest bit
-                if (std::find(keep.begin(), keep.end(), lb) != keep.end()) continue;
-                bool wanted = false;
-                for (int w : want) wanted = wanted || wire_at[lb] == w;
-                if (wanted) continue;
+            bool best_free = false;
+            for (int lb = nl - 1; lb >= 0; --lb) {
+                if (!candidate(lb)) continue;
                 const size_t score = next_use(wire_at[lb], 0);
-                if (best < 0 || score > best_use) best = lb, best_use = score;
+                const bool free_bit = !((prev_tile >> lb) & 1) && score + slack >= far;
+                if (best < 0 || (free_bit && !best_free) || (free_bit == best_free && score > best_use))
+                    best = lb, best_use = score, best_free = free_bit;
             }
             require(best >= 0, "dist: no local qubit available for a swap");
             keep.push_back(best);
@@ -220,6 +269,7 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         }
     }
     p.perm_out = phys;
+    fuse_swaps_into_passes(p);
 }
 
 } // namespace
@@ -411,7 +461,47 @@ void run_pair(Plan &p, int pi, State &st, cudaStream_t s) {
         out = st.scratch;
     }
     launch_pair(head, tail, st.d, out, st.batch, static_cast<unsigned *>(p.d_sync), nchunks, s);
-    if (tail.out_of_place) std::swap(st.d, st.scratch);
+    if (tail.out_of_place) {
+        std::swap(st.d, st.scratch);
+        st.p2p_cur ^= 1;
+    }
+}
+} // namespace
+
+namespace {
+// A pass that can do the swaps after it (PassHost::gperm) does so when every
+// rank has peer memory (set up on first use, collectively).
+bool use_gout(Plan &p, int pi, State &st) {
+    if (p.ctx->world == 1 || p.passes[pi].gperm.empty() || !p.dev[pi].jit) return false;
+    return dist_p2p_ready(st);
+}
+
+// The pass, then the swaps fused into it: every tile is stored straight into
+// its destination rank's scratch state (peer memory over NVLink); once every
+// rank's kernel is done (an all-reduce on the stream orders them) the scratch
+// states become the states on every rank.
+void run_gout(Plan &p, int pi, DevPass &dp, State &st, cudaStream_t s) {
+    const PassHost &ph = p.passes[pi];
+    DevPass &keep = p.dev[pi];
+    if (!keep.jit_gout) {
+        QSV_CUDA(cudaSetDevice(p.ctx->device));
+        jit_prepare_gout(keep, ph, p.dtype, p.ctx->sm_count);
+    }
+    dp.jit_gout = keep.jit_gout;
+    const int nl = p.nlocal, W = p.ctx->world;
+    uint64_t lconst = 0;
+    int rconst = 0;
+    for (int b = nl; b < p.n; ++b) {
+        const uint64_t bit = (static_cast<uint64_t>(p.ctx->rank) >> (b - nl)) & 1;
+        const int q = ph.gperm[b];
+        if (q < nl) lconst |= bit << q;
+        else rconst |= static_cast<int>(bit << (q - nl));
+    }
+    void *const *dst = st.d_peers + static_cast<size_t>(1 - st.p2p_cur) * W;
+    launch_gout(dp, st.d, st.batch, dst, lconst, rconst, s);
+    dist_p2p_barrier(st);
+    std::swap(st.d, st.scratch);
+    st.p2p_cur ^= 1;
 }
 } // namespace
 
@@ -424,6 +514,7 @@ void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *z
     ensure_scratch(st);
     launch_jit(dp, st.d, st.scratch, st.batch, s);
     std::swap(st.d, st.scratch);
+    st.p2p_cur ^= 1;
 }
 
 void upload_plan(Plan &p) {
@@ -556,8 +647,11 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
         }
         launch_prefix(p, brows, s);
     }
+    bool fused_done = false; // the last pass also did the swap steps after it
     for (size_t i = 0; i < p.steps.size(); ++i) {
         const Step &stp = p.steps[i];
+        if (stp.kind == 1 && stp.fused && fused_done) continue;
+        fused_done = false;
         if (stp.kind == 0 && p.dev[stp.pass].pair) {
             require(!zout || i + 1 < p.steps.size(), "fused <Z>: not on a super-pass");
             if (p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
@@ -566,7 +660,12 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
             dp.args.prefix = p.passes[stp.pass].synth ? p.d_prefix : nullptr;
-            run_pass(dp, p.dtype, st, s, i + 1 == p.steps.size() ? zout : nullptr);
+            if (use_gout(p, stp.pass, st)) {
+                run_gout(p, stp.pass, dp, st, s);
+                fused_done = true;
+            } else {
+                run_pass(dp, p.dtype, st, s, i + 1 == p.steps.size() ? zout : nullptr);
+            }
         } else {
             dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         }
@@ -626,10 +725,20 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
     std::vector<cudaEvent_t> ev(2 * p.steps.size());
     for (auto &e : ev) QSV_CUDA(cudaEventCreate(&e));
     size_t k = 0;
+    bool fused_done = false;
     for (const Step &stp : p.steps) {
         QSV_CUDA(cudaEventRecord(ev[2 * k], s));
-        if (stp.kind == 0 && p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
+        const bool skip = stp.kind == 1 && stp.fused && fused_done;
+        fused_done = false;
+        if (skip) {
+            fused_done = true;
+        } else if (stp.kind == 0 && p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
         else if (stp.kind == 0 && p.dev[stp.pass].pair == 2) {
+        } else if (stp.kind == 0 && use_gout(p, stp.pass, st)) {
+            DevPass dp = p.dev[stp.pass];
+            dp.args.batch = st.batch;
+            run_gout(p, stp.pass, dp, st, s);
+            fused_done = true;
         } else if (stp.kind == 0) run_pass(p.dev[stp.pass], p.dtype, st, s);
         else dist_swap_bits(st, stp.swap_bits, nullptr, 0);
         QSV_CUDA(cudaEventRecord(ev[2 * k + 1], s));

@@ -208,6 +208,11 @@ struct PassHost {
     // inside the chunk come first in ext_pos, so a chunk is a tile range)
     int pair = 0;
     int chunk_bits = 0;
+    // Multi-GPU: the qubit swaps that follow this pass, fused into it (when
+    // peer memory is available): input global bit -> output global bit
+    // (size n; rank bits >= nlocal). The pass then writes every tile straight
+    // into its destination rank's scratch state over NVLink.
+    std::vector<int> gperm;
     // The pass's gates in execution order, wires mapped to physical bits
     // (schedule export for host-side verification, qsv_plan_dry).
     std::vector<GateRec> exec_gates;
@@ -241,6 +246,16 @@ struct State {
     void *d = nullptr;          // batch * local_amps amplitudes
     void *scratch = nullptr;    // same size; target of out-of-place (permuting) passes
     std::vector<int> perm;      // logical wire -> physical bit (>= nlocal: rank bit)
+    // peer memory (multi-GPU swaps fused into passes, dist.cu): 0 = not set
+    // up, 1 = ready, -1 = unavailable (NCCL swaps). p2p_buf[i] are this
+    // rank's two state buffers (p2p_buf[p2p_cur] == d); d_peers holds
+    // 2 x world device pointers: buffer i of rank r at [i * world + r].
+    int p2p = 0;
+    int p2p_cur = 0;
+    void *p2p_buf[2] = {nullptr, nullptr};
+    std::vector<void *> p2p_opened;  // peer mappings to close
+    void **d_peers = nullptr;
+    double *d_barrier = nullptr;
     size_t amp_bytes() const { return dtype == QSV_C64 ? 8 : 16; }
     ~State();
 };
@@ -259,6 +274,7 @@ struct DevPass {
     int pair = 0;                 // L2 super-pass: 1 = head (jit_pair runs it and the next pass), 2 = tail
     const void *jit_pair = nullptr;
     int chunk_tiles_log = 0;      // log2 tiles per chunk (head)
+    const void *jit_gout = nullptr;  // variant writing through peer memory (PassHost::gperm), on first use
     double bytes = 0;
     int ngates = 0;
 };
@@ -268,6 +284,7 @@ struct Step {
     int kind = 0;              // 0 pass, 1 swap
     int pass = -1;             // index into passes
     std::vector<std::pair<int, int>> swap_bits;  // (global physical bit, local physical bit)
+    bool fused = false;        // swap: done by the preceding pass when peer memory is ready
 };
 
 struct Plan {
@@ -356,8 +373,16 @@ void jit_prepare_pair(DevPass &head, const PassHost &a, const PassHost &b, int d
 void launch_pair(const DevPass &head, const DevPass &tail, void *state, void *out, int rows, unsigned *sync,
                  uint64_t nchunks, cudaStream_t s);
 void jit_prepare_z(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
+// Pass variant whose last group stores straight into the destination rank's
+// buffer (PassHost::gperm; peers = world device pointers of the destination
+// buffers, out_lconst / out_rconst = this rank's own rank bits mapped to
+// local / rank output bits).
+void jit_prepare_gout(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
+void launch_gout(const DevPass &dp, void *state, int rows, void *const *peers, uint64_t out_lconst, int out_rconst,
+                 cudaStream_t s);
 std::string jit_source(const PassHost &ph, int dtype);
 std::string jit_pair_source(const PassHost &a, const PassHost &b, int dtype);
+std::string jit_gout_source(const PassHost &ph, int dtype);
 // Reductions write FP64 results to device memory, then copy to host.
 void reduce_norm2(State &st, double *host_out);
 void reduce_z_all(State &st, double *host_out /* batch x kZ: [total, S_bit0..] */);
@@ -377,5 +402,9 @@ void nccl_destroy(Ctx &ctx);
 // (m = pairs), for every batch row, chunked through persistent staging.
 void dist_swap_bits(State &st, const std::vector<std::pair<int, int>> &pairs, void *staging, size_t staging_bytes);
 void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count);
+// Peer memory for swaps fused into passes (collective; agreed by all ranks).
+bool dist_p2p_ready(State &st);
+void dist_p2p_barrier(State &st);
+void dist_p2p_release(State &st);
 
 } // namespace qsv

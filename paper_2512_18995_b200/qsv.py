@@ -113,6 +113,7 @@ _SIGS = {
     "qsv_state_download_raw": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
     "qsv_state_clone": (C.c_int, [_P, C.POINTER(_P)]),
     "qsv_state_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "qsv_state_peer_memory": (C.c_int, [_P, C.POINTER(C.c_int)]),
     "qsv_gate_matrix": (C.c_int, [C.POINTER(qsv_gate), C.c_void_p, C.POINTER(C.c_int)]),
     "qsv_apply_matrix": (C.c_int, [_P, C.c_int, C.POINTER(C.c_int32), C.c_int, C.POINTER(C.c_int32), C.c_void_p,
                                    C.c_int]),
@@ -150,7 +151,7 @@ def plan_dry(nqubit: int, gates, dtype: int = C128, world: int = 1, opts: dict |
     arr, keep = gate_array(gates)
     o = make_opts(opts)
     info = qsv_plan_info()
-    cap = 8 << 20 if source_of_pass >= 0 else 0
+    cap = 8 << 20 if source_of_pass >= 0 or source_of_pass <= -3 else 0
     buf = C.create_string_buffer(cap) if cap else None
     check(lib().qsv_plan_dry(nqubit, dtype, world, arr, len(gates), C.byref(o), C.byref(info), source_of_pass, buf,
                              cap))
@@ -440,6 +441,13 @@ class QubitState:
         out = QubitState(self._n, ctx=self.ctx, _handle=h)
         out._mixed = self._mixed
         return out
+
+    def peer_memory(self) -> int:
+        """Multi-GPU: 1 = qubit swaps fused into the passes (peer memory),
+        -1 = NCCL swaps, 0 = not decided yet."""
+        v = C.c_int(0)
+        check(lib().qsv_state_peer_memory(self.h, C.byref(v)))
+        return v.value
 
     def norm2(self) -> np.ndarray:
         out = np.zeros(self._batch)

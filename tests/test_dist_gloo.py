@@ -67,7 +67,44 @@ def permute_bits(sl, out_perm):
     return out
 
 
-def run_schedule(rank, world, sched, init_full):
+def global_permute(sl, gperm, rank, world, nl):
+    """The swaps fused into a pass (PassHost::gperm): every amplitude goes
+    straight to the rank and local index the global bit permutation puts it
+    at -- what the pass kernel's peer-memory stores do -- here as index/value
+    messages over gloo."""
+    import torch
+    import torch.distributed as dist
+
+    idx = np.arange(len(sl), dtype=np.int64)
+    glob = (np.int64(rank) << nl) | idx
+    out = np.zeros_like(glob)
+    for b, q in enumerate(gperm):
+        out |= ((glob >> b) & 1) << q
+    dest, dloc = out >> nl, out & ((1 << nl) - 1)
+    new = np.empty_like(sl)
+    mine = dest == rank
+    new[dloc[mine]] = sl[mine]
+    ops, bufs = [], []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        m = dest == peer
+        msg = np.concatenate([dloc[m].astype(np.float64), sl[m].view(np.float64)])
+        send = torch.from_numpy(msg)
+        recv = torch.empty_like(send)  # the exchange is symmetric in size
+        ops += [dist.P2POp(dist.isend, send, peer), dist.P2POp(dist.irecv, recv, peer)]
+        bufs.append(recv)
+    if ops:
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
+    for recv in bufs:
+        r = recv.numpy()
+        k = len(r) // 3
+        new[r[:k].astype(np.int64)] = r[k:].view(np.complex128)
+    return new
+
+
+def run_schedule(rank, world, sched, init_full, fused=False):
     import torch
     import torch.distributed as dist
 
@@ -75,6 +112,7 @@ def run_schedule(rank, world, sched, init_full):
     sl = init_full[rank << nl:(rank + 1) << nl].copy()
     idx = np.arange(len(sl), dtype=np.int64)
     sent = 0
+    fused_done = False
     for step in sched["steps"]:
         if step["kind"] == "pass":
             for g in step["gates"]:
@@ -82,7 +120,13 @@ def run_schedule(rank, world, sched, init_full):
                 apply_phys(sl, g, rank, nl)
             if step["out_perm"]:
                 sl = permute_bits(sl, step["out_perm"])
+            fused_done = fused and bool(step["gperm"])
+            if fused_done:
+                sl = global_permute(sl, step["gperm"], rank, world, nl)
             continue
+        if step["fused"] and fused_done:
+            continue
+        fused_done = False
         for gb, lb in step["pairs"]:
             r = gb - nl
             partner = rank ^ (1 << r)
@@ -98,14 +142,14 @@ def run_schedule(rank, world, sched, init_full):
     return sl, sent
 
 
-def _worker(rank, world, port, sched, init_full, out_dir):
+def _worker(rank, world, port, sched, init_full, out_dir, fused=False):
     import torch.distributed as dist
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        sl, sent = run_schedule(rank, world, sched, init_full)
+        sl, sent = run_schedule(rank, world, sched, init_full, fused)
         np.save(os.path.join(out_dir, f"r{rank}.npy"), sl)
         np.save(os.path.join(out_dir, f"s{rank}.npy"), np.array([sent]))
     finally:
@@ -120,11 +164,11 @@ def free_port():
     return p
 
 
-def run_distributed(n, gates, world, init_full, tmp_path):
+def run_distributed(n, gates, world, init_full, tmp_path, opts=None, fused=False):
     import torch.multiprocessing as mp
 
-    sched = qsv.plan_schedule(n, gates, world=world)
-    mp.spawn(_worker, args=(world, free_port(), sched, init_full, str(tmp_path)), nprocs=world, join=True)
+    sched = qsv.plan_schedule(n, gates, world=world, opts=opts)
+    mp.spawn(_worker, args=(world, free_port(), sched, init_full, str(tmp_path), fused), nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"r{r}.npy") for r in range(world)])
     sent = sum(int(np.load(tmp_path / f"s{r}.npy")[0]) for r in range(world))
     return got, sched, sent
@@ -180,3 +224,22 @@ def test_global_target_needs_one_exchange():  # test_dist.cpp:112-126
 def test_rejects_non_power_of_two_world():  # test_dist.cpp:90-94
     with pytest.raises(qsv.InvalidInput):
         qsv.plan_dry(4, [make_gate("h", [0])], world=3)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_swaps_fused_into_passes(world, tmp_path):
+    # with specialised kernels the swaps after a pass are fused into it (its
+    # stores go straight to the destination rank through peer memory); the
+    # fused schedule and the NCCL-swap schedule must both equal the reference
+    rng = Rng(17, "dist-fused")
+    cases = [(W.cfg4_circuit(9, layers=3), 9), (W.cfg3_circuit(9), 9), (random_circuit(rng, 8, 30), 8)]
+    nfused = 0
+    for cir, n in cases:
+        psi = random_state(rng, n)
+        want = O.port_forward(n, cir.gates(), init=psi)[0]
+        sched = qsv.plan_schedule(n, cir.gates(), world=world, opts={"jit": 1})
+        nfused += sum(1 for s in sched["steps"] if s["kind"] == "swap" and s["fused"])
+        for fused in (False, True):
+            got, _, _ = run_distributed(n, cir.gates(), world, psi, tmp_path, opts={"jit": 1}, fused=fused)
+            assert np.max(np.abs(got - want)) < 1e-12, (world, n, fused)
+    assert nfused > 0

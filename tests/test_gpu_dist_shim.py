@@ -66,14 +66,18 @@ def _rank_main(rank, world, uid, n, gates, init, dtype, obs, q, env=None, data=N
         ex = Q.expectation_many(st, [Q.Observable(w, b) for w, b in obs])[0] if obs else []
         local = st.amplitudes()  # again: expectations must leave the layout as they found it
         counts = Q.measure(st, 1000, [0, n - 1], Q.Rng(3, "shim-measure"), True)  # measure_dist
-        q.put((rank, local, z, nrm, list(ex) + [counts], plan.info["nswaps"]))
+        q.put((rank, local, z, nrm, list(ex) + [counts], plan.info["nswaps"], st.peer_memory()))
         del plan, st
         ctx.close()
     except Exception:
-        q.put((rank, traceback.format_exc(), None, None, None, None))
+        q.put((rank, traceback.format_exc(), None, None, None, None, None))
+
+
+PEER_MEMORY = {}  # rank -> QubitState.peer_memory() of the last run_ranks
 
 
 def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=(), env=None, data=None):
+    PEER_MEMORY.clear()
     uid = qsv.Context.nccl_unique_id()
     ctxm = mp.get_context("spawn")
     q = ctxm.Queue()
@@ -84,10 +88,11 @@ def run_ranks(n, gates, world, init=None, dtype=qsv.C128, obs=(), env=None, data
     res = {}
     try:
         for _ in range(world):
-            r, local, z, nrm, ex, nsw = q.get(timeout=180)
+            r, local, z, nrm, ex, nsw, p2p = q.get(timeout=180)
             if z is None:
                 raise AssertionError(f"rank {r} failed:\n{local}")
             res[r] = (local, z, nrm, ex, nsw)
+            PEER_MEMORY[r] = p2p
     finally:
         for p in procs:
             p.join(timeout=60)
@@ -274,3 +279,24 @@ def test_adjoint_dist_matches_single_rank():  # tests/test_dist.cpp:224-276
     res = run_adjoint(c, 4, data)
     for r in res:
         assert np.max(np.abs(np.asarray(res[r][1]) - want.data_grads)) <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_swaps_fused_into_passes_through_peer_memory(world):
+    # the swaps after a pass are done by the pass itself: its last register
+    # group stores every amplitude into the destination rank's scratch state
+    # (CUDA IPC mappings of every rank's buffers), then the states flip; with
+    # QSV_P2P_SWAP=0 the same plan runs its swaps as NCCL all-to-alls
+    rng = qsv.Rng(29, f"shim-fused-{world}")
+    for n, cir, dtype, tol in ((14, W.cfg4_circuit(14, layers=4), qsv.C128, 1e-12),
+                               (13, W.cfg3_circuit(13), qsv.C128, 1e-12),
+                               (14, W.cfg5_circuit(14, layers=3), qsv.C64, 1e-5)):
+        sched = qsv.plan_schedule(n, cir.gates(), dtype=dtype, world=world)
+        assert any(s["kind"] == "swap" and s["fused"] for s in sched["steps"]), n
+        psi = random_state(rng, n)
+        want = O.port_forward(n, cir.gates(), init=psi)[0]
+        for env, mode in (({}, 1), ({"QSV_P2P_SWAP": "0"}, -1)):
+            got, z, nrm, _, _ = run_ranks(n, cir.gates(), world, init=psi, dtype=dtype, env=env)
+            assert all(v == mode for v in PEER_MEMORY.values()), (PEER_MEMORY, env)
+            assert np.max(np.abs(got - want)) <= tol, (world, n, env)
+            assert abs(nrm - 1.0) <= 10 * tol
