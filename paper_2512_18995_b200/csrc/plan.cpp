@@ -97,6 +97,26 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
     // frontier needs.
     std::vector<int> rem(p.gates.size());
     for (size_t i = 0; i < rem.size(); ++i) rem[i] = static_cast<int>(i);
+    // Swap gates as relabelings (as on one GPU): a swap gate exchanges the
+    // two wires' physical bits in the mapping and moves no data -- local or
+    // global -- and the final layout restore absorbs them (a permuting,
+    // out-of-place pass for the local bits, so it needs room for a second
+    // local state; else swap gates stay gates).
+    bool relabel = cfg.fuse && p.opts.no_relabel == 0 && plan_uses_jit(p) && p.nslots == 0;
+    if (relabel && p.ctx->stream) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const double state = std::ldexp(static_cast<double>(p.dtype == QSV_C64 ? 8 : 16), nl);
+            if (2.0 * state > 0.92 * static_cast<double>(total_b)) relabel = false;
+        } else {
+            cudaGetLastError();
+        }
+    }
+    auto plain_swap = [](const GateRec &g) {
+        return g.kind == GK_SWAP && g.k == 2 && g.ctls.empty() && !g.encoded && g.flags == 0;
+    };
+    std::vector<int> ident(n);
+    for (int b = 0; b < n; ++b) ident[b] = b;
     auto next_use = [&](int wire, size_t from) -> size_t { // position in rem
         for (size_t j = from; j < rem.size(); ++j) {
             const GateRec &g = p.gates[rem[j]];
@@ -107,10 +127,24 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         return rem.size() + 1;
     };
     while (!rem.empty()) {
-        std::vector<int> front, blocked;
+        std::vector<int> blocked;
+        std::vector<GateRec> seg; // the front, on physical bits (as admitted)
         uint64_t bN = 0, bD = 0; // wires (logical) blocked non-diagonally / diagonally
         for (int gi : rem) {
             const GateRec &g = p.gates[gi];
+            if (relabel && plain_swap(g)) {
+                const uint64_t wm = (1ull << g.wires[0]) | (1ull << g.wires[1]);
+                if (wm & (bN | bD)) { // an earlier gate on either wire waits: so does the swap
+                    bN |= wm;
+                    blocked.push_back(gi);
+                    continue;
+                }
+                const int a = g.wires[0], b = g.wires[1];
+                std::swap(phys[a], phys[b]);
+                wire_at[phys[a]] = a;
+                wire_at[phys[b]] = b;
+                continue;
+            }
             uint64_t nm = 0, dm = 0;
             bool global_n = false;
             for (int t = 0; t < g.k; ++t) {
@@ -126,12 +160,15 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
                 bN |= nm;
                 bD |= dm;
                 blocked.push_back(gi);
-            } else front.push_back(gi);
+            } else {
+                GateRec e = g;
+                for (int t = 0; t < g.k; ++t) e.wires[t] = phys[g.wires[t]];
+                for (int &c : e.ctls) c = phys[c];
+                seg.push_back(std::move(e));
+            }
         }
-        if (!front.empty()) {
-            std::vector<GateRec> seg;
-            for (int gi : front) seg.push_back(p.gates[gi]);
-            auto passes = plan_passes(seg, phys, cfg, p.encs);
+        if (!seg.empty()) {
+            auto passes = plan_passes(seg, ident, cfg, p.encs);
             for (auto &ph : passes) {
                 Step s;
                 s.kind = 0;
@@ -237,8 +274,30 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         do_swap(back, gb, x);
     }
     if (!back.swap_bits.empty()) p.steps.push_back(std::move(back));
-    // Phase B: local bits permuted among themselves -> local swap gates,
-    // expressed on PHYSICAL bits (identity mapping) and fused into passes.
+    // Phase B: local bits permuted among themselves. With relabeled swap
+    // gates: one permutation-only pass (out of place, balanced read / write
+    // runs); else local swap gates, expressed on PHYSICAL bits (identity
+    // mapping) and fused into passes.
+    if (relabel) {
+        std::vector<int> out_perm(nl);
+        bool moved = false;
+        for (int b = 0; b < nl; ++b) {
+            out_perm[b] = canon[wire_at[b]];
+            moved = moved || out_perm[b] != b;
+        }
+        if (moved) {
+            PlanConfig c1 = cfg;
+            c1.super_bits = 0;
+            auto passes = plan_passes({}, ident, c1, p.encs, out_perm);
+            for (auto &ph : passes) {
+                Step st;
+                st.pass = static_cast<int>(p.passes.size());
+                p.passes.push_back(std::move(ph));
+                p.steps.push_back(std::move(st));
+            }
+            for (int w = 0; w < n; ++w) phys[w] = canon[w], wire_at[canon[w]] = w;
+        }
+    }
     std::vector<GateRec> fix;
     for (int w = 0; w < n; ++w) {
         if (phys[w] == canon[w]) continue;
@@ -258,8 +317,6 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         wire_at[b] = wa;
     }
     if (!fix.empty()) {
-        std::vector<int> ident(n);
-        for (int b = 0; b < n; ++b) ident[b] = b;
         auto passes = plan_passes(fix, ident, cfg, p.encs);
         for (auto &ph : passes) {
             Step s;
