@@ -145,6 +145,8 @@ def swap_accounting(n, cir, world, nl, amp_bytes, fused):
     fused_done = False
     for i, step in enumerate(sched["steps"]):
         if step["kind"] == "pass":
+            if step["fused"] and fused_done:
+                continue
             fused_done = fused and bool(step["gperm"])
             if fused_done:
                 m = sum(1 for b in range(nl) if step["gperm"][b] >= nl)

@@ -257,9 +257,10 @@ int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset,
                     int nthreads);
 /* Step kinds of a plan in execution order (0 = local pass launch, 1 = qubit
  * swap, 2 = local pass run inside the previous step's launch: the second half
- * of an L2 super-pass, whose profiled time is 0; 3 = qubit swap fused into
- * the preceding pass, which stores its tiles through peer memory when every
- * rank has it -- profiled time 0 -- else an NCCL swap like kind 1);
+ * of an L2 super-pass, whose profiled time is 0; 3 = a qubit swap, or the
+ * final permutation-only pass, fused into the preceding pass, which stores
+ * its tiles through peer memory when every rank has it -- profiled time 0 --
+ * else run as a swap / pass);
  * returns the step count (fills at most cap entries). */
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap);
 

@@ -699,7 +699,8 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
                     continue;
                 }
                 const PassHost &ph = p.passes[s.pass];
-                js += "{\"kind\":\"pass\",\"pair\":" + std::to_string(ph.pair) + ",\"tile\":[";
+                js += "{\"kind\":\"pass\",\"pair\":" + std::to_string(ph.pair) + ",\"fused\":" +
+                      (s.fused ? "true" : "false") + ",\"tile\":[";
                 for (size_t k = 0; k < ph.tile_pos.size(); ++k) js += (k ? "," : "") + std::to_string(ph.tile_pos[k]);
                 js += "],\"gperm\":[";
                 for (size_t k = 0; k < ph.gperm.size(); ++k) js += (k ? "," : "") + std::to_string(ph.gperm[k]);
@@ -761,7 +762,7 @@ int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
     const int n = static_cast<int>(plan->steps.size());
     for (int i = 0; i < n && i < cap && kinds; ++i) {
         const Step &s = plan->steps[i];
-        kinds[i] = s.kind == 0 && plan->passes[s.pass].pair == 2 ? 2 : s.kind == 1 && s.fused ? 3 : s.kind;
+        kinds[i] = s.fused ? 3 : s.kind == 0 && plan->passes[s.pass].pair == 2 ? 2 : s.kind;
     }
     return n;
 }

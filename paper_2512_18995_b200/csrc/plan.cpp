@@ -65,8 +65,13 @@ std::vector<int> canonical_perm(int n) {
 void fuse_swaps_into_passes(Plan &p) {
     const int n = p.n, nl = p.nlocal;
     if (!plan_uses_jit(p)) return;
+    auto perm_only = [&](const Step &st) {
+        if (st.kind != 0) return false;
+        const PassHost &q = p.passes[st.pass];
+        return !q.out_perm.empty() && q.ngates == 0;
+    };
     for (size_t i = 1; i < p.steps.size(); ++i) {
-        if (p.steps[i].kind != 1 || p.steps[i - 1].kind != 0) continue;
+        if ((p.steps[i].kind != 1 && !perm_only(p.steps[i])) || p.steps[i - 1].kind != 0) continue;
         PassHost &ph = p.passes[p.steps[i - 1].pass];
         if (!ph.out_perm.empty() || ph.synth || ph.pair || !ph.gperm.empty()) continue;
         std::vector<int> where(n); // input bit -> its position after the swaps
@@ -75,6 +80,24 @@ void fuse_swaps_into_passes(Plan &p) {
         for (; j < p.steps.size() && p.steps[j].kind == 1; ++j)
             for (const auto &[a, b] : p.steps[j].swap_bits)
                 for (int &w : where) w = w == a ? b : w == b ? a : w;
+        // a permutation-only pass right after (the final local layout) joins
+        // when its coalescing run stays in this pass's tile: the input bits
+        // landing on the L lowest output bits are tile bits
+        if (j < p.steps.size() && perm_only(p.steps[j])) {
+            const std::vector<int> &op = p.passes[p.steps[j].pass].out_perm;
+            std::vector<int> w2 = where;
+            for (int &x : w2)
+                if (x < nl) x = op[x];
+            bool ok = true;
+            for (int b = 0; b < n && ok; ++b)
+                if (w2[b] < ph.L)
+                    ok = std::find(ph.tile_pos.begin(), ph.tile_pos.end(), b) != ph.tile_pos.end();
+            if (ok) {
+                where = w2;
+                ++j;
+            }
+        }
+        if (j == i) continue;
         ph.gperm = where;
         for (size_t k = i; k < j; ++k) p.steps[k].fused = true;
         i = j - 1;
@@ -126,6 +149,7 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         }
         return rem.size() + 1;
     };
+    std::vector<GateRec> last_seg; // the final front: planned once the layout restore is known
     while (!rem.empty()) {
         std::vector<int> blocked;
         std::vector<GateRec> seg; // the front, on physical bits (as admitted)
@@ -167,6 +191,10 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
                 seg.push_back(std::move(e));
             }
         }
+        if (blocked.empty()) {
+            last_seg = std::move(seg);
+            break;
+        }
         if (!seg.empty()) {
             auto passes = plan_passes(seg, ident, cfg, p.encs);
             for (auto &ph : passes) {
@@ -178,7 +206,6 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
             }
         }
         rem.swap(blocked);
-        if (rem.empty()) break;
         // swap in the rank-bit targets of the first blocked gate (it is blocked
         // only by them: everything before it has run), plus those of the next
         // blocked gates (look-ahead) while rank bits remain, in one step
@@ -253,12 +280,15 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
     const std::vector<int> canon = p.perm_in;
     std::vector<int> wire_of_canon(n);
     for (int w = 0; w < n; ++w) wire_of_canon[canon[w]] = w;
+    std::vector<int> where(n); // physical bit after the last gate -> after the restore
+    for (int b = 0; b < n; ++b) where[b] = b;
     auto do_swap = [&](Step &s, int a, int b) { // exchange physical bits a, b
         s.swap_bits.emplace_back(a, b);
         const int wa = wire_at[a], wb = wire_at[b];
         std::swap(phys[wa], phys[wb]);
         wire_at[a] = wb;
         wire_at[b] = wa;
+        for (int &x : where) x = x == a ? b : x == b ? a : x;
     };
     Step back;
     back.kind = 1;
@@ -273,30 +303,54 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         }
         do_swap(back, gb, x);
     }
-    if (!back.swap_bits.empty()) p.steps.push_back(std::move(back));
     // Phase B: local bits permuted among themselves. With relabeled swap
     // gates: one permutation-only pass (out of place, balanced read / write
     // runs); else local swap gates, expressed on PHYSICAL bits (identity
     // mapping) and fused into passes.
+    std::vector<int> out_perm;
     if (relabel) {
-        std::vector<int> out_perm(nl);
+        out_perm.assign(nl, 0);
         bool moved = false;
         for (int b = 0; b < nl; ++b) {
             out_perm[b] = canon[wire_at[b]];
             moved = moved || out_perm[b] != b;
         }
-        if (moved) {
-            PlanConfig c1 = cfg;
-            c1.super_bits = 0;
-            auto passes = plan_passes({}, ident, c1, p.encs, out_perm);
-            for (auto &ph : passes) {
-                Step st;
-                st.pass = static_cast<int>(p.passes.size());
-                p.passes.push_back(std::move(ph));
-                p.steps.push_back(std::move(st));
+        if (!moved) out_perm.clear();
+        for (int &x : where)
+            if (x < nl && !out_perm.empty()) x = out_perm[x];
+    }
+    // the final front, with the restore's coalescing run in its last tile
+    // when it fits: the input bits that land on the L lowest output bits
+    // (so the restore can be fused into it, fuse_swaps_into_passes)
+    if (!last_seg.empty()) {
+        uint64_t need = 0;
+        bool ok = relabel;
+        for (int b = 0; b < n && ok; ++b)
+            if (where[b] < cfg.L) {
+                if (b >= nl) ok = false;
+                else need |= 1ull << b;
             }
-            for (int w = 0; w < n; ++w) phys[w] = canon[w], wire_at[canon[w]] = w;
+        auto passes = plan_passes(last_seg, ident, cfg, p.encs, {}, ok ? need : 0);
+        for (auto &ph : passes) {
+            Step s;
+            s.kind = 0;
+            s.pass = static_cast<int>(p.passes.size());
+            p.passes.push_back(std::move(ph));
+            p.steps.push_back(std::move(s));
         }
+    }
+    if (!back.swap_bits.empty()) p.steps.push_back(std::move(back));
+    if (!out_perm.empty()) {
+        PlanConfig c1 = cfg;
+        c1.super_bits = 0;
+        auto passes = plan_passes({}, ident, c1, p.encs, out_perm);
+        for (auto &ph : passes) {
+            Step st;
+            st.pass = static_cast<int>(p.passes.size());
+            p.passes.push_back(std::move(ph));
+            p.steps.push_back(std::move(st));
+        }
+        for (int w = 0; w < n; ++w) phys[w] = canon[w], wire_at[canon[w]] = w;
     }
     std::vector<GateRec> fix;
     for (int w = 0; w < n; ++w) {
@@ -707,7 +761,7 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     bool fused_done = false; // the last pass also did the swap steps after it
     for (size_t i = 0; i < p.steps.size(); ++i) {
         const Step &stp = p.steps[i];
-        if (stp.kind == 1 && stp.fused && fused_done) continue;
+        if (stp.fused && fused_done) continue;
         fused_done = false;
         if (stp.kind == 0 && p.dev[stp.pass].pair) {
             require(!zout || i + 1 < p.steps.size(), "fused <Z>: not on a super-pass");
@@ -785,7 +839,7 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
     bool fused_done = false;
     for (const Step &stp : p.steps) {
         QSV_CUDA(cudaEventRecord(ev[2 * k], s));
-        const bool skip = stp.kind == 1 && stp.fused && fused_done;
+        const bool skip = stp.fused && fused_done;
         fused_done = false;
         if (skip) {
             fused_done = true;

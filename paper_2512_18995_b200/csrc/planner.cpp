@@ -774,7 +774,7 @@ void fold_uniform(PassHost &ph, cplx f) {
 
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const std::vector<int> &phys,
                                   const PlanConfig &cfg, std::vector<EncDesc> &encs,
-                                  const std::vector<int> &out_perm) {
+                                  const std::vector<int> &out_perm, uint64_t last_need) {
     std::vector<int> last_took;
     uint64_t last_active = 0;
     const int nl = cfg.nlocal;
@@ -935,6 +935,18 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             ph.out_perm = out_perm;
             passes.push_back(std::move(ph));
             how.push_back({{}, lowmask | need, true});
+        }
+    }
+    // Bits the caller wants in the last pass's tile (the coalescing run of a
+    // permutation fused into it later, plan.cpp fuse_swaps_into_passes):
+    // added when they fit and the pass has no output permutation of its own.
+    if (last_need && !passes.empty() && passes.back().out_perm.empty() && how.back().took.size() &&
+        std::popcount(how.back().active | last_need) <= K) {
+        const uint64_t act = how.back().active | last_need;
+        PassHost ph = lower_pass(gates, pg, how.back().took, act, phys, cfg, K, L, passes.back().R, encs);
+        if (pass_program_bytes(ph, cfg.dtype) <= static_cast<size_t>(kProgramBudget)) {
+            passes.back() = std::move(ph);
+            how.back().active = act;
         }
     }
     // L2 super-passes: pair consecutive passes whose two tiles span at most

@@ -343,7 +343,7 @@ std::vector<GateRec> fuse_single_qubit_runs(const std::vector<GateRec> &gates);
 // non-diagonal target local) to tile passes.
 std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates, const std::vector<int> &phys_of_wire,
                                   const PlanConfig &cfg, std::vector<EncDesc> &encs,
-                                  const std::vector<int> &out_perm = {});
+                                  const std::vector<int> &out_perm = {}, uint64_t last_need = 0);
 int default_tile_bits(int dtype, int nlocal);
 int default_low_bits(int dtype, int nlocal);
 

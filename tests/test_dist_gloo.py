@@ -115,6 +115,8 @@ def run_schedule(rank, world, sched, init_full, fused=False):
     fused_done = False
     for step in sched["steps"]:
         if step["kind"] == "pass":
+            if step["fused"] and fused_done:
+                continue
             for g in step["gates"]:
                 assert g["enc"] < 0
                 apply_phys(sl, g, rank, nl)
