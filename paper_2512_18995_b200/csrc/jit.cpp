@@ -340,10 +340,16 @@ JArgs make_args(const DevPass &dp, void *state, void *out, int rows) {
 void launch_tiles(const void *kern, const DevPass &dp, JArgs &a, int grid_cap, cudaStream_t s) {
     require(kern != nullptr, "jit: kernel variant not prepared");
     uint64_t grid = std::min<uint64_t>(a.total_tiles, static_cast<uint64_t>(std::max(grid_cap, 1)));
-    static const int tpc = [] {
+    // tiles per CTA: 4 on large states; small ones (a few tiles per
+    // resident CTA slot) need every tile in flight at once -- measured:
+    // cfg1 20q (512 tiles) 59 -> 51 us with 1, 22q (2048 tiles) best with 2,
+    // cfg2 (4096 tiles) and >= 24q best with 4
+    static const int tpc_env = [] {
         const char *e = std::getenv("QSV_TILES_PER_CTA");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : -1;
     }();
+    const uint64_t cap = static_cast<uint64_t>(std::max(grid_cap, 1));
+    const int tpc = tpc_env >= 0 ? tpc_env : a.total_tiles <= 2 * cap ? 1 : a.total_tiles <= 8 * cap ? 2 : 4;
     static const bool blocked = [] {
         const char *e = std::getenv("QSV_TILE_ORDER");
         return !(e && e[0] == 's');
