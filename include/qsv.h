@@ -96,7 +96,9 @@ typedef struct qsv_opts {
     int32_t fuse;           /* 1 = fused tile passes (default), 0 = one kernel per gate */
     int32_t tile_bits;      /* qubits per shared-memory tile (K) */
     int32_t low_bits;       /* lowest physical qubits always in a tile (coalescing) */
-    int32_t use_graph;      /* capture the pass sequence in a CUDA graph */
+    int32_t use_graph;      /* 1 = replay the launch sequence as a CUDA graph (one
+                               per state buffer pair and row count; single GPU,
+                               no encoded data): for launch-bound small states */
     int32_t no_fuse_1q;     /* 1 = keep runs of single-qubit gates unfused */
     int32_t no_phase_flush; /* 1 = apply every diagonal gate eagerly */
     int32_t jit;            /* 1 = specialised (NVRTC) pass kernels, -1 = interpreter, 0 = auto */

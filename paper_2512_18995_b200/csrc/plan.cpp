@@ -45,6 +45,8 @@ Plan::~Plan() {
     cudaFree(d_prefix_mats);
     cudaFree(d_prefix);
     cudaFree(d_sync);
+    for (auto &g : graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
 }
 
 namespace {
@@ -717,6 +719,75 @@ void upload_plan(Plan &p) {
     }
 }
 
+namespace {
+void execute_steps(Plan &p, State &st, const void *enc_table, int rows, double *zout);
+}
+
+// opts.use_graph: one CUDA graph per (state, its two buffers, rows) replays
+// the whole launch sequence (prefix, passes, super-pass memsets) -- one
+// launch instead of one per pass, for launch-bound small states. Single GPU,
+// no encoded data (its host upload is per call), no fused <Z> epilogue.
+bool execute_graph(Plan &p, State &st) {
+    if (!p.opts.use_graph || p.ctx->world != 1 || p.nslots != 0 || !p.ctx->stream) return false;
+    cudaStream_t s = p.ctx->stream;
+    bool oop = false;
+    for (const DevPass &dp : p.dev) oop = oop || dp.out_of_place;
+    if (oop) ensure_scratch(st);
+    for (size_t i = 0; i < p.passes.size(); ++i)
+        if (p.dev[i].pair == 1) { // counters sized before capture (no allocation inside)
+            const uint64_t nchunks = static_cast<uint64_t>(st.batch) << (p.nlocal - p.passes[i].chunk_bits);
+            const size_t bytes = (nchunks + 1) * sizeof(unsigned);
+            if (bytes > p.d_sync_cap) {
+                cudaFree(p.d_sync);
+                p.d_sync = nullptr;
+                QSV_CUDA(cudaMalloc(&p.d_sync, bytes));
+                p.d_sync_cap = bytes;
+            }
+        }
+    if (p.synth && static_cast<size_t>(st.batch) > p.prefix_rows) {
+        cudaFree(p.d_prefix);
+        p.d_prefix = nullptr;
+        QSV_CUDA(cudaMalloc(&p.d_prefix, static_cast<size_t>(st.batch) * p.nlocal * 2 * (p.dtype == QSV_C64 ? 8 : 16)));
+        p.prefix_rows = st.batch;
+    }
+    // the graph bakes the device pointers and the row count, nothing else
+    for (auto &g : p.graphs)
+        if (g.d == st.d && g.scratch == st.scratch && g.batch == st.batch) {
+            QSV_CUDA(cudaGraphLaunch(g.exec, s));
+            if (g.flips) {
+                std::swap(st.d, st.scratch);
+                st.p2p_cur ^= 1;
+            }
+            return true;
+        }
+    if (p.graphs.size() >= 8) { // states come and go: keep the newest few
+        cudaGraphExecDestroy(p.graphs.front().exec);
+        p.graphs.erase(p.graphs.begin());
+    }
+    Plan::Graph g;
+    g.d = st.d;
+    g.scratch = st.scratch;
+    g.batch = st.batch;
+    cudaGraph_t graph = nullptr;
+    QSV_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+    try {
+        if (p.synth) launch_prefix(p, st.batch, s);
+        execute_steps(p, st, nullptr, 0, nullptr);
+    } catch (...) {
+        cudaStreamEndCapture(s, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+    }
+    QSV_CUDA(cudaStreamEndCapture(s, &graph));
+    g.flips = st.d != g.d;
+    const cudaError_t rc = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    QSV_CUDA(rc);
+    QSV_CUDA(cudaGraphLaunch(g.exec, s)); // capture recorded the work; now run it
+    p.graphs.push_back(g);
+    return true;
+}
+
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout) {
     require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
     require(st.ctx == p.ctx, "plan/state belong to different contexts");
@@ -729,6 +800,7 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     }
     cudaStream_t s = p.ctx->stream;
     QSV_CUDA(cudaSetDevice(p.ctx->device));
+    if (zout == nullptr && rows == 0 && execute_graph(p, st)) return;
     const void *enc_table = nullptr;
     if (!p.encs.empty()) {
         const size_t dbytes = sizeof(double) * static_cast<size_t>(rows) * slots;
@@ -758,6 +830,12 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
         }
         launch_prefix(p, brows, s);
     }
+    execute_steps(p, st, enc_table, rows, zout);
+}
+
+namespace {
+void execute_steps(Plan &p, State &st, const void *enc_table, int rows, double *zout) {
+    cudaStream_t s = p.ctx->stream;
     bool fused_done = false; // the last pass also did the swap steps after it
     for (size_t i = 0; i < p.steps.size(); ++i) {
         const Step &stp = p.steps[i];
@@ -782,6 +860,7 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
         }
     }
 }
+} // namespace
 
 namespace {
 // The last step can carry the fused <Z> epilogue: a specialised, in-place

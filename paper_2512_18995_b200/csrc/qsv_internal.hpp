@@ -315,6 +315,14 @@ struct Plan {
     size_t d_z_cap = 0;
     void *d_sync = nullptr;    // L2 super-passes: per-chunk counters + the item ticket
     size_t d_sync_cap = 0;
+    // opts.use_graph: the launch sequence captured per (state buffers, rows)
+    struct Graph {
+        void *d = nullptr, *scratch = nullptr;
+        int batch = 0;
+        bool flips = false;      // the sequence ends with d and scratch exchanged
+        cudaGraphExec_t exec = nullptr;
+    };
+    std::vector<Graph> graphs;
     std::vector<DevPass> dev;
     qsv_opts opts{};
     ~Plan();

@@ -34,6 +34,12 @@ ms = timed(f1)
 ms_z = timed(lambda: (f1(), st.expect_z_all()), reps=10)
 print(f"cfg1 20q c128 {p.info['ngates']} gates passes={p.info['npasses']}: forward {ms:.3f} ms "
       f"({p.info['ngates'] / ms * 1e3:.0f} gates/s); forward + <Z_i> (host sync) {ms_z:.3f} ms", flush=True)
+pg = qsv.Plan(20, cir.gates(), dtype=qsv.C128, opts={"use_graph": 1})
+def f1g():
+    qsv.check(L.qsv_state_set_basis(st.h, 0)); pg.execute(st)
+ms = timed(f1g)
+print(f"cfg1 20q c128 as a CUDA graph (opts.use_graph): forward {ms:.3f} ms ({p.info['ngates'] / ms * 1e3:.0f} gates/s)",
+      flush=True)
 
 cir, data = W.cfg2_circuit()
 p = qsv.Plan(12, cir.gates(), dtype=qsv.C64)

@@ -392,3 +392,36 @@ def test_l2_super_passes_match_reference(dtype):
     for b in range(2):
         want = O.port_forward(n, cir.gates(), init=rows[b])[0]
         assert np.max(np.abs(st.amplitudes(b) - want)) <= TOL[dtype], b
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+def test_graph_replay_matches_stream_launches(dtype):
+    # opts.use_graph: the launch sequence captured once per (state buffers,
+    # rows) and replayed; permuting last passes flip the buffers, so replays
+    # alternate between two graphs -- every execute must equal the reference
+    rng = Rng(43, "graph")
+    n = 16
+    cir = random_circuit(rng, n, 90)
+    for i in range(n // 2):
+        cir.swap(i, n - 1 - i)  # relabelled: the last pass permutes out of place
+    psi = random_state(rng, n)
+    want1 = O.port_forward(n, cir.gates(), init=psi)[0]
+    want2 = O.port_forward(n, cir.gates(), init=want1)[0]
+    p = qsv.Plan(n, cir.gates(), dtype=dtype, opts={"jit": 1, "use_graph": 1})
+    st = QubitState(n, 2, dtype)
+    for b in range(2):
+        st.upload(psi, b)
+    for rep in range(3):  # capture, replay, replay (alternating buffer pairs)
+        for b in range(2):
+            st.upload(psi, b)
+        p.execute(st)
+        for b in range(2):
+            assert np.max(np.abs(st.amplitudes(b) - want1)) <= TOL[dtype], (rep, b)
+    p.execute(st)  # applied twice in a row
+    assert np.max(np.abs(st.amplitudes(0) - want2)) <= 10 * TOL[dtype]
+    # a from-|0> plan: the product-state prefix kernel is part of the graph
+    pz = qsv.Plan(n, cir.gates(), dtype=dtype, opts={"jit": 1, "use_graph": 1, "from_zero": 1})
+    wz = O.port_forward(n, cir.gates())[0]
+    for rep in range(2):
+        pz.execute(st)
+        assert np.max(np.abs(st.amplitudes(1) - wz)) <= TOL[dtype], rep
