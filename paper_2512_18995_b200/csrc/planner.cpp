@@ -455,12 +455,23 @@ struct GroupLowering {
                 const bool real = g.m[0].imag() == 0 && g.m[1].imag() == 0 && g.m[2].imag() == 0 &&
                                   g.m[3].imag() == 0;
                 if (real) op.code = OP_DENSE1R;
-                // c * (+-1 entries), e.g. h: apply the +-1 butterfly and defer c to
-                // one scale per pass (scalars commute with every gate)
-                const double c = std::abs(g.m[0].real());
+                // Tangent form: a real uncontrolled matrix is divided by its
+                // largest |entry| c, which is deferred to one scale per pass
+                // (scalars commute with every gate). Each row then holds a +-1,
+                // so an output costs one FMA per component instead of a
+                // multiply and an FMA: an orthogonal R = [[a, b], [b, -a]]
+                // becomes a * [[1, t], [t, -1]], t = b / a (or its mirror with
+                // 1 / t when |b| > |a|), and h becomes the +-1 butterfly.
+                // |t| <= 1, so a pass's deferred scale stays >= 2^-(gates / 2).
+                // QSV_X_NOTAN=1 keeps the h-only rule (all |entries| equal).
+                double c = 0.0;
+                for (int i = 0; i < 4; ++i) c = std::max(c, std::abs(g.m[i].real()));
+                const char *notan_env = std::getenv("QSV_X_NOTAN");
+                const bool notan = notan_env && notan_env[0] == '1';
+                bool all_eq = true;
+                for (int i = 1; i < 4; ++i) all_eq = all_eq && std::abs(g.m[i].real()) == std::abs(g.m[0].real());
                 if (real && c != 0.0 && c != 1.0 && !(op.flags & OPF_ZERO_OFF_CONTROL) && op.rmask == 0 &&
-                    op.fmask == 0 && std::abs(g.m[1].real()) == c && std::abs(g.m[2].real()) == c &&
-                    std::abs(g.m[3].real()) == c) {
+                    op.fmask == 0 && (all_eq || !notan)) {
                     for (auto &x : op.pay) x /= c;
                     ph.scale *= c;
                 }
