@@ -125,6 +125,7 @@ int kernel_min_blocks(const PassHost &ph, int threads) {
 struct Gen {
     const PassHost &ph;
     bool f32;
+    bool packed; // complex64 arithmetic on f32x2 pairs (QSV_X_NOPACK=1: scalar FP32)
     int R;
     std::ostringstream o;
     std::string T, V;
@@ -132,6 +133,8 @@ struct Gen {
     Gen(const PassHost &p, int dtype) : ph(p), f32(dtype == QSV_C64), R(p.R) {
         T = f32 ? "float" : "double";
         V = f32 ? "cf" : "cd";
+        const char *np = std::getenv("QSV_X_NOPACK");
+        packed = f32 && !(np && np[0] == '1');
     }
 
     std::string c(double x) const { return lit(x, f32); }
@@ -226,12 +229,44 @@ struct Gen {
         return s;
     }
 
+    // complex64: sum_k m_k x_k as a chain of packed f32x2 operations (the
+    // helpers of common()): a real coefficient is one FMUL2/FFMA2, a complex
+    // one two (the i*x half reads x with its halves swapped, which ptxas
+    // folds into the operand), +-1 an FADD2.
+    std::string packed_sum(const std::vector<std::pair<cplx, std::string>> &ts) const {
+        std::string acc;
+        for (const auto &t : ts) {
+            const double a = snap(t.first.real()), b = snap(t.first.imag());
+            if (a == 0.0 && b == 0.0) continue;
+            const std::string &x = t.second;
+            if (acc.empty()) {
+                if (b == 0.0) acc = a == 1.0 ? x : a == -1.0 ? "cneg(" + x + ")" : "rmul(" + x + ", " + c(a) + ")";
+                else if (a == 0.0) acc = "imul(" + x + ", " + c(b) + ")";
+                else acc = "cmc(" + x + ", " + c(a) + ", " + c(b) + ")";
+            } else {
+                if (b == 0.0)
+                    acc = a == 1.0    ? "cadd(" + acc + ", " + x + ")"
+                          : a == -1.0 ? "csub(" + acc + ", " + x + ")"
+                                      : "rfma(" + acc + ", " + x + ", " + c(a) + ")";
+                else if (a == 0.0) acc = "ifma(" + acc + ", " + x + ", " + c(b) + ")";
+                else acc = "cfc(" + acc + ", " + x + ", " + c(a) + ", " + c(b) + ")";
+            }
+        }
+        return acc.empty() ? "mk(0, 0)" : acc;
+    }
+
     // v[r] = sum_k M[row][k] * x[k]
     void matvec(const std::vector<int> &regs, const std::vector<cplx> &m, int d, const std::string &ind) {
         o << ind << "{ ";
         for (int k = 0; k < d; ++k) o << "const " << V << " x" << k << " = v" << regs[k] << "; ";
         o << "\n";
         for (int r = 0; r < d; ++r) {
+            if (packed) {
+                std::vector<std::pair<cplx, std::string>> ts;
+                for (int k = 0; k < d; ++k) ts.emplace_back(m[r * d + k], "x" + std::to_string(k));
+                o << ind << "  v" << regs[r] << " = " << packed_sum(ts) << ";\n";
+                continue;
+            }
             std::vector<std::string> re, im;
             for (int k = 0; k < d; ++k) term(m[r * d + k], "x" + std::to_string(k), re, im);
             o << ind << "  v" << regs[r] << " = mk(" << sum(re) << ", " << sum(im) << ");\n";
@@ -241,9 +276,19 @@ struct Gen {
 
     void cmul_const(int r, const cplx &f, const std::string &ind) {
         if (snap(f.real()) == 1.0 && snap(f.imag()) == 0.0) return;
+        if (packed) {
+            o << ind << "v" << r << " = " << packed_sum({{f, "v" + std::to_string(r)}}) << ";\n";
+            return;
+        }
         std::vector<std::string> re, im;
         term(f, "v" + std::to_string(r), re, im);
         o << ind << "v" << r << " = mk(" << sum(re) << ", " << sum(im) << ");\n";
+    }
+
+    // x scaled by a real constant
+    std::string rscale(const std::string &x, double k) const {
+        if (packed) return "rmul(" + x + ", " + c(k) + ")";
+        return "mk(" + c(k) + "*" + x + ".x, " + c(k) + "*" + x + ".y)";
     }
 
     std::string fcond(uint64_t fmask, uint64_t fval) {
@@ -462,8 +507,7 @@ struct Gen {
         if (uniform) rc = op.regtab[0].real();
         if (nfac[R]) {
             root = "g" + std::to_string(R);
-            if (rc != 1.0) o << in << root << " = mk(" << c(rc) << "*" << root << ".x, " << c(rc) << "*" << root
-                             << ".y);\n";
+            if (rc != 1.0) o << in << root << " = " << rscale(root, rc) << ";\n";
         }
         int nph = 0;
         // ph: variable holding the product for slot r ("" = identity), or the
@@ -471,7 +515,7 @@ struct Gen {
         std::function<void(int, const std::string &, bool)> visit = [&](int r, const std::string &p, bool scaled) {
             if (!p.empty()) o << in << "v" << r << " = cmulv(v" << r << ", " << p << ");\n";
             else if (scaled && rc != 1.0)
-                o << in << "v" << r << " = mk(" << c(rc) << "*v" << r << ".x, " << c(rc) << "*v" << r << ".y);\n";
+                o << in << "v" << r << " = " << rscale("v" + std::to_string(r), rc) << ";\n";
             const int top = r ? 64 - __builtin_clzll(static_cast<unsigned long long>(r)) : 0;
             for (int b = top; b < R; ++b) {
                 const int ch = r | (1 << b);
@@ -486,8 +530,7 @@ struct Gen {
                     o << in << V << " " << q << " = cmulv(" << p << ", " << gb << ");\n";
                 } else if (scaled && rc != 1.0) {
                     q = "p" + std::to_string(nph++);
-                    o << in << V << " " << q << " = mk(" << c(rc) << "*" << gb << ".x, " << c(rc) << "*" << gb
-                      << ".y);\n";
+                    o << in << V << " " << q << " = " << rscale(gb, rc) << ";\n";
                 } else q = gb;
                 visit(ch, q, false);
             }
@@ -506,10 +549,37 @@ struct Gen {
         c << "struct __align__(" << (f32 ? 8 : 16) << ") " << V << " { " << T << " x, y; };\n";
         c << "static __device__ __forceinline__ " << V << " mk(" << T << " x, " << T << " y) { " << V
           << " r; r.x = x; r.y = y; return r; }\n";
-        c << "static __device__ __forceinline__ " << V << " cmulv(" << V << " a, " << V
-          << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
-        c << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
-          << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
+        if (packed) {
+            // complex64 arithmetic on packed f32x2 registers (FFMA2 / FMUL2 /
+            // FADD2, sm_100a): (a + ib) x = a (x.x, x.y) + b (-x.y, x.x), the
+            // swapped and sign-flipped halves fold into the operand modifiers
+            c << "#define QD static __device__ __forceinline__\n"
+                 "QD u64 pk(float a, float b) { u64 r; asm(\"mov.b64 %0, {%1,%2};\" : \"=l\"(r) : \"f\"(a), \"f\"(b)); return r; }\n"
+                 "QD u64 pv(cf v) { return pk(v.x, v.y); }\n"
+                 "QD u64 bc(float k) { return pk(k, k); }\n"
+                 "QD cf up(u64 r) { cf v; asm(\"mov.b64 {%0,%1}, %2;\" : \"=f\"(v.x), \"=f\"(v.y) : \"l\"(r)); return v; }\n"
+                 "QD u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm(\"fma.rn.f32x2 %0, %1, %2, %3;\" : \"=l\"(r) : \"l\"(a), \"l\"(b), \"l\"(c)); return r; }\n"
+                 "QD u64 mul2(u64 a, u64 b) { u64 r; asm(\"mul.rn.f32x2 %0, %1, %2;\" : \"=l\"(r) : \"l\"(a), \"l\"(b)); return r; }\n"
+                 "QD u64 add2(u64 a, u64 b) { u64 r; asm(\"add.rn.f32x2 %0, %1, %2;\" : \"=l\"(r) : \"l\"(a), \"l\"(b)); return r; }\n"
+                 "QD u64 sub2(u64 a, u64 b) { u64 r; asm(\"sub.rn.f32x2 %0, %1, %2;\" : \"=l\"(r) : \"l\"(a), \"l\"(b)); return r; }\n"
+                 "QD cf cneg(cf x) { return mk(-x.x, -x.y); }\n"
+                 "QD cf cadd(cf a, cf x) { return up(add2(pv(a), pv(x))); }\n"
+                 "QD cf csub(cf a, cf x) { return up(sub2(pv(a), pv(x))); }\n"
+                 "QD cf rmul(cf x, float k) { return up(mul2(bc(k), pv(x))); }\n"
+                 "QD cf rfma(cf a, cf x, float k) { return up(fma2(bc(k), pv(x), pv(a))); }\n"
+                 "QD u64 pn(cf v) { return pk(-v.y, v.x); }\n"
+                 "QD cf imul(cf x, float k) { return up(mul2(bc(k), pn(x))); }\n"
+                 "QD cf ifma(cf a, cf x, float k) { return up(fma2(bc(k), pn(x), pv(a))); }\n"
+                 "QD cf cmc(cf x, float re, float im) { return up(fma2(bc(im), pn(x), mul2(bc(re), pv(x)))); }\n"
+                 "QD cf cfc(cf a, cf x, float re, float im) { return up(fma2(bc(im), pn(x), fma2(bc(re), pv(x), pv(a)))); }\n"
+                 "QD cf cmulv(cf a, cf b) { return cmc(b, a.x, a.y); }\n"
+                 "QD cf cfmav(cf a, cf b, cf c) { return cfc(c, b, a.x, a.y); }\n";
+        } else {
+            c << "static __device__ __forceinline__ " << V << " cmulv(" << V << " a, " << V
+              << " b) { return mk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x); }\n";
+            c << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
+              << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
+        }
         // streaming (evict-first) 8/16-byte amplitude loads and stores; stwb:
         // a plain write-back store (the first pass of an L2 super-pass keeps
         // its output in L2 for the second)
