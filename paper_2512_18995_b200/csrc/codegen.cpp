@@ -126,6 +126,17 @@ struct Gen {
     const PassHost &ph;
     bool f32;
     bool packed; // complex64 arithmetic on f32x2 pairs (QSV_X_NOPACK=1: scalar FP32)
+    // Deferred per-register real scales (QSV_X_NOSCALE=1: off). Register r
+    // holds sc[r]^-1 times its amplitude: a constant phase p = d (1 + i t)
+    // costs one FMA per component (the real d joins sc[r]), a real matrix
+    // absorbs the scales of its inputs and leaves each output row divided by
+    // its largest entry (one +-1 term per row). Runtime complex factors
+    // commute with the scales; they are multiplied in by the group's last
+    // constant multiply or before its stores.
+    bool track = true;
+    bool untracked = false; // inside a runtime-conditional op
+    bool final_op = false;  // emitting the group's last op
+    std::vector<double> sc;
     int R;
     std::ostringstream o;
     std::string T, V;
@@ -135,6 +146,18 @@ struct Gen {
         V = f32 ? "cf" : "cd";
         const char *np = std::getenv("QSV_X_NOPACK");
         packed = f32 && !(np && np[0] == '1');
+        const char *ns = std::getenv("QSV_X_NOSCALE");
+        track = !(ns && ns[0] == '1');
+        sc.assign(static_cast<size_t>(1) << R, 1.0);
+    }
+
+    // multiplies the pending scales of the registers in `mask` into them
+    void materialize(const std::string &ind, uint64_t mask = ~0ull) {
+        for (size_t r = 0; r < sc.size(); ++r)
+            if (((mask >> r) & 1) && sc[r] != 1.0) {
+                o << ind << "v" << r << " = " << rscale("v" + std::to_string(r), sc[r]) << ";\n";
+                sc[r] = 1.0;
+            }
     }
 
     std::string c(double x) const { return lit(x, f32); }
@@ -256,7 +279,29 @@ struct Gen {
     }
 
     // v[r] = sum_k M[row][k] * x[k]
-    void matvec(const std::vector<int> &regs, const std::vector<cplx> &m, int d, const std::string &ind) {
+    void matvec(const std::vector<int> &regs, const std::vector<cplx> &m_in, int d, const std::string &ind) {
+        std::vector<cplx> m = m_in;
+        if (track && !untracked) {
+            // absorb the input scales, then divide every all-real row by its
+            // largest |entry| (the divisor becomes that output's scale)
+            for (int r = 0; r < d; ++r)
+                for (int k = 0; k < d; ++k) m[r * d + k] *= sc[regs[k]];
+            std::vector<double> out(d, 1.0);
+            for (int r = 0; r < d; ++r) {
+                bool real = true;
+                double big = 0.0, sgn = 1.0;
+                for (int k = 0; k < d; ++k) {
+                    const cplx &e = m[r * d + k];
+                    real = real && e.imag() == 0.0;
+                    if (std::abs(e.real()) > big) big = std::abs(e.real()), sgn = e.real() < 0 ? -1.0 : 1.0;
+                }
+                if (real && big != 0.0) {
+                    out[r] = big * sgn;
+                    for (int k = 0; k < d; ++k) m[r * d + k] /= out[r];
+                }
+            }
+            for (int r = 0; r < d; ++r) sc[regs[r]] = out[r];
+        }
         o << ind << "{ ";
         for (int k = 0; k < d; ++k) o << "const " << V << " x" << k << " = v" << regs[k] << "; ";
         o << "\n";
@@ -274,8 +319,32 @@ struct Gen {
         o << ind << "}\n";
     }
 
-    void cmul_const(int r, const cplx &f, const std::string &ind) {
+    void cmul_const(int r, const cplx &f_in, const std::string &ind) {
+        cplx f = f_in;
+        if (track) {
+            f *= sc[r];
+            sc[r] = 1.0;
+            const double a = f.real(), b = f.imag();
+            if (!final_op && !untracked) {
+                // f = d (1 + i t) or d (t + i), |t| <= 1; d joins the scale
+                if (b == 0.0 || std::abs(a) >= std::abs(b)) {
+                    sc[r] = a;
+                    f = cplx(1.0, b / a);
+                } else {
+                    sc[r] = b;
+                    f = cplx(a / b, 1.0);
+                }
+            }
+        }
         if (snap(f.real()) == 1.0 && snap(f.imag()) == 0.0) return;
+        if (packed && snap(f.real()) == 1.0) {
+            o << ind << "v" << r << " = cti(v" << r << ", " << c(f.imag()) << ");\n";
+            return;
+        }
+        if (packed && snap(f.imag()) == 1.0) {
+            o << ind << "v" << r << " = cit(v" << r << ", " << c(f.real()) << ");\n";
+            return;
+        }
         if (packed) {
             o << ind << "v" << r << " = " << packed_sum({{f, "v" + std::to_string(r)}}) << ";\n";
             return;
@@ -330,6 +399,17 @@ struct Gen {
         if (op.code == OP_FLUSH) {
             emit_flush(op, ind);
             return;
+        }
+        // a runtime condition (or a runtime matrix) makes the op's effect on
+        // the scales unknown at generation time: it sees materialised registers
+        struct Untrack {
+            bool &u;
+            bool prev;
+            ~Untrack() { u = prev; }
+        } untrack{untracked, untracked};
+        if (track && (fc || enc)) {
+            materialize(ind);
+            untracked = true;
         }
         if (fc && !zoc) {
             o << ind << "if " << fcond(op.fmask, op.fval) << " {\n";
@@ -505,6 +585,11 @@ struct Gen {
         std::string root;
         double rc = 1.0;
         if (uniform) rc = op.regtab[0].real();
+        if (track && uniform && rc != 1.0) {
+            for (double &x : sc) x *= rc;
+            rc = 1.0;
+            if (final_op) materialize(ind);
+        }
         if (nfac[R]) {
             root = "g" + std::to_string(R);
             if (rc != 1.0) o << in << root << " = " << rscale(root, rc) << ";\n";
@@ -572,6 +657,8 @@ struct Gen {
                  "QD cf ifma(cf a, cf x, float k) { return up(fma2(bc(k), pn(x), pv(a))); }\n"
                  "QD cf cmc(cf x, float re, float im) { return up(fma2(bc(im), pn(x), mul2(bc(re), pv(x)))); }\n"
                  "QD cf cfc(cf a, cf x, float re, float im) { return up(fma2(bc(im), pn(x), fma2(bc(re), pv(x), pv(a)))); }\n"
+                 "QD cf cti(cf x, float t) { return up(fma2(bc(t), pn(x), pv(x))); }\n"
+                 "QD cf cit(cf x, float t) { return up(fma2(bc(t), pv(x), pn(x))); }\n"
                  "QD cf cmulv(cf a, cf b) { return cmc(b, a.x, a.y); }\n"
                  "QD cf cfmav(cf a, cf b, cf c) { return cfc(c, b, a.x, a.y); }\n";
         } else {
@@ -1017,8 +1104,14 @@ struct Gen {
                 const char *e = std::getenv("QSV_DEBUG_NOCOMPUTE");
                 return e && e[0] == '1';
             }();
+            std::fill(sc.begin(), sc.end(), 1.0);
             if (!nocompute)
-                for (int oi = g.op_begin; oi < g.op_end; ++oi) emit_op(ph.ops[oi], "      ");
+                for (int oi = g.op_begin; oi < g.op_end; ++oi) {
+                    final_op = oi == g.op_end - 1;
+                    emit_op(ph.ops[oi], "      ");
+                }
+            final_op = false;
+            materialize("      ");
             if (zhere) {
                 o << "      { double zt = 0.0";
                 for (int j = 0; j < R; ++j) o << ", zs" << j << " = 0.0";
