@@ -321,7 +321,7 @@ struct Gen {
 
     void cmul_const(int r, const cplx &f_in, const std::string &ind) {
         cplx f = f_in;
-        if (track) {
+        if (track && !untracked) {
             f *= sc[r];
             sc[r] = 1.0;
             const double a = f.real(), b = f.imag();
@@ -408,7 +408,23 @@ struct Gen {
             ~Untrack() { u = prev; }
         } untrack{untracked, untracked};
         if (track && (fc || enc)) {
-            materialize(ind);
+            // equal scales commute with any linear map of the registers they
+            // share, so only a pair / quad with unequal scales is materialised;
+            // per-register (diagonal) factors commute with every scale
+            std::vector<int> touched;
+            if (op.code == OP_DENSE1 || op.code == OP_DENSE1R || op.code == OP_X1) touched = {0, 1 << op.a};
+            else if (op.code == OP_DENSE2) touched = {0, 1 << op.b, 1 << op.a, (1 << op.a) | (1 << op.b)};
+            const int span = touched.empty() ? 0 : touched.back();
+            for (int r = 0; r < NR && !touched.empty(); ++r) {
+                if (r & span) continue;
+                uint64_t mask = 0;
+                bool same = true;
+                for (int t : touched) {
+                    mask |= 1ull << (r | t);
+                    same = same && sc[r | t] == sc[r];
+                }
+                if (!same) materialize(ind, mask);
+            }
             untracked = true;
         }
         if (fc && !zoc) {
