@@ -880,24 +880,18 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
         }
         require(!took.empty(), "planner: no progress");
         size_t first_encs = encs.size();
-        if (cfg.R <= 0) { // auto: 4-qubit groups unless dense math dominates (register
-                          // pressure, and straight-line code size: 2^R slots per op)
-            bool heavy = false;
-            int nondiag = 0;
-            for (int i : took) nondiag += !gates[i].diag;
-            if (nondiag > K) heavy = true;
-            for (int i : took) {
-                const GateRec &g = gates[i];
-                if (g.diag) continue;
-                const int d = 1 << g.k;
-                bool complex_m = g.encoded;
-                for (int q = 0; q < d * d && !complex_m; ++q) complex_m = g.m[q].imag() != 0.0;
-                bool perm = !g.encoded;
-                for (int q = 0; q < d * d && perm; ++q)
-                    perm = g.m[q] == cplx(0, 0) || g.m[q] == cplx(1, 0);
-                if (complex_m || (g.k == 2 && !perm)) heavy = true;
-            }
-            R = std::min(heavy ? 3 : 4, K);
+        if (cfg.R <= 0) {
+            // auto: 4-qubit groups for complex128, 3-qubit groups for
+            // complex64. With the tangent form and per-register scales the
+            // c128 passes are FP64-bound and fewer groups (fewer shared-tile
+            // round trips, longer runs of deferred phases) win; the packed
+            // c64 passes are FMA-bound and a 16-register set costs more in
+            // flushes than it saves. Interleaved A/B at 28q against the
+            // earlier rule (3 when a pass held complex or dense 2-qubit
+            // matrices or more non-diagonal gates than tile qubits, else 4):
+            // cfg4 family 12.17 -> 11.52 ms, cfg5 family 7.72 -> 7.39 ms, QFT
+            // unchanged (it was already 4).
+            R = std::min(cfg.dtype == QSV_C64 ? 3 : 4, K);
         }
         PassHost ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         // keep the program within the shared-memory budget: give the tail of
