@@ -425,3 +425,25 @@ def test_graph_replay_matches_stream_launches(dtype):
     for rep in range(2):
         pz.execute(st)
         assert np.max(np.abs(st.amplitudes(1) - wz)) <= TOL[dtype], rep
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
+@pytest.mark.parametrize("variant", ["", "QSV_X_NOPACK", "QSV_X_NOSCALE", "QSV_X_NOTAN", "QSV_X_NOSPLIT"])
+@pytest.mark.parametrize("reg_slots", [0, 2, 3, 4])
+def test_generated_arithmetic_variants(dtype, variant, reg_slots, monkeypatch):
+    """The generated kernels' arithmetic forms -- tangent-form real matrices
+    (planner.cpp lower), per-register deferred scales and packed f32x2
+    complex64 (codegen.cpp) -- each switched off in turn, at every register
+    group size, on circuits with controls on register slots, tile bits and
+    bits outside the tile (runtime-conditional ops), against the oracle."""
+    if variant:
+        monkeypatch.setenv(variant, "1")
+    rng = Rng(77, "arith-variants")
+    n = 15
+    psi = random_state(rng, n)
+    gates = [random_gate(rng, n) for _ in range(90)]
+    fam = W.cfg4_circuit(n, 2).gates() + W.cfg5_circuit(n, 2).gates()
+    for gs in (gates, fam):
+        got, _ = run(n, gs, init=psi, dtype=dtype, opts={"jit": 1, "reg_slots": reg_slots})
+        want = O.port_forward(n, gs, init=psi)[0]
+        assert np.max(np.abs(got[0] - want)) <= TOL[dtype]
