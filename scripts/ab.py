@@ -33,7 +33,9 @@ res = {v: [] for v in variants}
 for rep in range(int(os.environ.get("AB_REPS", "20"))):
     for v, p in zip(variants, plans):
         p.profile(st)
-        res[v].append(p.profile(st)[: p.info["npasses"]])
+        # one entry per plan step: the second half of an L2 super-pass pair
+        # is an empty step (its work is timed in the first), so keep them all
+        res[v].append(p.profile(st))
 for v in variants:
     m = np.array(res[v])
     print(f"{cfg} n={n} [{v or 'default'}] median total {np.median(m.sum(1)):.3f} ms  min {m.sum(1).min():.3f}  "
