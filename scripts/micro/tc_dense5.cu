@@ -47,31 +47,35 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
-// K-major, no swizzle: element (row, k) of an operand with K = 64
-// (8-row x 16-byte core matrices; LBO = 128 B between the K chunks of one
-// core-matrix row group, SBO = 2048 B between 8-row groups)
+// K-major, 128-byte swizzle: an atom is 8 rows x 128 B (32 TF32 along K),
+// 16-byte chunk c of row r stored at chunk c ^ (r & 7); K = 64 is two atom
+// columns, the second ROWS / 8 atoms after the first. Lanes writing 8
+// consecutive chunks of one row hit 8 distinct bank groups.
+template <int ROWS>
 __device__ __forceinline__ uint32_t kmaj_off(int row, int chunk) {
-    return (row & 7) * 16 + (row >> 3) * 2048 + chunk * 128;
+    return (chunk >> 3) * (ROWS / 8) * 1024 + (row >> 3) * 1024 + (row & 7) * 128 + (((chunk & 7) ^ (row & 7)) << 4);
 }
 
 // input chunk (set row, 16-byte chunk c) handled by thread t at step j:
 // lanes 0..7 take the 8 rows of one core matrix (one 128-byte shared-memory
 // line per 8-lane phase: conflict-free), the 4 lane octets and 4 warps cover
 // the 16 row groups, the 16 steps the 16 chunks
-__device__ __forceinline__ int in_row(int t, int j) { return (t & 7) + 8 * (t >> 3); }
-__device__ __forceinline__ int in_chunk(int t, int j) { return j; }
-__device__ __forceinline__ float4 ld_in(const float4 *base, int t, int j) {
-    return __ldg(base + in_row(t, j) * 16 + in_chunk(t, j));
-}
+__device__ __forceinline__ int in_row(int t, int j) { return (t + 128 * j) >> 4; }
+__device__ __forceinline__ int in_chunk(int t, int j) { return (t + 128 * j) & 15; }
+__device__ __forceinline__ float4 ld_in(const float4 *base, int t, int j) { return __ldcs(base + t + 128 * j); }
 
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((addr >> 4) & 0x3fff);
-    d |= static_cast<uint64_t>((128 >> 4) & 0x3fff) << 16;   // LBO
-    d |= static_cast<uint64_t>((2048 >> 4) & 0x3fff) << 32;  // SBO
+    d |= 1ull << 16;                                          // LBO (unused with swizzle)
+    d |= static_cast<uint64_t>((1024 >> 4) & 0x3fff) << 32;  // SBO: 8-row atoms 1 KiB apart
     d |= 1ull << 46;                                          // version (sm_100)
-    return d;                                                 // layout type 0 = SWIZZLE_NONE
+    d |= 2ull << 61;                                          // SWIZZLE_128B
+    return d;
 }
+// start of MMA k-step ks (K = 8 TF32 = 32 B) of an operand with ROWS rows
+template <int ROWS>
+__device__ __forceinline__ uint32_t kstep(int ks) { return (ks >> 2) * (ROWS / 8) * 1024 + (ks & 3) * 32; }
 
 __device__ __forceinline__ float tf32_hi(float x) {
     uint32_t r;
@@ -79,32 +83,41 @@ __device__ __forceinline__ float tf32_hi(float x) {
     return __uint_as_float(r);
 }
 
-__global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ in, float4 *__restrict__ out,
-                                                    const float *__restrict__ Bg, uint64_t nsets_total) {
-    extern __shared__ __align__(1024) unsigned char sm[];
-    unsigned char *Ahi = sm, *Alo = sm + kAbytes, *Bhi = sm + 2 * kAbytes, *Blo = Bhi + kBbytes;
-    __shared__ uint64_t mbar;
+// G warpgroups per CTA share B; each has its own A hi / lo, TMEM columns and
+// mbarrier and runs the load / split / MMA / drain loop on its own sets
+template <int G>
+__global__ void __launch_bounds__(128 * G, G == 1 ? 2 : 1) tc_kernel(const float4 *__restrict__ in,
+                                                                    float4 *__restrict__ out,
+                                                                    const float *__restrict__ Bg,
+                                                                    uint64_t nsets_total) {
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char *sm = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);  // swizzle atoms need 1 KiB alignment
+    const int g = threadIdx.x >> 7, t = threadIdx.x & 127, warp = t >> 5;
+    unsigned char *Ahi = sm + g * 2 * kAbytes, *Alo = Ahi + kAbytes, *Bhi = sm + G * 2 * kAbytes,
+                  *Blo = Bhi + kBbytes;
+    constexpr uint32_t kCols = G == 1 ? 64 : G == 2 ? 128 : 256;
+    __shared__ uint64_t mbars[G];
+    uint64_t &mbar = mbars[g];
     __shared__ uint32_t tmem_base;
-    const int t = threadIdx.x, warp = t >> 5;
     // B hi / lo (row n = output, k contiguous)
-    for (int q = t; q < kN * kK / 4; q += 128) {
+    for (int q = threadIdx.x; q < kN * kK / 4; q += 128 * G) {
         const int n = q / (kK / 4), c = q % (kK / 4);
         float4 v = reinterpret_cast<const float4 *>(Bg)[q];
         float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
         float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
-        *reinterpret_cast<float4 *>(Bhi + kmaj_off(n, c)) = h;
-        *reinterpret_cast<float4 *>(Blo + kmaj_off(n, c)) = l;
+        *reinterpret_cast<float4 *>(Bhi + kmaj_off<kN>(n, c)) = h;
+        *reinterpret_cast<float4 *>(Blo + kmaj_off<kN>(n, c)) = l;
     }
-    if (warp == 0) {
+    if (threadIdx.x < 32) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
-                     "r"(64));
+                     "r"(kCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;");
-    const uint32_t tmem = tmem_base;
+    const uint32_t tmem = tmem_base + g * 64;
     // kind::tf32, D f32, A/B tf32 K-major, N = 64, M = 128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((128 >> 4) << 24);
     uint32_t phase = 0;
@@ -112,23 +125,24 @@ __global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ i
     // software pipeline: the next iteration's 32 KiB are loaded into
     // registers while this iteration's MMAs and output stores run
     float4 v[16];
-    uint64_t it = blockIdx.x;
+    const uint64_t step = static_cast<uint64_t>(gridDim.x) * G;
+    uint64_t it = static_cast<uint64_t>(blockIdx.x) * G + g;
     if (it < iters) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = ld_in(in + it * (kSets * kK / 4), t, j);
     }
-    for (; it < iters; it += gridDim.x) {
+    for (; it < iters; it += step) {
         // chunk q = t + 128 j = (set m, 4-real chunk c), split into hi / lo
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
             const int m = in_row(t, j), c = in_chunk(t, j);
             float4 h = make_float4(tf32_hi(v[j].x), tf32_hi(v[j].y), tf32_hi(v[j].z), tf32_hi(v[j].w));
             float4 l = make_float4(v[j].x - h.x, v[j].y - h.y, v[j].z - h.z, v[j].w - h.w);
-            *reinterpret_cast<float4 *>(Ahi + kmaj_off(m, c)) = h;
-            *reinterpret_cast<float4 *>(Alo + kmaj_off(m, c)) = l;
+            *reinterpret_cast<float4 *>(Ahi + kmaj_off<kSets>(m, c)) = h;
+            *reinterpret_cast<float4 *>(Alo + kmaj_off<kSets>(m, c)) = l;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncthreads();
+        asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory");
         if (t == 0) {
             asm volatile("tcgen05.fence::after_thread_sync;");
             const unsigned char *As[3] = {Ahi, Ahi, Alo};
@@ -136,8 +150,8 @@ __global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ i
             int acc = 0;
             for (int p = 0; p < 3; ++p)
                 for (int ks = 0; ks < kK / 8; ++ks) {
-                    const uint64_t ad = sdesc(smem_u32(As[p]) + ks * 256);
-                    const uint64_t bd = sdesc(smem_u32(Bs[p]) + ks * 256);
+                    const uint64_t ad = sdesc(smem_u32(As[p]) + kstep<kSets>(ks));
+                    const uint64_t bd = sdesc(smem_u32(Bs[p]) + kstep<kN>(ks));
                     asm volatile(
                         "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
@@ -147,9 +161,9 @@ __global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ i
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                 smem_u32(&mbar)));
         }
-        if (it + gridDim.x < iters) {
+        if (it + step < iters) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) v[j] = ld_in(in + (it + gridDim.x) * (kSets * kK / 4), t, j);
+            for (int j = 0; j < 16; ++j) v[j] = ld_in(in + (it + step) * (kSets * kK / 4), t, j);
         }
         // wait for the MMAs (bounded spin: a wrong descriptor must not hang the box)
         {
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ i
         for (int c = 0; c < 16; ++c)
             stg[t * 16 + (c ^ (t & 15))] = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
                                                        __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
-        __syncthreads();
+        asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory");
         float4 *dst = out + it * (kSets * kK / 4);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -198,11 +212,12 @@ __global__ void __launch_bounds__(128, 2) tc_kernel(const float4 *__restrict__ i
         // the next iteration overwrites A: every thread's TMEM read is done
         // and no MMA is in flight (waited above)
         asm volatile("tcgen05.fence::before_thread_sync;");
-        __syncthreads();
+        asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory");
     }
     asm volatile("tcgen05.fence::after_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(64));
+    if (threadIdx.x < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kCols));
 }
 
 // CUDA cores: thread = one set, D[n] = sum_k B[n][k] x[k] (B from shared memory)
@@ -266,8 +281,9 @@ int main(int argc, char **argv) {
             CK(cudaMemcpy(din + off, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
         }
     }
-    const int smem = 2 * kAbytes + 2 * kBbytes;
-    CK(cudaFuncSetAttribute(tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int smem = 2 * kAbytes + 2 * kBbytes + 1024, smem3 = 3 * 2 * kAbytes + 2 * kBbytes + 1024;
+    CK(cudaFuncSetAttribute(tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    CK(cudaFuncSetAttribute(tc_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem3));
     cudaEvent_t e0, e1;
     CK(cudaEventCreate(&e0));
     CK(cudaEventCreate(&e1));
@@ -292,7 +308,10 @@ int main(int argc, char **argv) {
     std::vector<float> got_fma(64 * 64 * 4);
     CK(cudaMemcpy(got_fma.data(), dout, got_fma.size() * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemset(dout, 0, namp * 8));
-    timeit("tc", [&] { tc_kernel<<<sms * 2, 128, smem>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 256.0);
+    timeit("tc", [&] { tc_kernel<1><<<sms * 2, 128, smem>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 256.0);
+    CK(cudaGetLastError());
+    CK(cudaMemset(dout, 0, namp * 8));
+    timeit("tc3", [&] { tc_kernel<3><<<sms, 384, smem3>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 256.0);
     CK(cudaGetLastError());
     // accuracy on the first 1024 sets against an FP64 host evaluation
     const int chk = 1024;
