@@ -108,3 +108,37 @@ def test_super_pass_planning_is_opt_in():
     assert small["npasses"] == 4
     _, src = qsv.plan_dry(30, cir.gates(), opts={"super_bits": 19}, source_of_pass=0)
     assert "qsv_pair" in src and "ld.acquire.gpu" in src and "namespace pb" in src
+
+
+@pytest.mark.parametrize("dtype,variant", [("c64", ""), ("c64", "QSV_X_NOPACK"), ("c128", ""),
+                                           ("c128", "QSV_X_NOSCALE")])
+def test_generated_pass_sources_compile_for_sm100a(dtype, variant, monkeypatch, tmp_path):
+    # the codegen's arithmetic forms (host logic, no GPU): complex64 passes
+    # compute on packed f32x2 registers unless QSV_X_NOPACK=1, the tangent
+    # form leaves +-1 terms, and every variant's source cross-compiles with
+    # nvcc for sm_100a exactly as NVRTC builds it on the GPU box
+    import shutil
+    import subprocess
+
+    from paper_2512_18995_b200 import workloads as W
+
+    if variant:
+        monkeypatch.setenv(variant, "1")
+    n = 20
+    dt = qsv.C64 if dtype == "c64" else qsv.C128
+    cir = W.cfg5_circuit(n, 2) if dtype == "c64" else W.cfg4_circuit(n, 2)
+    info, src = qsv.plan_dry(n, cir.gates(), dtype=dt, source_of_pass=1)
+    assert info["npasses"] >= 2 and "qsv_pass" in src
+    packed = "fma.rn.f32x2" in src
+    assert packed == (dtype == "c64" and variant != "QSV_X_NOPACK")
+    if dtype == "c128":
+        # tangent-form rows: a real rotation output is x0 + t*x1 (no multiply on x0)
+        assert "mk(x0.x+" in src or "mk(x1.x+" in src
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    if not Path(nvcc).exists():
+        pytest.skip("nvcc not available")
+    cu = tmp_path / "pass.cu"
+    cu.write_text(src)
+    r = subprocess.run([nvcc, "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o",
+                        str(tmp_path / "pass.cubin"), str(cu)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
