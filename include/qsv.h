@@ -63,7 +63,13 @@ enum qsv_dtype { QSV_C64 = 1, QSV_C128 = 2 };
 
 /* apply flags */
 enum {
-    QSV_ZERO_OFF_CONTROL = 1 /* apply_matrix_strided(..., zero_off_control=true) */
+    QSV_ZERO_OFF_CONTROL = 1, /* apply_matrix_strided(..., zero_off_control=true) */
+    /* Structure hints. The engine classifies every matrix
+     * itself (diagonal -> deferred phases, 0/1 permutation -> register
+     * relabel), so a hint changes nothing on the GPU path; a hint the matrix
+     * contradicts fails with QSV_ERR_INVALID. */
+    QSV_HINT_DIAGONAL = 2,
+    QSV_HINT_PERMUTATION = 4
 };
 
 typedef struct qsv_ctx qsv_ctx;

@@ -349,6 +349,22 @@ int qsv_apply_matrix(qsv_state *st, int k, const int32_t *wires, int nctl, const
             if (i / d != i % d && g.m[i] != cplx(0, 0)) diag = false;
         }
         g.diag = diag;
+        require((flags & ~(QSV_ZERO_OFF_CONTROL | QSV_HINT_DIAGONAL | QSV_HINT_PERMUTATION)) == 0,
+                "apply_matrix: unknown flags");
+        require(!(flags & QSV_HINT_DIAGONAL) || diag, "apply_matrix: DIAGONAL hint on a non-diagonal matrix");
+        if (flags & QSV_HINT_PERMUTATION) {
+            bool perm = true;
+            for (int r = 0; r < d && perm; ++r) {
+                int ones = 0;
+                for (int c = 0; c < d; ++c) {
+                    const cplx &e = g.m[r * d + c];
+                    if (e == cplx(1, 0)) ++ones;
+                    else if (e != cplx(0, 0)) perm = false;
+                }
+                perm = perm && ones == 1;
+            }
+            require(perm, "apply_matrix: PERMUTATION hint on a matrix that is not a 0/1 permutation");
+        }
         g.flags = (flags & QSV_ZERO_OFF_CONTROL) ? OPF_ZERO_OFF_CONTROL : 0;
         run_single(*st, g);
     });

@@ -35,6 +35,8 @@ LIB_PATH = _PKG / "libqsv.so"
 C64, C128 = 1, 2
 OK, ERR_INTERNAL, ERR_INVALID, ERR_GUARD, ERR_TRANSPORT = 0, 1, 2, 3, 4
 ZERO_OFF_CONTROL = 1
+HINT_DIAGONAL = 2      # structure hints: checked against the matrix, no effect on the path
+HINT_PERMUTATION = 4
 kPi = 3.141592653589793238462643383279502884
 
 
@@ -459,8 +461,9 @@ class QubitState:
         check(lib().qsv_expect_z_all(self.h, _ptr(out)))
         return out.reshape(self._batch, self._n)
 
-    def apply_matrix(self, m, wires, controls=(), zero_off_control=False):
-        """detail::apply_matrix_strided (state.hpp:111-143), in place."""
+    def apply_matrix(self, m, wires, controls=(), zero_off_control=False, hints=0):
+        """detail::apply_matrix_strided (state.hpp:111-143), in place. `hints`:
+        HINT_DIAGONAL / HINT_PERMUTATION (verified against the matrix)."""
         m = np.ascontiguousarray(m, dtype=np.complex128)
         k = len(wires)
         if m.shape != (1 << k, 1 << k):
@@ -468,7 +471,7 @@ class QubitState:
         w = (C.c_int32 * max(1, k))(*wires)
         c = (C.c_int32 * max(1, len(controls)))(*controls)
         check(lib().qsv_apply_matrix(self.h, k, w, len(controls), c, _ptr(m.view(np.float64)),
-                                     ZERO_OFF_CONTROL if zero_off_control else 0))
+                                     (ZERO_OFF_CONTROL if zero_off_control else 0) | hints))
 
     def close(self):
         if getattr(self, "h", None):

@@ -209,6 +209,28 @@ def test_apply_matrix_zero_off_control():
     assert np.max(np.abs(s.amplitudes() - want)) < 1e-15
 
 
+def test_apply_matrix_structure_hints():
+    # SURVEY.md §8b flags word: DIAGONAL / PERMUTATION hints are verified
+    # against the matrix (the engine classifies matrices itself) and change
+    # nothing in the result; a contradicted hint fails like invalid_input
+    rng = Rng(4, "hints")
+    psi = random_state(rng, 6)
+    d = np.diag([np.exp(0.3j), np.exp(-1.1j)])
+    x = np.array([[0, 1], [1, 0]], dtype=complex)
+    for m, h in ((d, qsv.HINT_DIAGONAL), (x, qsv.HINT_PERMUTATION)):
+        s = QubitState.from_amplitudes(6, psi)
+        s.apply_matrix(m, [3], [1], hints=h)
+        want = O.port_apply_matrix(psi, 6, m, [3], [1])
+        assert np.max(np.abs(s.amplitudes() - want)) < 1e-15
+    s = QubitState.from_amplitudes(6, psi)
+    with pytest.raises(qsv.InvalidInput):
+        s.apply_matrix(x, [3], hints=qsv.HINT_DIAGONAL)
+    with pytest.raises(qsv.InvalidInput):
+        s.apply_matrix(d, [3], hints=qsv.HINT_PERMUTATION)
+    with pytest.raises(qsv.InvalidInput):
+        s.apply_matrix(d, [3], hints=64)
+
+
 def test_expectations_all_pauli_strings_vs_reference():
     rng = Rng(17, "pauli")
     n = 6
