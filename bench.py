@@ -6,7 +6,7 @@ on the seeded, normalised Gaussian input state, one B200 (16 GiB state).
 
 Arms
   default      the engine (libqsv.so, fused sm_100a tile passes) through the C
-               ABI. A step = one full execution of the 495-gate circuit on the
+               ABI. A step = one full execution of the 480-gate circuit on the
                HBM-resident state. value = source gates applied per second
                (one "gate pass" = one reference gate applied to all 2^30
                amplitudes). Under torchrun (N > 1) the state is sharded over N
@@ -39,6 +39,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 N_QUBITS = 30
+METRIC = "gate passes/sec at n qubits (source gates applied to the full state per second)"
 WORKLOAD = "cfg3: 30-qubit complex128 QFT + 15 final swaps on a seeded normalised Gaussian state"
 
 
@@ -108,19 +109,89 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference_sample(cir, n, psi, gates_per_step, steps):
-    """The reference CPU path on a bounded sample: quasar::qubit::apply_gate
-    over `gates_per_step` gates of the same circuit, `steps` times."""
+NOMINAL_HBM_GBS = 8000.0  # north_star's "~8 TB/s"
+
+
+def config_dict(n):
+    """The workload; identical in both arms (engine details go under "plan")."""
+    return {"workload": WORKLOAD, "n_qubits": n, "gates": 480 if n == 30 else None, "dtype": "c128",
+            "input": "seeded normalised Gaussian state Rng(0,'cfg3')",
+            "l2": "state (16 GiB) >> L2 (126 MB); no flush needed"}
+
+
+def cfg3_gate_list(n):
+    """The cfg3 circuit built from the reference's own qft_circuit
+    (circuit.hpp:167-178, through oracle/_ref) plus the 15 final swaps --
+    no libqsv involved (the reference arm must not map it)."""
     from oracle import oracle as O
 
-    gl = cir.gates()
-    times = []
-    state = psi
-    for s in range(steps):
-        sample = [gl[(s * gates_per_step + j) % len(gl)] for j in range(gates_per_step)]
-        sec, state = O.ref_time_apply(n, sample, state)
-        times.append(sec)
-    return times
+    gl = list(O.ref_qft_gates(n))
+    for i in range(n // 2):
+        g = O.RefGate()
+        g.name = b"swap"
+        g.nwires = 2
+        g.wires[0], g.wires[1] = i, n - 1 - i
+        gl.append(g)
+    return gl
+
+
+class _G:  # RefGate -> the attribute view oracle.gate_struct expects
+    def __init__(self, r):
+        self.name = r.name.decode()
+        self.wires = [r.wires[i] for i in range(r.nwires)]
+        self.controls = [r.controls[i] for i in range(r.ncontrols)]
+        self.params = [r.params[i] for i in range(r.nparams)]
+        self.trainable = bool(r.trainable)
+        self.encode = bool(r.encode)
+        self.custom = None
+
+
+def stratified_sample(gl, k):
+    """k gates of the circuit with its gate kinds in proportion (h / cp /
+    swap = 30 / 435 / 15 of 480), evenly spread through the circuit within
+    each kind, in circuit order."""
+    kinds = {}
+    for i, g in enumerate(gl):
+        kinds.setdefault(g.name, []).append(i)
+    total = len(gl)
+    quota = {nm: max(1, round(k * len(ix) / total)) for nm, ix in kinds.items()}
+    big = max(quota, key=lambda nm: len(kinds[nm]))
+    quota[big] = max(1, k - sum(q for nm, q in quota.items() if nm != big))
+    pick = []
+    for nm, ix in kinds.items():
+        q = quota[nm]
+        pick += [ix[int((j + 0.5) * len(ix) / q)] for j in range(q)]
+    return [gl[i] for i in sorted(pick)][:k] if len(pick) >= k else [gl[i] for i in sorted(pick)]
+
+
+def reference_cpu_sample(n, nsteps, warmup):
+    """The reference's CPU path on a bounded sample of cfg3 at full size:
+    quasar::qubit::apply_gate (state.hpp:149-157; gate_matrix, unitarity
+    check, full copy, strided sweep) on a reference QubitState holding the
+    seeded 30-qubit input, one gate per step, `warmup` + `nsteps` gates drawn
+    by stratified_sample. The input comes from the oracle's threaded Rng
+    restatement (bit-identical to Rng(0,'cfg3')). Returns (per-step seconds,
+    sample description)."""
+    import gc
+
+    from oracle import oracle as O
+
+    psi = O.port_rng_normal(0, "cfg3", 2 << n).view(np.complex128)
+    psi /= np.sqrt(float(np.dot(psi.view(np.float64), psi.view(np.float64))))
+    st = O.RefState(n, psi)
+    del psi
+    gc.collect()
+    gl = [_G(r) for r in cfg3_gate_list(n)]
+    sample = stratified_sample(gl, warmup + nsteps)
+    times = [st.apply([g]) for g in sample]
+    st.close()
+    mix = {}
+    for g in sample[warmup:]:
+        mix[g.name] = mix.get(g.name, 0) + 1
+    desc = (f"{nsteps} gates of cfg3 at n={n} (kinds {mix}, spread through the circuit in proportion) after "
+            f"{warmup} warm-up gates, one per step, via quasar::qubit::apply_gate on a reference QubitState "
+            "(single-threaded: the reference qubit path never calls parallel_for)")
+    return times[warmup:], desc
 
 
 def swap_accounting(n, cir, world, nl, amp_bytes, fused):
@@ -174,35 +245,150 @@ def swap_accounting(n, cir, world, nl, amp_bytes, fused):
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU path (oracle/_ref, the
+    unmodified quasar headers) on this host, never loading libqsv.so."""
     rank, world, local = dist_env()
     if rank != 0:
         return 0
     from oracle import oracle as O
-    from paper_2512_18995_b200 import workloads as W
 
     if not O.REF_LIB.exists():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libquasar_ref.so not built"}))
         return 0
-    n = N_QUBITS
-    cir = W.cfg3_circuit(n)
-    psi = W.cfg3_input(n)
-    times = cpu_reference_sample(cir, n, psi, 1, args.warmup + args.steps)[args.warmup:]
+    n = args.qubits
+    times, desc = reference_cpu_sample(n, args.steps, args.warmup)
     t = float(np.sum(times))
     value = args.steps / t
     line = {
-        "metric": "gate passes/sec at n qubits (source gates applied to the full state per second)",
-        "value": value, "unit": "gates/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": 0, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state)",
-        "impl": "reference",
-        "config": {"workload": WORKLOAD, "n_qubits": n, "sample": "1 gate of the circuit per step, in order"},
-        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "kind": "reference",
-                         "sample": f"{args.steps} gates of cfg3 at n=30 via quasar::qubit::apply_gate "
-                                   "(single-threaded reference path; parallel_for is unused by it)"},
+        "impl": "reference", "config": config_dict(n), "sample": desc,
+        "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "host_cores": os.cpu_count(),
+                         "kind": "reference", "sample": desc},
         "e2e": {"value": value, "unit": "gates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
+
+
+def _median_events(fn, stream, reps, warm=1):
+    """1 warm-up + `reps` timed repeats, each bracketed by CUDA events on the
+    engine's stream; the median ms (the reference CLI's protocol,
+    tools/main.cpp:493-504)."""
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    out = []
+    for _ in range(reps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        out.append(e0.elapsed_time(e1))
+    return float(np.median(out)), out
+
+
+def run_aux(ctx, stream, hbm_peak, want_cpu):
+    """The other BASELINE.json configs on this GPU (device-resident, reference
+    protocol: 1 warm-up + 10 repeats, median), with the reference's CPU path
+    timed beside cfg1 / cfg2 on this host. Returns (aux dict, kernel launches)."""
+    import time as _t
+
+    from paper_2512_18995_b200 import qsv
+    from paper_2512_18995_b200 import workloads as W
+
+    L = qsv.lib()
+    aux = {"protocol": "1 warm-up + 10 repeats, median; CUDA events on the engine stream"}
+    launches = 0
+    # ---- cfg1: 20q c128, 10 layers rx/ry/rz + CNOT ladder, all <Z_i> ----
+    cir = W.cfg1_circuit()
+    p = qsv.Plan(20, cir.gates(), dtype=qsv.C128, opts={"from_zero": 1})
+    pg = qsv.Plan(20, cir.gates(), dtype=qsv.C128, opts={"from_zero": 1, "use_graph": 1})
+    st = qsv.QubitState(20, dtype=qsv.C128)
+    ms, _ = _median_events(lambda: p.execute(st), stream, 10)
+    msg, _ = _median_events(lambda: pg.execute(st), stream, 10)
+    p.execute_expect_z(st)  # warm-up (first use prepares the variant)
+    t0 = _t.perf_counter()
+    zs = [p.execute_expect_z(st) for _ in range(10)]
+    msz = (_t.perf_counter() - t0) / 10 * 1e3
+    npass = p.info["npasses"]
+    launches += 21 * (npass + 1) + 11 * 10 + 10 * (npass + 3)
+    l2_bytes = npass * 2 * 16 * (1 << 20)
+    c1 = {"workload": "cfg1: 20-qubit c128, 10 layers of rx/ry/rz on every qubit + CNOT ladder (619 gates), "
+                      "from |0>, all <Z_i>",
+          "passes": npass, "us_per_forward": 1e3 * ms, "us_per_forward_graph": 1e3 * msg,
+          "us_per_forward_plus_z_host": 1e3 * msz, "gates_per_s": 619 / (ms / 1e3),
+          "l2_GBps": l2_bytes / (ms / 1e3) / 1e9,
+          "note": "16 MiB state: L2-resident, launch/L2 bound (SURVEY.md 8(d))"}
+    if want_cpu:
+        from oracle import oracle as O
+
+        sec = [O.ref_time_forward_z(20, cir.gates())[0] for _ in range(4)]
+        c1["cpu_reference"] = {"ms_per_forward_plus_z": 1e3 * float(np.median(sec[1:])), "cores": 1,
+                               "protocol": "1 warm-up + 3 repeats, median (Circuit::forward + expectation)"}
+        want = O.ref_time_forward_z(20, cir.gates())[1][0]
+        c1["z_max_abs_err_vs_reference"] = float(np.max(np.abs(zs[-1][0] - want)))
+    aux["cfg1"] = c1
+    del st, p, pg
+    # ---- cfg2: 4096 x 12q c64 batched VQC, <Z_i> per circuit ----
+    cir, data = W.cfg2_circuit()
+    p = qsv.Plan(12, cir.gates(), dtype=qsv.C64, opts={"from_zero": 1})
+    st = qsv.QubitState(12, batch=4096, dtype=qsv.C64)
+    ms, _ = _median_events(lambda: p.execute(st, data), stream, 10)
+    p.execute_expect_z(st, data)  # warm-up (first use compiles the fused <Z> variant)
+    t0 = _t.perf_counter()
+    for _ in range(10):
+        z = p.execute_expect_z(st, data)
+    msz = (_t.perf_counter() - t0) / 10 * 1e3
+    launches += 11 * (p.info["npasses"] + 2) + 10 * (p.info["npasses"] + 2)
+    c2 = {"workload": "cfg2: 4096 circuits x 12 qubits c64, encoded Ry(x) + 6 x (U3 + ring CZ), <Z_i> per circuit",
+          "passes": p.info["npasses"], "ms_forward": ms, "circuits_per_s_forward": 4096 / (ms / 1e3),
+          "ms_forward_plus_all_z_on_host": msz, "circuits_per_s": 4096 / (msz / 1e3),
+          "note": "one pass, a whole circuit per CTA tile; <Z_i> fused into its last register group"}
+    if want_cpu:
+        from oracle import oracle as O
+
+        sub = 512
+        sec1, z1 = O.ref_time_forward_z(12, cir.gates(), data[:sub], 1)
+        hc = os.cpu_count() or 1
+        secs = [O.ref_time_forward_z(12, cir.gates(), data, hc)[0] for _ in range(6)]
+        c2["cpu_reference"] = {
+            "circuits_per_s_1core": sub / sec1, "sample_1core": f"first {sub} of the 4096 rows, 1 run",
+            "circuits_per_s_all_cores": 4096 / float(np.median(secs[1:])), "cores": hc,
+            "protocol_all_cores": "4096 rows fanned with quasar::parallel_for, 1 warm-up + 5 repeats, median"}
+        c2["z_max_abs_err_vs_reference"] = float(np.max(np.abs(z[:sub] - z1)))
+    aux["cfg2"] = c2
+    del st, p
+    # ---- cfg4 / cfg5 families at the largest single-GPU sizes ----
+    for name, n, cir, dt, desc in (
+            ("cfg4_32q", 32, W.cfg4_circuit(32), qsv.C128,
+             "cfg4 family at 32 qubits c128 (64 GiB): 20 layers of U3 + brickwork CNOT (950 gates)"),
+            ("cfg5_33q", 33, W.cfg5_circuit(33), qsv.C64,
+             "cfg5 family at 33 qubits c64 (64 GiB): 16 layers of rx/ry/rz + random-pair CZ (1856 gates)")):
+        tp = _t.perf_counter()
+        p = qsv.Plan(n, cir.gates(), dtype=dt)
+        plan_s = _t.perf_counter() - tp
+        st = qsv.QubitState(n, dtype=dt)
+        p.profile(st)  # warm-up
+        runs = [p.profile(st) for _ in range(3)]
+        per = np.array(runs)
+        tot = float(np.median(per.sum(axis=1)))
+        amp = 8 if dt == qsv.C64 else 16
+        bpl = 2.0 * amp * (1 << n)
+        avg = float(per.mean())
+        aux[name] = {"workload": desc, "passes": p.info["npasses"], "ms_per_forward": tot,
+                     "gates_per_s": p.info["ngates"] / (tot / 1e3), "plan_seconds": plan_s,
+                     "avg_pass_GBps": bpl / (avg / 1e3) / 1e9, "frac_of_measured_hbm": bpl / (avg / 1e3) / 1e9 / hbm_peak,
+                     "protocol": "1 warm-up + 3 repeats (each a full forward with per-pass events), median",
+                     "per_pass_ms": [round(float(x), 4) for x in per.mean(axis=0)]}
+        launches += 4 * p.info["npasses"]
+        del st, p
+    return aux, launches
 
 
 def main():
@@ -213,6 +399,7 @@ def main():
     ap.add_argument("--impl", default="qsv")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-aux", action="store_true")
     ap.add_argument("--qubits", type=int, default=N_QUBITS, help="(diagnostics only) qubit count")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -252,7 +439,6 @@ def main():
         torch.distributed.all_reduce(t)
         ss = float(t.item())
     mine /= np.sqrt(ss)
-    psi = mine  # full state when world == 1 (the CPU baseline samples it)
     plan = qsv.Plan(n, cir.gates(), dtype=qsv.C128, ctx=ctx)
     st = qsv.QubitState(n, dtype=qsv.C128, ctx=ctx)
     st.upload(mine)
@@ -288,7 +474,7 @@ def main():
     ngates = plan.info["ngates"]
     value = args.steps * ngates / (t_ms / 1e3)
 
-    # ---- roofline of the dominant kernel (tile_pass_kernel) ----
+    # ---- roofline of the dominant kernel (the fused tile pass) ----
     kinds = plan.step_kinds()
     lm = np.array(launch_ms)[:, kinds == 0]  # steps x passes (qubit-swap steps excluded)
     amp_bytes = 16
@@ -322,10 +508,12 @@ def main():
 
     # ---- end to end through the C ABI with pinned host buffers ----
     # Every step uploads its input state from pinned host memory, executes
-    # the plan and downloads the result (qsv_state_upload_raw / execute /
-    # qsv_state_download_raw). Two states on two contexts (two CUDA streams)
-    # alternate, so step i's download overlaps step i+1's upload (PCIe is
-    # full duplex); every step still moves its full input and output.
+    # the plan and downloads the result (qsv_state_upload_raw_async /
+    # execute / qsv_state_download_raw_async, all stream-ordered). Two states
+    # on two contexts (two CUDA streams) alternate, so step i's download
+    # overlaps step i+1's upload (PCIe is full duplex); every step still moves
+    # its full input and output. A lane waits for its own previous step
+    # (qsv_ctx_sync) before reusing its output buffer.
     e2e = None
     if args.e2e_steps > 0:
         if world > 1:
@@ -338,10 +526,10 @@ def main():
         st2 = qsv.QubitState(n, dtype=qsv.C128, ctx=ctx2)
         stream2 = torch.cuda.ExternalStream(ctx2.stream(), device=torch.device("cuda", local))
         host_in = torch.from_numpy(mine.view(np.float64)).pin_memory()
-        host_out = torch.empty_like(host_in).pin_memory()
+        host_out = [torch.empty_like(host_in).pin_memory(), torch.empty_like(host_in).pin_memory()]
         L = qsv.lib()
         cnt = 1 << nl
-        lanes = [(plan, st, stream), (plan2, st2, stream2)]
+        lanes = [(plan, st, ctx), (plan2, st2, ctx2)]
         plan2.execute(st2)  # warm-up (kernel loading) of the second lane
         ctx.sync()
         ctx2.sync()
@@ -351,13 +539,12 @@ def main():
         f0.record(stream)
         stream2.wait_event(f0)
         for i in range(args.e2e_steps):
-            p_i, s_i, _ = lanes[i % 2]
-            qsv.check(L.qsv_state_upload_raw(s_i.h, 0, host_in.data_ptr(), cnt))
+            p_i, s_i, c_i = lanes[i % 2]
+            if i >= 2:
+                c_i.sync()  # this lane's previous download has landed
+            qsv.check(L.qsv_state_upload_raw_async(s_i.h, 0, host_in.data_ptr(), cnt))
             p_i.execute(s_i)
-            if i >= 1:  # the previous step's result, while this step's upload streams in
-                qsv.check(L.qsv_state_download_raw(lanes[(i - 1) % 2][1].h, 0, host_out.data_ptr(), cnt))
-        last = lanes[(args.e2e_steps - 1) % 2]
-        qsv.check(L.qsv_state_download_raw(last[1].h, 0, host_out.data_ptr(), cnt))
+            qsv.check(L.qsv_state_download_raw_async(s_i.h, 0, host_out[i % 2].data_ptr(), cnt))
         done2 = torch.cuda.Event()
         done2.record(stream2)
         stream.wait_event(done2)
@@ -377,34 +564,41 @@ def main():
         ctx2.close()
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    want_cpu = rank == 0 and world == 1 and not args.no_cpu_baseline
+    aux = None
+    aux_launches = 0
+    if rank == 0 and world == 1 and not args.no_aux and n == N_QUBITS:
+        del st
+        aux, aux_launches = run_aux(ctx, stream, hbm_peak, want_cpu)
+    if want_cpu:
         from oracle import oracle as O
 
         if O.REF_LIB.exists():
-            times = cpu_reference_sample(cir, n, psi, 1, 2)
-            cpu = {"value": 2 / float(np.sum(times)), "unit": "gates/s", "cores": 1, "kind": "reference",
-                   "sample": "first 2 gates of cfg3 (h(0), cp(1,0)) at n=30 via quasar::qubit::apply_gate, "
-                             "single thread"}
+            times, desc = reference_cpu_sample(n, 4, 1)
+            cpu = {"value": len(times) / float(np.sum(times)), "unit": "gates/s", "cores": 1,
+                   "host_cores": os.cpu_count(), "kind": "reference", "sample": desc}
     if rank == 0:
         line = {
-            "metric": "gate passes/sec at n qubits (source gates applied to the full state per second)",
-            "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state, normalised in FP64)",
-            "config": {"workload": WORKLOAD, "n_qubits": n, "gates": ngates, "passes_per_step": npass,
-                       "swaps_per_step": plan.info["nswaps"], "parallelism": f"state sharded over {world} GPU(s)",
-                       "l2": "state (16 GiB) >> L2 (126 MB); no flush needed"},
+            "config": config_dict(n),
+            "plan": {"passes_per_step": npass, "swaps_per_step": plan.info["nswaps"],
+                     "parallelism": f"state sharded over {world} GPU(s)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                         "frac_nominal": achieved / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
                          "traffic_source": "profiles/r01_traffic_cfg3_30q.json (ncu dram__bytes_read+write per launch)",
                          "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},
             "gpu_launches": args.steps * (npass + swap_kern),
+            "gpu_launches_aux": aux_launches,
             "nvlink": nvlink,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "aux": aux,
             "clocks": clk.summary(),
         }
         print(json.dumps(line))

@@ -19,7 +19,8 @@
  *   qsv_marginal_probs   quasar::qubit::marginal_probabilities circuit.hpp:182-205
  *   qsv_state_*          quasar::qubit::QubitState (basis / from_amplitudes /
  *                        amplitudes(b)) state.hpp:29-91
- *   qsv_ctx_create_dist, qsv_state_global_bits, qsv_norm2 (global)
+ *   qsv_ctx_create_dist, qsv_ctx_create_multi, qsv_run_on_ranks,
+ *   qsv_ctx_comm_stats, qsv_state_info (global bits), qsv_norm2 (global)
  *                        quasar::dist::PartitionedState / run_on_ranks /
  *                        global_norm2 (source absent from the reference;
  *                        contract from tests/test_dist.cpp:66-174 and
@@ -146,6 +147,30 @@ int qsv_ctx_create(int device, qsv_ctx **out);
  * torch.distributed). world must be a power of two (test_dist.cpp:90-94). */
 int qsv_nccl_unique_id(void *out128);
 int qsv_ctx_create_dist(int device, int rank, int world, const void *unique_id128, qsv_ctx **out);
+/* One process, P GPUs (the reference's in-process
+ * dist::run_on_ranks, tests/test_dist.cpp:66-94, tools/main.cpp:95): rank r
+ * on devices[r] with its own stream, one NCCL communicator per rank from
+ * ncclCommInitAll, ndev a power of two. Every call on this context and on the
+ * states / plans made from it runs on all ranks (one host thread per rank,
+ * NCCL inside); a state's host view (upload / download) is the WHOLE state in
+ * logical order, and reductions return the all-reduced values. */
+int qsv_ctx_create_multi(int ndev, const int *devices, qsv_ctx **out);
+/* Rank r's own context inside a multi-device one (owned by it): the ABI
+ * calls on it act on that rank's slice, as with qsv_ctx_create_dist. */
+int qsv_ctx_rank_ctx(qsv_ctx *multi, int rank, qsv_ctx **out);
+/* dist::run_on_ranks: fn(rank context, rank, user) on one host thread per
+ * rank, all joined; the first failing rank's status is returned (its message
+ * in qsv_last_error). On a single-rank context fn runs inline. Collective
+ * calls inside fn must be made by every rank, as in the reference. */
+typedef int (*qsv_rank_fn)(qsv_ctx *rank_ctx, int rank, void *user);
+int qsv_run_on_ranks(qsv_ctx *multi, qsv_rank_fn fn, void *user);
+/* Transport counters (Transport::messages_sent / bytes_sent / reset_counters,
+ * tests/test_dist.cpp:96-126), measured as the rank issues them: one message
+ * per point-to-point send (per peer, per chunk round) and per destination
+ * rank of a swap fused into a pass (peer-memory stores), bytes = payload;
+ * all-reduces counted apart. On a multi-device context: summed over ranks. */
+int qsv_ctx_comm_stats(const qsv_ctx *ctx, uint64_t *messages, uint64_t *bytes, uint64_t *allreduces);
+int qsv_ctx_comm_reset(qsv_ctx *ctx);
 int qsv_ctx_destroy(qsv_ctx *ctx);
 int qsv_ctx_sync(qsv_ctx *ctx);
 /* The cudaStream_t the engine launches on (for events), as void*. */
@@ -166,10 +191,15 @@ int qsv_state_set_basis(qsv_state *st, uint64_t index);
  * 2^(n-g) indices whose top g bits equal the rank). */
 int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count);
 int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count);
-/* Raw dtype-native host buffers (float32 pairs for C64): the cheap path the
- * e2e benchmark uses (pinned host memory, one DMA each way). */
+/* Raw dtype-native host buffers (float32 pairs for C64): one DMA each way.
+ * Both return after the copy has completed (the host buffer may be reused). */
 int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t count);
 int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count);
+/* Stream-ordered variants (the e2e benchmark's pipeline): the copy is queued
+ * on the context's stream and the call returns at once; `host` (pinned for an
+ * asynchronous DMA) must stay untouched until qsv_ctx_sync. */
+int qsv_state_upload_raw_async(qsv_state *st, int row, const void *host, uint64_t count);
+int qsv_state_download_raw_async(qsv_state *st, int row, void *host, uint64_t count);
 int qsv_state_clone(const qsv_state *st, qsv_state **out);
 /* Device pointer of row `row` in the engine's PHYSICAL order (tests). */
 int qsv_state_device_ptr(qsv_state *st, int row, void **ptr);

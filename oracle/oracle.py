@@ -439,3 +439,117 @@ def port_density_marginal(n, rho, wires):
             o = (o << 1) | ((idx >> (n - 1 - w)) & 1)
         out[o] += d[idx]
     return out
+
+
+# ------------------------------------- full size (threaded / digests) -----
+def port_rng_normal(seed, label, count, offset=0, nthreads=0):
+    """Rng(seed, label).normal() draws [offset, offset + count), counter-parallel
+    on host threads (bit-identical to the sequential stream)."""
+    import os
+
+    L = port()
+    out = np.empty(count, dtype=np.float64)
+    rc = L.qo_rng_fill_normal(C.c_uint64(seed), None if label is None else label.encode(), C.c_uint64(offset),
+                              C.c_uint64(count), _p(out), nthreads or os.cpu_count() or 1)
+    if rc:  # the u1 == 0 rejection: replay sequentially
+        seq = port_rng(seed, label, 2, offset + count)
+        out[:] = seq[offset:]
+    return out
+
+
+def port_forward_mt(n, gates, psi, nthreads=0):
+    """Circuit::forward (no data) of `psi` in place, threaded restatement."""
+    import os
+
+    L = port()
+    arr, keep = gate_structs(gates)
+    a = np.ascontiguousarray(psi, dtype=np.complex128)
+    assert a.size == 1 << n
+    rc = L.qo_forward_mt(n, arr, len(gates), _p(a), nthreads or os.cpu_count() or 1)
+    if rc:
+        raise OracleError(rc, "qo_forward_mt failed")
+    return a
+
+
+def port_digest(n, psi, nblocks=4096, nthreads=0):
+    """(blocks[nblocks, 3], z[n + 2]) of a state (qo_digest)."""
+    import os
+
+    L = port()
+    a = np.ascontiguousarray(psi, dtype=np.complex128)
+    blocks = np.zeros((nblocks, 3))
+    z = np.zeros(n + 2)
+    rc = L.qo_digest(n, _p(a), nblocks, _p(blocks), _p(z), nthreads or os.cpu_count() or 1)
+    if rc:
+        raise OracleError(rc, "qo_digest failed")
+    return blocks, z
+
+
+def ref_forward_digest(n, gates, init_kind, seed, label, idx, nblocks=4096):
+    """The reference's own apply_gate loop at full size, reduced to a digest:
+    returns (blocks, z, samples at idx, seconds)."""
+    L = ref()
+    arr, keep = gate_structs(gates)
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    blocks = np.zeros((nblocks, 3))
+    z = np.zeros(n + 2)
+    samples = np.zeros(len(idx), dtype=np.complex128)
+    sec = C.c_double()
+    rc = L.ref_forward_digest(n, arr, len(gates), init_kind, C.c_uint64(seed), None if label is None else label.encode(),
+                              nblocks, _p(blocks), _p(z), len(idx), _p(idx), _p(samples), C.byref(sec))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return blocks, z, samples, sec.value
+
+
+class RefState:
+    """A reference QubitState kept across calls; apply() times
+    quasar::qubit::apply_gate on it (bench.py --impl reference)."""
+
+    def __init__(self, n, amps):
+        L = ref()
+        L.ref_state_new.restype = C.c_void_p
+        L.ref_state_new.argtypes = [C.c_int, C.c_void_p]
+        L.ref_state_free.argtypes = [C.c_void_p]
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        self.h = L.ref_state_new(n, _p(a))
+        if not self.h:
+            raise OracleError(1, L.ref_last_error().decode())
+
+    def apply(self, gates) -> float:
+        L = ref()
+        arr, keep = gate_structs(gates)
+        sec = C.c_double()
+        rc = L.ref_state_apply_timed(C.c_void_p(self.h), arr, len(gates), C.byref(sec))
+        if rc:
+            raise OracleError(rc, L.ref_last_error().decode())
+        return sec.value
+
+    def close(self):
+        if self.h:
+            ref().ref_state_free(C.c_void_p(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def ref_time_forward_z(n, gates, data=None, nthreads=1):
+    """Circuit::forward + expectation() of every single-Z observable, timed in
+    C++ (steady_clock); rows fanned over `nthreads` with quasar::parallel_for.
+    Returns (seconds, z[rows, n])."""
+    L = ref()
+    arr, keep = gate_structs(gates)
+    rows = 0 if data is None else len(data)
+    d = None if data is None else np.ascontiguousarray(np.asarray(data, dtype=np.float64).reshape(rows, -1))
+    slots = 0 if d is None else d.shape[1]
+    z = np.zeros((max(rows, 1), n))
+    sec = C.c_double()
+    rc = L.ref_time_forward_z(n, arr, len(gates), None if d is None else _p(d), rows, slots, nthreads, _p(z),
+                              C.byref(sec))
+    if rc:
+        raise OracleError(rc, L.ref_last_error().decode())
+    return sec.value, z

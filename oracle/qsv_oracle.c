@@ -344,3 +344,228 @@ double qo_norm2(int n, const double *psi) {
 }
 
 size_t qo_gate_sizeof(void) { return sizeof(qo_gate); }
+
+/* ------------------------------------------ threaded helpers (test infra) */
+/* Full-size parity fixtures (tests/golden/make_fullsize.py) and the bench's
+ * reference arm need the oracle at 30 qubits: the same arithmetic as above,
+ * with the independent work split over host threads. Pinned against the
+ * single-threaded restatement and oracle/_ref in tests/test_oracle.py. */
+#include <pthread.h>
+
+typedef struct {
+    void (*fn)(void *arg, uint64_t b, uint64_t e);
+    void *arg;
+    uint64_t b, e;
+} qo_job;
+
+static void *qo_job_run(void *p) {
+    qo_job *j = (qo_job *)p;
+    j->fn(j->arg, j->b, j->e);
+    return NULL;
+}
+
+/* runs fn over [0, total) split into nthreads contiguous ranges (multiples of
+ * `grain`) */
+static void qo_parallel(uint64_t total, uint64_t grain, int nthreads, void (*fn)(void *, uint64_t, uint64_t),
+                        void *arg) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    uint64_t units = (total + grain - 1) / grain;
+    if ((uint64_t)nthreads > units) nthreads = units ? (int)units : 1;
+    if (nthreads == 1) {
+        fn(arg, 0, total);
+        return;
+    }
+    pthread_t th[256];
+    qo_job jobs[256];
+    const uint64_t per = (units + nthreads - 1) / nthreads;
+    for (int t = 0; t < nthreads; ++t) {
+        uint64_t b = (uint64_t)t * per * grain, e = b + per * grain;
+        if (b > total) b = total;
+        if (e > total) e = total;
+        jobs[t] = (qo_job){fn, arg, b, e};
+        pthread_create(&th[t], NULL, qo_job_run, &jobs[t]);
+    }
+    for (int t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+}
+
+/* Rng(seed, label).normal() draws [offset, offset + count) (offset even):
+ * counter-based like rng.hpp:43 -- pair j uses counters 2j+1, 2j+2 -- so
+ * threads reproduce the sequential stream; returns 1 if the u1 == 0
+ * rejection of rng.hpp:59 (p = 2^-53 per pair) was met, in which case the
+ * caller must fall back to qo_rng_draw. */
+typedef struct {
+    uint64_t key, c0, count;
+    double *out;
+    int rejected;
+} qo_fill_arg;
+
+static void qo_fill_normal_part(void *p, uint64_t b, uint64_t e) {
+    qo_fill_arg *a = (qo_fill_arg *)p;
+    for (uint64_t j = b; j < e; ++j) {
+        const double u1 = (double)(qo_mix(a->key + 0x9e3779b97f4a7c15ull * (a->c0 + 2 * j + 1)) >> 11) * 0x1.0p-53;
+        const double u2 = (double)(qo_mix(a->key + 0x9e3779b97f4a7c15ull * (a->c0 + 2 * j + 2)) >> 11) * 0x1.0p-53;
+        if (u1 == 0.0) {
+            a->rejected = 1;
+            return;
+        }
+        const double rad = sqrt(-2.0 * log(u1));
+        a->out[2 * j] = rad * cos(2.0 * 3.141592653589793 * u2);
+        if (2 * j + 1 < a->count) a->out[2 * j + 1] = rad * sin(2.0 * 3.141592653589793 * u2);
+    }
+}
+
+int qo_rng_fill_normal(uint64_t seed, const char *label, uint64_t offset, uint64_t count, double *out, int nthreads) {
+    if (offset % 2) return -1;
+    qo_rng r;
+    qo_rng_init(&r, seed, label);
+    qo_fill_arg a = {r.key, offset, count, out, 0};
+    qo_parallel((count + 1) / 2, 1 << 14, nthreads, qo_fill_normal_part, &a);
+    return a.rejected;
+}
+
+/* apply_matrix_strided (state.hpp:111-143) with the group bases split over
+ * threads: every base belongs to one thread, so the groups stay disjoint. */
+typedef struct {
+    double *psi;
+    const double *m;
+    int gs;
+    uint64_t tmask, cmask, off[32];
+    int zoc;
+} qo_apply_arg;
+
+static void qo_apply_part(void *p, uint64_t b0, uint64_t b1) {
+    qo_apply_arg *a = (qo_apply_arg *)p;
+    double sre[32], sim[32];
+    const int gs = a->gs;
+    for (uint64_t base = b0; base < b1; ++base) {
+        if (base & a->tmask) continue;
+        if ((base & a->cmask) != a->cmask) {
+            if (a->zoc)
+                for (int j = 0; j < gs; ++j) a->psi[2 * (base + a->off[j])] = a->psi[2 * (base + a->off[j]) + 1] = 0.0;
+            continue;
+        }
+        for (int j = 0; j < gs; ++j) {
+            sre[j] = a->psi[2 * (base + a->off[j])];
+            sim[j] = a->psi[2 * (base + a->off[j]) + 1];
+        }
+        for (int r = 0; r < gs; ++r) {
+            double are = 0.0, aim = 0.0;
+            for (int c = 0; c < gs; ++c) {
+                const double mr = a->m[2 * (r * gs + c)], mi = a->m[2 * (r * gs + c) + 1];
+                are += mr * sre[c] - mi * sim[c];
+                aim += mr * sim[c] + mi * sre[c];
+            }
+            a->psi[2 * (base + a->off[r])] = are;
+            a->psi[2 * (base + a->off[r]) + 1] = aim;
+        }
+    }
+}
+
+int qo_apply_matrix_mt(double *psi, int n, const double *m, int k, const int32_t *wires, int nctl,
+                       const int32_t *ctls, int zero_off_control, int nthreads) {
+    if (k < 1 || k > 5) return -1;
+    for (int i = 0; i < k; ++i)
+        if (wires[i] < 0 || wires[i] >= n) return -1;
+    for (int i = 0; i < nctl; ++i)
+        if (ctls[i] < 0 || ctls[i] >= n) return -1;
+    qo_apply_arg a;
+    memset(&a, 0, sizeof a);
+    a.psi = psi;
+    a.m = m;
+    a.gs = 1 << k;
+    a.zoc = zero_off_control;
+    for (int i = 0; i < k; ++i) a.tmask |= 1ull << (n - 1 - wires[i]);
+    for (int i = 0; i < nctl; ++i) a.cmask |= 1ull << (n - 1 - ctls[i]);
+    for (int j = 0; j < a.gs; ++j)
+        for (int i = 0; i < k; ++i)
+            if ((j >> (k - 1 - i)) & 1) a.off[j] |= 1ull << (n - 1 - wires[i]);
+    qo_parallel(1ull << n, 1 << 12, nthreads, qo_apply_part, &a);
+    return 0;
+}
+
+/* Circuit::forward without data (circuit.hpp:124-128) on psi, in place. */
+int qo_forward_mt(int n, const qo_gate *gates, int ngates, double *psi, int nthreads) {
+    for (int i = 0; i < ngates; ++i) {
+        double m[32];
+        const int k = qo_gate_matrix(&gates[i], m);
+        if (k < 0 || k != gates[i].nwires) return -1;
+        int rc = qo_apply_matrix_mt(psi, n, m, k, gates[i].wires, gates[i].ncontrols, gates[i].controls, 0, nthreads);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
+/* Full-state digest (tests/golden/make_fullsize.py, tests/test_gpu_fullsize.py):
+ * the 2^n amplitudes in `nblocks` equal contiguous blocks; per block
+ * out[3b] = sum |a|^2 and out[3b+1], out[3b+2] = sum a_i w_i (re, im) with
+ * pseudo-random weights w_i = (+-1) + i(+-1) from the top two bits of
+ * i * 0x9e3779b97f4a7c15 (i = the GLOBAL index); z[0] = sum |a|^2,
+ * z[1 + w] = sum |a|^2 (-1)^{bit of wire w} (wire 0 = MSB), z[n + 1] = the
+ * same for Z_0 Z_{n-1}. Sequential FP64 sums inside each block. */
+typedef struct {
+    const double *psi;
+    int n;
+    uint64_t bsize;
+    double *out;
+} qo_digest_arg;
+
+static void qo_digest_part(void *p, uint64_t b0, uint64_t b1) {
+    qo_digest_arg *a = (qo_digest_arg *)p;
+    for (uint64_t b = b0; b < b1; ++b) {
+        double s2 = 0, wr = 0, wi = 0;
+        for (uint64_t i = b * a->bsize; i < (b + 1) * a->bsize; ++i) {
+            const double re = a->psi[2 * i], im = a->psi[2 * i + 1];
+            const uint64_t h = i * 0x9e3779b97f4a7c15ull;
+            const double sr = (h >> 63) ? -1.0 : 1.0, si = ((h >> 62) & 1) ? -1.0 : 1.0;
+            s2 += re * re + im * im;
+            /* (re + i im)(sr + i si) */
+            wr += re * sr - im * si;
+            wi += re * si + im * sr;
+        }
+        a->out[3 * b] = s2;
+        a->out[3 * b + 1] = wr;
+        a->out[3 * b + 2] = wi;
+    }
+}
+
+typedef struct {
+    const double *psi;
+    int n;
+    double *acc; /* [thread-chunk][n + 2] */
+    uint64_t chunk;
+} qo_z_arg;
+
+static void qo_z_part(void *p, uint64_t c0, uint64_t c1) {
+    qo_z_arg *a = (qo_z_arg *)p;
+    const int n = a->n;
+    for (uint64_t c = c0; c < c1; ++c) {
+        double *z = a->acc + c * (n + 2);
+        for (int k = 0; k < n + 2; ++k) z[k] = 0;
+        for (uint64_t i = c * a->chunk; i < (c + 1) * a->chunk; ++i) {
+            const double p2 = a->psi[2 * i] * a->psi[2 * i] + a->psi[2 * i + 1] * a->psi[2 * i + 1];
+            z[0] += p2;
+            for (int w = 0; w < n; ++w) z[1 + w] += ((i >> (n - 1 - w)) & 1) ? -p2 : p2;
+            z[n + 1] += (((i >> (n - 1)) ^ i) & 1) ? -p2 : p2;
+        }
+    }
+}
+
+int qo_digest(int n, const double *psi, int nblocks, double *blocks, double *z, int nthreads) {
+    const uint64_t dim = 1ull << n;
+    if (nblocks < 1 || dim % (uint64_t)nblocks) return -1;
+    qo_digest_arg a = {psi, n, dim / (uint64_t)nblocks, blocks};
+    qo_parallel((uint64_t)nblocks, 1, nthreads, qo_digest_part, &a);
+    const uint64_t nch = dim >= 4096 ? 4096 : 1;
+    double *acc = (double *)malloc(sizeof(double) * nch * (n + 2));
+    if (!acc) return -3;
+    qo_z_arg za = {psi, n, acc, dim / nch};
+    qo_parallel(nch, 1, nthreads, qo_z_part, &za);
+    for (int k = 0; k < n + 2; ++k) {
+        double s = 0;
+        for (uint64_t c = 0; c < nch; ++c) s += acc[c * (n + 2) + k];
+        z[k] = s;
+    }
+    free(acc);
+    return 0;
+}

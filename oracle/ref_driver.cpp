@@ -34,6 +34,7 @@
 #include "quasar/qubit/adjoint.hpp"
 #include "quasar/qubit/channel.hpp"
 #include "quasar/qubit/circuit.hpp"
+#include "quasar/parallel.hpp"
 #include "quasar/rng.hpp"
 
 using namespace quasar;
@@ -316,6 +317,150 @@ int ref_density_marginal(int n, const double *rho, int k, const int32_t *wires, 
         QubitState s = density_of(n, rho);
         auto p = marginal_probabilities(s, std::vector<int>(wires, wires + k));
         std::memcpy(out, p.data(), p.size() * sizeof(double));
+    });
+}
+
+// ---- full-size parity fixtures and the bench's reference arm --------------
+// Digest of a state, the same definition as qo_digest (oracle/qsv_oracle.c):
+// per contiguous block, sum |a|^2 and sum a_i w_i with w_i = (+-1) + i(+-1)
+// from the top bits of i * 0x9e3779b97f4a7c15; z[0] = norm, z[1 + w] = <Z_w>
+// (unnormalised), z[n + 1] = <Z_0 Z_{n-1}>. Plain sequential loops.
+static void digest_of(const cvec &v, int n, int nblocks, double *blocks, double *z) {
+    const std::uint64_t dim = std::uint64_t(1) << n, bs = dim / nblocks;
+    for (int b = 0; b < nblocks; ++b) {
+        double s2 = 0, wr = 0, wi = 0;
+        for (std::uint64_t i = b * bs; i < (b + 1) * bs; ++i) {
+            const double re = v(i).real(), im = v(i).imag();
+            const std::uint64_t h = i * 0x9e3779b97f4a7c15ull;
+            const double sr = (h >> 63) ? -1.0 : 1.0, si = ((h >> 62) & 1) ? -1.0 : 1.0;
+            s2 += re * re + im * im;
+            wr += re * sr - im * si;
+            wi += re * si + im * sr;
+        }
+        blocks[3 * b] = s2;
+        blocks[3 * b + 1] = wr;
+        blocks[3 * b + 2] = wi;
+    }
+    for (int k = 0; k < n + 2; ++k) z[k] = 0;
+    for (std::uint64_t i = 0; i < dim; ++i) {
+        const double p2 = std::norm(v(i));
+        z[0] += p2;
+        for (int w = 0; w < n; ++w) z[1 + w] += ((i >> (n - 1 - w)) & 1) ? -p2 : p2;
+        z[n + 1] += (((i >> (n - 1)) ^ i) & 1) ? -p2 : p2;
+    }
+}
+
+/// The reference's forward at full size, reduced to a digest: the state is
+/// |0..0> (init_kind 0) or the seeded Gaussian input (init_kind 1: a_i =
+/// (normal(), normal()) from Rng(seed, label), i ascending, divided by its
+/// FP64 norm), then s = apply_gate(s, g) for every gate -- the loop of
+/// Circuit::forward (circuit.hpp:124-128) without its extra copy of the
+/// initial state, so a 30-qubit run peaks at two states (32 GiB). Writes the
+/// block digest, the Z sums and the amplitudes at `idx`.
+int ref_forward_digest(int n, const RefGate *gates, int ngates, int init_kind, uint64_t seed, const char *label,
+                       int nblocks, double *blocks, double *z, int nsamp, const uint64_t *idx, double *samples,
+                       double *seconds) {
+    return guard([&] {
+        const std::size_t dim = std::size_t(1) << n;
+        QubitState s = QubitState::basis(n);
+        if (init_kind == 1) {
+            Rng rng(seed, label);
+            cvec &v = s.amplitudes(0);
+            double nrm = 0;
+            for (std::size_t i = 0; i < dim; ++i) {
+                const double re = rng.normal();
+                const double im = rng.normal();
+                v(i) = cdouble(re, im);
+                nrm += re * re + im * im;
+            }
+            const double inv = 1.0 / std::sqrt(nrm);
+            for (std::size_t i = 0; i < dim; ++i) v(i) *= inv;
+        }
+        std::vector<Gate> gs;
+        for (int i = 0; i < ngates; ++i) gs.push_back(to_gate(gates[i]));
+        const auto t0 = std::chrono::steady_clock::now();
+        for (const auto &g : gs) s = apply_gate(s, g);
+        const auto t1 = std::chrono::steady_clock::now();
+        if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+        const cvec &v = s.amplitudes(0);
+        digest_of(v, n, nblocks, blocks, z);
+        for (int j = 0; j < nsamp; ++j) {
+            samples[2 * j] = v(idx[j]).real();
+            samples[2 * j + 1] = v(idx[j]).imag();
+        }
+    });
+}
+
+/// A reference QubitState held across calls (bench.py --impl reference): the
+/// state is built once from host amplitudes, then every timed step is
+/// quasar::qubit::apply_gate on it (state.hpp:149-157: gate_matrix, unitarity
+/// check, full copy, strided sweep) -- only the gate loop is timed.
+void *ref_state_new(int n, const double *amps) {
+    QubitState *s = nullptr;
+    int rc = guard([&] {
+        const std::size_t dim = std::size_t(1) << n;
+        s = new QubitState(QubitState::basis(n));
+        cvec &v = s->amplitudes(0);
+        for (std::size_t i = 0; i < dim; ++i) v(i) = cdouble(amps[2 * i], amps[2 * i + 1]);
+    });
+    if (rc) {
+        delete s;
+        return nullptr;
+    }
+    return s;
+}
+
+int ref_state_apply_timed(void *h, const RefGate *gates, int ngates, double *seconds) {
+    return guard([&] {
+        QubitState &s = *static_cast<QubitState *>(h);
+        std::vector<Gate> gs;
+        for (int i = 0; i < ngates; ++i) gs.push_back(to_gate(gates[i]));
+        const auto t0 = std::chrono::steady_clock::now();
+        for (const auto &g : gs) s = apply_gate(s, g);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+void ref_state_free(void *h) { delete static_cast<QubitState *>(h); }
+
+/// Circuit::forward followed by expectation() of the n single-Z observables
+/// for every row (the cfg1 / cfg2 outputs), timed with steady_clock around
+/// both (main.cpp:60-64). nthreads > 1 fans the data rows over host threads
+/// with the reference's own quasar::parallel_for (parallel.hpp:28; rows are
+/// independent), each worker running forward on its rows.
+/// z_out: max(rows,1) x n.
+int ref_time_forward_z(int n, const RefGate *gates, int ngates, const double *data, int rows, int slots,
+                       int nthreads, double *z_out, double *seconds) {
+    return guard([&] {
+        Circuit cir = to_circuit(n, gates, ngates);
+        for (int w = 0; w < n; ++w) cir.observable({w}, "z");
+        const auto t0 = std::chrono::steady_clock::now();
+        if (rows == 0) {
+            QubitState s = cir.forward();
+            auto e = expectation(s, cir);
+            for (int w = 0; w < n; ++w) z_out[w] = e[w];
+        } else {
+            const int T = std::max(1, nthreads);
+            const int per = (rows + T - 1) / T;
+            const int chunks = (rows + per - 1) / per;
+            quasar::parallel_for(
+                static_cast<std::size_t>(chunks),
+                [&](std::size_t c) {
+                    const int r0 = static_cast<int>(c) * per, r1 = std::min(rows, r0 + per);
+                    std::vector<std::vector<double>> d;
+                    for (int r = r0; r < r1; ++r)
+                        d.emplace_back(data + std::size_t(r) * slots, data + std::size_t(r + 1) * slots);
+                    QubitState s = cir.forward(d);
+                    for (int r = r0; r < r1; ++r) {
+                        auto e = expectation(s, cir, static_cast<std::size_t>(r - r0));
+                        for (int w = 0; w < n; ++w) z_out[std::size_t(r) * n + w] = e[w];
+                    }
+                },
+                static_cast<unsigned>(T));
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
     });
 }
 

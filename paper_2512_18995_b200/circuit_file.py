@@ -184,12 +184,21 @@ def build_qubit_circuit(f: CircuitFile) -> Circuit:
     return cir
 
 
+def rank_devices(ranks: int) -> list:
+    """GPU of each rank: round-robin over the visible devices (ranks beyond
+    the device count share GPUs, which only an NCCL that allows it -- the test
+    shim -- accepts)."""
+    nd = max(1, qsv.lib().qsv_device_count())
+    return [r % nd for r in range(ranks)]
+
+
 def run_qubit(f: CircuitFile, seed: int = 0, shots: int = -1, ranks: int = 1, timings: bool = False,
               dtype: int = C128) -> ResultFile:
-    """tools/main.cpp:79-168, dense backend, on the GPU. `ranks` is recorded
-    as the reference does (job.ranks); the state runs on this process's GPU
-    (a multi-GPU run shards it over one process per GPU, results identical
-    by construction, tests/test_dist.cpp:59-62)."""
+    """tools/main.cpp:79-168, dense backend, on the GPU. ranks > 1 runs the
+    distributed branch (tools/main.cpp:86-131): one process driving `ranks`
+    GPUs (qsv_ctx_create_multi, the in-process dist::run_on_ranks), the state
+    sharded with the top log2(ranks) wires global, measurement, expectations
+    and adjoint gradients all-reduced, the state gathered up to 20 qubits."""
     if f.paradigm != "qubit":
         raise InvalidInput(f"paradigm '{f.paradigm}' is outside this engine (qubit state-vector path only)")
     _require(f.backend in ("", "dense"), f"backend '{f.backend}' is outside this engine (dense state vector only)")
@@ -198,11 +207,13 @@ def run_qubit(f: CircuitFile, seed: int = 0, shots: int = -1, ranks: int = 1, ti
     nshots = shots if shots >= 0 else f.shots
     wires = f.measure_wires or list(range(f.nqubit))
     differentiable = cir.encode_slots() > 0 or any(g.trainable and g.params for g in cir.gates())
+    ctx = None
     if ranks > 1:
+        _require(f.backend in ("", "dense"), "distributed runs use the dense backend")
         _require(len(f.data) <= 1, "distributed runs take at most one data row")
-        result.root["job"]["ranks"] = int(ranks)
+        ctx = qsv.Context.multi(rank_devices(ranks))
     t0 = time.perf_counter()
-    state = cir.forward(data=f.data if f.data else None, dtype=dtype)
+    state = cir.forward(data=f.data if f.data else None, dtype=dtype, ctx=ctx)
     if timings:
         result.set_timing("forward", (time.perf_counter() - t0) * 1e3)
     if nshots > 0:
@@ -212,10 +223,14 @@ def run_qubit(f: CircuitFile, seed: int = 0, shots: int = -1, ranks: int = 1, ti
     if cir.observables():
         result.add_expectations(qsv.expectation(state, cir))
     if differentiable and cir.observables() and len(f.data) <= 1:
-        g = qsv.adjoint_gradients(cir, None, f.data[0] if f.data else (), dtype=dtype)
+        g = qsv.adjoint_gradients(cir, None, f.data[0] if f.data else (), dtype=dtype, ctx=ctx)
         result.add_gradients(g.param_grads, g.data_grads)
-    if f.nqubit <= 16 and len(f.data) <= 1:
+    if f.nqubit <= (20 if ranks > 1 else 16) and len(f.data) <= 1:
         result.add_state(state.amplitudes(0))
+    if ranks > 1:
+        result.root["job"]["ranks"] = int(ranks)
+        del state
+        ctx.close()
     return result
 
 

@@ -4,15 +4,45 @@
 // transport_error -> 4, CUDA/internal -> 1. There is no CPU fallback: without
 // a usable CUDA device every state/plan call fails with QSV_ERR_INTERNAL.
 #include <algorithm>
+#include <bit>
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <thread>
 
 #include "qsv_internal.hpp"
 
-struct qsv_ctx : qsv::Ctx {};
-struct qsv_state : qsv::State {};
-struct qsv_plan : qsv::Plan {};
+// A handle is either one rank's object or, on a context made by
+// qsv_ctx_create_multi, a GROUP: one object per rank (`parts`, rank order),
+// every call on it run by one host thread per rank (the reference's
+// dist::run_on_ranks, tests/test_dist.cpp:66-94) with NCCL hidden inside.
+struct qsv_ctx : qsv::Ctx {
+    std::vector<qsv_ctx *> parts;
+    ~qsv_ctx();
+};
+struct qsv_state : qsv::State {
+    std::vector<qsv_state *> parts;
+    ~qsv_state() {
+        for (qsv_state *x : parts) delete x;
+    }
+};
+struct qsv_plan : qsv::Plan {
+    std::vector<qsv_plan *> parts;
+    ~qsv_plan() {
+        for (qsv_plan *x : parts) delete x;
+    }
+};
+
+qsv_ctx::~qsv_ctx() {
+    // NCCL teardown may synchronise with the peers: every rank in its own thread
+    std::vector<std::thread> th;
+    for (qsv_ctx *x : parts)
+        th.emplace_back([x] {
+            cudaSetDevice(x->device);
+            delete x;
+        });
+    for (auto &t : th) t.join();
+}
 
 namespace qsv {
 void build_plan(Plan &p, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts);
@@ -46,6 +76,29 @@ template <typename F> int guard(F &&f) {
     }
 }
 
+// Runs f(r) (an ABI call on rank r's object, returning its status) for every
+// rank of a group, one host thread per rank (collectives inside need every
+// rank to arrive); the first failing rank's status and message are raised.
+template <typename F> void on_ranks(const std::vector<qsv_ctx *> &ranks, F &&f) {
+    const int P = static_cast<int>(ranks.size());
+    std::vector<int> rc(P, 0);
+    std::vector<std::string> msg(P);
+    std::vector<std::thread> th;
+    for (int r = 0; r < P; ++r)
+        th.emplace_back([&, r] {
+            cudaSetDevice(ranks[r]->device);
+            rc[r] = f(r);
+            if (rc[r]) msg[r] = g_err;
+        });
+    for (auto &t : th) t.join();
+    for (int r = 0; r < P; ++r)
+        if (rc[r]) fail(rc[r], "rank " + std::to_string(r) + ": " + msg[r]);
+}
+bool is_group(const qsv_ctx *c) { return c && !c->parts.empty(); }
+bool is_group(const qsv_state *s) { return s && !s->parts.empty(); }
+bool is_group(const qsv_plan *p) { return p && !p->parts.empty(); }
+qsv_ctx *group_ctx(const qsv_state *s) { return static_cast<qsv_ctx *>(s->ctx); }
+
 void init_ctx(Ctx &c, int device) {
     int ndev = 0;
     const cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -63,6 +116,18 @@ void init_ctx(Ctx &c, int device) {
     QSV_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
 }
 
+// Device staging owned for the scope of one transfer (freed on every path,
+// after the stream has drained).
+struct StageBuf {
+    void *p = nullptr;
+    cudaStream_t s;
+    StageBuf(size_t bytes, cudaStream_t st) : s(st) { QSV_CUDA(cudaMalloc(&p, bytes)); }
+    ~StageBuf() {
+        cudaStreamSynchronize(s);
+        cudaFree(p);
+    }
+};
+
 // Chunked host(f64) -> device(dtype) transfer through a bounded staging buffer.
 void upload_f64(State &st, void *dst, const double *host, uint64_t count) {
     cudaStream_t s = st.ctx->stream;
@@ -72,15 +137,13 @@ void upload_f64(State &st, void *dst, const double *host, uint64_t count) {
         return;
     }
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24); // 16 Mi amplitudes (256 MiB f64)
-    void *stage = nullptr;
-    QSV_CUDA(cudaMalloc(&stage, chunk * 16));
+    StageBuf stage(chunk * 16, s);
     for (uint64_t off = 0; off < count; off += chunk) {
         const uint64_t c = std::min(chunk, count - off);
-        QSV_CUDA(cudaMemcpyAsync(stage, host + 2 * off, c * 16, cudaMemcpyHostToDevice, s));
-        launch_convert(static_cast<float *>(dst) + 2 * off, QSV_C64, stage, QSV_C128, 2 * c, s);
+        QSV_CUDA(cudaMemcpyAsync(stage.p, host + 2 * off, c * 16, cudaMemcpyHostToDevice, s));
+        launch_convert(static_cast<float *>(dst) + 2 * off, QSV_C64, stage.p, QSV_C128, 2 * c, s);
     }
     QSV_CUDA(cudaStreamSynchronize(s));
-    cudaFree(stage);
 }
 
 void download_f64(State &st, const void *src, double *host, uint64_t count) {
@@ -91,15 +154,13 @@ void download_f64(State &st, const void *src, double *host, uint64_t count) {
         return;
     }
     const uint64_t chunk = std::min<uint64_t>(count, 1ull << 24);
-    void *stage = nullptr;
-    QSV_CUDA(cudaMalloc(&stage, chunk * 16));
+    StageBuf stage(chunk * 16, s);
     for (uint64_t off = 0; off < count; off += chunk) {
         const uint64_t c = std::min(chunk, count - off);
-        launch_convert(stage, QSV_C128, static_cast<const float *>(src) + 2 * off, QSV_C64, 2 * c, s);
-        QSV_CUDA(cudaMemcpyAsync(host + 2 * off, stage, c * 16, cudaMemcpyDeviceToHost, s));
+        launch_convert(stage.p, QSV_C128, static_cast<const float *>(src) + 2 * off, QSV_C64, 2 * c, s);
+        QSV_CUDA(cudaMemcpyAsync(host + 2 * off, stage.p, c * 16, cudaMemcpyDeviceToHost, s));
         QSV_CUDA(cudaStreamSynchronize(s));
     }
-    cudaFree(stage);
 }
 
 void *row_ptr(State &st, int row) {
@@ -108,11 +169,36 @@ void *row_ptr(State &st, int row) {
 }
 
 // One-gate plan, executed immediately (apply_gate / apply_matrix_strided).
+// A single-qubit matrix on a global wire is the reference's pairwise
+// exchange instead (one message per rank, test_dist.cpp:112-126): cheaper for
+// one gate than a swap in and a swap back.
 void run_single(State &st, const GateRec &g) {
+    if (st.ctx->world > 1 && g.k == 1 && !g.diag && !g.encoded && st.perm[g.wires[0]] >= st.nlocal) {
+        uint64_t lc = 0;
+        bool on = true;
+        for (int c : g.ctls) {
+            const int pb = st.perm[c];
+            if (pb < st.nlocal) lc |= 1ull << pb;
+            else on = on && ((st.ctx->rank >> (pb - st.nlocal)) & 1);
+        }
+        QSV_CUDA(cudaSetDevice(st.ctx->device));
+        dist_exchange_apply(st, st.perm[g.wires[0]], g.m, lc, on, (g.flags & OPF_ZERO_OFF_CONTROL) != 0);
+        return;
+    }
     Plan p;
     build_plan(p, st.ctx, st.n, st.dtype, {g}, 0, nullptr);
     execute_plan(p, st, nullptr, 0, 0);
     QSV_CUDA(cudaStreamSynchronize(st.ctx->stream));
+}
+
+// A group's host view is the whole state: rank r takes amplitudes
+// [r * 2^(n-g), (r + 1) * 2^(n-g)).
+template <typename Ptr, typename F> void group_slices(qsv_state *st, Ptr host, uint64_t count, size_t elem, F &&f) {
+    require(count == st->local_amps, "QubitState: amplitude length mismatch");
+    const uint64_t per = st->parts[0]->local_amps;
+    on_ranks(group_ctx(st)->parts, [&](int r) {
+        return f(st->parts[r], reinterpret_cast<Ptr>(reinterpret_cast<uintptr_t>(host) + r * per * elem), per);
+    });
 }
 
 } // namespace
@@ -159,6 +245,81 @@ int qsv_ctx_create_dist(int device, int rank, int world, const void *uid, qsv_ct
     });
 }
 
+int qsv_ctx_create_multi(int ndev, const int *devices, qsv_ctx **out) {
+    return guard([&] {
+        require(out != nullptr && (ndev == 0 || devices != nullptr), "qsv_ctx_create_multi: null argument");
+        require(ndev >= 1 && (ndev & (ndev - 1)) == 0, "world size must be a power of two"); // test_dist.cpp:90-94
+        auto g = std::make_unique<qsv_ctx>();
+        for (int r = 0; r < ndev; ++r) {
+            auto c = std::make_unique<qsv_ctx>();
+            init_ctx(*c, devices[r]);
+            c->rank = r;
+            c->world = ndev;
+            c->gbits = std::countr_zero(static_cast<unsigned>(ndev));
+            c->in_process = true;
+            g->parts.push_back(c.release());
+        }
+        if (ndev > 1) {
+            std::vector<Ctx *> rk(g->parts.begin(), g->parts.end());
+            nccl_init_all(rk);
+        }
+        Ctx &c0 = *g->parts[0];
+        g->device = c0.device;
+        g->stream = nullptr;  // a group has no stream of its own (rank 0's is reported)
+        g->rank = 0;
+        g->world = ndev;
+        g->gbits = c0.gbits;
+        g->sm_count = c0.sm_count;
+        g->smem_optin = c0.smem_optin;
+        g->in_process = true;
+        *out = g.release();
+    });
+}
+
+int qsv_ctx_rank_ctx(qsv_ctx *group, int rank, qsv_ctx **out) {
+    return guard([&] {
+        require(group && out, "null argument");
+        require(is_group(group), "qsv_ctx_rank_ctx: not a multi-device context");
+        require(rank >= 0 && rank < static_cast<int>(group->parts.size()), "rank out of range");
+        *out = group->parts[rank];
+    });
+}
+
+int qsv_run_on_ranks(qsv_ctx *group, qsv_rank_fn fn, void *user) {
+    return guard([&] {
+        require(group && fn, "null argument");
+        if (!is_group(group)) { // a single rank: run inline
+            const int rc = fn(group, group->rank, user);
+            if (rc) fail(rc, g_err);
+            return;
+        }
+        on_ranks(group->parts, [&](int r) { return fn(group->parts[r], r, user); });
+    });
+}
+
+int qsv_ctx_comm_stats(const qsv_ctx *ctx, uint64_t *messages, uint64_t *bytes, uint64_t *allreduces) {
+    return guard([&] {
+        require(ctx != nullptr, "null ctx");
+        uint64_t m = ctx->stat_messages, b = ctx->stat_bytes, a = ctx->stat_allreduces;
+        for (const qsv_ctx *x : ctx->parts) {
+            m += x->stat_messages;
+            b += x->stat_bytes;
+            a += x->stat_allreduces;
+        }
+        if (messages) *messages = m;
+        if (bytes) *bytes = b;
+        if (allreduces) *allreduces = a;
+    });
+}
+
+int qsv_ctx_comm_reset(qsv_ctx *ctx) {
+    return guard([&] {
+        require(ctx != nullptr, "null ctx");
+        ctx->stat_messages = ctx->stat_bytes = ctx->stat_allreduces = 0;
+        for (qsv_ctx *x : ctx->parts) x->stat_messages = x->stat_bytes = x->stat_allreduces = 0;
+    });
+}
+
 int qsv_ctx_destroy(qsv_ctx *ctx) {
     return guard([&] { delete ctx; });
 }
@@ -166,6 +327,10 @@ int qsv_ctx_destroy(qsv_ctx *ctx) {
 int qsv_ctx_sync(qsv_ctx *ctx) {
     return guard([&] {
         require(ctx != nullptr, "null ctx");
+        if (is_group(ctx)) {
+            on_ranks(ctx->parts, [&](int r) { return qsv_ctx_sync(ctx->parts[r]); });
+            return;
+        }
         QSV_CUDA(cudaStreamSynchronize(ctx->stream));
     });
 }
@@ -173,7 +338,7 @@ int qsv_ctx_sync(qsv_ctx *ctx) {
 int qsv_ctx_stream(qsv_ctx *ctx, void **stream) {
     return guard([&] {
         require(ctx && stream, "null argument");
-        *stream = ctx->stream;
+        *stream = is_group(ctx) ? ctx->parts[0]->stream : ctx->stream;
     });
 }
 
@@ -192,6 +357,21 @@ int qsv_state_create(qsv_ctx *ctx, int nqubit, int batch, int dtype, qsv_state *
         require(batch >= 1, "QubitState: batch must be >= 1");
         require(dtype == QSV_C64 || dtype == QSV_C128, "QubitState: dtype must be QSV_C64 or QSV_C128");
         require(nqubit >= ctx->gbits, "QubitState: fewer amplitudes than ranks");
+        if (is_group(ctx)) { // one slice per rank; the host view is the whole state
+            auto g = std::make_unique<qsv_state>();
+            g->parts.assign(ctx->parts.size(), nullptr);
+            on_ranks(ctx->parts, [&](int r) { return qsv_state_create(ctx->parts[r], nqubit, batch, dtype, &g->parts[r]); });
+            g->ctx = ctx;
+            g->n = nqubit;
+            g->nlocal = nqubit;
+            g->batch = batch;
+            g->dtype = dtype;
+            g->local_amps = 1ull << nqubit;
+            g->perm.resize(nqubit);
+            for (int w = 0; w < nqubit; ++w) g->perm[w] = nqubit - 1 - w;
+            *out = g.release();
+            return;
+        }
         auto st = std::make_unique<qsv_state>();
         st->ctx = ctx;
         st->n = nqubit;
@@ -225,7 +405,7 @@ int qsv_state_info(const qsv_state *st, int *nqubit, int *batch, int *dtype, int
         if (nqubit) *nqubit = st->n;
         if (batch) *batch = st->batch;
         if (dtype) *dtype = st->dtype;
-        if (global_bits) *global_bits = st->ctx->gbits;
+        if (global_bits) *global_bits = st->ctx->gbits;  // a group: log2 of its ranks
         if (local_amps) *local_amps = st->local_amps;
     });
 }
@@ -234,6 +414,10 @@ int qsv_state_set_basis(qsv_state *st, uint64_t index) {
     return guard([&] {
         require(st != nullptr, "null state");
         require(st->n >= 64 || index < (1ull << st->n), "QubitState: basis index out of range"); // state.hpp:36
+        if (is_group(st)) {
+            on_ranks(group_ctx(st)->parts, [&](int r) { return qsv_state_set_basis(st->parts[r], index); });
+            return;
+        }
         const uint64_t owner = index >> st->nlocal;
         launch_set_basis(*st, index & (st->local_amps - 1), owner == static_cast<uint64_t>(st->ctx->rank));
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
@@ -243,6 +427,10 @@ int qsv_state_set_basis(qsv_state *st, uint64_t index) {
 int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count) {
     return guard([&] {
         require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, 16, [&](qsv_state *x, const double *h, uint64_t c) {
+                return qsv_state_upload(x, row, h, c);
+            });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
         upload_f64(*st, row_ptr(*st, row), host, count);
     });
@@ -251,6 +439,10 @@ int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count)
 int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count) {
     return guard([&] {
         require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, 16, [&](qsv_state *x, double *h, uint64_t c) {
+                return qsv_state_download(x, row, h, c);
+            });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
         download_f64(*st, row_ptr(*st, row), host, count);
     });
@@ -259,8 +451,39 @@ int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count) {
 int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t count) {
     return guard([&] {
         require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, st->amp_bytes(), [&](qsv_state *x, const void *h, uint64_t c) {
+                return qsv_state_upload_raw(x, row, h, c);
+            });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
         QSV_CUDA(cudaMemcpyAsync(row_ptr(*st, row), host, count * st->amp_bytes(), cudaMemcpyHostToDevice,
+                                 st->ctx->stream));
+        QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));  // the caller may reuse `host` on return
+    });
+}
+
+int qsv_state_upload_raw_async(qsv_state *st, int row, const void *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, st->amp_bytes(), [&](qsv_state *x, const void *h, uint64_t c) {
+                return qsv_state_upload_raw_async(x, row, h, c);
+            });
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        QSV_CUDA(cudaMemcpyAsync(row_ptr(*st, row), host, count * st->amp_bytes(), cudaMemcpyHostToDevice,
+                                 st->ctx->stream));
+    });
+}
+
+int qsv_state_download_raw_async(qsv_state *st, int row, void *host, uint64_t count) {
+    return guard([&] {
+        require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, st->amp_bytes(), [&](qsv_state *x, void *h, uint64_t c) {
+                return qsv_state_download_raw_async(x, row, h, c);
+            });
+        require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        QSV_CUDA(cudaMemcpyAsync(host, row_ptr(*st, row), count * st->amp_bytes(), cudaMemcpyDeviceToHost,
                                  st->ctx->stream));
     });
 }
@@ -268,6 +491,10 @@ int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t coun
 int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count) {
     return guard([&] {
         require(st && host, "null argument");
+        if (is_group(st))
+            return group_slices(st, host, count, st->amp_bytes(), [&](qsv_state *x, void *h, uint64_t c) {
+                return qsv_state_download_raw(x, row, h, c);
+            });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
         QSV_CUDA(cudaMemcpyAsync(host, row_ptr(*st, row), count * st->amp_bytes(), cudaMemcpyDeviceToHost,
                                  st->ctx->stream));
@@ -278,6 +505,14 @@ int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count) {
 int qsv_state_clone(const qsv_state *src, qsv_state **out) {
     return guard([&] {
         require(src && out, "null argument");
+        if (is_group(src)) {
+            auto g = std::make_unique<qsv_state>();
+            static_cast<qsv::State &>(*g) = static_cast<const qsv::State &>(*src);
+            g->parts.assign(src->parts.size(), nullptr);
+            on_ranks(group_ctx(src)->parts, [&](int r) { return qsv_state_clone(src->parts[r], &g->parts[r]); });
+            *out = g.release();
+            return;
+        }
         auto st = std::make_unique<qsv_state>();
         st->ctx = src->ctx;
         st->n = src->n;
@@ -297,6 +532,7 @@ int qsv_state_clone(const qsv_state *src, qsv_state **out) {
 int qsv_state_device_ptr(qsv_state *st, int row, void **ptr) {
     return guard([&] {
         require(st && ptr, "null argument");
+        require(!is_group(st), "device_ptr: a multi-device state has one pointer per rank (use the rank contexts)");
         *ptr = row_ptr(*st, row);
     });
 }
@@ -304,7 +540,7 @@ int qsv_state_device_ptr(qsv_state *st, int row, void **ptr) {
 int qsv_state_peer_memory(const qsv_state *st, int *out) {
     return guard([&] {
         require(st && out, "null argument");
-        *out = st->p2p;
+        *out = is_group(st) ? st->parts[0]->p2p : st->p2p;
     });
 }
 
@@ -326,6 +562,11 @@ int qsv_apply_matrix(qsv_state *st, int k, const int32_t *wires, int nctl, const
                      int flags) {
     return guard([&] {
         require(st && wires && m, "null argument");
+        if (is_group(st)) {
+            on_ranks(group_ctx(st)->parts,
+                     [&](int r) { return qsv_apply_matrix(st->parts[r], k, wires, nctl, ctls, m, flags); });
+            return;
+        }
         require(k >= 1 && k <= 2, "apply_matrix: 1 or 2 target wires supported");
         require(nctl >= 0 && nctl <= 6 && (nctl == 0 || ctls), "apply_matrix: bad controls");
         GateRec g;
@@ -373,6 +614,10 @@ int qsv_apply_matrix(qsv_state *st, int k, const int32_t *wires, int nctl, const
 int qsv_apply_gate(qsv_state *st, const qsv_gate *gate) {
     return guard([&] {
         require(st && gate, "null argument");
+        if (is_group(st)) {
+            on_ranks(group_ctx(st)->parts, [&](int r) { return qsv_apply_gate(st->parts[r], gate); });
+            return;
+        }
         int cursor = 0;
         qsv_gate g = *gate;
         g.encode = 0; // apply_gate uses the gate's own params (state.hpp:149-151)
@@ -385,6 +630,11 @@ int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const doub
                     const qsv_opts *opts) {
     return guard([&] {
         require(st != nullptr, "null state");
+        if (is_group(st)) {
+            on_ranks(group_ctx(st)->parts,
+                     [&](int r) { return qsv_run_circuit(st->parts[r], gates, ngates, data, rows, slots, opts); });
+            return;
+        }
         Plan p;
         build_plan_from_abi(p, st->ctx, st->n, st->dtype, gates, ngates, opts);
         execute_plan(p, *st, data, rows, slots);
@@ -397,6 +647,17 @@ int qsv_plan_create(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, 
     return guard([&] {
         require(ctx && out, "null argument");
         auto q = std::make_unique<qsv_plan>();
+        if (is_group(ctx)) {
+            q->parts.assign(ctx->parts.size(), nullptr);
+            on_ranks(ctx->parts, [&](int r) {
+                return qsv_plan_create(ctx->parts[r], nqubit, dtype, gates, ngates, opts, &q->parts[r]);
+            });
+            q->ctx = ctx;
+            q->n = nqubit;
+            q->dtype = dtype;
+            *out = q.release();
+            return;
+        }
         build_plan_from_abi(*q, ctx, nqubit, dtype, gates, ngates, opts);
         *out = q.release();
     });
@@ -409,6 +670,7 @@ int qsv_plan_destroy(qsv_plan *plan) {
 int qsv_plan_info_get(const qsv_plan *p, qsv_plan_info *info) {
     return guard([&] {
         require(p && info, "null argument");
+        if (is_group(p)) p = p->parts[0];
         std::memset(info, 0, sizeof(*info));
         info->ngates = p->ngates;
         for (const Step &s : p->steps) {
@@ -430,6 +692,13 @@ int qsv_plan_info_get(const qsv_plan *p, qsv_plan_info *info) {
 int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots) {
     return guard([&] {
         require(plan && st, "null argument");
+        if (is_group(plan) || is_group(st)) {
+            require(is_group(plan) && is_group(st) && plan->parts.size() == st->parts.size(),
+                    "plan/state belong to different contexts");
+            on_ranks(group_ctx(st)->parts,
+                     [&](int r) { return qsv_plan_execute(plan->parts[r], st->parts[r], data, rows, slots); });
+            return;
+        }
         execute_plan(*plan, *st, data, rows, slots);
     });
 }
@@ -437,6 +706,16 @@ int qsv_plan_execute(qsv_plan *plan, qsv_state *st, const double *data, int rows
 int qsv_plan_execute_expect_z(qsv_plan *plan, qsv_state *st, const double *data, int rows, int slots, double *out) {
     return guard([&] {
         require(plan && st && out, "null argument");
+        if (is_group(plan) || is_group(st)) {
+            require(is_group(plan) && is_group(st) && plan->parts.size() == st->parts.size(),
+                    "plan/state belong to different contexts");
+            std::vector<double> other(static_cast<size_t>(st->batch) * st->n * st->parts.size());
+            on_ranks(group_ctx(st)->parts, [&](int r) {
+                double *o = r == 0 ? out : other.data() + static_cast<size_t>(r) * st->batch * st->n;
+                return qsv_plan_execute_expect_z(plan->parts[r], st->parts[r], data, rows, slots, o);
+            });
+            return;
+        }
         execute_plan_z(*plan, *st, data, rows, slots, out);
     });
 }
@@ -444,6 +723,16 @@ int qsv_plan_execute_expect_z(qsv_plan *plan, qsv_state *st, const double *data,
 int qsv_plan_profile(qsv_plan *plan, qsv_state *st, double *launch_ms) {
     return guard([&] {
         require(plan && st && launch_ms, "null argument");
+        if (is_group(plan) || is_group(st)) {  // rank 0's launch times (every rank runs the same steps)
+            require(is_group(plan) && is_group(st) && plan->parts.size() == st->parts.size(),
+                    "plan/state belong to different contexts");
+            std::vector<double> other(plan->parts[0]->steps.size() * st->parts.size());
+            on_ranks(group_ctx(st)->parts, [&](int r) {
+                double *o = r == 0 ? launch_ms : other.data() + r * plan->parts[0]->steps.size();
+                return qsv_plan_profile(plan->parts[r], st->parts[r], o);
+            });
+            return;
+        }
         profile_plan(*plan, *st, launch_ms);
     });
 }
@@ -451,6 +740,12 @@ int qsv_plan_profile(qsv_plan *plan, qsv_state *st, double *launch_ms) {
 int qsv_norm2(qsv_state *st, double *out) {
     return guard([&] {
         require(st && out, "null argument");
+        if (is_group(st)) {
+            std::vector<double> other(static_cast<size_t>(st->batch) * st->parts.size());
+            on_ranks(group_ctx(st)->parts,
+                     [&](int r) { return qsv_norm2(st->parts[r], r == 0 ? out : other.data() + r * st->batch); });
+            return;
+        }
         reduce_norm2(*st, out);
     });
 }
@@ -458,6 +753,13 @@ int qsv_norm2(qsv_state *st, double *out) {
 int qsv_expect_z_all(qsv_state *st, double *out) {
     return guard([&] {
         require(st && out, "null argument");
+        if (is_group(st)) {
+            const size_t per = static_cast<size_t>(st->batch) * st->n;
+            std::vector<double> other(per * st->parts.size());
+            on_ranks(group_ctx(st)->parts,
+                     [&](int r) { return qsv_expect_z_all(st->parts[r], r == 0 ? out : other.data() + r * per); });
+            return;
+        }
         constexpr int kZ = 41;
         std::vector<double> z(static_cast<size_t>(st->batch) * kZ);
         reduce_z_all(*st, z.data());
@@ -511,6 +813,14 @@ void apply_swaps(qsv_state *st, const std::vector<std::pair<int, int>> &pairs) {
 int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
     return guard([&] {
         require(st && (nobs == 0 || (obs && out)), "null argument");
+        if (is_group(st)) {
+            const size_t per = static_cast<size_t>(st->batch) * std::max(nobs, 1);
+            std::vector<double> other(per * st->parts.size());
+            on_ranks(group_ctx(st)->parts, [&](int r) {
+                return qsv_expect_pauli(st->parts[r], nobs, obs, r == 0 ? out : other.data() + r * per);
+            });
+            return;
+        }
         for (int i = 0; i < nobs; ++i) {
             const qsv_obs &o = obs[i];
             const auto moved = localise_xy(st, o);
@@ -571,6 +881,14 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
         require(st && out, "null argument");
         require(k >= 1 && wires, "measure: empty wire list"); // circuit.hpp:185
         require(row >= 0 && row < st->batch, "batch index out of range");
+        if (is_group(st)) {
+            require(k <= 26, "marginal_probs: 1..26 wires supported");
+            std::vector<double> other((size_t(1) << k) * st->parts.size());
+            on_ranks(group_ctx(st)->parts, [&](int r) {
+                return qsv_marginal_probs(st->parts[r], row, k, wires, r == 0 ? out : other.data() + (size_t(r) << k));
+            });
+            return;
+        }
         std::vector<int> bits;
         for (int i = 0; i < k; ++i) {
             require(wires[i] >= 0 && wires[i] < st->n, "target wire out of range");
@@ -582,6 +900,7 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
 
 namespace {
 void require_canonical_density(const qsv_state *st) {
+    require(!is_group(st), "density: mixed states run on one GPU");
     require(st->n % 2 == 0 && st->n >= 2, "density: a mixed state of m qubits is held on 2m engine qubits");
     require(st->nlocal == st->n, "density: mixed states run on one GPU");
     for (int w = 0; w < st->n; ++w)
@@ -658,6 +977,22 @@ int qsv_adjoint_gradients(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *g
         require(nqubit >= 1 && nqubit <= kMaxQubits, "adjoint_gradients: nqubit out of range");
         require(dtype == QSV_C64 || dtype == QSV_C128, "adjoint_gradients: bad dtype");
         require(slots == 0 || data, "adjoint_gradients: data missing");
+        if (is_group(ctx)) {
+            const int P = static_cast<int>(ctx->parts.size());
+            std::vector<std::vector<double>> pgs(P, std::vector<double>(std::max(param_cap, 1))),
+                dgs(P, std::vector<double>(std::max(slots, 1)));
+            std::vector<int> nps(P, 0);
+            on_ranks(ctx->parts, [&](int r) {
+                return qsv_adjoint_gradients(ctx->parts[r], nqubit, dtype, gates, ngates, nobs, obs, init, data, slots,
+                                             pgs[r].data(), param_cap, &nps[r], dgs[r].data());
+            });
+            if (nparams) *nparams = nps[0];
+            if (param_grads)
+                for (int i = 0; i < std::min(param_cap, nps[0]); ++i) param_grads[i] = pgs[0][i];
+            if (data_grads)
+                for (int i = 0; i < slots; ++i) data_grads[i] = dgs[0][i];
+            return;
+        }
         std::vector<double> pg, dg;
         adjoint_gradients(ctx, nqubit, dtype, gates, ngates, nobs, obs, init, data, slots, pg, dg);
         if (nparams) *nparams = static_cast<int>(pg.size());
@@ -775,6 +1110,7 @@ int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset,
 
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
     if (!plan) return -QSV_ERR_INVALID;
+    if (is_group(plan)) plan = plan->parts[0];
     const int n = static_cast<int>(plan->steps.size());
     for (int i = 0; i < n && i < cap && kinds; ++i) {
         const Step &s = plan->steps[i];

@@ -20,6 +20,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <bit>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -42,6 +43,7 @@ struct Nccl {
     void *h = nullptr;
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommInitAll)(ncclComm_t *, int, const int *) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -72,6 +74,7 @@ std::unique_ptr<Nccl> load_nccl() {
     LOAD(GetUniqueId) LOAD(CommInitRank) LOAD(CommDestroy) LOAD(Send) LOAD(Recv) LOAD(GroupStart) LOAD(GroupEnd)
     LOAD(AllReduce) LOAD(GetErrorString)
 #undef LOAD
+    n->CommInitAll = reinterpret_cast<decltype(n->CommInitAll)>(dlsym(n->h, "ncclCommInitAll"));
     return n;
 }
 
@@ -110,6 +113,32 @@ __global__ void block_copy_kernel(V *__restrict__ state, V *__restrict__ stage, 
     }
 }
 
+// new = a * mine + b * theirs on control-satisfied elements (local control
+// bits cmask all set); zero_off_control zeroes the others
+template <typename T, typename V>
+__global__ void exchange_combine_kernel(V *__restrict__ mine, const V *__restrict__ theirs, uint64_t count,
+                                        uint64_t e0, uint64_t cmask, int zoc, double ar, double ai, double br,
+                                        double bi) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        if (((e0 + i) & cmask) != cmask) {
+            if (zoc) mine[i] = V{T(0), T(0)};
+            continue;
+        }
+        const V x = mine[i], y = theirs[i];
+        V o;
+        o.x = static_cast<T>(ar * x.x - ai * x.y + br * y.x - bi * y.y);
+        o.y = static_cast<T>(ar * x.y + ai * x.x + br * y.y + bi * y.x);
+        mine[i] = o;
+    }
+}
+
+template <typename V> __global__ void zero_kernel(V *p, uint64_t count) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+        p[i] = V{};
+}
+
 } // namespace
 
 void nccl_unique_id(void *out128) {
@@ -128,6 +157,20 @@ void nccl_init(Ctx &ctx, const void *uid) {
     ncclComm_t comm = nullptr;
     nccl_ok(*ctx.nccl, ctx.nccl->CommInitRank(&comm, ctx.world, id, ctx.rank), "CommInitRank");
     ctx.comm = comm;
+}
+
+void nccl_init_all(const std::vector<Ctx *> &ranks) {
+    const int W = static_cast<int>(ranks.size());
+    std::vector<int> devs(W);
+    for (int r = 0; r < W; ++r) {
+        ranks[r]->nccl = load_nccl().release();
+        devs[r] = ranks[r]->device;
+    }
+    const Nccl &n = *ranks[0]->nccl;
+    if (!n.CommInitAll) fail(QSV_ERR_TRANSPORT, "NCCL symbol missing: ncclCommInitAll");
+    std::vector<ncclComm_t> comms(W, nullptr);
+    nccl_ok(n, n.CommInitAll(comms.data(), W, devs.data()), "CommInitAll");
+    for (int r = 0; r < W; ++r) ranks[r]->comm = comms[r];
 }
 
 void nccl_destroy(Ctx &ctx) {
@@ -153,6 +196,7 @@ void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count) {
     const Nccl &n = *ctx.nccl;
     nccl_ok(n, n.AllReduce(d_buf, d_buf, count, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx.comm), ctx.stream),
             "AllReduce");
+    ctx.stat_allreduces += 1;
 }
 
 namespace {
@@ -168,6 +212,7 @@ int agree_failures(State &st, int mine) {
     QSV_CUDA(cudaMemcpyAsync(st.d_barrier, &f, sizeof f, cudaMemcpyHostToDevice, ctx.stream));
     nccl_ok(n, n.AllReduce(st.d_barrier, st.d_barrier, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx.comm),
                            ctx.stream), "AllReduce");
+    ctx.stat_allreduces += 1;
     double tot = 0;
     QSV_CUDA(cudaMemcpyAsync(&tot, st.d_barrier, sizeof tot, cudaMemcpyDeviceToHost, ctx.stream));
     QSV_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -195,13 +240,23 @@ bool dist_p2p_ready(State &st) {
         st.scratch = nullptr;
         bad = 1;
     }
-    cudaIpcMemHandle_t mine[2];
-    std::memset(mine, 0, sizeof mine);
+    // what every rank publishes: IPC handles of its two buffers (one process
+    // per GPU) or, when every rank lives in this process (qsv_ctx_create_multi),
+    // the raw pointers and the device they live on
+    struct Pub {
+        cudaIpcMemHandle_t h[2];
+        void *p[2];
+        int dev, pad;
+    };
+    Pub mine;
+    std::memset(&mine, 0, sizeof mine);
+    mine.dev = ctx.device;
     if (!bad) {
         st.p2p_buf[0] = st.d;
         st.p2p_buf[1] = st.scratch;
-        for (int i = 0; i < 2 && !bad; ++i)
-            if (cudaIpcGetMemHandle(&mine[i], st.p2p_buf[i]) != cudaSuccess) {
+        for (int i = 0; i < 2; ++i) mine.p[i] = st.p2p_buf[i];
+        for (int i = 0; i < 2 && !bad && !ctx.in_process; ++i)
+            if (cudaIpcGetMemHandle(&mine.h[i], st.p2p_buf[i]) != cudaSuccess) {
                 cudaGetLastError();
                 bad = 1;
             }
@@ -210,34 +265,40 @@ bool dist_p2p_ready(State &st) {
         st.p2p = -1;
         return false;
     }
-    // exchange: rank r's two handles land in slot r on every rank
+    // exchange: rank r's record lands in slot r on every rank
     const int W = ctx.world;
-    const size_t hb = sizeof mine;
+    const size_t hb = sizeof(Pub);
     unsigned char *d_h = nullptr;
     QSV_CUDA(cudaMalloc(&d_h, hb * W));
-    QSV_CUDA(cudaMemcpyAsync(d_h + hb * ctx.rank, mine, hb, cudaMemcpyHostToDevice, ctx.stream));
+    QSV_CUDA(cudaMemcpyAsync(d_h + hb * ctx.rank, &mine, hb, cudaMemcpyHostToDevice, ctx.stream));
     nccl_ok(n, n.GroupStart(), "GroupStart");
     for (int r = 0; r < W; ++r) {
         if (r == ctx.rank) continue;
         nccl_ok(n, n.Send(d_h + hb * ctx.rank, hb, ncclUint8, r, static_cast<ncclComm_t>(ctx.comm), ctx.stream),
                 "Send");
+        ctx.stat_messages += 1;
+        ctx.stat_bytes += hb;
         nccl_ok(n, n.Recv(d_h + hb * r, hb, ncclUint8, r, static_cast<ncclComm_t>(ctx.comm), ctx.stream), "Recv");
     }
     nccl_ok(n, n.GroupEnd(), "GroupEnd");
-    std::vector<cudaIpcMemHandle_t> all(2 * static_cast<size_t>(W));
+    std::vector<Pub> all(static_cast<size_t>(W));
     QSV_CUDA(cudaMemcpyAsync(all.data(), d_h, hb * W, cudaMemcpyDeviceToHost, ctx.stream));
     QSV_CUDA(cudaStreamSynchronize(ctx.stream));
     cudaFree(d_h);
     std::vector<void *> table(2 * static_cast<size_t>(W), nullptr);
-    for (int r = 0; r < W && !bad; ++r)
+    for (int r = 0; r < W && !bad; ++r) {
+        if (ctx.in_process && r != ctx.rank && all[r].dev != ctx.device) {
+            const cudaError_t e = cudaDeviceEnablePeerAccess(all[r].dev, 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) bad = 1;
+            cudaGetLastError();
+        }
         for (int i = 0; i < 2 && !bad; ++i) {
-            if (r == ctx.rank) {
-                table[static_cast<size_t>(i) * W + r] = st.p2p_buf[i];
+            if (r == ctx.rank || ctx.in_process) {
+                table[static_cast<size_t>(i) * W + r] = r == ctx.rank ? st.p2p_buf[i] : all[r].p[i];
                 continue;
             }
             void *ptr = nullptr;
-            if (cudaIpcOpenMemHandle(&ptr, all[2 * static_cast<size_t>(r) + i], cudaIpcMemLazyEnablePeerAccess) !=
-                cudaSuccess) {
+            if (cudaIpcOpenMemHandle(&ptr, all[r].h[i], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
                 cudaGetLastError();
                 bad = 1;
                 break;
@@ -245,6 +306,7 @@ bool dist_p2p_ready(State &st) {
             st.p2p_opened.push_back(ptr);
             table[static_cast<size_t>(i) * W + r] = ptr;
         }
+    }
     if (!bad) {
         if (cudaMalloc(reinterpret_cast<void **>(&st.d_peers), table.size() * sizeof(void *)) != cudaSuccess) {
             cudaGetLastError();
@@ -272,6 +334,7 @@ void dist_p2p_barrier(State &st) {
     const Nccl &n = *ctx.nccl;
     nccl_ok(n, n.AllReduce(st.d_barrier, st.d_barrier, 1, ncclFloat64, ncclSum, static_cast<ncclComm_t>(ctx.comm),
                            ctx.stream), "AllReduce");
+    ctx.stat_allreduces += 1;
 }
 
 void dist_p2p_release(State &st) {
@@ -400,6 +463,8 @@ void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
         for (int j = 0; j < nv; ++j) {
             nccl_ok(n, n.Send(sb + static_cast<size_t>(j) * r.c * amp, r.c * amp, ncclUint8, peers[j],
                               static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream), "Send");
+            ctx.stat_messages += 1;
+            ctx.stat_bytes += r.c * amp;
             nccl_ok(n, n.Recv(rb + static_cast<size_t>(j) * r.c * amp, r.c * amp, ncclUint8, peers[j],
                               static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream), "Recv");
         }
@@ -424,5 +489,81 @@ void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
     QSV_CUDA(cudaFreeAsync(d_vs, ctx.stream));
 }
 } // namespace
+
+void dist_exchange_apply(State &st, int gbit, const cplx *m, uint64_t local_cmask, bool on, bool zero_off_control) {
+    Ctx &ctx = *st.ctx;
+    require(ctx.world > 1 && ctx.comm, "exchange on a non-distributed state");
+    require(gbit >= st.nlocal && gbit < st.n, "exchange: target is not a rank bit");
+    const int amp = static_cast<int>(st.amp_bytes());
+    const uint64_t total = st.local_amps * static_cast<uint64_t>(st.batch);
+    const int blocks = 148 * 8;
+    if (!on) { // a global control is |0> on this rank and its partner alike
+        if (zero_off_control) {
+            if (amp == 16) zero_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(static_cast<double2 *>(st.d), total);
+            else zero_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(static_cast<float2 *>(st.d), total);
+            QSV_CUDA(cudaGetLastError());
+        }
+        return;
+    }
+    const Nccl &n = *ctx.nccl;
+    const int rb = gbit - st.nlocal;
+    const int peer = ctx.rank ^ (1 << rb);
+    const int b = (ctx.rank >> rb) & 1;
+    const cplx a = m[b * 2 + b], c = m[b * 2 + (1 - b)];
+    static const uint64_t set_cap = [] {
+        const char *e = std::getenv("QSV_SWAP_STAGE_BYTES");
+        return e ? std::max<uint64_t>(256, std::strtoull(e, nullptr, 10)) : (256ull << 20);
+    }();
+    const uint64_t chunk = std::max<uint64_t>(1, std::min<uint64_t>(total, std::bit_floor(set_cap / amp)));
+    const size_t need = 2 * chunk * static_cast<size_t>(amp);
+    if (ctx.stage_bytes < need) {
+        QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+        if (ctx.comm_stream) QSV_CUDA(cudaStreamSynchronize(ctx.comm_stream));
+        cudaFree(ctx.stage);
+        ctx.stage = nullptr;
+        ctx.stage_bytes = 0;
+        QSV_CUDA(cudaMalloc(&ctx.stage, need));
+        ctx.stage_bytes = need;
+    }
+    if (!ctx.comm_stream) QSV_CUDA(cudaStreamCreateWithFlags(&ctx.comm_stream, cudaStreamNonBlocking));
+    cudaEvent_t ready, done;
+    QSV_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    QSV_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    // rounds alternate between the two halves of the staging buffer; each
+    // round's send reads the state chunk BEFORE its combine rewrites it
+    int k = 0;
+    for (uint64_t e0 = 0; e0 < total; e0 += chunk, ++k) {
+        const uint64_t cnt = std::min(chunk, total - e0);
+        unsigned char *mine = static_cast<unsigned char *>(st.d) + e0 * amp;
+        unsigned char *recv = static_cast<unsigned char *>(ctx.stage) + (k % 2) * chunk * amp;
+        QSV_CUDA(cudaEventRecord(ready, ctx.stream));
+        QSV_CUDA(cudaStreamWaitEvent(ctx.comm_stream, ready, 0));
+        nccl_ok(n, n.GroupStart(), "GroupStart");
+        nccl_ok(n, n.Send(mine, cnt * amp, ncclUint8, peer, static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream),
+                "Send");
+        nccl_ok(n, n.Recv(recv, cnt * amp, ncclUint8, peer, static_cast<ncclComm_t>(ctx.comm), ctx.comm_stream),
+                "Recv");
+        nccl_ok(n, n.GroupEnd(), "GroupEnd");
+        ctx.stat_messages += 1;
+        ctx.stat_bytes += cnt * amp;
+        QSV_CUDA(cudaEventRecord(done, ctx.comm_stream));
+        QSV_CUDA(cudaStreamWaitEvent(ctx.stream, done, 0));
+        // element e of the flat (row, index) range: only its bits below nlocal
+        // (its local index) meet the control mask
+        const int g = static_cast<int>(std::min<uint64_t>((cnt + 255) / 256, blocks));
+        if (amp == 16)
+            exchange_combine_kernel<double, double2><<<g, 256, 0, ctx.stream>>>(
+                reinterpret_cast<double2 *>(mine), reinterpret_cast<const double2 *>(recv), cnt, e0, local_cmask,
+                zero_off_control, a.real(), a.imag(), c.real(), c.imag());
+        else
+            exchange_combine_kernel<float, float2><<<g, 256, 0, ctx.stream>>>(
+                reinterpret_cast<float2 *>(mine), reinterpret_cast<const float2 *>(recv), cnt, e0, local_cmask,
+                zero_off_control, a.real(), a.imag(), c.real(), c.imag());
+        QSV_CUDA(cudaGetLastError());
+    }
+    QSV_CUDA(cudaStreamSynchronize(ctx.stream));
+    cudaEventDestroy(ready);
+    cudaEventDestroy(done);
+}
 
 } // namespace qsv

@@ -408,6 +408,7 @@ struct DevBuf {
     void *p = nullptr;
     size_t cap = 0;
     int dev = 0;
+    int unwinding = std::uncaught_exceptions();
     explicit DevBuf(size_t bytes) {
         bytes = std::max<size_t>(bytes, 256);
         QSV_CUDA(cudaGetDevice(&dev));
@@ -426,6 +427,13 @@ struct DevBuf {
         cap = bytes;
     }
     ~DevBuf() {
+        if (std::uncaught_exceptions() > unwinding) {
+            // a reduction threw part-way: kernels using the block may still run
+            // and the host never synchronised, so the block must not be reused;
+            // cudaFree waits for the device before releasing it
+            cudaFree(p);
+            return;
+        }
         BufCache &c = buf_cache();
         std::lock_guard<std::mutex> lk(c.mu);
         c.free_blocks.emplace(cap, std::make_pair(dev, p));

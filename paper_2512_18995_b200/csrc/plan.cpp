@@ -541,6 +541,14 @@ bool plan_uses_jit(const Plan &p) {
     return p.opts.jit > 0 || (p.opts.jit == 0 && p.ngates >= 8 && p.nlocal >= 10);
 }
 
+// Cached CUDA graphs bake the device pointers of p.d_sync / p.d_prefix: a
+// reallocation of either must drop them.
+void drop_graphs(Plan &p) {
+    for (auto &g : p.graphs)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    p.graphs.clear();
+}
+
 namespace {
 void ensure_scratch(State &st) {
     if (!st.scratch) {
@@ -562,6 +570,8 @@ void run_pair(Plan &p, int pi, State &st, cudaStream_t s) {
     const uint64_t nchunks = static_cast<uint64_t>(st.batch) << (p.nlocal - ph.chunk_bits);
     const size_t bytes = (nchunks + 1) * sizeof(unsigned);
     if (bytes > p.d_sync_cap) {
+        QSV_CUDA(cudaStreamSynchronize(s));
+        drop_graphs(p);
         cudaFree(p.d_sync);
         p.d_sync = nullptr;
         QSV_CUDA(cudaMalloc(&p.d_sync, bytes));
@@ -611,7 +621,20 @@ void run_gout(Plan &p, int pi, DevPass &dp, State &st, cudaStream_t s) {
         else rconst |= static_cast<int>(bit << (q - nl));
     }
     void *const *dst = st.d_peers + static_cast<size_t>(1 - st.p2p_cur) * W;
+    // write-after-read: a peer may still be reading the buffer this pass is
+    // about to store into (its own out-of-place step, or the previous plan
+    // execution's last step), so every rank must be here before anyone stores
+    dist_p2p_barrier(st);
     launch_gout(dp, st.d, st.batch, dst, lconst, rconst, s);
+    {  // transport counters: the amplitudes whose destination is another rank
+        int m = 0;
+        for (int b = 0; b < nl; ++b) m += ph.gperm[b] >= nl;
+        if (m > 0) {
+            p.ctx->stat_messages += (1ull << m) - 1;
+            p.ctx->stat_bytes += static_cast<uint64_t>(std::ldexp(
+                static_cast<double>(st.amp_bytes()) * st.batch * (1.0 - std::ldexp(1.0, -m)), nl));
+        }
+    }
     dist_p2p_barrier(st);
     std::swap(st.d, st.scratch);
     st.p2p_cur ^= 1;
@@ -738,6 +761,8 @@ bool execute_graph(Plan &p, State &st) {
             const uint64_t nchunks = static_cast<uint64_t>(st.batch) << (p.nlocal - p.passes[i].chunk_bits);
             const size_t bytes = (nchunks + 1) * sizeof(unsigned);
             if (bytes > p.d_sync_cap) {
+                QSV_CUDA(cudaStreamSynchronize(s));
+                drop_graphs(p);
                 cudaFree(p.d_sync);
                 p.d_sync = nullptr;
                 QSV_CUDA(cudaMalloc(&p.d_sync, bytes));
@@ -745,6 +770,8 @@ bool execute_graph(Plan &p, State &st) {
             }
         }
     if (p.synth && static_cast<size_t>(st.batch) > p.prefix_rows) {
+        QSV_CUDA(cudaStreamSynchronize(s));
+        drop_graphs(p);
         cudaFree(p.d_prefix);
         p.d_prefix = nullptr;
         QSV_CUDA(cudaMalloc(&p.d_prefix, static_cast<size_t>(st.batch) * p.nlocal * 2 * (p.dtype == QSV_C64 ? 8 : 16)));
@@ -823,6 +850,8 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     if (p.synth) {
         const size_t need = static_cast<size_t>(brows) * p.nlocal * 2 * (p.dtype == QSV_C64 ? 8 : 16);
         if (static_cast<size_t>(brows) > p.prefix_rows) {
+            QSV_CUDA(cudaStreamSynchronize(s));
+            drop_graphs(p);
             cudaFree(p.d_prefix);
             p.d_prefix = nullptr;
             QSV_CUDA(cudaMalloc(&p.d_prefix, need));

@@ -236,6 +236,15 @@ struct Ctx {
     void *stage = nullptr;      // qubit-swap staging (2 sets of send + receive), persistent
     size_t stage_bytes = 0;
     cudaStream_t comm_stream = nullptr;  // NCCL transfers of a swap, overlapped with its copies
+    // Transport counters (the reference's Transport::messages_sent /
+    // bytes_sent, tests/test_dist.cpp:96-126), counted as this rank issues
+    // them: point-to-point sends (one per peer per chunk round) and peer-memory
+    // stores of swaps fused into passes (one message per destination rank);
+    // all-reduces (reductions and the peer-memory ordering barrier) apart.
+    uint64_t stat_messages = 0, stat_bytes = 0, stat_allreduces = 0;
+    // every rank is driven from this process (qsv_ctx_create_multi): peer
+    // memory is shared by raw pointers instead of CUDA IPC handles
+    bool in_process = false;
     ~Ctx();
 };
 
@@ -404,12 +413,22 @@ void reduce_dm_marginal(State &st, int m, int row, const std::vector<int> &bits_
 // ---- distributed (dist.cu) -------------------------------------------------
 void nccl_unique_id(void *out128);
 void nccl_init(Ctx &ctx, const void *uid);
+// One process driving every rank: ncclCommInitAll over the ranks' devices.
+void nccl_init_all(const std::vector<Ctx *> &ranks);
 void nccl_destroy(Ctx &ctx);
 // Exchange: swap every physical rank bit `gbit` (>= nlocal) with its local
 // bit `lbit` at once -- one in-place all-to-all over the 2^m - 1 peer ranks
 // (m = pairs), for every batch row, chunked through persistent staging.
 void dist_swap_bits(State &st, const std::vector<std::pair<int, int>> &pairs, void *staging, size_t staging_bytes);
 void dist_allreduce_sum(Ctx &ctx, double *d_buf, size_t count);
+// A single-qubit matrix on a GLOBAL target (physical rank bit gbit): the
+// reference's pairwise exchange (tests/test_dist.cpp:112-126) --
+// each rank sends its whole slice to the partner across that bit and
+// combines the partner's slice with its own, new = m[b][b] * mine +
+// m[b][1-b] * theirs (b = this rank's bit); local controls select elements,
+// global controls whole slices (off-control: untouched, or zeroed with
+// zero_off_control). One message per rank per chunk round.
+void dist_exchange_apply(State &st, int gbit, const cplx *m, uint64_t local_cmask, bool on, bool zero_off_control);
 // Peer memory for swaps fused into passes (collective; agreed by all ranks).
 bool dist_p2p_ready(State &st);
 void dist_p2p_barrier(State &st);

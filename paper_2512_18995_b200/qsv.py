@@ -101,6 +101,11 @@ _SIGS = {
     "qsv_nccl_unique_id": (C.c_int, [C.c_void_p]),
     "qsv_ctx_create_dist": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(_P)]),
     "qsv_ctx_destroy": (C.c_int, [_P]),
+    "qsv_ctx_create_multi": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.POINTER(_P)]),
+    "qsv_ctx_rank_ctx": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
+    "qsv_run_on_ranks": (C.c_int, [_P, C.c_void_p, C.c_void_p]),
+    "qsv_ctx_comm_stats": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "qsv_ctx_comm_reset": (C.c_int, [_P]),
     "qsv_ctx_sync": (C.c_int, [_P]),
     "qsv_ctx_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "qsv_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -113,6 +118,8 @@ _SIGS = {
     "qsv_state_download": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
     "qsv_state_upload_raw": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
     "qsv_state_download_raw": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
+    "qsv_state_upload_raw_async": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
+    "qsv_state_download_raw_async": (C.c_int, [_P, C.c_int, C.c_void_p, C.c_uint64]),
     "qsv_state_clone": (C.c_int, [_P, C.POINTER(_P)]),
     "qsv_state_device_ptr": (C.c_int, [_P, C.c_int, C.POINTER(_P)]),
     "qsv_state_peer_memory": (C.c_int, [_P, C.POINTER(C.c_int)]),
@@ -216,17 +223,53 @@ def _ptr(a: np.ndarray):
 
 # ---------------------------------------------------------------- context ---
 class Context:
-    """Owns one GPU's stream (and, when distributed, its NCCL communicator)."""
+    """Owns one GPU's stream (and, when distributed, its NCCL communicator).
 
-    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None):
+    Context(device)                       one GPU
+    Context(device, rank, world, uid)     one rank of a one-process-per-GPU job
+    Context.multi(devices)                one process driving len(devices) ranks
+                                          (ncclCommInitAll; every call runs on
+                                          all ranks -- dist::run_on_ranks)"""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1, unique_id: bytes | None = None,
+                 _handle=None, _owned: bool = True):
         h = C.c_void_p()
-        if world == 1:
+        if _handle is not None:
+            h = _handle
+        elif world == 1:
             check(lib().qsv_ctx_create(device, C.byref(h)))
         else:
             buf = C.create_string_buffer(unique_id, 128)
             check(lib().qsv_ctx_create_dist(device, rank, world, buf, C.byref(h)))
         self.h = h
+        self._owned = _owned
         self.device, self.rank, self.world = device, rank, world
+        self.multi_ranks = 0
+
+    @staticmethod
+    def multi(devices) -> "Context":
+        devs = [int(d) for d in devices]
+        arr = (C.c_int * max(1, len(devs)))(*devs)
+        h = C.c_void_p()
+        check(lib().qsv_ctx_create_multi(len(devs), arr, C.byref(h)))
+        c = Context(devs[0] if devs else 0, 0, len(devs), _handle=h)
+        c.multi_ranks = len(devs)
+        return c
+
+    def rank_context(self, rank: int) -> "Context":
+        """Rank `rank`'s own context inside a multi-device one (not owned)."""
+        h = C.c_void_p()
+        check(lib().qsv_ctx_rank_ctx(self.h, int(rank), C.byref(h)))
+        return Context(self.device, int(rank), self.world, _handle=h, _owned=False)
+
+    def comm_stats(self) -> dict:
+        """Transport counters (messages, bytes sent; all-reduces apart)."""
+        m, b, a = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(lib().qsv_ctx_comm_stats(self.h, C.byref(m), C.byref(b), C.byref(a)))
+        return {"messages": m.value, "bytes": b.value, "allreduces": a.value}
+
+    def reset_counters(self):
+        check(lib().qsv_ctx_comm_reset(self.h))
 
     @staticmethod
     def nccl_unique_id() -> bytes:

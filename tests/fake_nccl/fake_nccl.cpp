@@ -168,6 +168,30 @@ int ncclCommInitRank(void **comm, int nranks, ncclUniqueId id, int rank) {
     return 0;
 }
 
+// One process driving every rank (qsv_ctx_create_multi): the ranks share one
+// control block; each rank's calls still come from its own host thread
+// (qsv's per-rank workers), so the barriers above work unchanged.
+int ncclCommInitAll(void **comms, int ndev, const int *) {
+    if (ndev < 1 || ndev > kMaxRanks) return 4;
+    ncclUniqueId id;
+    ncclGetUniqueId(&id);
+    for (int r = 0; r < ndev; ++r) {
+        auto *c = new Comm();
+        c->rank = r;
+        c->nranks = ndev;
+        std::memcpy(c->name, id.internal, sizeof(c->name));
+        const int fd = shm_open(c->name, O_CREAT | O_RDWR, 0600);
+        if (fd < 0 || ftruncate(fd, sizeof(Ctl)) != 0) return 2;
+        void *m = mmap(nullptr, sizeof(Ctl), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+        close(fd);
+        if (m == MAP_FAILED) return 2;
+        c->ctl = static_cast<Ctl *>(m);
+        c->ctl->joined.fetch_add(1);
+        comms[r] = c;
+    }
+    return 0;
+}
+
 int ncclCommDestroy(void *comm) {
     auto *c = static_cast<Comm *>(comm);
     barrier(c);

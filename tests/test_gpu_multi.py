@@ -1,0 +1,288 @@
+"""One process driving P ranks (qsv_ctx_create_multi): the reference's
+in-process dist::run_on_ranks model (tests/test_dist.cpp:66-94,
+tools/main.cpp:86-131), run on ONE GPU with every rank on device 0.
+
+NCCL is the host-driven stand-in tests/fake_nccl (ncclCommInitAll; real NCCL
+refuses two ranks on one device). Every rank is a host thread of this process
+with its own stream; kernels never wait on each other -- each rank's
+communication completes on the host (the stand-in synchronises the streams)
+-- so sharing the GPU is safe. Peer memory is shared by raw pointers
+(in-process), so the swaps fused into passes run too. The reference's own
+distributed KATs are restated here, including the two that assert on the
+Transport counters (test_dist.cpp:96-126), which qsv now measures.
+"""
+import os
+import subprocess
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2512_18995_b200 import qsv
+from paper_2512_18995_b200 import workloads as W
+from tests.helpers import random_circuit, random_state
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+SHIM = ROOT / "tests" / "fake_nccl" / "_build" / "libnccl_fake.so"
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _shim():
+    if qsv.lib().qsv_device_count() < 1:
+        pytest.fail("no CUDA device: the -m gpu suite needs a B200")
+    if not SHIM.exists():
+        subprocess.run(["make", "-C", str(SHIM.parent.parent)], check=True, capture_output=True)
+    old = os.environ.get("QSV_NCCL_LIB")
+    os.environ["QSV_NCCL_LIB"] = str(SHIM)
+    yield
+    if old is None:
+        os.environ.pop("QSV_NCCL_LIB", None)
+    else:
+        os.environ["QSV_NCCL_LIB"] = old
+
+
+def multi(world):
+    return qsv.Context.multi([0] * world)
+
+
+def ref_state(n, gates, init=None, data=None):
+    return O.ref_forward(n, gates, init=init, data=data)[0]
+
+
+def test_slice_sizes_match_arithmetic():  # test_dist.cpp:66-78
+    for world, n, per in ((4, 4, 4), (8, 12, 512)):
+        ctx = multi(world)
+        seen = {}
+
+        def body(rc, rank):
+            st = qsv.QubitState(n, ctx=rc)
+            seen[rank] = (st.local_amps, st.global_bits)
+            del st
+
+        qsv.run_on_ranks(ctx, body)
+        assert all(v == (per, world.bit_length() - 1) for v in seen.values()), seen
+        # the group's host view is the whole state
+        g = qsv.QubitState(n, ctx=ctx)
+        assert g.local_amps == 1 << n and g.global_bits == world.bit_length() - 1
+        del g
+        ctx.close()
+
+
+def test_single_rank_degenerates_to_local_simulation():  # test_dist.cpp:80-89
+    rng = qsv.Rng(3, "dist-r1")
+    cir = random_circuit(rng, 5, 15)
+    ctx = multi(1)
+    got = cir.forward(ctx=ctx).amplitudes()
+    assert np.max(np.abs(got - ref_state(5, cir.gates()))) <= 1e-12
+    ctx.close()
+
+
+def test_rejects_non_power_of_two_world():  # test_dist.cpp:90-94
+    with pytest.raises(qsv.InvalidInput):
+        qsv.Context.multi([0, 0, 0])
+
+
+def test_local_gates_send_nothing():  # test_dist.cpp:96-110, on the measured counters
+    ctx = multi(4)
+    stats = {}
+
+    def body(rc, rank):
+        st = qsv.QubitState(6, ctx=rc)
+        rc.reset_counters()
+        for g in (qsv.make_gate("h", [3]), qsv.make_gate("x", [2]), qsv.make_gate("rzz", [4, 5], [], [0.7]),
+                  qsv.make_gate("rz", [0], [], [0.3]), qsv.make_gate("p", [1], [0], [0.9])):
+            st = qsv.apply_gate(st, g)
+        stats[rank] = rc.comm_stats()
+        del st
+
+    qsv.run_on_ranks(ctx, body)
+    for r in range(4):
+        assert stats[r]["messages"] == 0 and stats[r]["bytes"] == 0, stats
+    ctx.close()
+
+
+def test_global_target_does_one_pairwise_exchange():  # test_dist.cpp:112-126
+    cir = qsv.Circuit(3)
+    cir.h(0)
+    want = ref_state(3, cir.gates())
+    ctx = multi(2)
+    stats, parts = {}, {}
+
+    def body(rc, rank):
+        st = qsv.QubitState(3, ctx=rc)
+        rc.reset_counters()
+        st = qsv.apply_gate(st, qsv.make_gate("h", [0]))  # wire 0 is global at R = 2
+        stats[rank] = rc.comm_stats()
+        parts[rank] = st.amplitudes()
+        del st
+
+    qsv.run_on_ranks(ctx, body)
+    for r in range(2):
+        assert stats[r]["messages"] == 1, stats
+        assert stats[r]["bytes"] == 4 * 16, stats  # the whole slice, sizeof(cdouble) per amplitude
+    got = np.concatenate([parts[0], parts[1]])
+    assert np.max(np.abs(got - want)) <= 1e-12
+    ctx.close()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_random_circuits_across_world_sizes(world):  # test_dist.cpp:128-145
+    rng = qsv.Rng(7, "dist-equiv")
+    ctx = multi(world)
+    for trial in range(6):
+        n = 4 + rng.next_below(5)
+        if (1 << n) < 2 * world:
+            continue
+        cir = random_circuit(rng, n, 18)
+        got = cir.forward(ctx=ctx).amplitudes()
+        assert np.max(np.abs(got - ref_state(n, cir.gates()))) <= 1e-12, (world, trial)
+    ctx.close()
+
+
+def test_qft_matches_single_rank_and_is_uniform():  # test_dist.cpp:147-160
+    qft = qsv.qft_circuit(10)
+    ctx = multi(4)
+    got = qft.forward(ctx=ctx).amplitudes()
+    assert np.max(np.abs(got - ref_state(10, qft.gates()))) <= 1e-12
+    assert np.max(np.abs(np.abs(got) - 2.0 ** -5)) <= 1e-12
+    ctx.close()
+
+
+def test_norm_preserved_across_exchanges():  # test_dist.cpp:162-174
+    rng = qsv.Rng(11, "dist-norm")
+    cir = random_circuit(rng, 6, 25)
+    ctx = multi(4)
+    st = qsv.QubitState(6, ctx=ctx)
+    for g in cir.gates():
+        st = qsv.apply_gate(st, g)
+        assert abs(float(st.norm2()[0]) - 1.0) <= 1e-10
+    ctx.close()
+
+
+def test_bell_histogram_and_encoded_expectations():  # test_dist.cpp:176-205
+    ctx = multi(2)
+    st = qsv.QubitState(2, ctx=ctx)
+    st = qsv.apply_gate(st, qsv.make_gate("h", [0]))
+    st = qsv.apply_gate(st, qsv.make_gate("x", [1], [0]))
+    p = qsv.marginal_probabilities(st, [0, 1])
+    assert abs(p[0] - 0.5) <= 1e-12 and abs(p[3] - 0.5) <= 1e-12
+    counts = qsv.measure(st, 1000, [0, 1], qsv.Rng(0, "dist-bell"), True)
+    assert counts["00"]["count"] + counts["11"]["count"] == 1000
+    del st
+    ctx.close()
+    cir = qsv.Circuit(4)
+    cir.rylayer(encode=True)
+    cir.cnot_ring()
+    cir.observable([0], "z")
+    cir.observable([1], "x")
+    data = [[0.0, 1.0, 2.0, 3.0]]
+    single = ref_state(4, cir.gates(), data=data)
+    want = O.ref_expectation(4, single, [([0], "z"), ([1], "x")])
+    ctx = multi(4)
+    st = cir.forward(data=data, ctx=ctx)
+    got = qsv.expectation(st, cir)
+    assert np.max(np.abs(np.array(got) - want)) <= 1e-12
+    del st
+    ctx.close()
+
+
+def test_histogram_matches_seeded_single_rank():  # test_dist.cpp:207-222
+    cir = qsv.Circuit(3)
+    cir.h(0)
+    cir.cnot(0, 1)
+    cir.ry(2, 0.7)
+    single = ref_state(3, cir.gates())
+    want = O.ref_measure(3, single, 500, [0, 1, 2], 9, "hist")
+    ctx = multi(2)
+    st = cir.forward(ctx=ctx)
+    got = qsv.measure(st, 500, [0, 1, 2], qsv.Rng(9, "hist"))
+    for i, c in enumerate(want):
+        key = qsv.bits_to_string(i, 3)
+        assert (got[key]["count"] if key in got else 0) == c
+    del st
+    ctx.close()
+
+
+def test_adjoint_matches_single_rank():  # test_dist.cpp:224-262
+    rng = qsv.Rng(13, "dist-adj")
+    for world in (2, 4):
+        ctx = multi(world)
+        for trial in range(3):
+            c = random_circuit(rng, 5, 14)
+            c.observable([0], "z")
+            c.observable([2], "x")
+            want, _ = O.ref_adjoint(5, c.gates(), [([0], "z"), ([2], "x")])
+            got = qsv.adjoint_gradients(c, ctx=ctx)
+            assert len(got.param_grads) == len(want)
+            assert np.max(np.abs(np.array(got.param_grads) - want)) <= 1e-10, (world, trial)
+        ctx.close()
+
+
+@pytest.mark.parametrize("world,dtype,tol", [(4, qsv.C128, 1e-12), (8, qsv.C64, 1e-5)])
+def test_fused_peer_memory_swaps_in_process(world, dtype, tol):
+    """cfg4 / cfg5 families large enough for specialised passes: the swaps
+    fuse into the passes through in-process peer pointers (no CUDA IPC)."""
+    n = 14
+    cir = W.cfg4_circuit(n, layers=4) if dtype == qsv.C128 else W.cfg5_circuit(n, layers=3)
+    want = ref_state(n, cir.gates())
+    ctx = multi(world)
+    ctx.reset_counters()
+    st = qsv.QubitState(n, dtype=dtype, ctx=ctx)
+    plan = qsv.Plan(n, cir.gates(), dtype=dtype, ctx=ctx)
+    plan.execute(st)
+    assert st.peer_memory() == 1
+    got = st.amplitudes()
+    err = np.max(np.abs(got - want))
+    assert err <= tol, err
+    if dtype == qsv.C64:
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6
+    stats = ctx.comm_stats()
+    assert stats["messages"] > 0 and stats["bytes"] > 0 and stats["allreduces"] > 0
+    # a second execute straight after the first (no host barrier in between):
+    # the write-after-read barrier before each peer-store pass keeps it exact
+    plan.execute(st)
+    plan.execute(st)
+    want3 = O.port_forward(n, cir.gates() * 3)[0]
+    assert np.max(np.abs(st.amplitudes() - want3)) <= 3 * tol
+    del st, plan
+    ctx.close()
+
+
+def test_run_on_ranks_reraises_the_failing_rank():
+    ctx = multi(2)
+
+    def body(rc, rank):
+        if rank == 1:
+            raise ValueError("rank one fails")
+
+    with pytest.raises(ValueError, match="rank one fails"):
+        qsv.run_on_ranks(ctx, body)
+    ctx.close()
+
+
+def test_circuit_file_runs_distributed_like_single():  # tools/main.cpp:86-131
+    from paper_2512_18995_b200 import circuit_file as CF
+
+    src = {"version": 1, "paradigm": "qubit", "nqubit": 6, "shots": 400,
+           "ops": [{"gate": "h", "wires": [0]}, {"gate": "cnot", "wires": [0, 3]},
+                   {"gate": "ry", "wires": [1], "params": [0.4], "trainable": True},
+                   {"gate": "rx", "wires": [0], "params": [1.1], "trainable": True},
+                   {"gate": "cz", "wires": [1, 5]}],
+           "observables": [{"wires": [0], "basis": "z"}, {"wires": [1, 5], "basis": "xz"}]}
+    import json
+    import tempfile
+
+    with tempfile.NamedTemporaryFile("w", suffix=".json", delete=False) as fh:
+        json.dump(src, fh)
+        path = fh.name
+    f = CF.load_circuit_file(path)
+    one = CF.run_qubit(f, seed=5).root
+    four = CF.run_qubit(CF.load_circuit_file(path), seed=5, ranks=4).root
+    assert four["job"]["ranks"] == 4
+    assert one["counts"] == four["counts"]
+    assert np.max(np.abs(np.array(one["expectations"]) - four["expectations"])) <= 1e-12
+    assert np.max(np.abs(np.array(one["gradients"]["params"]) - four["gradients"]["params"])) <= 1e-10
+    assert np.max(np.abs(np.array(one["state"]["re"]) - four["state"]["re"])) <= 1e-12

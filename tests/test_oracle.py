@@ -246,3 +246,66 @@ def test_mixed_state_port_matches_reference():
             assert abs(O.port_density_expectation(n, want, wires, basis) - e) <= 1e-14
         assert np.allclose(O.port_density_marginal(n, want, [2, 0]), O.ref_density_marginal(n, want, [2, 0]),
                            atol=1e-15, rtol=0)
+
+
+# ------------------------------------- threaded oracle and digests (pins) ---
+def test_threaded_rng_fill_matches_sequential_stream():
+    seq = O.port_rng(0, "cfg3", 2, 4096)
+    for off in (0, 2, 1000):
+        got = O.port_rng_normal(0, "cfg3", 4096 - off, offset=off, nthreads=5)
+        assert np.array_equal(got, seq[off:])
+
+
+def test_threaded_forward_matches_reference_and_single_thread():
+    from paper_2512_18995_b200 import workloads as W
+
+    needs_ref()
+    n = 12
+    rng = Rng(17, "mt-forward")
+    for cir in (W.cfg3_circuit(n), W.cfg4_circuit(n, layers=6), W.cfg5_circuit(n, layers=4),
+                random_circuit(rng, n, 120)):
+        psi = random_state(rng, n)
+        want = O.ref_forward(n, cir.gates(), init=psi)[0]
+        single = O.port_forward(n, cir.gates(), init=psi)[0]
+        got = O.port_forward_mt(n, cir.gates(), psi.copy(), nthreads=7)
+        assert np.max(np.abs(got - single)) == 0.0  # same arithmetic, disjoint groups per thread
+        assert np.max(np.abs(got - want)) <= 1e-14
+
+
+def test_digest_of_reference_forward_matches_port_digest():
+    """ref_forward_digest (the reference's apply_gate loop + the C++ digest)
+    against port_forward_mt + qo_digest, Gaussian input from Rng(0,'cfg3')."""
+    from paper_2512_18995_b200 import workloads as W
+
+    needs_ref()
+    n = 14
+    cir = W.cfg3_circuit(n)
+    idx = np.arange(0, 1 << n, 97, dtype=np.uint64)
+    blocks, z, samples, _ = O.ref_forward_digest(n, cir.gates(), 1, 0, "cfg3", idx, nblocks=256)
+    psi = O.port_rng_normal(0, "cfg3", 2 << n).view(np.complex128)
+    psi /= np.sqrt(float(np.dot(psi.view(np.float64), psi.view(np.float64))))
+    O.port_forward_mt(n, cir.gates(), psi)
+    b2, z2 = O.port_digest(n, psi, nblocks=256, nthreads=3)
+    assert np.max(np.abs(samples - psi[idx.astype(np.int64)])) <= 1e-14
+    assert np.max(np.abs(blocks - b2)) <= 1e-13
+    assert np.max(np.abs(z - z2)) <= 1e-13
+    # the digest's Z sums are the reference's expectation_one values
+    want = O.ref_expectation(n, psi, [([w], "z") for w in range(n)] + [([0, n - 1], "zz")])
+    assert np.max(np.abs(z[1:] - want)) <= 1e-13
+
+
+@pytest.mark.parametrize("case", ["cfg3_30", "cfg4_26", "cfg5_26"])
+def test_fullsize_fixtures_are_reference_made_and_self_consistent(case):
+    """The committed full-size fixtures come from the reference (impl "ref");
+    when a threaded-port run of the same case was cross-checked, they agree."""
+    path = GOLD / "fullsize" / f"{case}.npz"
+    if not path.exists():
+        pytest.skip(f"{path.name} not generated yet")
+    d = np.load(path, allow_pickle=False)
+    meta = json.loads(str(d["meta"]))
+    assert meta["impl"] == "ref", meta
+    assert abs(d["z"][0] - 1.0) <= 1e-12  # norm
+    assert abs(d["blocks"][:, 0].sum() - 1.0) <= 1e-12
+    if "cross_check" in meta:
+        cc = meta["cross_check"]
+        assert max(cc["max_abs_sample"], cc["max_abs_z"]) <= 1e-12, cc
