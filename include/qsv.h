@@ -171,6 +171,14 @@ int qsv_run_on_ranks(qsv_ctx *multi, qsv_rank_fn fn, void *user);
  * all-reduces counted apart. On a multi-device context: summed over ranks. */
 int qsv_ctx_comm_stats(const qsv_ctx *ctx, uint64_t *messages, uint64_t *bytes, uint64_t *allreduces);
 int qsv_ctx_comm_reset(qsv_ctx *ctx);
+/* Batched small circuits as independent units: the
+ * `rows` data rows split into contiguous chunks over the devices of a
+ * multi-device context (one independent single-GPU context per device, no
+ * communication), each chunk a from-|0...0> forward with its rows' encode data
+ * followed by every <Z_w>: out[row * nqubit + w] (circuit.hpp:121-157,
+ * 248-282). On a single-GPU context the whole batch runs there. */
+int qsv_run_rows_expect_z(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, const double *data,
+                          int rows, int slots, const qsv_opts *opts, double *out);
 int qsv_ctx_destroy(qsv_ctx *ctx);
 int qsv_ctx_sync(qsv_ctx *ctx);
 /* The cudaStream_t the engine launches on (for events), as void*. */

@@ -33,7 +33,7 @@ def _sources():
 
 def _compile(src: Path) -> Path:
     obj = BUILD / (src.name + ".o")
-    deps = [src, CSRC / "qsv_internal.hpp", INCLUDE / "qsv.h"]
+    deps = [src, CSRC / "qsv_internal.hpp", INCLUDE / "qsv.h"] + sorted(CSRC.glob("*.cuh"))
     if obj.exists() and all(obj.stat().st_mtime >= d.stat().st_mtime for d in deps):
         return obj
     cmd = [NVCC] + CUFLAGS + ["-c", str(src), "-o", str(obj)]

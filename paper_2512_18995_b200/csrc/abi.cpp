@@ -18,6 +18,9 @@
 // dist::run_on_ranks, tests/test_dist.cpp:66-94) with NCCL hidden inside.
 struct qsv_ctx : qsv::Ctx {
     std::vector<qsv_ctx *> parts;
+    // independent single-GPU contexts on the same devices (row sharding of
+    // batched circuits: no communicator, made on first use)
+    std::vector<qsv_ctx *> solo;
     ~qsv_ctx();
 };
 struct qsv_state : qsv::State {
@@ -34,6 +37,7 @@ struct qsv_plan : qsv::Plan {
 };
 
 qsv_ctx::~qsv_ctx() {
+    for (qsv_ctx *x : solo) delete x;
     // NCCL teardown may synchronise with the peers: every rank in its own thread
     std::vector<std::thread> th;
     for (qsv_ctx *x : parts)
@@ -201,6 +205,31 @@ template <typename Ptr, typename F> void group_slices(qsv_state *st, Ptr host, u
     });
 }
 
+// Batched circuit on one context: forward from |0...0> with the rows' encode
+// data, then every <Z_w> per row (the fused epilogue when the pass holds a
+// whole row); the plan and state are freed on every path.
+void detail_run_rows(qsv_ctx *c, int n, int dtype, const qsv_gate *gates, int ngates, const double *data, int rows,
+                     int slots, const qsv_opts *opts, double *out, qsv_plan **pp, qsv_state **ps) {
+    struct Free {
+        qsv_plan **p;
+        qsv_state **s;
+        ~Free() {
+            if (*s) qsv_state_destroy(*s);
+            if (*p) qsv_plan_destroy(*p);
+        }
+    } fr{pp, ps};
+    qsv_opts o{};
+    if (opts) o = *opts;
+    else o.fuse = 1;
+    o.from_zero = 1;
+    auto chk = [](int rc) {
+        if (rc) fail(rc, g_err);
+    };
+    chk(qsv_plan_create(c, n, dtype, gates, ngates, &o, pp));
+    chk(qsv_state_create(c, n, rows, dtype, ps));
+    chk(qsv_plan_execute_expect_z(*pp, *ps, slots ? data : nullptr, slots ? rows : 0, slots, out));
+}
+
 } // namespace
 
 extern "C" {
@@ -317,6 +346,37 @@ int qsv_ctx_comm_reset(qsv_ctx *ctx) {
         require(ctx != nullptr, "null ctx");
         ctx->stat_messages = ctx->stat_bytes = ctx->stat_allreduces = 0;
         for (qsv_ctx *x : ctx->parts) x->stat_messages = x->stat_bytes = x->stat_allreduces = 0;
+    });
+}
+
+int qsv_run_rows_expect_z(qsv_ctx *ctx, int nqubit, int dtype, const qsv_gate *gates, int ngates, const double *data,
+                          int rows, int slots, const qsv_opts *opts, double *out) {
+    return guard([&] {
+        require(ctx && out && rows >= 1 && (slots == 0 || data), "null argument");
+        if (!is_group(ctx)) {  // one GPU: the whole batch
+            qsv_plan *p = nullptr;
+            qsv_state *st = nullptr;
+            detail_run_rows(ctx, nqubit, dtype, gates, ngates, data, rows, slots, opts, out, &p, &st);
+            return;
+        }
+        const int P = static_cast<int>(ctx->parts.size());
+        if (ctx->solo.empty())
+            for (int r = 0; r < P; ++r) {
+                auto c = std::make_unique<qsv_ctx>();
+                init_ctx(*c, ctx->parts[r]->device);
+                ctx->solo.push_back(c.release());
+            }
+        const int per = (rows + P - 1) / P;
+        on_ranks(ctx->solo, [&](int r) {
+            const int r0 = std::min(rows, r * per), r1 = std::min(rows, r0 + per);
+            if (r1 <= r0) return static_cast<int>(QSV_OK);
+            return guard([&] {
+                qsv_plan *p = nullptr;
+                qsv_state *st = nullptr;
+                detail_run_rows(ctx->solo[r], nqubit, dtype, gates, ngates, data + static_cast<size_t>(r0) * slots,
+                                r1 - r0, slots, opts, out + static_cast<size_t>(r0) * nqubit, &p, &st);
+            });
+        });
     });
 }
 
@@ -789,6 +849,9 @@ std::vector<std::pair<int, int>> localise_xy(qsv_state *st, const qsv_obs &o) {
         if (c == 'z' || o.wires[j] < 0 || o.wires[j] >= st->n) continue;
         const int gb = st->perm[o.wires[j]];
         if (gb < st->nlocal) continue;
+        bool done = false;  // a repeated wire is localised once
+        for (const auto &pr : pairs) done = done || pr.first == gb;
+        if (done) continue;
         while (next_lb < st->nlocal && used[next_lb]) ++next_lb;
         require(next_lb < st->nlocal, "observable: no free local qubit to localise a global x/y");
         used[next_lb] = 1;
@@ -838,35 +901,34 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out) {
             require(o.nwires >= 0 && (o.nwires == 0 || (o.wires && o.basis)), "observable: bad wires");
             require(static_cast<int>(std::strlen(o.basis ? o.basis : "")) == o.nwires,
                     "observable: one basis letter per wire"); // circuit.hpp:97
+            // the Paulis applied wire by wire like expectation_one
+            // (circuit.hpp:255-259): per wire the product is i^k X^x Z^z
+            // (X = X, Z = Z, Y = i X Z; Q * i^k X^x Z^z = i^(q+k) (-1)^(b x)
+            // X^(a^x) Z^(b^z) for Q = i^q X^a Z^b), so a repeated wire composes
             uint64_t flip = 0, zy = 0;
-            int ny = 0;
-            // apply the Paulis wire by wire like expectation_one: repeated wires
-            // compose (X X = I etc.), so track the product explicitly.
-            // phase accumulates as i^k from Y/X products on the same wire.
-            std::vector<int> seen;
+            int kph = 0;
             for (int j = 0; j < o.nwires; ++j) {
                 const char c = o.basis[j];
                 require(c == 'x' || c == 'y' || c == 'z', "observable: basis letter outside {x,y,z}");
                 const int w = o.wires[j];
                 require(w >= 0 && w < st->n, "target wire out of range");
-                if (std::find(seen.begin(), seen.end(), w) != seen.end())
-                    fail(QSV_ERR_INVALID, "observable: repeated wire not supported");
-                seen.push_back(w);
                 const int pb = st->perm[w];
                 require(pb < st->nlocal || c == 'z', "observable: internal: x/y on a global qubit after localisation");
                 const uint64_t bit = 1ull << pb;
-                if (c == 'x') flip |= bit;
-                if (c == 'y') flip |= bit, zy |= bit, ++ny;
-                if (c == 'z') zy |= bit;
+                const int q = c == 'y' ? 1 : 0, a = c != 'z', b = c != 'x';
+                kph += q + ((b && (flip & bit)) ? 2 : 0);
+                if (a) flip ^= bit;
+                if (b) zy ^= bit;
             }
+            // the kernel sums conj(a_i) (-1)^popc(i & zy) a_(i ^ flip); X^x Z^z
+            // reads (-1)^popc((i ^ x) & z): a further (-1)^popc(x & z)
+            const int ny = (kph + 2 * std::popcount(flip & zy)) & 3;  // result = i^ny * sum
             std::vector<double> v(static_cast<size_t>(st->batch) * 2);
             reduce_pauli(*st, flip, zy, v.data());
-            // (-i)^ny factor (Y = -i * (-1)^b * X on |b>)
-            const int q = ny & 3;
             for (int b = 0; b < st->batch; ++b) {
                 double re = v[2 * b], im = v[2 * b + 1];
-                for (int t = 0; t < q; ++t) {
-                    const double nre = im, nim = -re; // multiply by -i
+                for (int t = 0; t < ny; ++t) {
+                    const double nre = -im, nim = re; // multiply by i
                     re = nre, im = nim;
                 }
                 if (std::abs(im) >= 1e-10) fail(QSV_ERR_INVALID, "expectation: imaginary residue"); // circuit.hpp:261
@@ -918,29 +980,27 @@ int qsv_density_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double
             require(o.nwires >= 0 && (o.nwires == 0 || (o.wires && o.basis)), "observable: bad wires");
             require(static_cast<int>(std::strlen(o.basis ? o.basis : "")) == o.nwires,
                     "observable: one basis letter per wire"); // circuit.hpp:97
+            // per wire the product i^k X^x Z^z, composed like expectation_one
             uint64_t flip = 0, zy = 0;
-            int ny = 0;
-            std::vector<int> seen;
+            int kph = 0;
             for (int j = 0; j < o.nwires; ++j) {
                 const char c = o.basis[j];
                 require(c == 'x' || c == 'y' || c == 'z', "observable: basis letter outside {x,y,z}");
                 const int w = o.wires[j];
                 require(w >= 0 && w < m, "target wire out of range");
-                if (std::find(seen.begin(), seen.end(), w) != seen.end())
-                    fail(QSV_ERR_INVALID, "observable: repeated wire not supported");
-                seen.push_back(w);
                 const uint64_t bit = 1ull << (m - 1 - w);
-                if (c == 'x') flip |= bit;
-                if (c == 'y') flip |= bit, zy |= bit, ++ny;
-                if (c == 'z') zy |= bit;
+                const int q = c == 'y' ? 1 : 0, a = c != 'z', b = c != 'x';
+                kph += q + ((b && (flip & bit)) ? 2 : 0);
+                if (a) flip ^= bit;
+                if (b) zy ^= bit;
             }
+            const int ny = kph & 3;
             std::vector<double> v(static_cast<size_t>(st->batch) * 2);
             reduce_dm_pauli(*st, m, flip, zy, v.data());
-            // Tr[rho P] = i^ny * sum_r rho[r, r ^ flip] (-1)^popc(r & zy)
-            const int q = ny & 3;
+            // Tr[rho X^x Z^z] = sum_r rho[r, r ^ x] (-1)^popc(r & z)
             for (int b = 0; b < st->batch; ++b) {
                 double re = v[2 * b], im = v[2 * b + 1];
-                for (int t = 0; t < q; ++t) {
+                for (int t = 0; t < ny; ++t) {
                     const double nre = -im, nim = re; // multiply by i
                     re = nre, im = nim;
                 }

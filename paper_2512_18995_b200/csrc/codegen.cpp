@@ -168,16 +168,25 @@ struct Gen {
     // pass so that every 8-thread phase of the pass's shared-memory accesses
     // (each group's set -> slot mapping, the permuted copy-out) hits 8
     // distinct 16-byte bank groups; the default folds bits 3+i, 6+i, 9+i, 12+i.
+    //
+    // complex64 (8-byte amplitudes): the same construction on 16-byte CHUNKS
+    // (amplitude pairs u, u ^ 1 stay together, so the 16-byte cp.async copies
+    // and the pair accesses below keep working): chunk w = u >> 1 becomes
+    // w ^ f(w). A group whose slots hold tile bit 0 moves each register pair
+    // as one 16-byte access (8 threads per shared-memory wavefront: the set's
+    // first three bits must reach 8 distinct chunks); otherwise a thread moves
+    // 8 bytes (16 threads per wavefront: tile bit 0 is the set's first bit,
+    // and its next three bits must reach 8 distinct chunks).
     int swm[3] = {0, 0, 0};
-    bool noswz() const { return !f32 && swm[0] == 0 && swm[1] == 0 && swm[2] == 0; }
+    bool noswz() const { return swm[0] == 0 && swm[1] == 0 && swm[2] == 0; }
     int swz_of(int u) const {
-        if (f32) return swz_host(u, true);
+        const int w = f32 ? u >> 1 : u;
         int f = 0;
-        for (int i = 0; i < 3; ++i) f |= (__builtin_popcount(u & swm[i]) & 1) << i;
-        return u ^ f;
+        for (int i = 0; i < 3; ++i) f |= (__builtin_popcount(w & swm[i]) & 1) << i;
+        return f32 ? (((w ^ f) << 1) | (u & 1)) : u ^ f;
     }
     void choose_swizzle(const std::vector<std::vector<int>> &patterns) {
-        const int K = ph.K;
+        const int K = f32 ? ph.K - 1 : ph.K;  // bits of the swizzled unit (chunk for complex64)
         auto ok = [&](const int m[3], const std::vector<int> &b) {
             // the three phase-varying tile bits must map to independent low-bit vectors
             int v[3];
@@ -704,6 +713,19 @@ struct Gen {
         return c.str();
     }
 
+    // complex64: the register slot whose tile bit is 0 (its register pairs
+    // are adjacent amplitudes, one 16-byte shared-memory access), or -1
+    int pair_slot(const HostGroup &g) const {
+        for (int j = 0; j < R; ++j)
+            if (g.slot_bit[j] == 0) return j;
+        return -1;
+    }
+    // QSV_X_NOPAIR=1 (A/B switch): complex64 register pairs as two 8-byte accesses
+    bool noswz_pairs = [] {
+        const char *e = std::getenv("QSV_X_NOPAIR");
+        return e && e[0] == '1';
+    }();
+
     int threads_of() const { return (kernel_threads(ph, f32 ? QSV_C64 : QSV_C128) + 31) / 32 * 32; }
 
     // A whole single-pass kernel: the pass body over this CTA's tiles (a
@@ -736,10 +758,38 @@ struct Gen {
         const int nsets = 1 << (K - R);
         const int threads = threads_of();
         const bool dbuf = double_buffer;
-        if (f32)
-            o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; const int f = (w >> 3) ^ "
-                 "(w >> 6) ^ (w >> 9) ^ (w >> 12); return ((w ^ (f & 7)) << 1) | (u & 1); }\n";
-        else {
+        if (f32) {
+            // patterns in chunk bits (tile bit b >= 1 is chunk bit b - 1): per
+            // group the first three thread-varying chunk bits of one wavefront
+            std::vector<std::vector<int>> pats;
+            for (const HostGroup &g : ph.groups) {
+                if (ph.K - ph.R < 4) continue;
+                const bool pair = pair_slot(g) >= 0;
+                const int first = pair ? 0 : 1;  // tile bit 0 is ng_bit[0] when it is not a slot
+                if (!pair && g.ng_bit[0] != 0) continue;
+                pats.push_back({g.ng_bit[first] - 1, g.ng_bit[first + 1] - 1, g.ng_bit[first + 2] - 1});
+            }
+            if (!ph.out_perm.empty()) {
+                std::vector<std::pair<int, int>> q;
+                for (int i = 0; i < ph.K; ++i) q.emplace_back(ph.out_perm[ph.tile_pos[i]], i);
+                std::sort(q.begin(), q.end());
+                // 8-byte reads in output order: 16 per wavefront
+                std::vector<int> b;
+                for (int i = 0; i < 4 && i < ph.K; ++i)
+                    if (q[i].second != 0) b.push_back(q[i].second - 1);
+                if (b.size() >= 3) pats.push_back({b[0], b[1], b[2]});
+            }
+            choose_swizzle(pats);
+            const bool oldswz = [] {  // QSV_X_OLDSWZ=1 (A/B): the fixed fold of round 1
+                const char *e = std::getenv("QSV_X_OLDSWZ");
+                return e && e[0] == '1';
+            }();
+            if (oldswz)
+                for (int i = 0; i < 3; ++i) swm[i] = (1 << (3 + i)) | (1 << (6 + i)) | (1 << (9 + i)) | (1 << (12 + i));
+            o << "static __device__ __forceinline__ int swz(int u) { const int w = u >> 1; return ((w ^ ((__popc(w & "
+              << swm[0] << ") & 1) | ((__popc(w & " << swm[1] << ") & 1) << 1) | ((__popc(w & " << swm[2]
+              << ") & 1) << 2))) << 1) | (u & 1); }\n";
+        } else {
             // patterns of this pass: each group's first three set bits, the
             // copy-out's first three input bits
             std::vector<std::vector<int>> pats;
@@ -1075,6 +1125,7 @@ struct Gen {
                           << " + s];\n";
             }
             std::vector<int> uoff(NR, 0);
+            const int pj = f32 && !noswz_pairs ? pair_slot(g) : -1;  // complex64: register slot holding tile bit 0
             std::vector<uint64_t> poff(NR, 0); // physical offsets of the register amplitudes
             for (int r = 0; r < NR; ++r)
                 for (int j = 0; j < R; ++j)
@@ -1111,7 +1162,13 @@ struct Gen {
                 for (int r = 0; r < NR; ++r) {
                     if (from_hbm)
                         o << "      " << V << " v" << r << " = " << ld_in << "(&st[gb + " << poff[r] << "ull]);\n";
-                    else o << "      " << V << " v" << r << " = tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r])
+                    else if (pj >= 0) {  // complex64 pair (tile bit 0 is slot pj): one 16-byte load
+                        if ((r >> pj) & 1) continue;
+                        const int r1 = r | (1 << pj);
+                        o << "      " << V << " v" << r << ", v" << r1 << "; { const float4 q = *(const float4 *)&tile[sb "
+                          << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "]; v" << r << " = mk(q.x, q.y); v" << r1
+                          << " = mk(q.z, q.w); }\n";
+                    } else o << "      " << V << " v" << r << " = tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r])
                            << "];\n";
                 }
             // QSV_DEBUG_NOCOMPUTE=1 (diagnostics only): the pass moves data without
@@ -1148,7 +1205,12 @@ struct Gen {
             for (int r = 0; r < NR; ++r) {
                 if (to_hbm && gout) o << "      " << st_out << "(&pd" << rkr[r] << "[tbo + " << poffo[r] << "ull], v" << r << ");\n";
                 else if (to_hbm) o << "      " << st_out << "(&st[gb + " << poff[r] << "ull], v" << r << ");\n";
-                else o << "      tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = v" << r << ";\n";
+                else if (pj >= 0) {
+                    if ((r >> pj) & 1) continue;
+                    const int r1 = r | (1 << pj);
+                    o << "      *(float4 *)&tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = make_float4(v"
+                      << r << ".x, v" << r << ".y, v" << r1 << ".x, v" << r1 << ".y);\n";
+                } else o << "      tile[sb " << (noswz() ? "+ " : "^ ") << swz_of(uoff[r]) << "] = v" << r << ";\n";
             }
             o << "      (void)pb;\n    }\n";
             if (zhere) {

@@ -82,36 +82,7 @@ void nccl_ok(const Nccl &n, ncclResult_t r, const char *what) {
     if (r != 0) fail(QSV_ERR_TRANSPORT, std::string("NCCL ") + what + ": " + n.GetErrorString(r));
 }
 
-// The m local bits of a swap step (ascending positions) and one block's
-// values: element e of block v <-> the local index with v's bits deposited
-// at those positions.
-struct BlockBits {
-    int m;
-    int pos[8];
-};
-__device__ __forceinline__ uint64_t deposit(uint64_t e, const BlockBits &bb, unsigned v) {
-    uint64_t x = e;
-    for (int i = 0; i < bb.m; ++i) {
-        const int p = bb.pos[i];
-        x = ((x >> p) << (p + 1)) | (static_cast<uint64_t>((v >> i) & 1u) << p) | (x & ((1ull << p) - 1));
-    }
-    return x;
-}
-// gather (dir 0: state -> staging) or scatter (dir 1) of `count` elements
-// starting at e0 of every block listed in vs[0..nv) (slot j <-> vs[j])
-template <typename V>
-__global__ void block_copy_kernel(V *__restrict__ state, V *__restrict__ stage, BlockBits bb, uint64_t e0,
-                                  uint64_t count, const unsigned *__restrict__ vs, int nv, int dir) {
-    const uint64_t total = count * static_cast<uint64_t>(nv);
-    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const int j = static_cast<int>(i / count);
-        const uint64_t e = e0 + (i - static_cast<uint64_t>(j) * count);
-        const uint64_t idx = deposit(e, bb, vs[j]);
-        if (dir == 0) stage[i] = state[idx];
-        else state[idx] = stage[i];
-    }
-}
+#include "swap_copy.cuh"  // BlockBits, deposit, block_copy_kernel
 
 // new = a * mine + b * theirs on control-satisfied elements (local control
 // bits cmask all set); zero_off_control zeroes the others
@@ -407,7 +378,8 @@ void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
         return e ? std::max<uint64_t>(256, std::strtoull(e, nullptr, 10)) : (256ull << 20);
     }();
     const uint64_t want = std::min<uint64_t>(block * nv, set_cap / amp);
-    const uint64_t chunk = std::max<uint64_t>(1, want / nv);  // elements per block per round
+    // elements per block per round, a power of two (rounds stay aligned)
+    const uint64_t chunk = std::bit_floor(std::max<uint64_t>(1, want / nv));
     const size_t set_bytes = 2 * chunk * nv * static_cast<size_t>(amp);
     if (ctx.stage_bytes < 2 * set_bytes) {
         QSV_CUDA(cudaStreamSynchronize(ctx.stream));
@@ -442,17 +414,26 @@ void swap_disjoint(State &st, const std::vector<std::pair<int, int>> &pairs) {
     auto set_ptr = [&](size_t k, int recv) {
         return static_cast<unsigned char *>(ctx.stage) + (k % 2) * set_bytes + (recv ? set_bytes / 2 : 0);
     };
+    // 16-byte vectors: a c64 pair of neighbouring amplitudes moves as one
+    // float4 when bit 0 is not a swapped bit (element e = amplitude pair)
+    const bool pair64 = amp == 8 && bb.pos[0] >= 1 && chunk % 2 == 0;
+    BlockBits bbv = bb;
+    if (pair64)
+        for (int i = 0; i < m; ++i) bbv.pos[i] -= 1;
     auto copy = [&](size_t k, int dir) {
         const Round &r = rounds[k];
         unsigned char *base = static_cast<unsigned char *>(st.d) + static_cast<size_t>(r.row) * st.local_amps * amp;
-        const int blocks = static_cast<int>(std::min<uint64_t>((r.c * nv + 255) / 256, 148 * 8));
         unsigned char *buf = set_ptr(k, dir);
-        if (amp == 16)
-            block_copy_kernel<double2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
-                reinterpret_cast<double2 *>(buf), bb, r.e0, r.c, d_vs, nv, dir);
+        const uint64_t cnt = pair64 ? r.c / 2 : r.c, e0 = pair64 ? r.e0 / 2 : r.e0;
+        const dim3 grid(static_cast<unsigned>(std::max<uint64_t>(1, std::min<uint64_t>((cnt + 255) / 256,
+                                                                                       (148 * 8 + nv - 1) / nv))),
+                        static_cast<unsigned>(nv));
+        if (amp == 16 || pair64)
+            block_copy_kernel<double2><<<grid, 256, 0, ctx.stream>>>(reinterpret_cast<double2 *>(base),
+                reinterpret_cast<double2 *>(buf), pair64 ? bbv : bb, e0, cnt, d_vs, dir);
         else
-            block_copy_kernel<float2><<<blocks, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
-                reinterpret_cast<float2 *>(buf), bb, r.e0, r.c, d_vs, nv, dir);
+            block_copy_kernel<float2><<<grid, 256, 0, ctx.stream>>>(reinterpret_cast<float2 *>(base),
+                reinterpret_cast<float2 *>(buf), bb, r.e0, r.c, d_vs, dir);
         QSV_CUDA(cudaGetLastError());
     };
     auto transfer = [&](size_t k) {

@@ -106,6 +106,8 @@ _SIGS = {
     "qsv_run_on_ranks": (C.c_int, [_P, C.c_void_p, C.c_void_p]),
     "qsv_ctx_comm_stats": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "qsv_ctx_comm_reset": (C.c_int, [_P]),
+    "qsv_run_rows_expect_z": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.c_void_p, C.c_int,
+                                        C.c_int, C.POINTER(qsv_opts), C.c_void_p]),
     "qsv_ctx_sync": (C.c_int, [_P]),
     "qsv_ctx_stream": (C.c_int, [_P, C.POINTER(_P)]),
     "qsv_ctx_rank": (C.c_int, [_P, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
@@ -767,6 +769,24 @@ def make_opts(opts: dict | None) -> qsv_opts:
     for k, v in (opts or {}).items():
         setattr(o, k, int(v))
     return o
+
+
+def run_rows_expect_z(cir: "Circuit", data, dtype: int = C64, ctx: Context | None = None,
+                      opts: dict | None = None) -> np.ndarray:
+    """Batched small circuits as independent units (cfg2): every data row a
+    from-|0...0> forward of `cir`, then all <Z_w> -- rows x n. On a
+    multi-device context the rows split over the devices with no
+    communication (qsv_run_rows_expect_z)."""
+    ctx = ctx or default_context()
+    d = np.ascontiguousarray(np.asarray(data, dtype=np.float64))
+    rows = d.shape[0]
+    slots = d.shape[1] if d.ndim == 2 else 0
+    arr, keep = gate_array(cir.gates())
+    o = make_opts(opts)
+    out = np.zeros(rows * cir.nqubit())
+    check(lib().qsv_run_rows_expect_z(ctx.h, cir.nqubit(), dtype, arr, len(cir.gates()), _ptr(d) if slots else None,
+                                      rows, slots, C.byref(o), _ptr(out)))
+    return out.reshape(rows, cir.nqubit())
 
 
 class Plan:

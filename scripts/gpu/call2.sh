@@ -1,0 +1,4 @@
+python -c "from paper_2512_18995_b200 import build; build.build()"
+make -C tests/fake_nccl >/dev/null
+timeout 900 python -m pytest tests/test_gpu_multi.py -q -x 2>&1 | tail -30
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -30

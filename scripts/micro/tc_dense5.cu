@@ -220,6 +220,134 @@ __global__ void __launch_bounds__(128 * G, G == 1 ? 2 : 1) tc_kernel(const float
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(kCols));
 }
 
+// NB dense blocks per tile, back to back: the question a fused pass with
+// several 5-qubit stages asks (cfg5: ~7 one-layer blocks per 13-qubit tile).
+// After each block's MMAs the accumulator is drained to registers, split
+// into hi / lo again and written as the next block's A (thread t = set row
+// t, conflict-free in the 128-byte-swizzled K-major layout); only the last
+// block's output goes back to HBM. Same B for every block (timing only).
+template <int NB>
+__global__ void __launch_bounds__(128, 2) tc_chain_kernel(const float4 *__restrict__ in, float4 *__restrict__ out,
+                                                         const float *__restrict__ Bg, uint64_t nsets_total) {
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char *sm = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);
+    const int t = threadIdx.x, warp = t >> 5;
+    unsigned char *Ahi = sm, *Alo = Ahi + kAbytes, *Bhi = sm + 2 * kAbytes, *Blo = Bhi + kBbytes;
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base;
+    for (int q = t; q < kN * kK / 4; q += 128) {
+        const int n = q / (kK / 4), c = q % (kK / 4);
+        float4 v = reinterpret_cast<const float4 *>(Bg)[q];
+        float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+        float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+        *reinterpret_cast<float4 *>(Bhi + kmaj_off<kN>(n, c)) = h;
+        *reinterpret_cast<float4 *>(Blo + kmaj_off<kN>(n, c)) = l;
+    }
+    if (t < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(64));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)));
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((128 >> 4) << 24);
+    uint32_t phase = 0;
+    const uint64_t iters = nsets_total / kSets;
+    for (uint64_t it = blockIdx.x; it < iters; it += gridDim.x) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const float4 v = ld_in(in + it * (kSets * kK / 4), t, j);
+            const int m = in_row(t, j), c = in_chunk(t, j);
+            float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+            float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+            *reinterpret_cast<float4 *>(Ahi + kmaj_off<kSets>(m, c)) = h;
+            *reinterpret_cast<float4 *>(Alo + kmaj_off<kSets>(m, c)) = l;
+        }
+        uint32_t r[64];
+        for (int b = 0; b < NB; ++b) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (t == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const unsigned char *As[3] = {Ahi, Ahi, Alo};
+                const unsigned char *Bs[3] = {Bhi, Blo, Bhi};
+                int acc = 0;
+                for (int p = 0; p < 3; ++p)
+                    for (int ks = 0; ks < kK / 8; ++ks) {
+                        const uint64_t ad = sdesc(smem_u32(As[p]) + kstep<kSets>(ks));
+                        const uint64_t bd = sdesc(smem_u32(Bs[p]) + kstep<kN>(ks));
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                            "l"(ad), "l"(bd), "r"(idesc), "r"(acc));
+                        acc = 1;
+                    }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    smem_u32(&mbar)));
+            }
+            {
+                uint32_t done = 0;
+                for (long spin = 0; !done; ++spin) {
+                    asm volatile(
+                        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                        : "=r"(done)
+                        : "r"(smem_u32(&mbar)), "r"(phase));
+                    if (spin > (1l << 26)) __trap();
+                }
+            }
+            phase ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            const uint32_t taddr = tmem + ((static_cast<uint32_t>(warp) * 32) << 16);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+                "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%"
+                "46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                  "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                  "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]),
+                  "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]),
+                  "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]),
+                  "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]),
+                  "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            __syncthreads();  // every MMA read of A is done (waited) before A is rewritten
+            if (b + 1 < NB) {
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const float4 v = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                                 __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+                    float4 h = make_float4(tf32_hi(v.x), tf32_hi(v.y), tf32_hi(v.z), tf32_hi(v.w));
+                    float4 l = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+                    *reinterpret_cast<float4 *>(Ahi + kmaj_off<kSets>(t, c)) = h;
+                    *reinterpret_cast<float4 *>(Alo + kmaj_off<kSets>(t, c)) = l;
+                }
+            }
+        }
+        float4 *stg = reinterpret_cast<float4 *>(Alo);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+            stg[t * 16 + (c ^ (t & 15))] = make_float4(__uint_as_float(r[4 * c]), __uint_as_float(r[4 * c + 1]),
+                                                       __uint_as_float(r[4 * c + 2]), __uint_as_float(r[4 * c + 3]));
+        __syncthreads();
+        float4 *dst = out + it * (kSets * kK / 4);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const int q = t + 128 * j, m = q >> 4, c = q & 15;
+            __stcs(dst + q, stg[m * 16 + (c ^ (m & 15))]);
+        }
+        __syncthreads();
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();
+    if (t < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(64));
+}
+
 // CUDA cores: thread = one set, D[n] = sum_k B[n][k] x[k] (B from shared memory)
 __global__ void __launch_bounds__(128) fma_kernel(const float4 *__restrict__ in, float4 *__restrict__ out,
                                                   const float *__restrict__ Bg, uint64_t nsets_total) {
@@ -328,5 +456,17 @@ int main(int argc, char **argv) {
             mag = std::fmax(mag, std::fabs(y));
         }
     std::printf("max |err| vs FP64: tc (3xTF32) %.3e, fma %.3e (max |y| %.3f)\n", err_tc, err_fma, mag);
+    // several dense blocks per tile (one HBM sweep): does the TC side stay
+    // under the memory time as a pass fuses more 5-qubit stages?
+    const int smemc = 2 * kAbytes + 2 * kBbytes + 1024;
+    CK(cudaFuncSetAttribute(tc_chain_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemc));
+    CK(cudaFuncSetAttribute(tc_chain_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemc));
+    CK(cudaFuncSetAttribute(tc_chain_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemc));
+    CK(cudaFuncSetAttribute(tc_chain_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, smemc));
+    timeit("chn1", [&] { tc_chain_kernel<1><<<sms * 2, 128, smemc>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 256.0);
+    timeit("chn2", [&] { tc_chain_kernel<2><<<sms * 2, 128, smemc>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 512.0);
+    timeit("chn4", [&] { tc_chain_kernel<4><<<sms * 2, 128, smemc>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 1024.0);
+    timeit("chn7", [&] { tc_chain_kernel<7><<<sms * 2, 128, smemc>>>((const float4 *)din, (float4 *)dout, dB, nsets); }, 1792.0);
+    CK(cudaGetLastError());
     return 0;
 }

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <string>
 
+#include "quasar/qubit/adjoint.hpp"
 #include "quasar/qubit/circuit.hpp"
 #include "qsv/quasar_bridge.hpp"
 
@@ -112,6 +113,45 @@ int main() {
         for (int i = 0; i < 7; ++i) q.swap(i, 13 - i);
         QubitState init = QubitState::basis(14, 12345);
         CHECK(maxdiff(q.forward(init).amplitudes(), gpu::forward(q, init).amplitudes()) < 1e-12, "qft14");
+    }
+    {   // measure: seeded histograms equal to the reference's (circuit.hpp:217-244)
+        Circuit cir(3);
+        cir.h(0);
+        cir.cnot(0, 1);
+        cir.ry(2, 0.7);
+        QubitState s = cir.forward();
+        Rng r1(9, "hist"), r2(9, "hist");
+        const auto want = measure(s, 500, {0, 1, 2}, r1, true);
+        const auto got = gpu::measure(gpu::forward(cir), 500, {0, 1, 2}, r2, true);
+        bool same = want.size() == got.size();
+        for (const auto &[k, e] : want)
+            same = same && got.count(k) && got.at(k).count == e.count &&
+                   std::abs(got.at(k).probability - e.probability) < 1e-12;
+        CHECK(same, "measure histogram");
+        const auto pw = marginal_probabilities(s, {2, 0}), pg = gpu::marginal_probabilities(s, {2, 0});
+        double d = 0;
+        for (size_t i = 0; i < pw.size(); ++i) d = std::max(d, std::abs(pw[i] - pg[i]));
+        CHECK(d < 1e-12, "marginal_probabilities");
+    }
+    {   // adjoint_gradients (adjoint.hpp:52-110), trainable + encoded
+        Circuit cir(4);
+        cir.rylayer(true);
+        cir.cnot_ring();
+        cir.rx(1, 0.3, true);
+        cir.cry(2, 3, 1.1, true);
+        cir.add(make_gate("u3", {0}, {}, {0.2, 0.4, 0.6}, true));
+        cir.observable({0}, "z");
+        cir.observable({1, 3}, "xy");
+        const std::vector<double> data{0.1, 0.5, -0.9, 2.0};
+        const auto want = adjoint_gradients(cir, QubitState::basis(4), data);
+        const auto got = gpu::adjoint_gradients(cir, QubitState::basis(4), data);
+        double d = 0;
+        bool shape = want.param_grads.size() == got.param_grads.size() && want.data_grads.size() == got.data_grads.size();
+        for (size_t i = 0; shape && i < want.param_grads.size(); ++i)
+            d = std::max(d, std::abs(want.param_grads[i] - got.param_grads[i]));
+        for (size_t i = 0; shape && i < want.data_grads.size(); ++i)
+            d = std::max(d, std::abs(want.data_grads[i] - got.data_grads[i]));
+        CHECK(shape && d < 1e-10, "adjoint_gradients");
     }
     std::printf("%d/%d checks passed\n", checks - failures, checks);
     return failures ? 1 : 0;

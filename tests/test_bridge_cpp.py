@@ -7,6 +7,8 @@ from pathlib import Path
 import pytest
 
 BIN = Path(__file__).resolve().parent / "cpp" / "_build" / "test_bridge"
+BIN_DIST = BIN.parent / "test_bridge_dist"
+SHIM = Path(__file__).resolve().parent / "fake_nccl" / "_build" / "libnccl_fake.so"
 
 
 @pytest.mark.gpu
@@ -25,3 +27,20 @@ def test_cpp_bridge_builds():
     r = subprocess.run(["make", "-C", str(BIN.parent.parent)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
     assert BIN.exists()
+
+
+@pytest.mark.gpu
+def test_cpp_bridge_dist_kats(built):
+    """tests/test_dist.cpp's KATs through quasar::qubit::gpu::dist, P ranks as
+    host threads of one process on device 0 (the NCCL stand-in)."""
+    import os
+
+    if not BIN_DIST.exists():
+        pytest.skip("tests/cpp/_build/test_bridge_dist not built (needs /root/reference at build time)")
+    if not SHIM.exists():
+        subprocess.run(["make", "-C", str(SHIM.parent.parent)], check=True, capture_output=True)
+    env = dict(os.environ, QSV_NCCL_LIB=str(SHIM))
+    r = subprocess.run([str(BIN_DIST)], capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "checks passed" in r.stdout

@@ -286,3 +286,18 @@ def test_circuit_file_runs_distributed_like_single():  # tools/main.cpp:86-131
     assert np.max(np.abs(np.array(one["expectations"]) - four["expectations"])) <= 1e-12
     assert np.max(np.abs(np.array(one["gradients"]["params"]) - four["gradients"]["params"])) <= 1e-10
     assert np.max(np.abs(np.array(one["state"]["re"]) - four["state"]["re"])) <= 1e-12
+
+
+def test_cfg2_rows_sharded_over_devices_match_one_device():
+    """cfg2's circuits are independent units -- rows split
+    over the devices of a multi-device context, no communication."""
+    cir, data = W.cfg2_circuit(12, layers=6, rows=1000)
+    one = qsv.run_rows_expect_z(cir, data, dtype=qsv.C64)
+    ctx = multi(4)
+    four = qsv.run_rows_expect_z(cir, data, dtype=qsv.C64, ctx=ctx)
+    ctx.close()
+    assert np.max(np.abs(one - four)) <= 1e-6
+    want = O.port_forward(12, cir.gates(), data=data[:8])
+    for r in range(8):
+        wz = [O.port_expectation(12, want[r], [q], "z")[0] for q in range(12)]
+        assert np.max(np.abs(four[r] - wz)) <= 1e-5

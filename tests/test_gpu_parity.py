@@ -255,6 +255,40 @@ def test_expectations_all_pauli_strings_vs_reference():
         assert abs(z[q] - O.port_expectation(n, psi, [q], "z")[0]) < 1e-12
 
 
+def test_expectations_with_repeated_wires_compose_like_the_reference():
+    """expectation_one applies the Paulis wire by wire (circuit.hpp:255-259):
+    a repeated wire composes (Z Z = I, Z X = iY, ...); an imaginary result is
+    refused like circuit.hpp:261."""
+    rng = Rng(23, "pauli-repeat")
+    n = 5
+    psi = random_state(rng, n)
+    s = QubitState.from_amplitudes(n, psi)
+    cases = [([0, 0], "zz"), ([1, 1], "xx"), ([2, 2], "yy"), ([0, 1, 0], "xzx"), ([3, 3, 3], "xyz"),
+             ([1, 1], "xz"), ([4, 2, 4], "yzx"), ([0, 0, 1, 1], "xyyx")]
+    for _ in range(30):
+        k = 2 + rng.next_below(4)
+        wires = [rng.next_below(3) for _ in range(k)]
+        cases.append((wires, "".join("xyz"[rng.next_below(3)] for _ in wires)))
+    seen_err = seen_ok = 0
+    for w, b in cases:
+        want, im = O.port_expectation(n, psi, w, b)
+        if O.REF_LIB.exists():
+            try:
+                ref = O.ref_expectation(n, psi, [(w, b)])[0]
+                assert abs(ref - want) < 1e-14
+            except O.OracleError as e:
+                assert e.code == 2 and abs(im) >= 1e-10
+        if abs(im) >= 1e-10:
+            with pytest.raises(qsv.InvalidInput):
+                qsv.expectation_many(s, [qsv.Observable(w, b)])
+            seen_err += 1
+        else:
+            got = qsv.expectation_many(s, [qsv.Observable(w, b)])[0][0]
+            assert abs(got - want) < 1e-12, (w, b)
+            seen_ok += 1
+    assert seen_err and seen_ok
+
+
 # ------------------------------------------------ config families ----
 def test_cfg1_full_20q_vs_reference():
     cir = W.cfg1_circuit(20)
