@@ -575,7 +575,125 @@ struct Gen {
     // against 2^(R-1) per single-bit target + 2^R per all-slot target when
     // every target is applied on its own. A uniform real register scale
     // (the deferred 1/sqrt(2)^h of the butterflies) rides on the root.
+    // Every value a flush target's factor can take is exactly +-1 (CZ-type
+    // phases against bits outside the register group, e.g. cfg5's random-pair
+    // CZs): the factor is then a sign and the flush a sign-bit XOR on the
+    // integer pipe instead of complex multiplies on the FMA pipe.
+    static bool pm1(const cplx &v) { return v.imag() == 0.0 && (v.real() == 1.0 || v.real() == -1.0); }
+    bool target_is_sign(const FlushTarget &t) const {
+        auto tab_ok = [&](int off, int len) {
+            for (int i = 0; i < len; ++i)
+                if (!pm1(ph.tables[off + i])) return false;
+            return true;
+        };
+        auto rec_ok = [&](int b, int e) {
+            for (int k = b; k < e; ++k) {
+                const DiagRec &r = ph.recs[k];
+                for (int i = 0; i < (1 << r.nt); ++i)
+                    if (!pm1(cplx(r.val[2 * i], r.val[2 * i + 1]))) return false;
+            }
+            return true;
+        };
+        const int nb = ph.K - ph.R;
+        if (t.ext_tab >= 0 && !tab_ok(t.ext_tab, 256 * t.ext_chunks)) return false;
+        if (!rec_ok(t.ext_rest, t.ext_end) || !rec_ok(t.mix_begin, t.mix_end)) return false;
+        if (t.table >= 0 && !tab_ok(t.table, 1 << nb)) return false;
+        if (t.table_lo >= 0 && !tab_ok(t.table_lo, 1 << t.lo_bits)) return false;
+        if (t.table_hi >= 0 && !tab_ok(t.table_hi, 1 << (nb - t.lo_bits))) return false;
+        return true;
+    }
+    std::string sgn(const std::string &x) const { return "(" + std::string(f32 ? "__float_as_uint" : "__double2hiint") + "(" + x + ".x) & 0x80000000u)"; }
+    void emit_rec_sign(const DiagRec &r, const std::string &base, const std::string &f, const std::string &ind) {
+        std::string cond = r.fmask ? "((" + base + " & " + std::to_string(r.fmask) + "ull) == " +
+                                         std::to_string(r.fval) + "ull)"
+                                   : "true";
+        const int nv = 1 << r.nt;
+        unsigned m[4];
+        for (int i = 0; i < nv; ++i) m[i] = r.val[2 * i] < 0 ? 0x80000000u : 0u;
+        if (nv == 1) {
+            if (m[0]) o << ind << "if (" << cond << ") " << f << " ^= 0x80000000u;\n";
+            return;
+        }
+        o << ind << "if (" << cond << ") {\n" << ind << "  const int ix = ";
+        if (r.nt == 1) o << "(int)((" << base << " >> " << r.tpos0 << ") & 1ull);\n";
+        else
+            o << "(int)(((" << base << " >> " << r.tpos0 << ") & 1ull) << 1 | ((" << base << " >> " << r.tpos1
+              << ") & 1ull));\n";
+        o << ind << "  " << f << " ^= ";
+        for (int i = 0; i < nv; ++i) o << (i + 1 < nv ? "ix == " + std::to_string(i) + " ? " : "") << m[i] << "u" << (i + 1 < nv ? " : " : "");
+        o << ";\n" << ind << "}\n";
+    }
+    bool emit_flush_sign(const HostOp &op, const std::string &ind) {
+        const bool off = [] {  // QSV_X_NOSIGN=1 (A/B): complex multiplies
+            const char *e = std::getenv("QSV_X_NOSIGN");
+            return e && e[0] == '1';
+        }();
+        if (off || op.flush.tgt_end <= op.flush.tgt_begin) return false;
+        for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti)
+            if (!target_is_sign(ph.targets[ti])) return false;
+        const int NR = 1 << R;
+        bool uniform = op.flush.regmask == (NR >= 32 ? 0xffffffffu : ((1u << NR) - 1)) &&
+                       static_cast<int>(op.regtab.size()) >= NR && op.regtab[0].imag() == 0.0;
+        for (int r = 1; uniform && r < NR; ++r) uniform = op.regtab[r] == op.regtab[0];
+        const double rc = uniform ? op.regtab[0].real() : 1.0;
+        if (rc != 1.0 && !track) return false;  // a runtime scale would need a multiply anyway
+        if (rc != 1.0) {
+            for (double &x : sc) x *= rc;
+            if (final_op) materialize(ind);
+        }
+        o << ind << "{\n";
+        const std::string in = ind + "  ";
+        std::vector<int> nfac(R + 1, 0);
+        for (int ti = op.flush.tgt_begin; ti < op.flush.tgt_end; ++ti) {
+            const FlushTarget &t = ph.targets[ti];
+            const int cls = t.slot < 0 ? R : t.slot;
+            const std::string g = "m" + std::to_string(cls);
+            const std::string f = "n" + std::to_string(ti);
+            std::vector<std::string> terms;
+            if (t.eidx >= 0) terms.push_back(sgn("E[" + eoff() + std::to_string(ebase[cur_group] + t.eidx) + "]"));
+            if (t.table >= 0) terms.push_back(sgn("tab" + std::to_string(ti)));
+            if (t.table_lo >= 0)
+                terms.push_back(sgn("stab[" + std::to_string(stab_off.at(t.table_lo)) + " + (s & " +
+                                    std::to_string((1 << t.lo_bits) - 1) + ")]"));
+            if (t.table_hi >= 0)
+                terms.push_back(sgn("stab[" + std::to_string(stab_off.at(t.table_hi)) + " + (s >> " +
+                                    std::to_string(t.lo_bits) + ")]"));
+            o << in << "unsigned " << f << " = " << (terms.empty() ? std::string("0u") : terms[0]);
+            for (size_t k = 1; k < terms.size(); ++k) o << " ^ " << terms[k];
+            o << ";\n";
+            for (int k = t.mix_begin; k < t.mix_end; ++k) emit_rec_sign(ph.recs[k], "pb", f, in);
+            if (nfac[cls]++ == 0) o << in << "unsigned " << g << " = " << f << ";\n";
+            else o << in << g << " ^= " << f << ";\n";
+        }
+        int nph = 0;
+        std::function<void(int, const std::string &)> visit = [&](int r, const std::string &p) {
+            if (!p.empty()) o << in << "v" << r << " = sxor(v" << r << ", " << p << ");\n";
+            const int top = r ? 64 - __builtin_clzll(static_cast<unsigned long long>(r)) : 0;
+            for (int b = top; b < R; ++b) {
+                const int ch = r | (1 << b);
+                if (!nfac[b]) {
+                    visit(ch, p);
+                    continue;
+                }
+                const std::string gb = "m" + std::to_string(b);
+                std::string q = gb;
+                if (!p.empty()) {
+                    q = "q" + std::to_string(nph++);
+                    o << in << "const unsigned " << q << " = " << p << " ^ " << gb << ";\n";
+                }
+                visit(ch, q);
+            }
+        };
+        visit(0, nfac[R] ? "m" + std::to_string(R) : "");
+        o << ind << "}\n";
+        if (op.flush.regmask && !uniform)
+            for (int r = 0; r < NR; ++r)
+                if ((op.flush.regmask >> r) & 1) cmul_const(r, op.regtab[r], ind);
+        return true;
+    }
+
     void emit_flush(const HostOp &op, const std::string &ind) {
+        if (emit_flush_sign(op, ind)) return;
         const int NR = 1 << R;
         o << ind << "{\n";
         const std::string in = ind + "  ";
@@ -692,6 +810,13 @@ struct Gen {
             c << "static __device__ __forceinline__ " << V << " cfmav(" << V << " a, " << V << " b, " << V
               << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
         }
+        // a +-1 factor as a sign mask (0 or 0x80000000 on the high word of each component)
+        if (f32)
+            c << "static __device__ __forceinline__ cf sxor(cf v, unsigned s) { return mk(__uint_as_float(__float_as_uint(v.x) ^ s), "
+                 "__uint_as_float(__float_as_uint(v.y) ^ s)); }\n";
+        else
+            c << "static __device__ __forceinline__ cd sxor(cd v, unsigned s) { return mk(__hiloint2double(__double2hiint(v.x) ^ (int)s, "
+                 "__double2loint(v.x)), __hiloint2double(__double2hiint(v.y) ^ (int)s, __double2loint(v.y))); }\n";
         // streaming (evict-first) 8/16-byte amplitude loads and stores; stwb:
         // a plain write-back store (the first pass of an L2 super-pass keeps
         // its output in L2 for the second)

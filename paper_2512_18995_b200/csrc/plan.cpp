@@ -215,6 +215,8 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
         s.kind = 1;
         std::vector<int> keep, want; // local bits that must stay / rank-bit wires to bring in
         {
+            // look-ahead wants are bounded by the local bits left for victims
+            // (a state with few local qubits cannot take the whole frontier)
             const size_t look = std::min<size_t>(rem.size(), 64);
             for (size_t j = 0; j < look && static_cast<int>(want.size()) < p.ctx->gbits; ++j) {
                 const GateRec &h = p.gates[rem[j]];
@@ -224,10 +226,14 @@ void schedule_dist(Plan &p, const PlanConfig &cfg) {
                     if (b < nl) {
                         if (j == 0) keep.push_back(b);
                     } else if (std::find(want.begin(), want.end(), h.wires[t]) == want.end() &&
-                               (j == 0 || static_cast<int>(want.size()) < p.ctx->gbits))
+                               (j == 0 || (static_cast<int>(want.size()) < p.ctx->gbits &&
+                                           static_cast<int>(want.size() + keep.size()) < nl)))
                         want.push_back(h.wires[t]);
                 }
             }
+            require(static_cast<int>(want.size() + keep.size()) <= nl,
+                    "dist: a gate needs more local qubits than each rank holds (" + std::to_string(nl) +
+                        "); use fewer ranks");
         }
         for (int w : want) {
             const int gb = phys[w];

@@ -288,15 +288,39 @@ class Context:
         return s.value or 0
 
     def close(self):
-        if self.h:
+        if self.h and self._owned:
             lib().qsv_ctx_destroy(self.h)
-            self.h = None
+        self.h = None
 
     def __del__(self):
         try:
             self.close()
         except Exception:
             pass
+
+
+_RANK_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.c_void_p)
+
+
+def run_on_ranks(ctx: Context, fn) -> None:
+    """dist::run_on_ranks (tests/test_dist.cpp:66-94): fn(rank_ctx, rank) on one
+    host thread per rank of a multi-device context, all joined; the first
+    failing rank's exception is re-raised."""
+    errors: dict = {}
+
+    def tramp(h, rank, _user):
+        try:
+            fn(Context(ctx.device, rank, ctx.world, _handle=C.c_void_p(h), _owned=False), rank)
+            return OK
+        except BaseException as e:  # noqa: BLE001 -- carried to the caller
+            errors[rank] = e
+            return ERR_INTERNAL
+
+    cb = _RANK_FN(tramp)
+    rc = lib().qsv_run_on_ranks(ctx.h, C.cast(cb, C.c_void_p), None)
+    if errors:
+        raise errors[min(errors)]
+    check(rc)
 
 
 _default_ctx: Context | None = None

@@ -84,7 +84,7 @@ int main() {
         for (int world : {2, 4, 8})
             for (int trial = 0; trial < 6; ++trial) {
                 const int n = 4 + static_cast<int>(rng.next_below(5));
-                if ((1 << n) < 2 * world) continue;
+                if ((1 << n) < 4 * world) continue;  // two local qubits per rank
                 Circuit cir = random_circuit(rng, n, 18);
                 const cvec want = cir.forward().amplitudes();
                 D::run_on_ranks(world, [&](D::Transport &tr) {

@@ -40,11 +40,18 @@ struct Slot {
     uint64_t off, bytes;
     int valid;
 };
+// Point-to-point is pairwise (only the two ranks of a send / receive meet:
+// ranks whose global control is |0> skip an exchange, as with NCCL): src
+// posts its bytes and bumps seq[src][dst]; dst waits for that sequence
+// number, copies, and acknowledges in ack[src][dst]; src's staging area is
+// reused only once every receiver has acknowledged.
 struct Ctl {
     std::atomic<int> joined;
     std::atomic<int> count;
     std::atomic<int> gen;
     Slot send[kMaxRanks][kMaxRanks];  // [src][dst]
+    std::atomic<uint64_t> seq[kMaxRanks][kMaxRanks];
+    std::atomic<uint64_t> ack[kMaxRanks][kMaxRanks];
     double red[kMaxRanks][kRedDoubles];
     unsigned char area[kMaxRanks][kArea];
 };
@@ -52,6 +59,7 @@ struct Comm {
     Ctl *ctl = nullptr;
     int rank = 0, nranks = 1;
     char name[128] = {};
+    uint64_t sent[kMaxRanks] = {}, recvd[kMaxRanks] = {};  // this rank's sequence numbers per peer
 };
 struct Op {
     bool send;
@@ -96,6 +104,7 @@ bool cu_ok(CUresult r, const char *what) {
 int run_group(std::vector<Op> &ops) {
     if (ops.empty()) return 0;
     Comm *c = ops[0].comm;
+    Ctl *k = c->ctl;
     for (const Op &o : ops)
         if (!cu_ok(cuCtxSynchronize(), "cuCtxSynchronize") || !cu_ok(cuStreamSynchronize(o.stream), "cuStreamSynchronize"))
             return 1;
@@ -106,34 +115,34 @@ int run_group(std::vector<Op> &ops) {
             std::fprintf(stderr, "fake nccl: more than %zu bytes sent per rank per group\n", kArea);
             return 4;
         }
-        if (!cu_ok(cuMemcpyDtoH(c->ctl->area[c->rank] + used, reinterpret_cast<CUdeviceptr>(o.buf), o.bytes),
+        if (!cu_ok(cuMemcpyDtoH(k->area[c->rank] + used, reinterpret_cast<CUdeviceptr>(o.buf), o.bytes),
                    "cuMemcpyDtoH"))
             return 1;
-        Slot &s = c->ctl->send[c->rank][o.peer];
-        s.off = used;
-        s.bytes = o.bytes;
-        s.valid = 1;
+        Slot &sl = k->send[c->rank][o.peer];
+        sl.off = used;
+        sl.bytes = o.bytes;
+        sl.valid = 1;
+        k->seq[c->rank][o.peer].store(++c->sent[o.peer], std::memory_order_release);
         used += (o.bytes + 255) & ~uint64_t(255);
     }
-    barrier(c);
     int rc = 0;
     for (const Op &o : ops) {
         if (o.send) continue;
-        Slot &s = c->ctl->send[o.peer][c->rank];
-        if (!s.valid || s.bytes != o.bytes) {
+        const uint64_t want = ++c->recvd[o.peer];
+        while (k->seq[o.peer][c->rank].load(std::memory_order_acquire) < want) sched_yield();
+        Slot &sl = k->send[o.peer][c->rank];
+        if (!sl.valid || sl.bytes != o.bytes) {
             std::fprintf(stderr, "fake nccl: unmatched receive from rank %d\n", o.peer);
             rc = 4;
-            continue;
-        }
-        if (!cu_ok(cuMemcpyHtoD(reinterpret_cast<CUdeviceptr>(o.buf), c->ctl->area[o.peer] + s.off, o.bytes),
-                   "cuMemcpyHtoD"))
+        } else if (!cu_ok(cuMemcpyHtoD(reinterpret_cast<CUdeviceptr>(o.buf), k->area[o.peer] + sl.off, o.bytes),
+                          "cuMemcpyHtoD"))
             rc = 1;
+        k->ack[o.peer][c->rank].store(want, std::memory_order_release);
     }
     if (cuCtxSynchronize() != CUDA_SUCCESS) rc = 1;  // the copies land before the caller's stream goes on
-    barrier(c);
-    for (const Op &o : ops)
-        if (o.send) c->ctl->send[c->rank][o.peer].valid = 0;
-    barrier(c);
+    for (const Op &o : ops)  // the staging area is reused by the next group: wait for every receiver
+        if (o.send)
+            while (k->ack[c->rank][o.peer].load(std::memory_order_acquire) < c->sent[o.peer]) sched_yield();
     return rc;
 }
 } // namespace

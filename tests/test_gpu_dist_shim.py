@@ -135,6 +135,7 @@ def test_cfg5_family_c64_and_global_pauli_2_ranks():
     got, z, nrm, ex, nsw = run_ranks(n, cir.gates(), 2, dtype=qsv.C64, obs=obs)
     want = O.port_forward(n, cir.gates())[0]
     assert np.max(np.abs(got - want)) <= 1e-5
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6  # complex64 relative L2
     for (w, b), e in zip(obs, ex):
         assert abs(e - O.port_expectation(n, want, w, b)[0]) <= 1e-5
 
@@ -299,4 +300,6 @@ def test_swaps_fused_into_passes_through_peer_memory(world):
             got, z, nrm, _, _ = run_ranks(n, cir.gates(), world, init=psi, dtype=dtype, env=env)
             assert all(v == mode for v in PEER_MEMORY.values()), (PEER_MEMORY, env)
             assert np.max(np.abs(got - want)) <= tol, (world, n, env)
+            if dtype == qsv.C64:
+                assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-6, (world, n, env)
             assert abs(nrm - 1.0) <= 10 * tol

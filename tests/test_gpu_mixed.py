@@ -60,6 +60,8 @@ def test_gates_and_channels_match_reference(dtype, tol):
         want = mixed_ref(n, OPS, init)
         assert s.is_mixed() and s.nqubit() == n
         assert np.max(np.abs(s.density() - want)) <= tol
+        if dtype == C64:  # complex64 relative L2
+            assert np.linalg.norm(s.density() - want) / np.linalg.norm(want) <= 1e-6
         obs = [([0], "z"), ([1, 2], "xy"), ([0, 1, 3], "zzx"), ([2], "y")]
         got = qsv.expectation_many(s, [qsv.Observable(w, b) for w, b in obs])[0]
         ref = O.ref_density_expectation(n, want, obs) if HAVE_REF else \
