@@ -419,6 +419,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        # NCCL's own init lines (ranks, devices, transports: NVLS / P2P) go to
+        # stderr, so a scaling run records what the communicator saw
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo", init_method="env://")
         uid = [qsv.Context.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
