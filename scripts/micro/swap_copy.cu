@@ -51,19 +51,22 @@ int main(int argc, char **argv) {
         CK(cudaMalloc(&d_vs, sizeof(unsigned) * nv));
         CK(cudaMemcpy(d_vs, vs.data(), sizeof(unsigned) * nv, cudaMemcpyHostToDevice));
         const uint64_t block = n >> c.m;
-        const uint64_t chunk = std::min<uint64_t>(block, (set_cap / amp) / nv);  // elements per block per round
-        const bool pair64 = amp == 8 && bb.pos[0] >= 1;
+        // elements per block per round: a power of two, as dist.cu
+        uint64_t chunk = 1;
+        while (chunk * 2 <= std::min<uint64_t>(block, (set_cap / amp) / nv)) chunk *= 2;
+        const bool pair64 = amp == 8 && bb.pos[0] >= 1 && chunk % 2 == 0;
         BlockBits bbv = bb;
         if (pair64)
             for (int i = 0; i < c.m; ++i) bbv.pos[i] -= 1;
         auto run = [&](int dir) {
             for (uint64_t e0 = 0; e0 < block; e0 += chunk) {
-                const uint64_t cnt = pair64 ? chunk / 2 : chunk, s0 = pair64 ? e0 / 2 : e0;
+                const uint64_t c = std::min(chunk, block - e0);
+                const uint64_t cnt = pair64 ? c / 2 : c, s0 = pair64 ? e0 / 2 : e0;
                 dim3 grid((unsigned)std::max<uint64_t>(1, std::min<uint64_t>((cnt + 255) / 256, (148 * 8 + nv - 1) / nv)), nv);
                 if (amp == 16 || pair64)
                     block_copy_kernel<double2><<<grid, 256>>>((double2 *)state, (double2 *)stage, pair64 ? bbv : bb, s0, cnt, d_vs, dir);
                 else
-                    block_copy_kernel<float2><<<grid, 256>>>((float2 *)state, (float2 *)stage, bb, e0, chunk, d_vs, dir);
+                    block_copy_kernel<float2><<<grid, 256>>>((float2 *)state, (float2 *)stage, bb, e0, c, d_vs, dir);
             }
         };
         const double moved = double(block) * nv * amp;  // bytes per gather (read + write each)
