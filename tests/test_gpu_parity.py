@@ -497,6 +497,33 @@ def test_graph_replay_matches_stream_launches(dtype):
 
 
 @pytest.mark.parametrize("dtype", [C128, C64])
+def test_graph_cache_survives_buffer_reallocation(dtype):
+    """a graph plan bakes the device pointers of its product-state
+    prefix buffer; a larger batch reallocates that buffer, so the cached
+    graphs must be dropped. Alternate batch-1 and batch-4 states on one
+    from-|0> graph plan (and an L2 super-pass graph plan, whose counters are
+    reallocated the same way)."""
+    rng = Rng(47, "graph-realloc")
+    n = 15
+    cir = random_circuit(rng, n, 60)
+    psi = random_state(rng, n)
+    for opts, init in (({"jit": 1, "use_graph": 1, "from_zero": 1}, None),
+                       ({"jit": 1, "use_graph": 1, "super_bits": 14}, psi)):
+        want = O.port_forward(n, cir.gates(), init=init)[0]
+        p = qsv.Plan(n, cir.gates(), dtype=dtype, opts=opts)
+        s1 = QubitState(n, 1, dtype)
+        s4 = QubitState(n, 4, dtype)
+        for rep in range(3):
+            for st in (s1, s4, s1):
+                if init is not None:
+                    for b in range(st.batch()):
+                        st.upload(init, b)
+                p.execute(st)
+                for b in range(st.batch()):
+                    assert_close(st.amplitudes(b), want, dtype, (opts, rep, b))
+
+
+@pytest.mark.parametrize("dtype", [C128, C64])
 @pytest.mark.parametrize("variant", ["", "QSV_X_NOPACK", "QSV_X_NOSCALE", "QSV_X_NOTAN", "QSV_X_NOSPLIT",
                                      "QSV_X_NOSIGN", "QSV_X_NOPAIR", "QSV_X_OLDSWZ"])
 @pytest.mark.parametrize("reg_slots", [0, 2, 3, 4])
