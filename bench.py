@@ -388,6 +388,24 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
                      "per_pass_ms": [round(float(x), 4) for x in per.mean(axis=0)]}
         launches += 4 * p.info["npasses"]
         del st, p
+    # ---- north_star (2)'s tensor-core blocks, measured where they are
+    # genuinely dense (NOT a BASELINE config): a 30-qubit c64 brickwork of
+    # Haar-random two-qubit unitaries, the fused FFMA passes against the
+    # dense-block tensor-core passes (opts.dense_blocks) on the same circuit
+    cir = W.dense_brickwork_circuit(30, 20)
+    st = qsv.QubitState(30, dtype=qsv.C64)
+    dz = {"workload": "demonstration (not a BASELINE config): 30-qubit c64 brickwork, 20 layers of Haar-random "
+                      "two-qubit unitaries (290 gates)",
+          "protocol": "1 warm-up + 3 repeats (per-pass events), median"}
+    for key, opts in (("ffma_passes", None), ("tensor_core_blocks", {"dense_blocks": 1})):
+        p = qsv.Plan(30, cir.gates(), dtype=qsv.C64, opts=opts)
+        p.profile(st)
+        tot = float(np.median([p.profile(st).sum() for _ in range(3)]))
+        dz[key] = {"ms_per_forward": tot, "passes": p.info["npasses"], "blocks": p.info["nblocks"]}
+        launches += 4 * p.info["npasses"]
+        del p
+    del st
+    aux["dense_su4_30q"] = dz
     return aux, launches
 
 

@@ -119,7 +119,13 @@ typedef struct qsv_opts {
                                most this many qubits run as one launch, chunk by
                                chunk through L2 (> 0 = on with this chunk size;
                                0 = $QSV_SUPER_BITS, default off; -1 = off) */
-    int32_t reserved[1];
+    int32_t dense_blocks;   /* complex64, one GPU: fuse the circuit into dense <= 5-qubit
+                               blocks (32 x 32 unitaries) applied on the tcgen05 tensor
+                               cores (3xTF32, TMEM accumulators), up to 3 blocks per HBM
+                               pass (1 = on, 0 / -1 = off: the fused FFMA tile passes).
+                               Pays for genuinely dense circuits (random two-qubit
+                               unitaries); the BASELINE configs run faster without it
+                                */
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */
@@ -131,7 +137,7 @@ typedef struct qsv_plan_info {
     double bytes_per_exec;   /* algorithmic HBM bytes per execute (all passes) */
     double comm_bytes_per_exec; /* bytes sent per rank per execute */
     int32_t ntile_passes;    /* tile passes per execute (>= npasses: super-passes run two) */
-    int32_t reserved;
+    int32_t nblocks;         /* dense-block plans (opts.dense_blocks): fused 5-qubit blocks */
 } qsv_plan_info;
 
 /* ---- library --------------------------------------------------------- */

@@ -733,6 +733,13 @@ int qsv_plan_info_get(const qsv_plan *p, qsv_plan_info *info) {
         if (is_group(p)) p = p->parts[0];
         std::memset(info, 0, sizeof(*info));
         info->ngates = p->ngates;
+        if (p->dense) {
+            info->npasses = info->ntile_passes = static_cast<int>(p->dpasses.size());
+            info->nblocks = static_cast<int>(p->dblocks.size());
+            info->max_tile_bits = kDenseTile;
+            info->bytes_per_exec = p->dpasses.size() * 2.0 * 8 * std::ldexp(1.0, p->nlocal);
+            return;
+        }
         for (const Step &s : p->steps) {
             if (s.kind == 0) {
                 info->ntile_passes += 1;
@@ -1077,6 +1084,12 @@ int qsv_plan_dry(int nqubit, int dtype, int world, const qsv_gate *gates, int ng
             std::memset(info, 0, sizeof(*info));
             info->ngates = p.ngates;
             const double amp = dtype == QSV_C64 ? 8 : 16;
+            if (p.dense) {
+                info->npasses = info->ntile_passes = static_cast<int>(p.dpasses.size());
+                info->nblocks = static_cast<int>(p.dblocks.size());
+                info->max_tile_bits = kDenseTile;
+                info->bytes_per_exec = p.dpasses.size() * 2.0 * amp * std::ldexp(1.0, p.nlocal);
+            }
             for (const Step &s : p.steps) {
                 if (s.kind == 0) {
                     info->ntile_passes += 1;
@@ -1171,6 +1184,11 @@ int qsv_rng_fill_at(uint64_t seed, const char *label, int kind, uint64_t offset,
 int qsv_plan_steps(const qsv_plan *plan, int *kinds, int cap) {
     if (!plan) return -QSV_ERR_INVALID;
     if (is_group(plan)) plan = plan->parts[0];
+    if (plan->dense) {  // one launch per dense-block pass
+        const int n = static_cast<int>(plan->dpasses.size());
+        for (int i = 0; i < n && i < cap && kinds; ++i) kinds[i] = 0;
+        return n;
+    }
     const int n = static_cast<int>(plan->steps.size());
     for (int i = 0; i < n && i < cap && kinds; ++i) {
         const Step &s = plan->steps[i];

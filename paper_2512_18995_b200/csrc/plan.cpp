@@ -47,6 +47,7 @@ Plan::~Plan() {
     cudaFree(d_sync);
     for (auto &g : graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
+    dense_free(*this);
 }
 
 namespace {
@@ -475,6 +476,23 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : 0; // 0: per pass (planner.cpp)
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
+    if (p->opts.dense_blocks > 0) {
+        // dense-block plan (tensor cores): every gate fused into <= 5-qubit
+        // blocks on physical bits (canonical layout: wire w is bit n-1-w)
+        require(dtype == QSV_C64, "dense blocks: complex64 plans only (tf32 tensor cores)");
+        require(ctx->world == 1, "dense blocks: one GPU");
+        require(p->nslots == 0, "dense blocks: encoded gates are not supported");
+        std::vector<GateRec> phys = p->gates;
+        for (GateRec &g : phys) {
+            for (int t = 0; t < g.k; ++t) g.wires[t] = p->perm_in[g.wires[t]];
+            for (int &c : g.ctls) c = p->perm_in[c];
+        }
+        plan_dense(phys, p->nlocal, p->dblocks, p->dpasses);
+        p->dense = true;
+        p->perm_out = p->perm_in;
+        if (ctx->stream || ctx->device >= 0) dense_upload(*p);
+        return;
+    }
     if (p->opts.from_zero && ctx->world == 1 && cfg.fuse && plan_uses_jit(*p)) extract_prefix(*p);
     // L2 super-passes (planner.cpp), opt-in: opts.super_bits (or
     // QSV_SUPER_BITS) = the largest chunk, e.g. 19 (C128) / 20 (C64) = 8 MiB.
@@ -833,6 +851,11 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     }
     cudaStream_t s = p.ctx->stream;
     QSV_CUDA(cudaSetDevice(p.ctx->device));
+    if (p.dense) {
+        require(zout == nullptr, "dense blocks: no fused <Z> epilogue");
+        dense_execute(p, st, s);
+        return;
+    }
     if (zout == nullptr && rows == 0 && execute_graph(p, st)) return;
     const void *enc_table = nullptr;
     if (!p.encs.empty()) {
@@ -947,6 +970,10 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
     require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
     require(p.nslots == 0, "profile: encoded plans not supported");
     cudaStream_t s = p.ctx->stream;
+    if (p.dense) {
+        dense_execute(p, st, s, launch_ms);
+        return;
+    }
     std::vector<cudaEvent_t> ev(2 * p.steps.size());
     for (auto &e : ev) QSV_CUDA(cudaEventCreate(&e));
     size_t k = 0;

@@ -222,6 +222,38 @@ std::vector<unsigned char> serialize_program(const PassHost &ph, int dtype, int 
                                              int *off_ops);
 size_t op_record_bytes(const HostOp &op, int dtype, int R);
 
+// ---- dense-block passes (tensor cores, complex64) -------------------------
+// A fused block: up to 5 physical bits (q[i] <-> bit i of the block index)
+// and its 2^5 x 2^5 unitary (row-major, padded to exactly 5 bits).
+constexpr int kDenseQ = 5;
+constexpr int kDenseTile = 12;   // tile bits of a dense-block pass: 128 sets x 32 amplitudes
+constexpr int kDenseMaxBlocks = 3;
+struct DenseBlock {
+    int q[kDenseQ] = {0, 0, 0, 0, 0};
+    std::vector<cplx> u;         // 32 x 32
+    int ngates = 0;
+};
+struct DensePass {
+    int tile_pos[kDenseTile];    // physical bit of tile-local bit i (0..3 = the low bits)
+    std::vector<int> ext_pos;    // the other local bits, ascending
+    std::vector<int> blocks;     // indices into Plan::dblocks, in order
+    int bbit[kDenseMaxBlocks][kDenseQ];  // tile-local bit of each block qubit
+    int swm[4] = {0, 0, 0, 0};   // shared-tile swizzle masks (slot bit i ^= parity(u & swm[i]))
+};
+// Fuses gates (wires = physical bits, canonical layout) into dense blocks of
+// at most 5 qubits (greedy, gate order kept: a gate joins the open block when
+// its qubits fit and none is held by an earlier skipped gate), then packs the
+// blocks into passes of a 12-bit tile with the 4 low bits always in it.
+void plan_dense(const std::vector<GateRec> &gates, int nlocal, std::vector<DenseBlock> &blocks,
+                std::vector<DensePass> &passes);
+// B operand of a block: the real 64 x 64 matrix on (re, im) pairs split into
+// TF32 hi / lo, in the K-major 128-byte-swizzled UMMA layout (2 x 16 KiB).
+void dense_b_operand(const DenseBlock &b, std::vector<float> &out);
+struct DenseDev;  // device state of a dense plan (block_pass.cu)
+void dense_upload(struct Plan &p);
+void dense_execute(struct Plan &p, struct State &st, cudaStream_t s, double *launch_ms = nullptr);
+void dense_free(struct Plan &p);
+
 // ---- runtime objects ----------------------------------------------------
 struct Nccl;  // dlopen'd NCCL
 
@@ -334,6 +366,11 @@ struct Plan {
     std::vector<Graph> graphs;
     std::vector<DevPass> dev;
     qsv_opts opts{};
+    // dense-block plan (opts.dense_blocks): blocks, passes, device buffers
+    bool dense = false;
+    std::vector<DenseBlock> dblocks;
+    std::vector<DensePass> dpasses;
+    DenseDev *ddev = nullptr;
     ~Plan();
 };
 

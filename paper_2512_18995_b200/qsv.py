@@ -82,13 +82,13 @@ class qsv_opts(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_bits", C.c_int32), ("low_bits", C.c_int32), ("use_graph", C.c_int32),
                 ("no_fuse_1q", C.c_int32), ("no_phase_flush", C.c_int32), ("jit", C.c_int32), ("reg_slots", C.c_int32),
                 ("no_relabel", C.c_int32), ("from_zero", C.c_int32), ("super_bits", C.c_int32),
-                ("reserved", C.c_int32 * 1)]
+                ("dense_blocks", C.c_int32)]
 
 
 class qsv_plan_info(C.Structure):
     _fields_ = [("ngates", C.c_int32), ("npasses", C.c_int32), ("nswaps", C.c_int32), ("max_tile_bits", C.c_int32),
                 ("bytes_per_exec", C.c_double), ("comm_bytes_per_exec", C.c_double), ("ntile_passes", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("nblocks", C.c_int32)]
 
 
 # every symbol include/qsv.h declares, with its ctypes signature

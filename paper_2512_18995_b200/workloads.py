@@ -156,3 +156,31 @@ def mirror(cir: Circuit) -> Circuit:
         m = gate_matrix(g).conj().T
         out.add(make_gate("custom", g.wires, g.controls, [], custom=m))
     return out
+
+
+def haar_su4(rng: Rng) -> np.ndarray:
+    """A Haar-random 4 x 4 unitary from seeded Gaussian draws (QR with the
+    phases of R's diagonal folded in); draws sequenced re then im."""
+    z = np.empty((4, 4), dtype=np.complex128)
+    for i in range(4):
+        for j in range(4):
+            re = rng.normal()
+            im = rng.normal()
+            z[i, j] = complex(re, im)
+    q, r = np.linalg.qr(z)
+    d = np.diag(r)
+    return q * (d / np.abs(d))
+
+
+def dense_brickwork_circuit(n: int = 30, depth: int = 20, seed_label: str = "dense-su4") -> Circuit:
+    """Random-circuit-sampling style workload (NOT a BASELINE.json config --
+    the demonstration of north_star (2)'s tensor-core blocks where they pay):
+    `depth` layers of Haar-random two-qubit unitaries on a brickwork of
+    neighbouring wires (even layers (2i, 2i+1), odd layers (2i+1, 2i+2))."""
+    rng = Rng(0, seed_label)
+    cir = Circuit(n)
+    for layer in range(depth):
+        for i in range((n - (layer % 2)) // 2):
+            a = 2 * i + (layer % 2)
+            cir.add(make_gate("custom", [a, a + 1], custom=haar_su4(rng)))
+    return cir
