@@ -263,6 +263,17 @@ int qsv_expect_pauli(qsv_state *st, int nobs, const qsv_obs *obs, double *out);
 /* marginal_probabilities on row `row`: out has 2^k entries. */
 int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, double *out);
 
+/* measure (circuit.hpp:217-244) on row `row`: the marginals of `wires` on the
+ * device, then `shots` draws u = Rng(seed, label).uniform() * total (the
+ * stream continues after *rng_counter draws and the counter is advanced; NULL
+ * = from the start), outcome = lower_bound over the running sums -- the
+ * reference's seeded histogram exactly. counts[2^k] per outcome (wires[0] is
+ * the outcome's MSB); probs[2^k] receives the exact marginals (may be NULL:
+ * the with_prob = false form). A multi-device state all-reduces the marginals
+ * first (measure_dist). */
+int qsv_measure(qsv_state *st, int row, int k, const int32_t *wires, int shots, uint64_t seed, const char *label,
+                uint64_t *rng_counter, uint64_t *counts, double *probs);
+
 /* ---- mixed states (density matrices, channels) --------------------------
  * A batch of m-qubit density matrices is an engine state of 2m qubits holding
  * vec(rho)[r * 2^m + c] per row (row wires = engine wires 0..m-1, column

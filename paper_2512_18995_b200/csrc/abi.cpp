@@ -54,6 +54,8 @@ void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *ga
                          const qsv_opts *opts);
 void profile_plan(Plan &p, State &st, double *launch_ms);
 int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *out, int nthreads, uint64_t offset);
+void sample_counts(const double *probs, int k, int shots, uint64_t seed, const char *label, uint64_t *counter,
+                   uint64_t *counts);
 void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates, int nobs, const qsv_obs *obs,
                        const double *init, const double *data, int slots, std::vector<double> &pg,
                        std::vector<double> &dg);
@@ -964,6 +966,20 @@ int qsv_marginal_probs(qsv_state *st, int row, int k, const int32_t *wires, doub
             bits.push_back(st->perm[wires[i]]);
         }
         reduce_marginal(*st, row, bits, out);
+    });
+}
+
+int qsv_measure(qsv_state *st, int row, int k, const int32_t *wires, int shots, uint64_t seed, const char *label,
+                uint64_t *rng_counter, uint64_t *counts, double *probs) {
+    return guard([&] {
+        require(st && counts, "null argument");
+        require(shots >= 1, "measure: shots must be >= 1");  // circuit.hpp:221
+        require(k >= 1 && k <= 26 && wires, "measure: 1..26 wires");
+        std::vector<double> p(size_t(1) << k);
+        const int rc = qsv_marginal_probs(st, row, k, wires, p.data());
+        if (rc) fail(rc, g_err);
+        sample_counts(p.data(), k, shots, seed, label, rng_counter, counts);
+        if (probs) std::copy(p.begin(), p.end(), probs);
     });
 }
 

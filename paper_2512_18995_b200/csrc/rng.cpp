@@ -109,4 +109,28 @@ int rng_fill(uint64_t seed, const char *label, int kind, uint64_t count, void *o
     return 0;
 }
 
+// measure()'s sampling (circuit.hpp:217-236) over given marginals: shots
+// draws of Rng(seed, label).uniform() * total starting after *counter draws,
+// lower_bound over the running sums; counts per outcome index.
+void sample_counts(const double *probs, int k, int shots, uint64_t seed, const char *label, uint64_t *counter,
+                   uint64_t *counts) {
+    if (label) seed ^= fnv1a(label);
+    const uint64_t key = mix(seed ^ kPhi);
+    const size_t np = size_t(1) << k;
+    std::vector<double> cdf(np);
+    double acc = 0.0;
+    for (size_t i = 0; i < np; ++i) {
+        acc += probs[i];
+        cdf[i] = acc;
+    }
+    std::fill(counts, counts + np, 0ull);
+    uint64_t c = counter ? *counter : 0;
+    for (int s = 0; s < shots; ++s) {
+        const double u = to_unit(mix(key + kPhi * ++c)) * acc;
+        const size_t idx = std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin();
+        counts[std::min(idx, np - 1)] += 1;
+    }
+    if (counter) *counter = c;
+}
+
 } // namespace qsv

@@ -106,6 +106,8 @@ _SIGS = {
     "qsv_run_on_ranks": (C.c_int, [_P, C.c_void_p, C.c_void_p]),
     "qsv_ctx_comm_stats": (C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     "qsv_ctx_comm_reset": (C.c_int, [_P]),
+    "qsv_measure": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int, C.c_uint64, C.c_char_p,
+                              C.POINTER(C.c_uint64), C.c_void_p, C.c_void_p]),
     "qsv_run_rows_expect_z": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(qsv_gate), C.c_int, C.c_void_p, C.c_int,
                                         C.c_int, C.POINTER(qsv_opts), C.c_void_p]),
     "qsv_ctx_sync": (C.c_int, [_P]),
@@ -971,8 +973,29 @@ def measure(state: QubitState, shots: int, wires, rng: "Rng", with_prob: bool = 
     """circuit.hpp:217-244: CDF sampling over the device-computed marginals."""
     if shots < 1:
         raise InvalidInput("measure: shots must be >= 1")
-    probs = marginal_probabilities(state, wires, batch_index)
     k = len(wires)
+    if not state.is_mixed() and 1 <= k <= 26:
+        # qsv_measure: the marginals on the device, the seeded sampling in the
+        # library, continuing this Rng's stream
+        w = (C.c_int32 * k)(*wires)
+        counts = np.zeros(1 << k, dtype=np.uint64)
+        probs = np.zeros(1 << k)
+        ctr = C.c_uint64(rng.counter)
+        check(lib().qsv_measure(state.h, batch_index, k, w, int(shots), C.c_uint64(rng.seed0),
+                                None if rng.label is None else rng.label.encode(), C.byref(ctr), _ptr(counts),
+                                _ptr(probs)))
+        rng.counter = ctr.value
+        out: dict = {}
+        for i in np.nonzero(counts)[0]:
+            out[bits_to_string(int(i), k)] = {"count": int(counts[i]), "probability": 0.0}
+        if with_prob:
+            for i, p in enumerate(probs):
+                key = bits_to_string(i, k)
+                if p <= 0 and key not in out:
+                    continue
+                out.setdefault(key, {"count": 0, "probability": 0.0})["probability"] = float(p)
+        return dict(sorted(out.items()))
+    probs = marginal_probabilities(state, wires, batch_index)
     cdf = np.cumsum(probs)
     # the reference accumulates sequentially; np.cumsum is sequential too
     acc = float(cdf[-1])
@@ -1015,6 +1038,7 @@ class Rng:
 
     def __init__(self, seed: int = 0, stream: str | None = None):
         seed &= _M64
+        self.seed0, self.label = seed, stream
         if stream is not None:
             seed ^= _fnv1a(stream)
         self.seed_eff = seed

@@ -142,3 +142,24 @@ def test_generated_pass_sources_compile_for_sm100a(dtype, variant, monkeypatch, 
     r = subprocess.run([nvcc, "-cubin", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-o",
                         str(tmp_path / "pass.cubin"), str(cu)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+def test_dense_block_planning_on_host():
+    """opts.dense_blocks: the host-side fusion into <= 5-qubit blocks and their
+    packing into 12-bit-tile passes (plan_dry, no GPU): every circuit family
+    plans, blocks never exceed 3 per pass, and what the tensor-core pass does
+    not cover is refused."""
+    from paper_2512_18995_b200 import workloads as W
+    from tests.helpers import random_circuit
+
+    rng = qsv.Rng(3, "dense-plan")
+    for n, cir in ((12, W.dense_brickwork_circuit(12, 10)), (20, W.dense_brickwork_circuit(20, 20)),
+                   (16, W.cfg5_circuit(16, 4)), (14, random_circuit(rng, 14, 200))):
+        info, _ = qsv.plan_dry(n, cir.gates(), dtype=qsv.C64, opts={"dense_blocks": 1})
+        assert info["nblocks"] >= 1 and 1 <= info["npasses"] <= info["nblocks"]
+        assert info["nblocks"] <= 3 * info["npasses"]
+        assert info["ngates"] == len(cir.gates())
+    with pytest.raises(qsv.InvalidInput):
+        qsv.plan_dry(14, W.dense_brickwork_circuit(14, 2).gates(), dtype=qsv.C128, opts={"dense_blocks": 1})
+    with pytest.raises(qsv.InvalidInput):
+        qsv.plan_dry(10, W.dense_brickwork_circuit(10, 2).gates(), dtype=qsv.C64, opts={"dense_blocks": 1})
