@@ -1510,6 +1510,9 @@ std::string generate_pass_source(const PassHost &ph, int dtype, const std::strin
     Gen g(ph, dtype);
     g.zsum = zsum;
     g.gout = gout;
+    // a one-GPU output permutation by scattered stores: plain write-back
+    // stores, so the partial lines of neighbouring tiles merge in L2
+    if (gout && ph.local_gperm) g.st_out = "stwb";
     require(!gout || !ph.gperm.empty(), "codegen: peer-memory pass without a global permutation");
     require(!gout || (!zsum && ph.out_perm.empty()), "codegen: peer-memory stores on a permuting / <Z> pass");
     g.double_buffer = false;

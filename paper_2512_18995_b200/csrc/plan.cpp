@@ -524,6 +524,12 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
         }
         std::vector<GateRec> gl = p->gates;
         std::vector<int> phys = p->perm_in, out_perm;
+        {  // QSV_SCATTER_OUT=1 (opt-in, measured slower): a final
+           // permutation that does not fit the last tile by scattered stores
+           // instead of an extra copy-out pass
+            const char *e = std::getenv("QSV_SCATTER_OUT");
+            cfg.scatter_out = relabel && e && e[0] == '1';
+        }
         if (relabel) {
             std::vector<int> fin;
             gl = relabel_swaps(p->gates, p->perm_in, fin);
@@ -615,11 +621,33 @@ void run_pair(Plan &p, int pi, State &st, cudaStream_t s) {
 }
 } // namespace
 
+// One GPU: the device array of the state's two buffers (the "peers" of a
+// local_gperm pass's scattered stores), in the p2p_cur convention of the
+// multi-GPU path: buffer i at [i], the current state at [p2p_cur].
+void local_out_ready(State &st) {
+    ensure_scratch(st);
+    void *want[2];
+    want[st.p2p_cur] = st.d;
+    want[1 - st.p2p_cur] = st.scratch;
+    if (st.d_peers && st.p2p_buf[0] == want[0] && st.p2p_buf[1] == want[1]) return;
+    if (!st.d_peers) QSV_CUDA(cudaMalloc(reinterpret_cast<void **>(&st.d_peers), 2 * sizeof(void *)));
+    st.p2p_buf[0] = want[0];
+    st.p2p_buf[1] = want[1];
+    QSV_CUDA(cudaMemcpy(st.d_peers, want, sizeof want, cudaMemcpyHostToDevice));
+}
+
+void run_local_gout(const DevPass &dp, State &st, cudaStream_t s) {
+    local_out_ready(st);
+    launch_gout(dp, st.d, st.batch, st.d_peers + (1 - st.p2p_cur), 0, 0, s);
+    std::swap(st.d, st.scratch);
+    st.p2p_cur ^= 1;
+}
+
 namespace {
 // A pass that can do the swaps after it (PassHost::gperm) does so when every
 // rank has peer memory (set up on first use, collectively).
 bool use_gout(Plan &p, int pi, State &st) {
-    if (p.ctx->world == 1 || p.passes[pi].gperm.empty() || !p.dev[pi].jit) return false;
+    if (p.ctx->world == 1 || p.passes[pi].gperm.empty() || !p.dev[pi].jit || p.passes[pi].local_gperm) return false;
     return dist_p2p_ready(st);
 }
 
@@ -760,6 +788,7 @@ void upload_plan(Plan &p) {
         if (use_jit && ph.pair == 1) jit_prepare_pair(dp, ph, p.passes[i + 1], p.dtype, p.ctx->sm_count);
         else if (use_jit && ph.pair == 2) dp.pair = 2;  // runs inside its head's launch
         else if (use_jit) jit_prepare(dp, ph, p.dtype, p.ctx->sm_count);
+        if (use_jit && ph.local_gperm) jit_prepare_gout(dp, ph, p.dtype, p.ctx->sm_count);  // scattered stores
         dp.bytes = 2.0 * amp * static_cast<double>(1ull << p.nlocal);
         dp.ngates = ph.ngates;
         p.dev.push_back(dp);
@@ -777,9 +806,11 @@ void execute_steps(Plan &p, State &st, const void *enc_table, int rows, double *
 bool execute_graph(Plan &p, State &st) {
     if (!p.opts.use_graph || p.ctx->world != 1 || p.nslots != 0 || !p.ctx->stream) return false;
     cudaStream_t s = p.ctx->stream;
-    bool oop = false;
+    bool oop = false, lg = false;
     for (const DevPass &dp : p.dev) oop = oop || dp.out_of_place;
-    if (oop) ensure_scratch(st);
+    for (const PassHost &ph : p.passes) lg = lg || ph.local_gperm;
+    if (oop || lg) ensure_scratch(st);
+    if (lg) local_out_ready(st);  // no allocation or copy inside the capture
     for (size_t i = 0; i < p.passes.size(); ++i)
         if (p.dev[i].pair == 1) { // counters sized before capture (no allocation inside)
             const uint64_t nchunks = static_cast<uint64_t>(st.batch) << (p.nlocal - p.passes[i].chunk_bits);
@@ -907,7 +938,10 @@ void execute_steps(Plan &p, State &st, const void *enc_table, int rows, double *
             dp.args.enc_table = enc_table;
             dp.args.batch = rows > 0 ? rows : st.batch;
             dp.args.prefix = p.passes[stp.pass].synth ? p.d_prefix : nullptr;
-            if (use_gout(p, stp.pass, st)) {
+            if (p.passes[stp.pass].local_gperm) {
+                require(!zout, "fused <Z>: not on a permuting pass");
+                run_local_gout(dp, st, s);
+            } else if (use_gout(p, stp.pass, st)) {
                 run_gout(p, stp.pass, dp, st, s);
                 fused_done = true;
             } else {
@@ -928,7 +962,8 @@ bool z_fusable(Plan &p) {
     const int pi = p.steps.back().pass;
     const PassHost &ph = p.passes[pi];
     const DevPass &dp = p.dev[pi];
-    return dp.jit != nullptr && !dp.out_of_place && ph.ext_pos.empty() && ph.out_perm.empty() && ph.K == p.nlocal;
+    return dp.jit != nullptr && !dp.out_of_place && !ph.local_gperm && ph.ext_pos.empty() && ph.out_perm.empty() &&
+           ph.K == p.nlocal;
 }
 } // namespace
 
@@ -986,6 +1021,10 @@ void profile_plan(Plan &p, State &st, double *launch_ms) {
             fused_done = true;
         } else if (stp.kind == 0 && p.dev[stp.pass].pair == 1) run_pair(p, stp.pass, st, s);
         else if (stp.kind == 0 && p.dev[stp.pass].pair == 2) {
+        } else if (stp.kind == 0 && p.passes[stp.pass].local_gperm) {
+            DevPass dp = p.dev[stp.pass];
+            dp.args.batch = st.batch;
+            run_local_gout(dp, st, s);
         } else if (stp.kind == 0 && use_gout(p, stp.pass, st)) {
             DevPass dp = p.dev[stp.pass];
             dp.args.batch = st.batch;

@@ -855,7 +855,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             if (admit(ord, pg, act, K, localmask).empty()) return 1 << 30;
             ++np;
         }
-        if (out_need && (np == 0 || std::popcount(act | out_need) > K)) ++np;
+        if (out_need && !cfg.scatter_out && (np == 0 || std::popcount(act | out_need) > K)) ++np;
         return np;
     };
     const char *ext_env = std::getenv("QSV_RUN_EXTEND");
@@ -935,6 +935,20 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
                 done = true;
             }
         }
+        if (!done && cfg.scatter_out && !passes.empty() && !last_took.empty()) {
+            // scattered permuted stores: the last pass keeps its tile; the
+            // input bits landing on the output's low bits become its lowest
+            // tile-index bits, so neighbouring tiles complete the same output
+            // lines while they sit in L2
+            PassHost ph = lower_pass(gates, pg, last_took, last_active, phys, cfg, K, L, passes.back().R, encs,
+                                     nullptr, need);
+            if (pass_program_bytes(ph, cfg.dtype) <= static_cast<size_t>(kProgramBudget)) {
+                ph.gperm = out_perm;
+                ph.local_gperm = true;
+                passes.back() = std::move(ph);
+                done = true;
+            }
+        }
         if (!done) {
             PassHost ph = lower_pass(gates, pg, {}, lowmask | need, phys, cfg, K, L, R, encs, &out_perm);
             ph.out_perm = out_perm;
@@ -970,6 +984,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             for (int b : B.tile_pos) cm |= 1ull << b;
             const int cb = std::popcount(cm);
             const bool ok = A.K == B.K && A.R == B.R && !A.synth && !B.synth && A.out_perm.empty() &&
+                            !A.local_gperm && !B.local_gperm &&
                             cb <= cfg.super_bits && cb >= A.K + 2 && cb < nl;
             if (!ok) {
                 ++i;

@@ -213,6 +213,12 @@ struct PassHost {
     // (size n; rank bits >= nlocal). The pass then writes every tile straight
     // into its destination rank's scratch state over NVLink.
     std::vector<int> gperm;
+    // One GPU: gperm (size nlocal) is the plan's final layout permutation,
+    // applied by the last register group storing every amplitude straight to
+    // its output position (out of place, write-back stores merged into whole
+    // lines in L2) instead of a shared-memory copy-out in output order -- so
+    // the pass needs no room in its tile for the output's coalescing run.
+    bool local_gperm = false;
     // The pass's gates in execution order, wires mapped to physical bits
     // (schedule export for host-side verification, qsv_plan_dry).
     std::vector<GateRec> exec_gates;
@@ -384,6 +390,10 @@ struct PlanConfig {
     // L2 super-passes: consecutive passes whose tiles together span at most
     // this many bits run as one launch, chunk by chunk (0: off)
     int super_bits = 0;
+    // one GPU, specialised kernels: a final layout permutation that does not
+    // fit the last pass's tile is applied by scattered stores (local_gperm)
+    // instead of an extra permutation-only pass
+    bool scatter_out = false;
 };
 // Swap gates as qubit relabelings: rewrites `gates` onto physical bits (the
 // returned gates' wires ARE physical bits), dropping uncontrolled swaps and
