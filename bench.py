@@ -392,20 +392,27 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
     # genuinely dense (NOT a BASELINE config): a 30-qubit c64 brickwork of
     # Haar-random two-qubit unitaries, the fused FFMA passes against the
     # dense-block tensor-core passes (opts.dense_blocks) on the same circuit
-    cir = W.dense_brickwork_circuit(30, 20)
     st = qsv.QubitState(30, dtype=qsv.C64)
-    dz = {"workload": "demonstration (not a BASELINE config): 30-qubit c64 brickwork, 20 layers of Haar-random "
-                      "two-qubit unitaries (290 gates)",
-          "protocol": "1 warm-up + 3 repeats (per-pass events), median"}
-    for key, opts in (("ffma_passes", None), ("tensor_core_blocks", {"dense_blocks": 1})):
-        p = qsv.Plan(30, cir.gates(), dtype=qsv.C64, opts=opts)
-        p.profile(st)
-        tot = float(np.median([p.profile(st).sum() for _ in range(3)]))
-        dz[key] = {"ms_per_forward": tot, "passes": p.info["npasses"], "blocks": p.info["nblocks"]}
-        launches += 4 * p.info["npasses"]
-        del p
+    for name, cir, desc in (
+            ("dense_local_30q", W.dense_local_circuit(30, 5, 20),
+             "demonstration (not a BASELINE config): 30-qubit c64, 6 windows of 5 wires, each a 20-layer brickwork "
+             "of Haar-random two-qubit unitaries (240 gates, ~40 dense gates per 5-qubit block)"),
+            ("dense_brickwork_30q", W.dense_brickwork_circuit(30, 20),
+             "demonstration (not a BASELINE config): 30-qubit c64 brickwork over all wires, 20 layers of "
+             "Haar-random two-qubit unitaries (290 gates, ~4 per 5-qubit block)")):
+        dz = {"workload": desc, "protocol": "1 warm-up + 3 repeats (per-pass events), median"}
+        for key, opts in (("ffma_passes", {"dense_blocks": -1}), ("tensor_core_blocks", {"dense_blocks": 1})):
+            p = qsv.Plan(30, cir.gates(), dtype=qsv.C64, opts=opts)
+            p.profile(st)
+            tot = float(np.median([p.profile(st).sum() for _ in range(3)]))
+            dz[key] = {"ms_per_forward": tot, "passes": p.info["npasses"], "blocks": p.info["nblocks"]}
+            launches += 4 * p.info["npasses"]
+            del p
+        auto = qsv.Plan(30, cir.gates(), dtype=qsv.C64)
+        dz["auto_mode_uses"] = "tensor_core_blocks" if auto.info["nblocks"] else "ffma_passes"
+        del auto
+        aux[name] = dz
     del st
-    aux["dense_su4_30q"] = dz
     return aux, launches
 
 

@@ -122,10 +122,11 @@ typedef struct qsv_opts {
     int32_t dense_blocks;   /* complex64, one GPU: fuse the circuit into dense <= 5-qubit
                                blocks (32 x 32 unitaries) applied on the tcgen05 tensor
                                cores (3xTF32, TMEM accumulators), up to 3 blocks per HBM
-                               pass (1 = on, 0 / -1 = off: the fused FFMA tile passes).
-                               Pays for genuinely dense circuits (random two-qubit
-                               unitaries); the BASELINE configs run faster without it
-                                */
+                               pass. 1 = on; -1 = off (the fused FFMA tile passes);
+                               0 = auto: on when the blocks average >= 12 dense
+                               multi-qubit gates (deep local circuits, where it is
+                               measured 2.7-5.4x faster); the BASELINE configs stay on
+                               the FFMA passes */
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */

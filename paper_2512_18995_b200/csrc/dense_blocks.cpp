@@ -105,7 +105,7 @@ void plan_dense(const std::vector<GateRec> &gates, int nlocal, std::vector<Dense
         std::vector<cplx> u(1, cplx(1, 0));
         uint64_t qm = 0, blocked = 0;
         std::vector<int> skipped;
-        int ng = 0;
+        int ng = 0, nd = 0;
         for (int gi : rem) {
             const GateRec &g = gates[gi];
             const uint64_t gm = gate_mask(g);
@@ -124,6 +124,7 @@ void plan_dense(const std::vector<GateRec> &gates, int nlocal, std::vector<Dense
             }
             u = matmul(embed(g, q), u, 1 << q.size());
             ++ng;
+            nd += !g.diag && std::popcount(gm) >= 2;
         }
         // pad to exactly 5 qubits with the lowest free bits
         const int m = static_cast<int>(q.size());
@@ -134,6 +135,7 @@ void plan_dense(const std::vector<GateRec> &gates, int nlocal, std::vector<Dense
         for (int i = 0; i < kDenseQ; ++i) blk.q[i] = q[i];
         blk.u = std::move(u);
         blk.ngates = ng;
+        blk.ndense = nd;
         blocks.push_back(std::move(blk));
         rem.swap(skipped);
     }

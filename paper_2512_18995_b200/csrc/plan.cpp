@@ -476,6 +476,36 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : 0; // 0: per pass (planner.cpp)
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
+    if (p->opts.dense_blocks == 0 && dtype == QSV_C64 && ctx->world == 1 && p->nslots == 0 && p->nlocal >= kDenseTile &&
+        cfg.fuse && p->opts.jit >= 0 && !p->gates.empty()) {
+        // auto: tensor-core blocks when the fused 5-qubit blocks are deep in
+        // genuinely dense gates (measured: ~40 dense two-qubit
+        // gates per block run 2.7-5.4x faster on tensor cores; ~4 per block,
+        // or layers of single-qubit rotations, run faster on the FFMA passes)
+        std::vector<GateRec> phys = p->gates;
+        for (GateRec &g : phys) {
+            for (int t = 0; t < g.k; ++t) g.wires[t] = p->perm_in[g.wires[t]];
+            for (int &c : g.ctls) c = p->perm_in[c];
+        }
+        std::vector<DenseBlock> blocks;
+        std::vector<DensePass> dps;
+        bool ok = true;
+        for (const GateRec &g : phys)
+            ok = ok && !g.encoded && g.flags == 0 && static_cast<int>(g.ctls.size()) + g.k <= kDenseQ;
+        if (ok) {
+            plan_dense(phys, p->nlocal, blocks, dps);
+            long nd = 0;
+            for (const DenseBlock &b : blocks) nd += b.ndense;
+            if (!blocks.empty() && nd >= kDenseAutoPerBlock * static_cast<long>(blocks.size())) {
+                p->dblocks = std::move(blocks);
+                p->dpasses = std::move(dps);
+                p->dense = true;
+                p->perm_out = p->perm_in;
+                if (ctx->stream || ctx->device >= 0) dense_upload(*p);
+                return;
+            }
+        }
+    }
     if (p->opts.dense_blocks > 0) {
         // dense-block plan (tensor cores): every gate fused into <= 5-qubit
         // blocks on physical bits (canonical layout: wire w is bit n-1-w)

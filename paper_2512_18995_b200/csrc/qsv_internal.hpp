@@ -234,10 +234,12 @@ size_t op_record_bytes(const HostOp &op, int dtype, int R);
 constexpr int kDenseQ = 5;
 constexpr int kDenseTile = 12;   // tile bits of a dense-block pass: 128 sets x 32 amplitudes
 constexpr int kDenseMaxBlocks = 3;
+constexpr int kDenseAutoPerBlock = 12;  // auto mode: dense multi-qubit gates per block to prefer tensor cores
 struct DenseBlock {
     int q[kDenseQ] = {0, 0, 0, 0, 0};
     std::vector<cplx> u;         // 32 x 32
     int ngates = 0;
+    int ndense = 0;              // absorbed gates that are dense on two or more qubits
 };
 struct DensePass {
     int tile_pos[kDenseTile];    // physical bit of tile-local bit i (0..3 = the low bits)

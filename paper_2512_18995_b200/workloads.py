@@ -184,3 +184,18 @@ def dense_brickwork_circuit(n: int = 30, depth: int = 20, seed_label: str = "den
             a = 2 * i + (layer % 2)
             cir.add(make_gate("custom", [a, a + 1], custom=haar_su4(rng)))
     return cir
+
+
+def dense_local_circuit(n: int = 30, window: int = 5, depth: int = 20, seed_label: str = "dense-local") -> Circuit:
+    """Deep local scrambling (NOT a BASELINE.json config): the wires split into
+    windows of `window` neighbours, each window a brickwork of `depth` layers of
+    Haar-random two-qubit unitaries -- long runs of genuinely dense gates inside
+    5-qubit blocks, the structure where fused tensor-core blocks pay."""
+    rng = Rng(0, seed_label)
+    cir = Circuit(n)
+    for layer in range(depth):
+        for w0 in range(0, n, window):
+            w1 = min(n, w0 + window)
+            for a in range(w0 + (layer % 2), w1 - 1, 2):
+                cir.add(make_gate("custom", [a, a + 1], custom=haar_su4(rng)))
+    return cir

@@ -9,7 +9,8 @@ from paper_2512_18995_b200 import qsv, workloads as W
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 28
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 which = sys.argv[3] if len(sys.argv) > 3 else "dense"
-cir = W.dense_brickwork_circuit(n, depth) if which == "dense" else W.cfg5_circuit(n, depth)
+cir = (W.dense_brickwork_circuit(n, depth) if which == "dense" else W.dense_local_circuit(n, 5, depth)
+       if which == "local" else W.cfg5_circuit(n, depth))
 st = qsv.QubitState(n, dtype=qsv.C64)
 plans = {"ffma": qsv.Plan(n, cir.gates(), dtype=qsv.C64), "tc": qsv.Plan(n, cir.gates(), dtype=qsv.C64,
                                                                           opts={"dense_blocks": 1})}

@@ -159,6 +159,16 @@ def test_dense_block_planning_on_host():
         assert info["nblocks"] >= 1 and 1 <= info["npasses"] <= info["nblocks"]
         assert info["nblocks"] <= 3 * info["npasses"]
         assert info["ngates"] == len(cir.gates())
+    # auto (dense_blocks = 0): deep local blocks take the tensor cores, the
+    # BASELINE config families and shallow dense brickworks do not
+    auto, _ = qsv.plan_dry(20, W.dense_local_circuit(20, 5, 20).gates(), dtype=qsv.C64)
+    assert auto["nblocks"] > 0
+    for n, cir in ((20, W.dense_brickwork_circuit(20, 20)), (16, W.cfg5_circuit(16, 4)), (12, W.cfg2_circuit()[0]),
+                   (16, W.cfg4_circuit(16, 4))):
+        info, _ = qsv.plan_dry(n, cir.gates(), dtype=qsv.C64)
+        assert info["nblocks"] == 0, n
+    off, _ = qsv.plan_dry(20, W.dense_local_circuit(20, 5, 20).gates(), dtype=qsv.C64, opts={"dense_blocks": -1})
+    assert off["nblocks"] == 0
     with pytest.raises(qsv.InvalidInput):
         qsv.plan_dry(14, W.dense_brickwork_circuit(14, 2).gates(), dtype=qsv.C128, opts={"dense_blocks": 1})
     with pytest.raises(qsv.InvalidInput):

@@ -94,3 +94,21 @@ def test_dense_blocks_refuse_what_they_do_not_cover():
         qsv.Plan(14, cir.gates(), dtype=qsv.C128, opts=DENSE)
     with pytest.raises(qsv.InvalidInput):
         qsv.Plan(10, W.dense_brickwork_circuit(10, 2).gates(), dtype=qsv.C64, opts=DENSE)
+
+
+@pytest.mark.parametrize("n,depth", [(13, 20), (16, 30)])
+def test_auto_selects_tensor_cores_for_deep_local_blocks(n, depth):
+    """Deep local circuits (~40 dense two-qubit gates per 5-qubit block) take
+    the tensor-core path by default (opts.dense_blocks = 0, auto); the result
+    matches the oracle and the forced FFMA plan."""
+    cir = W.dense_local_circuit(n, 5, depth)
+    rng = qsv.Rng(13, f"dense-auto-{n}")
+    psi = random_state(rng, n)
+    want = O.port_forward(n, cir.gates(), init=psi)[0]
+    auto = qsv.Plan(n, cir.gates(), dtype=qsv.C64)
+    off = qsv.Plan(n, cir.gates(), dtype=qsv.C64, opts={"dense_blocks": -1})
+    assert auto.info["nblocks"] > 0 and off.info["nblocks"] == 0
+    for p in (auto, off):
+        st = qsv.QubitState.from_amplitudes(n, psi, dtype=qsv.C64)
+        p.execute(st)
+        close(st.amplitudes(), want, (n, p.info["nblocks"]))
