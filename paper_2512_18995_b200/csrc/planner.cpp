@@ -868,8 +868,35 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             if (count_passes() > base) extra[pi] = 0;
         }
     }
+    // Tile search: besides the greedy admission (tile bits claimed by the
+    // first admissible gates in order), every window of contiguous bits
+    // above the coalescing run is tried as the tile and whichever admits the
+    // most gates wins. Light-cone-shaped circuits (cfg4's brickwork) then get
+    // a trapezoid of neighbouring wires per pass instead of ~one layer of
+    // scattered ones (32q cfg4: 32 -> 17 passes). QSV_TILE_SEARCH=0: greedy.
+    static const bool tile_search = [] {
+        const char *e = std::getenv("QSV_TILE_SEARCH");
+        return !(e && e[0] == '0');
+    }();
     while (!order.empty()) {
         uint64_t active = lowmask_of(passes.size());
+        if (cfg.fuse && tile_search) {
+            std::vector<int> ord = order;
+            uint64_t act = active;
+            size_t best = admit(ord, pg, act, K, localmask).size();
+            uint64_t best_pre = 0;
+            const int free_bits = K - std::popcount(active);
+            for (int s0 = 0; free_bits > 0 && s0 + free_bits <= nl; ++s0) {
+                uint64_t win = 0;
+                for (int b = s0; b < s0 + free_bits; ++b) win |= 1ull << b;
+                if (win & active) continue;
+                ord = order;
+                act = active | win;
+                const size_t got = admit(ord, pg, act, K, localmask).size();
+                if (got > best) best = got, best_pre = win;
+            }
+            active |= best_pre;
+        }
         std::vector<int> took;
         if (cfg.fuse) took = admit(order, pg, active, K, localmask);
         else {
