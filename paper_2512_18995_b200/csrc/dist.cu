@@ -507,9 +507,14 @@ void dist_exchange_apply(State &st, int gbit, const cplx *m, uint64_t local_cmas
         ctx.stage_bytes = need;
     }
     if (!ctx.comm_stream) QSV_CUDA(cudaStreamCreateWithFlags(&ctx.comm_stream, cudaStreamNonBlocking));
-    cudaEvent_t ready, done;
-    QSV_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-    QSV_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+    struct Ev {  // destroyed on every path (an NCCL failure throws mid-loop)
+        cudaEvent_t e = nullptr;
+        Ev() { QSV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+        ~Ev() {
+            if (e) cudaEventDestroy(e);
+        }
+    } ev_ready, ev_done;
+    cudaEvent_t ready = ev_ready.e, done = ev_done.e;
     // rounds alternate between the two halves of the staging buffer; each
     // round's send reads the state chunk BEFORE its combine rewrites it
     int k = 0;
@@ -543,8 +548,6 @@ void dist_exchange_apply(State &st, int gbit, const cplx *m, uint64_t local_cmas
         QSV_CUDA(cudaGetLastError());
     }
     QSV_CUDA(cudaStreamSynchronize(ctx.stream));
-    cudaEventDestroy(ready);
-    cudaEventDestroy(done);
 }
 
 } // namespace qsv
