@@ -59,6 +59,12 @@ def test_no_gpu_fails_loudly():
     assert b"no CPU fallback" in L.qsv_last_error()
     with pytest.raises(qsv.QsvError):
         qsv.Context(0)
+    # the multi-device context fails the same way (and validates its world first)
+    with pytest.raises(qsv.InvalidInput):
+        qsv.Context.multi([0, 0, 0])
+    with pytest.raises(qsv.QsvError):
+        qsv.Context.multi([0, 0])
+    assert b"no CPU fallback" in L.qsv_last_error()
 
 
 @pytest.mark.parametrize("name,wires,params", [
