@@ -251,7 +251,212 @@ __global__ void __launch_bounds__(256, 1) dense_pass_kernel(const DenseArgs a) {
     if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(128));
 }
 
+#define ST64(ADDR, R)                                                                                                 \
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"    \
+                 "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,"  \
+                 "%43,%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};" ::"r"(ADDR),     \
+                 "r"(R[0]), "r"(R[1]), "r"(R[2]), "r"(R[3]), "r"(R[4]), "r"(R[5]), "r"(R[6]), "r"(R[7]), "r"(R[8]),          \
+                 "r"(R[9]), "r"(R[10]), "r"(R[11]), "r"(R[12]), "r"(R[13]), "r"(R[14]), "r"(R[15]), "r"(R[16]), "r"(R[17]),   \
+                 "r"(R[18]), "r"(R[19]), "r"(R[20]), "r"(R[21]), "r"(R[22]), "r"(R[23]), "r"(R[24]), "r"(R[25]), "r"(R[26]),  \
+                 "r"(R[27]), "r"(R[28]), "r"(R[29]), "r"(R[30]), "r"(R[31]), "r"(R[32]), "r"(R[33]), "r"(R[34]), "r"(R[35]),  \
+                 "r"(R[36]), "r"(R[37]), "r"(R[38]), "r"(R[39]), "r"(R[40]), "r"(R[41]), "r"(R[42]), "r"(R[43]), "r"(R[44]),  \
+                 "r"(R[45]), "r"(R[46]), "r"(R[47]), "r"(R[48]), "r"(R[49]), "r"(R[50]), "r"(R[51]), "r"(R[52]), "r"(R[53]),  \
+                 "r"(R[54]), "r"(R[55]), "r"(R[56]), "r"(R[57]), "r"(R[58]), "r"(R[59]), "r"(R[60]), "r"(R[61]), "r"(R[62]),  \
+                 "r"(R[63]))
+#define LD64(R, ADDR)                                                                                                 \
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"   \
+                 "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,"   \
+                 "%44,%45,%46,%47,%48,%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63}, [%64];"                 \
+                 : "=r"(R[0]), "=r"(R[1]), "=r"(R[2]), "=r"(R[3]), "=r"(R[4]), "=r"(R[5]), "=r"(R[6]), "=r"(R[7]),       \
+                   "=r"(R[8]), "=r"(R[9]), "=r"(R[10]), "=r"(R[11]), "=r"(R[12]), "=r"(R[13]), "=r"(R[14]), "=r"(R[15]), \
+                   "=r"(R[16]), "=r"(R[17]), "=r"(R[18]), "=r"(R[19]), "=r"(R[20]), "=r"(R[21]), "=r"(R[22]),           \
+                   "=r"(R[23]), "=r"(R[24]), "=r"(R[25]), "=r"(R[26]), "=r"(R[27]), "=r"(R[28]), "=r"(R[29]),           \
+                   "=r"(R[30]), "=r"(R[31]), "=r"(R[32]), "=r"(R[33]), "=r"(R[34]), "=r"(R[35]), "=r"(R[36]),           \
+                   "=r"(R[37]), "=r"(R[38]), "=r"(R[39]), "=r"(R[40]), "=r"(R[41]), "=r"(R[42]), "=r"(R[43]),           \
+                   "=r"(R[44]), "=r"(R[45]), "=r"(R[46]), "=r"(R[47]), "=r"(R[48]), "=r"(R[49]), "=r"(R[50]),           \
+                   "=r"(R[51]), "=r"(R[52]), "=r"(R[53]), "=r"(R[54]), "=r"(R[55]), "=r"(R[56]), "=r"(R[57]),           \
+                   "=r"(R[58]), "=r"(R[59]), "=r"(R[60]), "=r"(R[61]), "=r"(R[62]), "=r"(R[63])                         \
+                 : "r"(ADDR))
+
+// Two tiles in flight per SM: warpgroup g (0 / 1) owns tile slot g -- its
+// own double-buffered shared tile, mbarrier and 256 TMEM columns (A_hi,
+// A_lo, the hi x hi accumulator, the correction accumulator) -- so one
+// slot's gather / scatter overlaps the other's tensor-core products. A goes
+// to TMEM with tcgen05.st (thread t = TMEM lane t = set row t, one TF32 per
+// column) and the MMAs read it from there (the kind::tf32 TS form), so the
+// shared memory holds only the tiles and the B images.
+__global__ void __launch_bounds__(256, 1) dense_pass_kernel_v3(const DenseArgs a) {
+    extern __shared__ __align__(1024) unsigned char sm_raw[];
+    unsigned char *sm = sm_raw + ((1024 - (smem_u32(sm_raw) & 1023)) & 1023);
+    unsigned char *Bs = sm;
+    float2 *const T0 = reinterpret_cast<float2 *>(Bs + a.nb * 2 * kBbytes);  // [slot][buffer] tiles
+    __shared__ uint64_t mbar[2];
+    __shared__ uint32_t tmem_base;
+    __shared__ int sj[kDenseMaxBlocks][32];
+    __shared__ uint64_t gk[32];  // tile offsets of u = 128 k (copies by 128 threads)
+    __shared__ int sk[32];
+    const int tid = threadIdx.x, g = tid >> 7, t = tid & 127, warp = tid >> 5;
+    {
+        const int n4 = a.nb * 2 * kBbytes / 16;
+        float4 *dst = reinterpret_cast<float4 *>(Bs);
+        for (int i = tid; i < n4; i += 256) dst[i] = a.bimg[i];
+    }
+    if (tid < a.nb * 32) {
+        const int b = tid >> 5, j = tid & 31;
+        int u = 0;
+        for (int i = 0; i < kDenseQ; ++i) u |= ((j >> i) & 1) << a.bbit[b][i];
+        sj[b][j] = swz(u, a.swm);
+    }
+    if (tid < 32) {
+        gk[tid] = scatter_bits(static_cast<uint64_t>(tid) << 7, a.tile_pos, kDenseTile);
+        sk[tid] = swz(tid << 7, a.swm);
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[0])));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar[1])));
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t col0 = tmem_base + 256u * g;                         // this slot's columns
+    const uint32_t lane = (static_cast<uint32_t>(warp & 3) * 32) << 16;  // this warp's TMEM lanes
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((kN >> 3) << 17) | ((kRows >> 4) << 24);
+    uint32_t phase = 0;
+    int stb[kDenseMaxBlocks];
+    for (int b = 0; b < kDenseMaxBlocks; ++b) {
+        int ut = 0;
+        if (b < a.nb) {
+            int k = 0;
+            for (int i = 0; i < kDenseTile; ++i) {
+                bool in = false;
+                for (int q = 0; q < kDenseQ; ++q) in = in || a.bbit[b][q] == i;
+                if (!in) ut |= ((t >> k++) & 1) << i;
+            }
+        }
+        stb[b] = swz(ut, a.swm);
+    }
+    const uint64_t gt = scatter_bits(static_cast<uint64_t>(t), a.tile_pos, 7);
+    const int swt = swz(t, a.swm);
+    auto tile_base = [&](uint64_t tile) {
+        const uint64_t row = tile >> a.tpr_log, tl = tile & ((1ull << a.tpr_log) - 1);
+        return row * a.row_stride + scatter_bits(tl, a.ext_pos, a.next);
+    };
+    auto issue = [&](uint64_t tile, float2 *buf) {
+        const float2 *src = a.state + tile_base(tile) + gt;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(&buf[swt ^ sk[k]])),
+                         "l"(src + gk[k])
+                         : "memory");
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    auto slot_sync = [&] { asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory"); };
+    float2 *const Tg = T0 + static_cast<size_t>(g) * 2 * kTileAmps;
+    const uint64_t step = 2ull * gridDim.x;
+    uint64_t tile = 2ull * blockIdx.x + g;
+    int buf = 0;
+    if (tile < a.ntiles) issue(tile, Tg);
+    for (; tile < a.ntiles; tile += step) {
+        if (tile + step < a.ntiles) {
+            issue(tile + step, Tg + (buf ^ 1) * kTileAmps);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        slot_sync();
+        float2 *tl = Tg + buf * kTileAmps;
+        for (int b = 0; b < a.nb; ++b) {
+            const int st = stb[b];
+            {
+                uint32_t hi[64], lo[64];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float2 x = tl[st ^ sj[b][j]];
+                    const float hr = tf32_hi(x.x), hm = tf32_hi(x.y);
+                    hi[2 * j] = __float_as_uint(hr);
+                    hi[2 * j + 1] = __float_as_uint(hm);
+                    lo[2 * j] = __float_as_uint(x.x - hr);
+                    lo[2 * j + 1] = __float_as_uint(x.y - hm);
+                }
+                ST64(col0 + lane, hi);
+                ST64(col0 + lane + 64u, lo);
+                asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            slot_sync();
+            if (t == 0) {
+                asm volatile("tcgen05.fence::after_thread_sync;");
+                const unsigned char *Bhi = Bs + b * 2 * kBbytes, *Blo = Bhi + kBbytes;
+                // D0 (cols +128) = A_hi B_hi; Dc (cols +192) = A_hi B_lo + A_lo B_hi + A_lo B_lo
+                const uint32_t Acol[4] = {col0, col0, col0 + 64u, col0 + 64u};
+                const unsigned char *Bp[4] = {Bhi, Blo, Bhi, Blo};
+                for (int p = 0; p < 4; ++p) {
+                    int acc = p >= 2 ? 1 : 0;
+                    const uint32_t d = col0 + (p == 0 ? 128u : 192u);
+                    for (int ks = 0; ks < kK / 8; ++ks) {
+                        const uint64_t bd = sdesc(smem_u32(Bp[p]) + kstep<kN>(ks));
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d),
+                            "r"(Acol[p] + 8u * ks), "l"(bd), "r"(idesc), "r"(acc));
+                        acc = 1;
+                    }
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                    smem_u32(&mbar[g])));
+            }
+            {
+                uint32_t done = 0;
+                for (long spin = 0; !done; ++spin) {
+                    asm volatile(
+                        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, "
+                        "p;\n}\n"
+                        : "=r"(done)
+                        : "r"(smem_u32(&mbar[g])), "r"(phase));
+                    if (spin > (1l << 28)) __trap();
+                }
+            }
+            phase ^= 1;
+            asm volatile("tcgen05.fence::after_thread_sync;");
+            {
+                uint32_t r[64], q[64];
+                LD64(r, col0 + lane + 128u);
+                LD64(q, col0 + lane + 192u);
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    tl[st ^ sj[b][j]] = make_float2(__uint_as_float(r[2 * j]) + __uint_as_float(q[2 * j]),
+                                                    __uint_as_float(r[2 * j + 1]) + __uint_as_float(q[2 * j + 1]));
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;");
+            slot_sync();
+        }
+        {
+            float2 *dst = a.state + tile_base(tile) + gt;
+#pragma unroll 8
+            for (int k = 0; k < 32; ++k) __stcs(dst + gk[k], tl[swt ^ sk[k]]);
+        }
+        slot_sync();
+        buf ^= 1;
+    }
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    __syncthreads();
+    if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+}
+
 size_t dense_smem(int nb) { return 2 * kAbytes + static_cast<size_t>(nb) * 2 * kBbytes + 2 * kTileAmps * 8 + 1024; }
+size_t dense_smem_v3(int nb) { return static_cast<size_t>(nb) * 2 * kBbytes + 4 * kTileAmps * 8 + 1024; }
+// QSV_DENSE_V2=1: the single-slot kernel with A in shared memory (A/B)
+bool dense_v2() {
+    static const bool v = [] {
+        const char *e = std::getenv("QSV_DENSE_V2");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
 
 } // namespace
 
@@ -270,6 +475,8 @@ void dense_upload(Plan &p) {
     if (!all.empty()) QSV_CUDA(cudaMemcpy(d->bimg, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice));
     QSV_CUDA(cudaFuncSetAttribute(dense_pass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(dense_smem(kDenseMaxBlocks))));
+    QSV_CUDA(cudaFuncSetAttribute(dense_pass_kernel_v3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(dense_smem_v3(kDenseMaxBlocks))));
 }
 
 void dense_free(Plan &p) {
@@ -302,9 +509,14 @@ void dense_execute(Plan &p, State &st, cudaStream_t s, double *launch_ms) {
             for (int i = 0; i < kDenseQ; ++i) a.bbit[b][i] = dp.bbit[b][i];
         for (int i = 0; i < 4; ++i) a.swm[i] = dp.swm[i];
         a.state = static_cast<float2 *>(st.d);
-        const int grid = static_cast<int>(std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(p.ctx->sm_count)));
         if (launch_ms) QSV_CUDA(cudaEventRecord(ev[2 * pi], s));
-        dense_pass_kernel<<<grid, 256, dense_smem(a.nb), s>>>(a);
+        if (dense_v2()) {
+            const int grid = static_cast<int>(std::min<uint64_t>(a.ntiles, static_cast<uint64_t>(p.ctx->sm_count)));
+            dense_pass_kernel<<<grid, 256, dense_smem(a.nb), s>>>(a);
+        } else {  // two tiles in flight per CTA
+            const int grid = static_cast<int>(std::min<uint64_t>((a.ntiles + 1) / 2, static_cast<uint64_t>(p.ctx->sm_count)));
+            dense_pass_kernel_v3<<<grid, 256, dense_smem_v3(a.nb), s>>>(a);
+        }
         QSV_CUDA(cudaGetLastError());
         if (launch_ms) QSV_CUDA(cudaEventRecord(ev[2 * pi + 1], s));
     }
