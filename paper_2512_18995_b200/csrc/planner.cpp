@@ -118,6 +118,12 @@ bool is_unitary_diag(const GateRec &g) {
     return true;
 }
 
+// QSV_X_NOHOIST=1 (A/B switch): deferred diagonals stay in program order
+bool hoist_diagonals() {
+    const char *e = std::getenv("QSV_X_NOHOIST");
+    return !(e && e[0] == '1');
+}
+
 cplx eval_rec(const DiagRec &r, uint64_t pb) {
     if ((pb & r.fmask) != r.fval) return cplx(1, 0);
     int idx = 0;
@@ -169,6 +175,10 @@ struct GroupLowering {
     std::vector<cplx> pend_reg;               // register table
     unsigned pend_reg_slots = 0;
     int n_ext = 0;
+    bool x_through = [] {  // QSV_X_NOXPERM=1 (A/B): flush before every X instead
+        const char *e = std::getenv("QSV_X_NOXPERM");
+        return !(e && e[0] == '1');
+    }();
 
     GroupLowering(PassHost &p, const std::vector<GateRec> &g, const std::vector<int> &ph_, const int *sop, int r,
                   std::vector<EncDesc> &e, bool fe)
@@ -390,9 +400,36 @@ struct GroupLowering {
         return false;
     }
 
+    // An X on a register slot whose controls are register slots (or none) only
+    // relabels registers: the pending register table is permuted through it
+    // instead of flushed, so one layer's closing phases and the next layer's
+    // opening phases meet in one flush (brickwork CNOT layers).
+    bool try_permute(const GateRec &g) {
+        if (!flush_enabled || !x_through || g.diag || g.encoded || g.flags || g.k != 1) return false;
+        if (!(g.m[0] == cplx(0, 0) && g.m[3] == cplx(0, 0) && g.m[1] == cplx(1, 0) && g.m[2] == cplx(1, 0)))
+            return false;
+        const int t = slot(g.wires[0]);
+        if (t < 0) return false;
+        unsigned rc = 0;
+        for (int c : g.ctls) {
+            const int s = slot(c);
+            if (s < 0) return false;
+            rc |= 1u << s;
+        }
+        if (!pend[t].empty()) flush(1u << t, false, false);
+        if (pend_reg_slots) {
+            for (int r = 0; r < (1 << R); ++r)
+                if (!((r >> t) & 1) && (r & rc) == rc) std::swap(pend_reg[r], pend_reg[r | (1 << t)]);
+            pend_reg_slots |= (1u << t) | rc;
+        }
+        lower(g);
+        return true;
+    }
+
     void add(int gi) {
         const GateRec &g = gates[gi];
         if (try_defer(g)) return;
+        if (try_permute(g)) return;
         if (!g.diag) { // flush pending phases on the slots it acts on non-diagonally
             unsigned need = 0;
             for (int t = 0; t < g.k; ++t) {
@@ -575,6 +612,22 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
         for (int i = 0; i < K - R; ++i) low.ng_phys.push_back(ph.tile_pos[hg.ng_bit[i]]);
         hg.op_begin = static_cast<int>(ph.ops.size());
         hg.tgt_begin = static_cast<int>(ph.targets.size());
+        if (cfg.phase_flush && hoist_diagonals()) {
+            // deferred diagonals move to the front of the group as far as they
+            // commute, so phases that are flushed anyway share one flush (an
+            // Euler-split layer's opening phases diag(1, r) of all R slots
+            // land before the layer's first rotation: one register-table
+            // flush instead of one per slot)
+            std::vector<int> ord;
+            for (int gi : gtook) {
+                size_t pos = ord.size();
+                const GateRec &g = gates[gi];
+                if (g.diag && !g.encoded && !g.flags && is_unitary_diag(g))
+                    while (pos > 0 && !conflicts(pg[gi], pg[ord[pos - 1]].nmask, pg[ord[pos - 1]].dmask)) --pos;
+                ord.insert(ord.begin() + static_cast<std::ptrdiff_t>(pos), gi);
+            }
+            gtook.swap(ord);
+        }
         for (int gi : gtook) {
             GateRec e = gates[gi];
             for (int t = 0; t < e.k; ++t) e.wires[t] = phys[e.wires[t]];
