@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <map>
 #include <sstream>
@@ -160,7 +161,38 @@ struct Gen {
             }
     }
 
-    std::string c(double x) const { return lit(x, f32); }
+    // complex128 constants: hexfloat immediates (a DFMA takes no 64-bit
+    // immediate, so each distinct value costs two UMOVs in the instruction
+    // stream), or with `pool` one __constant__ table per kernel read by
+    // LDCU.128 (two values per instruction)
+    bool pool = [] {
+        const char *e = std::getenv("QSV_X_CPOOL");
+        return e && e[0] == '1';
+    }();
+    mutable std::map<uint64_t, int> pool_idx;
+    mutable std::vector<double> pool_vals;
+    std::string c(double x) const {
+        if (f32 || !pool) return lit(x, f32);
+        const double a = std::fabs(x);
+        uint64_t bits;
+        std::memcpy(&bits, &a, 8);
+        auto it = pool_idx.find(bits);
+        int i;
+        if (it == pool_idx.end()) {
+            i = static_cast<int>(pool_vals.size());
+            pool_idx.emplace(bits, i);
+            pool_vals.push_back(a);
+        } else i = it->second;
+        return std::string(x < 0 ? "(-KC[" : "(KC[") + std::to_string(i) + "])";
+    }
+    std::string pool_decl() const {
+        if (pool_vals.empty()) return "";
+        std::ostringstream d;
+        d << "__constant__ double KC[" << pool_vals.size() << "] = {";
+        for (size_t i = 0; i < pool_vals.size(); ++i) d << (i ? ", " : "") << lit(pool_vals[i], false);
+        d << "};\n";
+        return d.str();
+    }
 
     // complex128 tile swizzle: the 16-byte slot of amplitude u is u with its
     // low 3 bits XORed with parities of the high bits (swm[i] = the high bits
@@ -860,7 +892,7 @@ struct Gen {
         const int threads = threads_of();
         const std::string body = body_fn("pass_body");
         std::ostringstream k;
-        k << "// generated by qsv codegen.cpp: one fused tile pass\n" << common() << body;
+        k << "// generated by qsv codegen.cpp: one fused tile pass\n" << common() << pool_decl() << body;
         k << "extern \"C\" __global__ void __launch_bounds__(" << threads << ", "
           << (double_buffer ? 1 : kernel_min_blocks(ph, threads)) << ") " << name << "(const Args a) {\n";
         k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
@@ -1457,6 +1489,7 @@ std::string generate_pair_source(const PassHost &A, const PassHost &B, int dtype
                                  int *threads, bool dbuf, size_t *smem) {
     Gen ga(A, dtype), gb(B, dtype);
     for (Gen *g : {&ga, &gb}) {
+        g->pool = false;
         g->double_buffer = false;
         g->prefetch = dbuf;
         g->stages = dbuf_stages(g->ph, dtype);

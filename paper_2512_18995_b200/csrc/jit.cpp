@@ -183,13 +183,29 @@ JitKernel load_kernel(const std::string &src, const std::string &name) {
     return jk;
 }
 
-bool use_prefetch(const PassHost &ph, int dtype) {
+bool use_prefetch(const PassHost &ph, int dtype) { return pass_prefetches(ph, dtype); }
+} // namespace
+
+// Double-buffered (prefetching) tiles hide HBM latency; a pass whose gate
+// math outweighs its memory time runs better single-buffered, with a CTA
+// more per SM (more warps to hide the FP64 / FMA latencies). Heavy = more
+// dense register-group matrices than 3x the tile bits (the QFT passes: ~8
+// per 11-bit tile, prefetching; the brickwork passes of cfg4: 40-130).
+// Interleaved A/B, cfg4 family: 32q 912 -> 887 ms, 28q 51.9 -> 49.6 ms; QFT
+// with prefetching off 22.6 -> 26.2 ms. QSV_PREFETCH=0 / 1 forces it.
+bool pass_prefetches(const PassHost &ph, int dtype) {
     const int amp0 = dtype == QSV_C64 ? 8 : 16;
     const char *pe = std::getenv("QSV_PREFETCH");
-    return (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && !(pe && pe[0] == '0') &&
-           (1 << ph.K) * amp0 >= 16 * 32 && !ph.synth;
+    if (pe && pe[0] == '0') return false;
+    const bool fits = (2 * (static_cast<size_t>(amp0) << ph.K) <= (64u << 10)) && (1 << ph.K) * amp0 >= 16 * 32 &&
+                      !ph.synth;
+    if (!fits) return false;
+    if (pe && pe[0] == '1') return true;
+    int dense = 0;
+    for (const HostOp &op : ph.ops)
+        if (op.code == OP_DENSE1 || op.code == OP_DENSE1R || op.code == OP_DENSE2) ++dense;
+    return dense <= 3 * ph.K;
 }
-} // namespace
 
 void jit_prepare_pair(DevPass &head, const PassHost &a, const PassHost &b, int dtype, int sm_count) {
     (void)sm_count;

@@ -587,6 +587,9 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
         for (int t = 0; t < K - R; ++t) hg.ng_bit[t] = t;
         ph.groups.push_back(hg);
     }
+    // groups: admission first (all of them), then the lowering
+    std::vector<std::vector<int>> gtooks;
+    std::vector<std::vector<int>> gslots;  // slot tile bits per group
     while (!gorder.empty()) {
         uint64_t gact = 0;
         std::vector<int> gtook = admit(gorder, pg, gact, R, active);
@@ -598,6 +601,12 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
             if (gact & (1ull << b)) slot_tile.push_back(tile_of_phys[b]);
         for (int t = K - 1; t >= 0 && static_cast<int>(slot_tile.size()) < R; --t)
             if (std::find(slot_tile.begin(), slot_tile.end(), t) == slot_tile.end()) slot_tile.push_back(t);
+        gtooks.push_back(std::move(gtook));
+        gslots.push_back(std::move(slot_tile));
+    }
+    for (size_t gix = 0; gix < gtooks.size(); ++gix) {
+        std::vector<int> &gtook = gtooks[gix];
+        const std::vector<int> &slot_tile = gslots[gix];
         HostGroup hg;
         int slot_of_phys[64];
         for (int &x : slot_of_phys) x = -1;
@@ -1065,6 +1074,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             const int cb = std::popcount(cm);
             const bool ok = A.K == B.K && A.R == B.R && !A.synth && !B.synth && A.out_perm.empty() &&
                             !A.local_gperm && !B.local_gperm &&
+                            pass_prefetches(A, cfg.dtype) == pass_prefetches(B, cfg.dtype) &&
                             cb <= cfg.super_bits && cb >= A.K + 2 && cb < nl;
             if (!ok) {
                 ++i;

@@ -11,7 +11,8 @@ from paper_2512_18995_b200 import qsv, workloads as W
 n = int(sys.argv[1]); cfg = sys.argv[2]; variants = sys.argv[3:]
 mk = {"cfg3": lambda: (W.cfg3_circuit(n), qsv.C128), "cfg4": lambda: (W.cfg4_circuit(n, 4), qsv.C128),
       "cfg5": lambda: (W.cfg5_circuit(n, 4), qsv.C64),
-      "cfg4f": lambda: (W.cfg4_circuit(n), qsv.C128), "cfg5f": lambda: (W.cfg5_circuit(n), qsv.C64)}[cfg]
+      "cfg4f": lambda: (W.cfg4_circuit(n), qsv.C128), "cfg5f": lambda: (W.cfg5_circuit(n), qsv.C64),
+      "brick": lambda: (W.dense_brickwork_circuit(n, 20), qsv.C64), "cfg3c64": lambda: (W.cfg3_circuit(n), qsv.C64)}[cfg]
 cir, dt = mk()
 st = qsv.QubitState(n, dtype=dt)
 psi = W.cfg3_slice(0, 1 << n)

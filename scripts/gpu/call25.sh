@@ -1,0 +1,9 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
+make -C tests/fake_nccl >/dev/null
+export AB_REPS=3
+timeout 900 python scripts/ab.py 32 cfg4f "" "QSV_PREFETCH=1" 2>&1 | grep median
+timeout 900 python scripts/ab.py 30 cfg3 "" "QSV_PREFETCH=1" 2>&1 | grep median
+timeout 900 python scripts/ab.py 30 brick "OPT_dense_blocks=-1" "OPT_dense_blocks=-1,QSV_PREFETCH=1" 2>&1 | grep median
+for f in tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_multi.py tests/test_gpu_dist_shim.py tests/test_gpu_mixed.py tests/test_gpu_adjoint.py; do
+  echo "=== $f"; timeout 1500 python -m pytest $f -q -x -m gpu 2>&1 | tail -2
+done

@@ -526,7 +526,7 @@ def test_graph_cache_survives_buffer_reallocation(dtype):
 @pytest.mark.parametrize("dtype", [C128, C64])
 @pytest.mark.parametrize("variant", ["", "QSV_X_NOPACK", "QSV_X_NOSCALE", "QSV_X_NOTAN", "QSV_X_NOSPLIT",
                                      "QSV_X_NOSIGN", "QSV_X_NOPAIR", "QSV_X_OLDSWZ", "QSV_X_NOXPERM",
-                                     "QSV_X_NOHOIST"])
+                                     "QSV_X_NOHOIST", "QSV_X_CPOOL"])
 @pytest.mark.parametrize("reg_slots", [0, 2, 3, 4])
 def test_generated_arithmetic_variants(dtype, variant, reg_slots, monkeypatch):
     """The generated kernels' arithmetic forms -- tangent-form real matrices
