@@ -297,7 +297,14 @@ struct Gen {
     // helpers of common()): a real coefficient is one FMUL2/FFMA2, a complex
     // one two (the i*x half reads x with its halves swapped, which ptxas
     // folds into the operand), +-1 an FADD2.
-    std::string packed_sum(const std::vector<std::pair<cplx, std::string>> &ts) const {
+    std::string packed_sum(const std::vector<std::pair<cplx, std::string>> &ts_in) const {
+        // a +1 term starts the chain (acc = x, no instruction), so a real
+        // row [c, 1] is one FFMA2 instead of FMUL2 + FADD2 (the scale
+        // tracking leaves a +1 in every real row)
+        std::vector<std::pair<cplx, std::string>> ts = ts_in;
+        std::stable_partition(ts.begin(), ts.end(), [&](const std::pair<cplx, std::string> &t) {
+            return snap(t.first.real()) == 1.0 && snap(t.first.imag()) == 0.0;
+        });
         std::string acc;
         for (const auto &t : ts) {
             const double a = snap(t.first.real()), b = snap(t.first.imag());

@@ -568,7 +568,31 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
             for (int w = 0; w < n; ++w) out_perm[fin[w]] = p->perm_in[w];
         }
         if (!p->gates.empty()) {
+            const size_t encs0 = p->encs.size();
             auto passes = plan_passes(gl, phys, cfg, p->encs, out_perm);
+            // complex64, default geometry: a memory-bound circuit (at most
+            // 1.5 K dense register-group matrices per pass on average: the
+            // QFT ~7.5, SU(4) brickworks ~17; cfg5's rotation layers ~27
+            // stay on 13-bit tiles) runs faster on
+            // 12-bit double-buffered tiles with 4-qubit register groups than
+            // on the 13-bit single-buffered tiles that suit the compute-bound
+            // ones (cfg5). Interleaved A/B, c64 QFT: 28q 4.10 -> 2.97 ms, 30q
+            // 15.4 -> 12.0 ms, 32q 60.1 -> 53.8 ms. QSV_X_NOLIGHT=1: off.
+            const char *nl_env = std::getenv("QSV_X_NOLIGHT");
+            if (dtype == QSV_C64 && p->opts.tile_bits <= 0 && p->opts.reg_slots <= 0 && cfg.K == 13 &&
+                p->nlocal > 13 && !(nl_env && nl_env[0] == '1')) {
+                long dense = 0;
+                for (const PassHost &ph : passes)
+                    for (const HostOp &op : ph.ops)
+                        if (op.code == OP_DENSE1 || op.code == OP_DENSE1R || op.code == OP_DENSE2) ++dense;
+                if (2 * dense <= 3L * cfg.K * static_cast<long>(passes.size())) {  // <= 1.5 K per pass
+                    PlanConfig light = cfg;
+                    light.K = 12;
+                    light.R = 4;
+                    p->encs.resize(encs0);
+                    passes = plan_passes(gl, phys, light, p->encs, out_perm);
+                }
+            }
             if (p->synth) {
                 require(!passes.empty(), "plan: product-state prefix without a pass");
                 passes.front().synth = true;

@@ -373,6 +373,25 @@ def test_mirror_circuits_return_to_zero(dtype, n):
         assert np.max(np.abs(a[1:])) <= 10 * TOL[dtype]
 
 
+@pytest.mark.parametrize("light", ["", "QSV_X_NOLIGHT"])
+def test_c64_memory_bound_geometry(light, monkeypatch):
+    """complex64 circuits with few dense matrices per pass (the QFT, SU(4)
+    brickworks) plan on 12-bit double-buffered tiles with 4-qubit register
+    groups (plan.cpp); QSV_X_NOLIGHT=1 keeps the 13-bit geometry. Both
+    against the oracle on a seeded random state, above the 13-qubit switch."""
+    if light:
+        monkeypatch.setenv(light, "1")
+    n = 18
+    rng = Rng(5, "light-c64")
+    psi = random_state(rng, n)
+    for cir in (W.cfg3_circuit(n), W.dense_brickwork_circuit(n, 4)):
+        info, _ = qsv.plan_dry(n, cir.gates(), dtype=C64, opts={"dense_blocks": -1})
+        assert info["max_tile_bits"] == (13 if light else 12)
+        got, _ = run(n, cir.gates(), init=psi, dtype=C64, opts={"dense_blocks": -1})
+        want = O.port_forward(n, cir.gates(), init=psi)[0]
+        assert_close(got[0], want, C64)
+
+
 def test_cfg5_family_c64_vs_reference():
     cir = W.cfg5_circuit(16, layers=4)
     s = cir.forward(dtype=C64)
