@@ -12,6 +12,10 @@ elif cfg == "cfg4":
     cir, dt = W.cfg4_circuit(n, 4), qsv.C128
 elif cfg == "cfg5":
     cir, dt = W.cfg5_circuit(n, 4), qsv.C64
+elif cfg == "cfg4f":
+    cir, dt = W.cfg4_circuit(n), qsv.C128
+elif cfg == "cfg5f":
+    cir, dt = W.cfg5_circuit(n), qsv.C64
 else:
     cir, dt = W.cfg1_circuit(n), qsv.C128
 p = qsv.Plan(n, cir.gates(), dtype=dt)
