@@ -261,7 +261,7 @@ def run_reference(args):
     value = args.steps / t
     line = {
         "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": 0, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "c128", "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state)",
         "impl": "reference", "config": config_dict(n), "sample": desc,
         "cpu_baseline": {"value": value, "unit": "gates/s", "cores": 1, "host_cores": os.cpu_count(),
@@ -610,7 +610,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": "gates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "c128",
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128",
             "data": "synthetic (seeded Rng(0,'cfg3') Gaussian state, normalised in FP64)",
             "config": config_dict(n),
             "plan": {"passes_per_step": npass, "swaps_per_step": plan.info["nswaps"],
