@@ -544,6 +544,7 @@ PassHost lower_pass(const std::vector<GateRec> &gates, const std::vector<PG> &pg
                     std::vector<EncDesc> &encs, const std::vector<int> *out_perm = nullptr,
                     uint64_t ext_first = 0) {
     const int nl = cfg.nlocal;
+    K = std::max(K, std::popcount(active));  // passenger bits (QSV_PASSENGERS) widen the tile
     PassHost ph;
     ph.K = K;
     ph.L = L;
@@ -996,6 +997,33 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             for (int i : took) active |= pg[i].nmask;
             encs.resize(first_encs);
             ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
+        }
+        {
+            // Passenger bit: a compute-bound pass (more dense register-group
+            // matrices than 3x its tile bits: single-buffered, jit.cpp) also
+            // carries the lowest free bit in its tile, untouched by its gates,
+            // so one CTA runs two of the planned tiles in lock-step through
+            // the same group code. The deep straight-line passes are
+            // instruction-cache bound (ncu: no_instruction the top stall);
+            // half as many CTAs at different points of the code per SM.
+            // Interleaved A/B, cfg4 family: 28q 49.4 -> 47.0 ms, 30q 201.7 ->
+            // 188.5 ms; two passenger bits lose (215.5 ms). QSV_PASSENGERS=P
+            // overrides (0 = off); the widened tile must stay <= 64 KiB.
+            const char *e = std::getenv("QSV_PASSENGERS");
+            const int P = e ? std::atoi(e) : 1;
+            int dense = 0;
+            for (const HostOp &op : ph.ops)
+                if (op.code == OP_DENSE1 || op.code == OP_DENSE1R || op.code == OP_DENSE2) ++dense;
+            const size_t amp = cfg.dtype == QSV_C64 ? 8 : 16;
+            if (P > 0 && dense > 3 * K && std::popcount(active) + P <= nl &&
+                (amp << (std::popcount(active) + P)) <= (64u << 10)) {
+                uint64_t a2 = active;
+                for (int b = 0, got = 0; b < nl && got < P; ++b)
+                    if (!((a2 >> b) & 1)) a2 |= 1ull << b, ++got;
+                encs.resize(first_encs);
+                ph = lower_pass(gates, pg, took, a2, phys, cfg, K, L, R, encs);
+                active = a2;
+            }
         }
         passes.push_back(std::move(ph));
         how.push_back({took, active, false});

@@ -392,6 +392,23 @@ def test_c64_memory_bound_geometry(light, monkeypatch):
         assert_close(got[0], want, C64)
 
 
+@pytest.mark.parametrize("passengers", ["0", "1"])
+def test_passenger_bit_tiles(passengers, monkeypatch):
+    """Compute-bound complex128 passes carry one passenger bit (planner.cpp:
+    two planned tiles per CTA in lock-step); QSV_PASSENGERS=0 plans without.
+    Both against the oracle on a seeded random state."""
+    monkeypatch.setenv("QSV_PASSENGERS", passengers)
+    n = 18
+    rng = Rng(6, "passengers")
+    psi = random_state(rng, n)
+    cir = W.cfg4_circuit(n, layers=6)
+    info, _ = qsv.plan_dry(n, cir.gates())
+    assert info["max_tile_bits"] == 11 + int(passengers)
+    got, _ = run(n, cir.gates(), init=psi)
+    want = O.port_forward(n, cir.gates(), init=psi)[0]
+    assert_close(got[0], want, C128)
+
+
 def test_cfg5_family_c64_vs_reference():
     cir = W.cfg5_circuit(16, layers=4)
     s = cir.forward(dtype=C64)
