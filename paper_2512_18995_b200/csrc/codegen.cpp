@@ -109,10 +109,26 @@ std::string scatter(const std::string &x, const std::vector<int> &pos, bool wide
 
 // One register set per thread per group (up to 512 threads: 2 CTAs x 16 warps
 // per SM), at least one 16-byte chunk per thread for the tile copies.
-int kernel_threads(const PassHost &ph, int dtype) {
-    (void)dtype;
-    const int nsets = 1 << (ph.K - ph.R); // exactly one register set per thread per group
-    const int th = std::max(32, std::min(512, nsets));
+//
+// A compute-bound complex64 pass (more dense register-group matrices than
+// tile bits) runs 256-thread CTAs instead: several register sets per thread,
+// three CTAs per SM (shared memory) instead of two, so one CTA's tile load
+// overlaps two others' arithmetic. Interleaved A/B: cfg5 family 30q 99.2 ->
+// 95.5 ms, 33q 855 -> 823 ms; cfg2 execute 0.358 -> 0.297 ms; the light
+// (memory-bound) passes keep 512 (the cfg5 tail passes lose 5-17 % at 256).
+// QSV_MAX_THREADS overrides the cap.
+int threads_for(const PassHost &ph, int dtype) {
+    const int nsets = 1 << (ph.K - ph.R); // one register set per thread per group, up to the cap
+    int cap = 512;
+    if (dtype == QSV_C64) {
+        int dense = 0;
+        for (const HostOp &op : ph.ops)
+            if (op.code == OP_DENSE1 || op.code == OP_DENSE1R || op.code == OP_DENSE2) ++dense;
+        if (dense > ph.K) cap = 256;
+    }
+    const char *mt = std::getenv("QSV_MAX_THREADS");
+    if (mt && std::atoi(mt) > 0) cap = std::atoi(mt);
+    const int th = std::max(32, std::min(cap, nsets));
     return (th + 31) / 32 * 32;
 }
 
@@ -890,7 +906,7 @@ struct Gen {
         return e && e[0] == '1';
     }();
 
-    int threads_of() const { return (kernel_threads(ph, f32 ? QSV_C64 : QSV_C128) + 31) / 32 * 32; }
+    int threads_of() const { return (threads_for(ph, f32 ? QSV_C64 : QSV_C128) + 31) / 32 * 32; }
 
     // A whole single-pass kernel: the pass body over this CTA's tiles (a
     // block of a.tpc consecutive tiles, or with a.tpc == 0 a grid-strided
@@ -1468,6 +1484,8 @@ struct Gen {
 };
 
 } // namespace
+
+int kernel_threads(const PassHost &ph, int dtype) { return threads_for(ph, dtype); }
 
 // Shared tile buffers of a prefetching pass: QSV_STAGES (default 2), capped
 // so the ring stays within 160 KiB.

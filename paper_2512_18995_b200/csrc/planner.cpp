@@ -1103,6 +1103,7 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
             const bool ok = A.K == B.K && A.R == B.R && !A.synth && !B.synth && A.out_perm.empty() &&
                             !A.local_gperm && !B.local_gperm &&
                             pass_prefetches(A, cfg.dtype) == pass_prefetches(B, cfg.dtype) &&
+                            kernel_threads(A, cfg.dtype) == kernel_threads(B, cfg.dtype) &&
                             cb <= cfg.super_bits && cb >= A.K + 2 && cb < nl;
             if (!ok) {
                 ++i;

@@ -433,6 +433,8 @@ int tile_kernel_blocks_per_sm(int dtype, int R, int threads, size_t smem);
 // ---- pass specialisation (codegen.cpp, jit.cpp) ----------------------------
 // whether a pass's kernel double-buffers its tiles (jit.cpp)
 bool pass_prefetches(const PassHost &ph, int dtype);
+// threads per CTA of a pass's generated kernel (codegen.cpp)
+int kernel_threads(const PassHost &ph, int dtype);
 void jit_prepare(DevPass &dp, const PassHost &ph, int dtype, int sm_count);
 void launch_jit(const DevPass &dp, void *state, void *out, int rows, cudaStream_t s, double *zout = nullptr);
 // L2 super-pass (PassHost::pair): compiles the pair kernel into head; the

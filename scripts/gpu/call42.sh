@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
+timeout 300 python scripts/cfg2_bench.py 2>&1 | head -1
+export AB_REPS=3
+timeout 900 python scripts/ab.py 30 cfg5f "" "QSV_MAX_THREADS=512" 2>&1 | grep median
+timeout 900 python scripts/ab.py 30 cfg3c64 "" "QSV_MAX_THREADS=512" 2>&1 | grep median
+bash scripts/gpu/call8.sh
