@@ -109,7 +109,7 @@ typedef struct qsv_opts {
     int32_t no_fuse_1q;     /* 1 = keep runs of single-qubit gates unfused */
     int32_t no_phase_flush; /* 1 = apply every diagonal gate eagerly */
     int32_t jit;            /* 1 = specialised (NVRTC) pass kernels, -1 = interpreter, 0 = auto */
-    int32_t reg_slots;      /* qubits per register group R (1..4; 0 = 3 for C128, 4 for C64) */
+    int32_t reg_slots;      /* qubits per register group R (1..4; 0 = 4) */
     int32_t no_relabel;     /* 1 = apply swap gates as data moves (no scratch state needed) */
     int32_t from_zero;      /* 1 = execute starts from |0...0> whatever the state holds
                                (Circuit::forward without init); the leading

@@ -971,17 +971,16 @@ std::vector<PassHost> plan_passes(const std::vector<GateRec> &gates_in, const st
         require(!took.empty(), "planner: no progress");
         size_t first_encs = encs.size();
         if (cfg.R <= 0) {
-            // auto: 4-qubit groups for complex128, 3-qubit groups for
-            // complex64. With the tangent form and per-register scales the
-            // c128 passes are FP64-bound and fewer groups (fewer shared-tile
-            // round trips, longer runs of deferred phases) win; the packed
-            // c64 passes are FMA-bound and a 16-register set costs more in
-            // flushes than it saves. Interleaved A/B at 28q against the
-            // earlier rule (3 when a pass held complex or dense 2-qubit
-            // matrices or more non-diagonal gates than tile qubits, else 4):
-            // cfg4 family 12.17 -> 11.52 ms, cfg5 family 7.72 -> 7.39 ms, QFT
-            // unchanged (it was already 4).
-            R = std::min(cfg.dtype == QSV_C64 ? 3 : 4, K);
+            // auto: 4-qubit register groups. With the tangent form and
+            // per-register scales the c128 passes are FP64-bound and fewer
+            // groups (fewer shared-tile round trips, longer runs of deferred
+            // phases) win (28q A/B against 3 when a pass held complex or
+            // dense 2-qubit matrices: cfg4 family 12.17 -> 11.52 ms). For
+            // complex64, 3-qubit groups won while the passes ran 512-thread
+            // CTAs; with the 256-thread CTAs of compute-bound c64 passes
+            // (codegen.cpp threads_for) 4 wins: cfg5 family 28q 22.8 -> 22.3
+            // ms, 30q 95.3 -> 89.3 ms, 32q 413 -> 395 ms, cfg2 unchanged.
+            R = std::min(4, K);
         }
         PassHost ph = lower_pass(gates, pg, took, active, phys, cfg, K, L, R, encs);
         // keep the program within the shared-memory budget: give the tail of
