@@ -364,6 +364,33 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
         c2["z_max_abs_err_vs_reference"] = float(np.max(np.abs(z[:sub] - z1)))
     aux["cfg2"] = c2
     del st, p
+    # ---- adjoint gradients (adjoint.hpp:52-110) on the cfg1
+    # circuit with every rotation trainable (600 parameters, sum of <Z_i>) ----
+    n_adj = 20
+    acir = W.cfg1_circuit(n_adj, trainable=True)
+    qsv.adjoint_gradients(acir)  # warm-up (plans, kernels)
+    ta = []
+    for _ in range(5):
+        t0 = _t.perf_counter()
+        ag = qsv.adjoint_gradients(acir)
+        ta.append(_t.perf_counter() - t0)
+    nparams_adj = len(ag.param_grads)
+    launches += 6 * (len(acir.gates()) + 4)
+    adj = {"workload": f"adjoint_gradients of the cfg1 circuit at {n_adj} qubits c128 with every rotation trainable "
+                       f"({nparams_adj} parameters, gradient of sum <Z_i>)",
+           "ms_per_gradient": 1e3 * float(np.median(ta)), "protocol": "1 warm-up + 5 repeats, median, host wall clock "
+           "(forward plan, reverse sweep, one gradient read-back)",
+           "note": "one fused kernel per reverse-sweep gate: psi' = U^dag psi, every parameter's Re<lambda|dU psi'>, "
+                   "lambda' = U^dag lambda"}
+    if want_cpu:
+        from oracle import oracle as O
+
+        t0 = _t.perf_counter()
+        want, _ = O.ref_adjoint(n_adj, acir.gates(), [(list(o.wires), o.basis) for o in acir.observables()])
+        adj["cpu_reference"] = {"ms_per_gradient": 1e3 * (_t.perf_counter() - t0), "cores": 1,
+                                "protocol": "1 run of quasar::qubit::adjoint_gradients (oracle/_ref)"}
+        adj["max_abs_err_vs_reference"] = float(np.max(np.abs(np.asarray(ag.param_grads) - want)))
+    aux["adjoint_20q"] = adj
     # ---- cfg4 / cfg5 families at the largest single-GPU sizes ----
     for name, n, cir, dt, desc in (
             ("cfg4_32q", 32, W.cfg4_circuit(32), qsv.C128,

@@ -228,7 +228,7 @@ def ref_adjoint(n, gates, obs, data=()):
     arr, keep = gate_structs(gates)
     oarr, okeep = _obs_array(obs)
     d = np.ascontiguousarray(np.asarray(data, dtype=np.float64))
-    pout = np.zeros(256)
+    pout = np.zeros(max(1, sum(len(g.params) for g in gates)))  # ref_driver.cpp writes every param gradient
     dout = np.zeros(max(1, len(d)))
     npar = C.c_int()
     rc = L.ref_adjoint(n, arr, len(gates), len(obs), oarr, _p(d) if d.size else None, len(d), _p(pout),

@@ -9,7 +9,9 @@
 //   * lambda = sum_obs O psi (adjoint.hpp:30-45, 87);
 //   * reverse sweep (adjoint.hpp:93-108): psi <- U^dagger psi; for each
 //     parameter mu = dU psi with zero_off_control, grad = 2 Re<lambda|mu>;
-//     lambda <- U^dagger lambda.
+//     lambda <- U^dagger lambda. On one GPU each gate is ONE fused kernel
+//     (fused_sweep below); across ranks the steps run as whole-state
+//     operations through one-gate plans.
 // The derivative matrices restate gate_dmatrix (gate.hpp:157-190).
 #include <cmath>
 #include <cstring>
@@ -123,6 +125,148 @@ double re_dot(const DState &a, const DState &b) {
     return re;
 }
 
+// ---- fused single-GPU path ---------------------------------------------
+// One kernel per reverse-sweep gate instead of the reference's sequence of
+// full-state operations (apply U^dagger to psi; per parameter a copy, a
+// zero-off-control dU apply and a dot; apply U^dagger to lambda): each thread
+// owns groups of 2^k amplitudes (k <= 2), loads psi and lambda once, forms
+// psi' = U^dagger psi, accumulates Re sum conj(lambda) (dU_q psi') over the
+// groups whose controls are on (off-control groups contribute 0, as
+// zero_off_control makes them, and keep psi / lambda unchanged), writes
+// psi' and lambda' = U^dagger lambda, and adds its FP64 partial sums to the
+// gradient slots. Same arithmetic as adjoint.hpp:93-108 per group; the
+// gradients are read back once at the end.
+struct AdjGate {
+    int k = 1, t0 = 0, t1 = 0, nq = 0;
+    uint64_t cmask = 0;
+    int slot = -1;    // first gradient slot (params, then data slots)
+    double u[32];     // U^dagger, 2^k x 2^k row-major (re, im)
+    double du[3][32]; // d U / d params[q]
+};
+
+__device__ __forceinline__ uint64_t insert_zero(uint64_t x, int b) {
+    const uint64_t lo = x & ((1ull << b) - 1);
+    return ((x >> b) << (b + 1)) | lo;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *__restrict__ psi,
+                                                       typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
+                                                       const AdjGate g, double *__restrict__ grads) {
+    constexpr int D = 1 << K;
+    double acc[3] = {0.0, 0.0, 0.0};
+    const int lo = K == 2 ? (g.t0 < g.t1 ? g.t0 : g.t1) : g.t0, hi = K == 2 ? (g.t0 < g.t1 ? g.t1 : g.t0) : g.t0;
+    for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < ngroups;
+         gi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t base = insert_zero(gi, lo);
+        if (K == 2) base = insert_zero(base, hi);
+        if ((base & g.cmask) != g.cmask) continue;
+        uint64_t off[D];
+        if (K == 1) off[0] = 0, off[1] = 1ull << g.t0;
+        else
+            for (int r = 0; r < D; ++r) off[r] = ((r >> 1) & 1 ? 1ull << g.t0 : 0ull) | (r & 1 ? 1ull << g.t1 : 0ull);
+        double pr[D], pi[D], lr[D], li[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            const auto a = psi[base | off[r]];
+            const auto b = lam[base | off[r]];
+            pr[r] = a.x, pi[r] = a.y, lr[r] = b.x, li[r] = b.y;
+        }
+        double nr[D], ni[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double ur = g.u[2 * (r * D + c)], ui = g.u[2 * (r * D + c) + 1];
+                xr += ur * pr[c] - ui * pi[c];
+                xi += ur * pi[c] + ui * pr[c];
+            }
+            nr[r] = xr, ni[r] = xi;
+        }
+        for (int q = 0; q < g.nq; ++q) {
+            double s = 0.0;
+#pragma unroll
+            for (int r = 0; r < D; ++r) {
+                double mr = 0.0, mi = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) {
+                    const double dr = g.du[q][2 * (r * D + c)], di = g.du[q][2 * (r * D + c) + 1];
+                    mr += dr * nr[c] - di * ni[c];
+                    mi += dr * ni[c] + di * nr[c];
+                }
+                s += lr[r] * mr + li[r] * mi;  // Re(conj(lambda) mu)
+            }
+            acc[q] += s;
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double xr = 0.0, xi = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double ur = g.u[2 * (r * D + c)], ui = g.u[2 * (r * D + c) + 1];
+                xr += ur * lr[c] - ui * li[c];
+                xi += ur * li[c] + ui * lr[c];
+            }
+            typename Vec2<T>::type a, b;
+            a.x = static_cast<T>(nr[r]), a.y = static_cast<T>(ni[r]);
+            b.x = static_cast<T>(xr), b.y = static_cast<T>(xi);
+            psi[base | off[r]] = a;
+            lam[base | off[r]] = b;
+        }
+    }
+    if (g.nq == 0) return;
+    __shared__ double red[3][8];
+    for (int q = 0; q < g.nq; ++q) {
+        const double v = dev::warp_sum(acc[q]);
+        if ((threadIdx.x & 31) == 0) red[q][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < g.nq) {
+        double s = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
+        atomicAdd(grads + g.slot + threadIdx.x, 2.0 * s);
+    }
+}
+
+// lambda = sum_obs O psi (adjoint.hpp:30-45): each observable's Paulis are
+// applied wire by wire in order, so lambda_i walks them back from i: the row
+// of the last-applied Pauli first. Entries: (bit, letter) runs per
+// observable, `first[o]` .. `first[o + 1]`.
+template <typename T>
+__global__ void pauli_sum_kernel(const typename Vec2<T>::type *__restrict__ psi, typename Vec2<T>::type *__restrict__ lam,
+                                 uint64_t n, int nobs, const int *__restrict__ first, const int *__restrict__ bit,
+                                 const char *__restrict__ letter) {
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        double sr = 0.0, si = 0.0;
+        for (int o = 0; o < nobs; ++o) {
+            uint64_t j = i;
+            double cr = 1.0, ci = 0.0;  // coefficient: (P_m ... P_1 psi)_i = c psi_j
+            for (int e = first[o + 1] - 1; e >= first[o]; --e) {
+                const uint64_t m = 1ull << bit[e];
+                const int r = (j & m) ? 1 : 0;
+                double er, ei;  // P[r][c], c = the one nonzero column of row r
+                if (letter[e] == 'z') {
+                    er = r ? -1.0 : 1.0, ei = 0.0;
+                } else {
+                    j ^= m;
+                    if (letter[e] == 'x') er = 1.0, ei = 0.0;
+                    else er = 0.0, ei = r ? 1.0 : -1.0;  // Y = [[0, -i], [i, 0]]
+                }
+                const double tr = cr * er - ci * ei, ti = cr * ei + ci * er;
+                cr = tr, ci = ti;
+            }
+            const auto a = psi[j];
+            sr += cr * a.x - ci * a.y;
+            si += cr * a.y + ci * a.x;
+        }
+        typename Vec2<T>::type out;
+        out.x = static_cast<T>(sr), out.y = static_cast<T>(si);
+        lam[i] = out;
+    }
+}
+
 GateRec pauli_rec(char c, int wire) {
     GateRec g;
     g.k = 1;
@@ -192,6 +336,104 @@ GateRec with_matrix(const GateRec &base, const cplx *m, int flags) {
     return g;
 }
 
+void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound, const std::vector<GateRec> &recs,
+                 const std::vector<int> &pbase, const std::vector<int> &dbase, int nparams, int nobs,
+                 const qsv_obs *obs, DState &psi, DState &lam, std::vector<double> &pg, std::vector<double> &dg) {
+    cudaStream_t s = ctx->stream;
+    const uint64_t N = psi.st.local_amps;
+    const std::vector<int> &perm = psi.st.perm;  // wire -> physical bit after the forward plan
+    const int blocks_all = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((N + 255) / 256, ctx->sm_count * 8)));
+    // lambda
+    std::vector<int> first(1, 0), bit;
+    std::vector<char> letter;
+    for (int o = 0; o < nobs; ++o) {
+        require(obs[o].nwires >= 0 && (obs[o].nwires == 0 || (obs[o].wires && obs[o].basis)), "observable: bad wires");
+        for (int j = 0; j < obs[o].nwires; ++j) {
+            const char c = obs[o].basis[j];
+            require(c == 'x' || c == 'y' || c == 'z', "observable: basis letter outside {x,y,z}");
+            const int w = obs[o].wires[j];
+            require(w >= 0 && w < n, "observable: wire out of range");
+            bit.push_back(perm[w]);
+            letter.push_back(c);
+        }
+        first.push_back(static_cast<int>(bit.size()));
+    }
+    const size_t tb = sizeof(int) * (first.size() + bit.size()) + letter.size() + 16;
+    char *dtab = nullptr;
+    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&dtab), tb, s));
+    int *d_first = reinterpret_cast<int *>(dtab), *d_bit = d_first + first.size();
+    char *d_letter = reinterpret_cast<char *>(d_bit + bit.size());
+    QSV_CUDA(cudaMemcpyAsync(d_first, first.data(), sizeof(int) * first.size(), cudaMemcpyHostToDevice, s));
+    if (!bit.empty()) {
+        QSV_CUDA(cudaMemcpyAsync(d_bit, bit.data(), sizeof(int) * bit.size(), cudaMemcpyHostToDevice, s));
+        QSV_CUDA(cudaMemcpyAsync(d_letter, letter.data(), letter.size(), cudaMemcpyHostToDevice, s));
+    }
+    if (dtype == QSV_C64)
+        pauli_sum_kernel<float><<<blocks_all, 256, 0, s>>>(static_cast<const float2 *>(psi.st.d),
+                                                           static_cast<float2 *>(lam.st.d), N, nobs, d_first, d_bit,
+                                                           d_letter);
+    else
+        pauli_sum_kernel<double><<<blocks_all, 256, 0, s>>>(static_cast<const double2 *>(psi.st.d),
+                                                            static_cast<double2 *>(lam.st.d), N, nobs, d_first, d_bit,
+                                                            d_letter);
+    QSV_CUDA(cudaGetLastError());
+    // gradient slots: params, then data slots
+    const int nslots = static_cast<int>(dg.size());
+    double *d_grad = nullptr;
+    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_grad), sizeof(double) * std::max(1, nparams + nslots), s));
+    QSV_CUDA(cudaMemsetAsync(d_grad, 0, sizeof(double) * std::max(1, nparams + nslots), s));
+    for (int i = static_cast<int>(recs.size()) - 1; i >= 0; --i) {
+        const GateRec &g = recs[i];
+        require(g.k >= 1 && g.k <= 2, "adjoint_gradients: gates act on 1 or 2 targets");
+        const int d = 1 << g.k;
+        AdjGate a;
+        a.k = g.k;
+        a.t0 = perm[g.wires[0]];
+        a.t1 = g.k == 2 ? perm[g.wires[1]] : 0;
+        a.cmask = 0;
+        for (int c : g.ctls) a.cmask |= 1ull << perm[c];
+        for (int r = 0; r < d; ++r)
+            for (int c = 0; c < d; ++c) {
+                const cplx v = std::conj(g.m[c * d + r]);
+                a.u[2 * (r * d + c)] = v.real();
+                a.u[2 * (r * d + c) + 1] = v.imag();
+            }
+        a.nq = 0;
+        if (pbase[i] >= 0 || dbase[i] >= 0) {
+            a.nq = bound[i].nparams;
+            require(a.nq <= 3, "adjoint_gradients: at most 3 parameters per gate");
+            a.slot = pbase[i] >= 0 ? pbase[i] : nparams + dbase[i];
+            for (int q = 0; q < a.nq; ++q) {
+                cplx dm[16];
+                dmatrix(bound[i], q, dm);
+                for (int e = 0; e < d * d; ++e) a.du[q][2 * e] = dm[e].real(), a.du[q][2 * e + 1] = dm[e].imag();
+            }
+        }
+        const uint64_t groups = N >> g.k;
+        const int blocks = static_cast<int>(
+            std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * 8)));
+        if (dtype == QSV_C64) {
+            auto *P = static_cast<float2 *>(psi.st.d);
+            auto *Lm = static_cast<float2 *>(lam.st.d);
+            if (g.k == 1) adj_gate_kernel<float, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+            else adj_gate_kernel<float, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+        } else {
+            auto *P = static_cast<double2 *>(psi.st.d);
+            auto *Lm = static_cast<double2 *>(lam.st.d);
+            if (g.k == 1) adj_gate_kernel<double, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+            else adj_gate_kernel<double, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+        }
+        QSV_CUDA(cudaGetLastError());
+    }
+    std::vector<double> h(std::max(1, nparams + nslots));
+    QSV_CUDA(cudaMemcpyAsync(h.data(), d_grad, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    QSV_CUDA(cudaFreeAsync(d_grad, s));
+    QSV_CUDA(cudaFreeAsync(dtab, s));
+    QSV_CUDA(cudaStreamSynchronize(s));
+    for (int q = 0; q < nparams; ++q) pg[q] = h[q];
+    for (int q = 0; q < nslots; ++q) dg[q] = h[nparams + q];
+}
+
 } // namespace
 
 void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates, int nobs, const qsv_obs *obs,
@@ -225,7 +467,7 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
         recs.push_back(resolve_gate(bound[i], n, &cur));
     }
     cudaStream_t s = ctx->stream;
-    DState psi(ctx, n, dtype), lam(ctx, n, dtype), mu(ctx, n, dtype);
+    DState psi(ctx, n, dtype), lam(ctx, n, dtype);
     // init (QubitState::basis(n) by default, adjoint.hpp:84)
     if (init) {
         const uint64_t la = psi.st.local_amps;
@@ -246,6 +488,15 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
         build_plan(fw, ctx, n, dtype, recs, 0, nullptr);
         execute_plan(fw, psi.st, nullptr, 0, 0);
     }
+    pg.assign(nparams, 0.0);
+    dg.assign(nslots, 0.0);
+    if (ctx->world == 1) {
+        fused_sweep(ctx, n, dtype, bound, recs, pbase, dbase, nparams, nobs, obs, psi, lam, pg, dg);
+        return;
+    }
+    // multi-rank: the reference's sequence of whole-state operations, every
+    // gate through a one-gate plan (global wires take the swap path)
+    DState mu(ctx, n, dtype);
     // lambda = sum_obs O psi (adjoint.hpp:30-45)
     QSV_CUDA(cudaMemsetAsync(lam.st.d, 0, lam.bytes(), s));
     for (int o = 0; o < nobs; ++o) {
@@ -267,8 +518,6 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
                                                                     static_cast<const double2 *>(mu.st.d), nn);
         QSV_CUDA(cudaGetLastError());
     }
-    pg.assign(nparams, 0.0);
-    dg.assign(nslots, 0.0);
     // reverse sweep (adjoint.hpp:93-108)
     for (int i = ngates - 1; i >= 0; --i) {
         const GateRec &g = recs[i];

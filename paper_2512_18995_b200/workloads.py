@@ -18,9 +18,10 @@ from .qsv import Circuit, Rng, make_gate, rng_fill, kPi
 TWO_PI = 2.0 * kPi
 
 
-def cfg1_circuit(n: int = 20, layers: int = 10) -> Circuit:
+def cfg1_circuit(n: int = 20, layers: int = 10, trainable: bool = False) -> Circuit:
     """20q c128: `layers` x (rx, ry, rz on every qubit; angles U[0,2pi)), then
-    the CNOT ladder cnot(q, q+1). Observables: Z_i for every i."""
+    the CNOT ladder cnot(q, q+1). Observables: Z_i for every i. `trainable`
+    marks every rotation trainable (the adjoint-gradient workload)."""
     rng = Rng(0, "cfg1")
     cir = Circuit(n)
     for _ in range(layers):
@@ -28,9 +29,9 @@ def cfg1_circuit(n: int = 20, layers: int = 10) -> Circuit:
             tx = rng.uniform(0.0, TWO_PI)
             ty = rng.uniform(0.0, TWO_PI)
             tz = rng.uniform(0.0, TWO_PI)
-            cir.rx(q, tx)
-            cir.ry(q, ty)
-            cir.rz(q, tz)
+            cir.rx(q, tx, trainable)
+            cir.ry(q, ty, trainable)
+            cir.rz(q, tz, trainable)
     for q in range(n - 1):
         cir.cnot(q, q + 1)
     for q in range(n):

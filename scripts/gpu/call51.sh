@@ -1,0 +1,4 @@
+python -c "import __graft_entry__ as g; g.build()" > /dev/null
+timeout 600 python -m pytest tests/test_gpu_adjoint.py -q -x -m gpu 2>&1 | tail -1
+timeout 900 python scripts/adjoint_time.py 16 18 20 22
+QSV_ADJ_FWD_JIT=1 timeout 900 python scripts/adjoint_time.py 20 22

@@ -125,6 +125,21 @@ def test_c64_gradients_within_single_precision():
     assert np.max(np.abs(np.array(got.param_grads) - want_p), initial=0) < 1e-4
 
 
+def test_trainable_cfg1_family_matches_reference():
+    """The fused single-GPU reverse sweep (one kernel per gate, adjoint.cu)
+    on 420 parameters, with X / Y observables and a repeated wire (lambda =
+    sum O psi applied wire by wire, adjoint.hpp:30-45)."""
+    from paper_2512_18995_b200 import workloads as W
+
+    cir = W.cfg1_circuit(14, trainable=True)
+    cir.observable([1, 4], "xy")
+    cir.observable([2, 2, 5], "zxy")
+    want_p, _ = ref_grads(cir)
+    got = qsv.adjoint_gradients(cir)
+    assert len(got.param_grads) == 420
+    assert np.max(np.abs(np.array(got.param_grads) - want_p)) < 1e-11
+
+
 def test_errors_mirror_reference():
     cir = Circuit(2)
     cir.ry(0, 0.0, False, True)
