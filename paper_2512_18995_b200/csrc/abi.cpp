@@ -191,6 +191,7 @@ void run_single(State &st, const GateRec &g) {
         dist_exchange_apply(st, st.perm[g.wires[0]], g.m, lc, on, (g.flags & OPF_ZERO_OFF_CONTROL) != 0);
         return;
     }
+    if (apply_direct(st, g)) return;
     Plan p;
     build_plan(p, st.ctx, st.n, st.dtype, {g}, 0, nullptr);
     execute_plan(p, st, nullptr, 0, 0);

@@ -367,6 +367,101 @@ void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaS
     QSV_CUDA(cudaGetLastError());
 }
 
+namespace {
+// One gate, one launch (qsv_apply_gate / qsv_apply_matrix on one GPU): the
+// reference's apply_matrix_strided (state.hpp:111-143) as a single sweep --
+// each thread owns groups of 2^k amplitudes whose target bits are 0, applies
+// the 2^k x 2^k matrix where every control bit is 1, and with
+// zero_off_control zeroes the groups where one is 0. No plan, no program
+// upload, no host synchronisation: a loop of apply_gate calls (the
+// reference's usage) runs at one sweep per gate.
+struct DirectGate {
+    int t0 = 0, t1 = 0, zoc = 0;
+    uint64_t cmask = 0;
+    double m[32];  // 2^k x 2^k row-major (re, im); wires[0] is the matrix MSB
+};
+
+__device__ __forceinline__ uint64_t ins0(uint64_t x, int b) {
+    return ((x >> b) << (b + 1)) | (x & ((1ull << b) - 1));
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(256) direct_gate_kernel(typename Vec2<T>::type *__restrict__ st, uint64_t local_amps,
+                                                          int log_groups, uint64_t total, const DirectGate g) {
+    constexpr int D = 1 << K;
+    const int lo = K == 2 ? min(g.t0, g.t1) : g.t0, hi = K == 2 ? max(g.t0, g.t1) : g.t0;
+    for (uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; w < total;
+         w += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t row = w >> log_groups, gi = w & ((1ull << log_groups) - 1);
+        uint64_t base = ins0(gi, lo);
+        if (K == 2) base = ins0(base, hi);
+        typename Vec2<T>::type *v = st + row * local_amps;
+        uint64_t off[D];
+        if (K == 1) off[0] = 0, off[1] = 1ull << g.t0;
+        else
+            for (int r = 0; r < D; ++r) off[r] = ((r >> 1) & 1 ? 1ull << g.t0 : 0ull) | (r & 1 ? 1ull << g.t1 : 0ull);
+        if ((base & g.cmask) != g.cmask) {
+            if (g.zoc) {
+                typename Vec2<T>::type z;
+                z.x = 0, z.y = 0;
+#pragma unroll
+                for (int r = 0; r < D; ++r) v[base | off[r]] = z;
+            }
+            continue;
+        }
+        double xr[D], xi[D];
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            const auto a = v[base | off[r]];
+            xr[r] = a.x, xi[r] = a.y;
+        }
+#pragma unroll
+        for (int r = 0; r < D; ++r) {
+            double yr = 0.0, yi = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double mr = g.m[2 * (r * D + c)], mi = g.m[2 * (r * D + c) + 1];
+                yr += mr * xr[c] - mi * xi[c];
+                yi += mr * xi[c] + mi * xr[c];
+            }
+            typename Vec2<T>::type o;
+            o.x = static_cast<T>(yr), o.y = static_cast<T>(yi);
+            v[base | off[r]] = o;
+        }
+    }
+}
+} // namespace
+
+bool apply_direct(State &st, const GateRec &g) {
+    static const bool off = [] {  // QSV_X_NODIRECT=1: one-gate plans instead
+        const char *e = std::getenv("QSV_X_NODIRECT");
+        return e && e[0] == '1';
+    }();
+    if (off || st.ctx->world != 1 || g.encoded || g.k < 1 || g.k > 2) return false;
+    DirectGate a;
+    a.t0 = st.perm[g.wires[0]];
+    a.t1 = g.k == 2 ? st.perm[g.wires[1]] : 0;
+    for (int c : g.ctls) a.cmask |= 1ull << st.perm[c];
+    a.zoc = (g.flags & OPF_ZERO_OFF_CONTROL) ? 1 : 0;
+    const int d = 1 << g.k;
+    for (int i = 0; i < d * d; ++i) a.m[2 * i] = g.m[i].real(), a.m[2 * i + 1] = g.m[i].imag();
+    const int log_groups = st.nlocal - g.k;
+    const uint64_t total = static_cast<uint64_t>(st.batch) << log_groups;
+    const int grid = grid_for(total, 256, st.ctx->sm_count);
+    cudaStream_t s = st.ctx->stream;
+    if (st.dtype == QSV_C64) {
+        auto *v = static_cast<float2 *>(st.d);
+        if (g.k == 1) direct_gate_kernel<float, 1><<<grid, 256, 0, s>>>(v, st.local_amps, log_groups, total, a);
+        else direct_gate_kernel<float, 2><<<grid, 256, 0, s>>>(v, st.local_amps, log_groups, total, a);
+    } else {
+        auto *v = static_cast<double2 *>(st.d);
+        if (g.k == 1) direct_gate_kernel<double, 1><<<grid, 256, 0, s>>>(v, st.local_amps, log_groups, total, a);
+        else direct_gate_kernel<double, 2><<<grid, 256, 0, s>>>(v, st.local_amps, log_groups, total, a);
+    }
+    QSV_CUDA(cudaGetLastError());
+    return true;
+}
+
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank) {
     const uint64_t total = st.local_amps * st.batch;
     const int g = grid_for(total, 256, st.ctx->sm_count);
