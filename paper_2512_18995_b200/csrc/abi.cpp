@@ -7,7 +7,10 @@
 #include <bit>
 #include <cmath>
 #include <cstring>
+#include <list>
 #include <memory>
+#include <mutex>
+#include <string>
 #include <thread>
 
 #include "qsv_internal.hpp"
@@ -16,11 +19,21 @@
 // qsv_ctx_create_multi, a GROUP: one object per rank (`parts`, rank order),
 // every call on it run by one host thread per rank (the reference's
 // dist::run_on_ranks, tests/test_dist.cpp:66-94) with NCCL hidden inside.
+// Plans of recent qsv_run_circuit calls (Circuit::forward through the ABI):
+// a training loop calls forward with the same gates and new data every
+// step; planning and kernel specialisation are done once per distinct
+// (gates, n, dtype, opts) and the plan is re-executed.
+struct PlanCache {
+    static constexpr size_t kCap = 8;
+    std::mutex mu;
+    std::list<std::pair<std::string, std::unique_ptr<qsv::Plan>>> lru;  // most recent first
+};
 struct qsv_ctx : qsv::Ctx {
     std::vector<qsv_ctx *> parts;
     // independent single-GPU contexts on the same devices (row sharding of
     // batched circuits: no communicator, made on first use)
     std::vector<qsv_ctx *> solo;
+    std::unique_ptr<PlanCache> plans = std::make_unique<PlanCache>();
     ~qsv_ctx();
 };
 struct qsv_state : qsv::State {
@@ -37,6 +50,10 @@ struct qsv_plan : qsv::Plan {
 };
 
 qsv_ctx::~qsv_ctx() {
+    if (parts.empty() && plans && !plans->lru.empty()) {
+        cudaSetDevice(device);
+        plans.reset();  // cached plans free their device buffers while the context lives
+    }
     for (qsv_ctx *x : solo) delete x;
     // NCCL teardown may synchronise with the peers: every rank in its own thread
     std::vector<std::thread> th;
@@ -698,9 +715,55 @@ int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const doub
                      [&](int r) { return qsv_run_circuit(st->parts[r], gates, ngates, data, rows, slots, opts); });
             return;
         }
-        Plan p;
-        build_plan_from_abi(p, st->ctx, st->n, st->dtype, gates, ngates, opts);
-        execute_plan(p, *st, data, rows, slots);
+        qsv_ctx *c = static_cast<qsv_ctx *>(st->ctx);
+        static const bool nocache = [] {  // QSV_NO_PLAN_CACHE=1: plan every call
+            const char *e = std::getenv("QSV_NO_PLAN_CACHE");
+            return e && e[0] == '1';
+        }();
+        if (nocache || c->world != 1 || ngates > 4096) {
+            Plan p;
+            build_plan_from_abi(p, st->ctx, st->n, st->dtype, gates, ngates, opts);
+            execute_plan(p, *st, data, rows, slots);
+            QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
+            return;
+        }
+        // key: everything build_plan reads -- n, dtype, the options and every
+        // gate field except the encoded parameters' values (bound per row at
+        // execute) and `trainable`; custom matrices by value
+        std::string key;
+        auto put = [&](const void *p, size_t b) { key.append(static_cast<const char *>(p), b); };
+        put(&st->n, sizeof(int));
+        put(&st->dtype, sizeof(int));
+        const int has_opts = opts != nullptr;
+        put(&has_opts, sizeof(int));
+        if (opts) put(opts, sizeof(qsv_opts));
+        require(ngates >= 0 && (ngates == 0 || gates != nullptr), "plan: bad gate list");
+        for (int i = 0; i < ngates; ++i) {
+            const qsv_gate &g = gates[i];
+            put(g.name, sizeof(g.name));
+            put(&g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
+                               sizeof(g.nparams));
+            put(&g.encode, sizeof(g.encode));
+            if (!g.encode) put(g.params, sizeof(g.params));
+            if (g.custom) {
+                const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
+                put(g.custom, sizeof(double) * 2 * (1u << (2 * k)));
+            }
+        }
+        std::lock_guard<std::mutex> lk(c->plans->mu);
+        auto &lru = c->plans->lru;
+        auto it = std::find_if(lru.begin(), lru.end(), [&](const auto &e) { return e.first == key; });
+        if (it == lru.end()) {
+            auto np = std::make_unique<Plan>();
+            build_plan_from_abi(*np, st->ctx, st->n, st->dtype, gates, ngates, opts);
+            lru.emplace_front(std::move(key), std::move(np));
+            if (lru.size() > PlanCache::kCap) lru.pop_back();
+            it = lru.begin();
+        } else if (it != lru.begin()) {
+            lru.splice(lru.begin(), lru, it);
+            it = lru.begin();
+        }
+        execute_plan(*it->second, *st, data, rows, slots);
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
     });
 }
