@@ -410,8 +410,14 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
             }
         }
         const uint64_t groups = N >> g.k;
+        // gradient gates: fewer, fuller blocks (one atomic per block and
+        // parameter lands on the same slot); QSV_ADJ_BLOCKS_PER_SM overrides
+        static const int bps = [] {
+            const char *e = std::getenv("QSV_ADJ_BLOCKS_PER_SM");
+            return e ? std::max(1, std::atoi(e)) : 2;
+        }();
         const int blocks = static_cast<int>(
-            std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * 8)));
+            std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * (a.nq ? bps : 8))));
         if (dtype == QSV_C64) {
             auto *P = static_cast<float2 *>(psi.st.d);
             auto *Lm = static_cast<float2 *>(lam.st.d);
