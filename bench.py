@@ -391,6 +391,76 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
                                 "protocol": "1 run of quasar::qubit::adjoint_gradients (oracle/_ref)"}
         adj["max_abs_err_vs_reference"] = float(np.max(np.abs(np.asarray(ag.param_grads) - want)))
     aux["adjoint_20q"] = adj
+    # ---- seeded measurement (circuit.hpp:217-244): marginals
+    # over 20 wires of a 24-qubit state on the device, 10^6 shots sampled on
+    # the host with the reference's Rng stream; the histogram must equal the
+    # reference's own ----
+    n_m, wires_m, shots_m = 24, list(range(20)), 1_000_000
+    amps_m = W.cfg3_slice(0, 1 << n_m)
+    amps_m /= np.sqrt(float(np.vdot(amps_m, amps_m).real))
+    sm = qsv.QubitState.from_amplitudes(n_m, amps_m)
+    qsv.measure_counts(sm, shots_m, wires_m, qsv.Rng(5, "bench-measure"))  # warm-up
+    tm = []
+    for _ in range(3):
+        t0 = _t.perf_counter()
+        got_m, _ = qsv.measure_counts(sm, shots_m, wires_m, qsv.Rng(5, "bench-measure"))
+        tm.append(_t.perf_counter() - t0)
+    launches += 4 * 2
+    meas = {"workload": f"measure: {shots_m} shots over wires 0..19 of a 24-qubit c128 state (seeded Gaussian), "
+                        "histogram as an array (qsv_measure)",
+            "ms_per_call": 1e3 * float(np.median(tm)), "protocol": "1 warm-up + 3 repeats, median, host wall clock"}
+    if want_cpu:
+        from oracle import oracle as O
+
+        t0 = _t.perf_counter()
+        want_m = O.ref_measure(n_m, amps_m, shots_m, wires_m, 5, "bench-measure")
+        meas["cpu_reference"] = {"ms_per_call": 1e3 * (_t.perf_counter() - t0), "cores": 1,
+                                 "protocol": "1 run of quasar::qubit::measure (oracle/_ref)"}
+        meas["histogram_identical_to_reference"] = bool(np.array_equal(got_m, want_m))
+    aux["measure_24q"] = meas
+    del sm
+    # ---- density matrices and channels (state.hpp:159-172,
+    # channel.hpp:73-100): 10 qubits (rho 1024 x 1024 as a 20-qubit vector),
+    # 4 layers of ry on every wire, a depolarizing channel on every wire and a
+    # CNOT ladder; value semantics like the reference (every op returns a new
+    # state) ----
+    n_d = 10
+    rng_d = qsv.Rng(0, "bench-density")
+    ops_d = []
+    for _ in range(4):
+        for q in range(n_d):
+            ops_d.append(qsv.make_gate("ry", [q], [], [rng_d.uniform(0.0, 6.283185307179586)]))
+            ops_d.append(("depolarizing", q, 0.01))
+        for q in range(n_d - 1):
+            ops_d.append(qsv.make_gate("x", [q + 1], [q]))
+
+    def run_density():
+        sd = qsv.QubitState.basis(n_d)
+        for op in ops_d:
+            sd = qsv.apply_channel(sd, qsv.depolarizing(op[1], op[2])) if isinstance(op, tuple) else \
+                qsv.apply_gate(sd, op)
+        return sd
+
+    run_density()
+    td = []
+    for _ in range(3):
+        t0 = _t.perf_counter()
+        sd = run_density()
+        sd.ctx.sync()
+        td.append(_t.perf_counter() - t0)
+    launches += 4 * 3 * len(ops_d)
+    dens = {"workload": f"density matrix, {n_d} qubits c128: {len(ops_d)} ops (ry + depolarizing on every wire, "
+                        "CNOT ladder) x 4 layers from |0><0|",
+            "ms_per_run": 1e3 * float(np.median(td)), "protocol": "1 warm-up + 3 repeats, median, host wall clock"}
+    if want_cpu:
+        from oracle import oracle as O
+
+        t0 = _t.perf_counter()
+        want_d = O.ref_mixed_run(n_d, ops_d)
+        dens["cpu_reference"] = {"ms_per_run": 1e3 * (_t.perf_counter() - t0), "cores": 1,
+                                 "protocol": "1 run of to_mixed + apply_gate / apply_channel (oracle/_ref)"}
+        dens["max_abs_err_vs_reference"] = float(np.max(np.abs(sd.density() - want_d)))
+    aux["density_10q"] = dens
     # ---- cfg4 / cfg5 families at the largest single-GPU sizes ----
     for name, n, cir, dt, desc in (
             ("cfg4_32q", 32, W.cfg4_circuit(32), qsv.C128,

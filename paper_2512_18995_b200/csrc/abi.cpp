@@ -464,7 +464,7 @@ int qsv_state_create(qsv_ctx *ctx, int nqubit, int batch, int dtype, qsv_state *
         for (int w = 0; w < nqubit; ++w) st->perm[w] = nqubit - 1 - w;
         QSV_CUDA(cudaSetDevice(ctx->device));
         const size_t bytes = st->local_amps * st->amp_bytes() * static_cast<size_t>(batch);
-        const cudaError_t e = cudaMalloc(&st->d, bytes);
+        const cudaError_t e = state_alloc(&st->d, bytes);
         if (e != cudaSuccess) {
             cudaGetLastError();
             fail(QSV_ERR_INTERNAL, "QubitState: cannot allocate " + std::to_string(bytes) + " bytes of HBM");
@@ -602,7 +602,7 @@ int qsv_state_clone(const qsv_state *src, qsv_state **out) {
         st->local_amps = src->local_amps;
         st->perm = src->perm;
         const size_t bytes = st->local_amps * st->amp_bytes() * static_cast<size_t>(st->batch);
-        QSV_CUDA(cudaMalloc(&st->d, bytes));
+        QSV_CUDA(state_alloc(&st->d, bytes));
         QSV_CUDA(cudaMemcpyAsync(st->d, src->d, bytes, cudaMemcpyDeviceToDevice, src->ctx->stream));
         QSV_CUDA(cudaStreamSynchronize(src->ctx->stream));
         *out = st.release();

@@ -537,6 +537,72 @@ struct DevBuf {
 };
 } // namespace
 
+namespace {
+// State buffers up to 256 MiB are recycled per device (512 MiB cached at
+// most): the reference's value semantics make every apply_gate /
+// apply_channel return a new state, and a cudaMalloc + cudaFree pair
+// synchronises the device and costs far more than a small state's sweep.
+// A buffer is cached once its stream has drained.
+constexpr size_t kStateCacheBlock = size_t(256) << 20, kStateCacheTotal = size_t(512) << 20;
+struct StateCache {
+    std::mutex mu;
+    std::multimap<size_t, std::pair<int, void *>> blocks;  // bytes -> (device, ptr)
+    size_t total = 0;
+};
+StateCache &state_cache() {
+    static StateCache *c = new StateCache();  // intentionally leaked: outlives static destruction
+    return *c;
+}
+} // namespace
+
+cudaError_t state_alloc(void **p, size_t bytes) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (bytes <= kStateCacheBlock) {
+        StateCache &c = state_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto range = c.blocks.equal_range(bytes);
+        for (auto it = range.first; it != range.second; ++it)
+            if (it->second.first == dev) {
+                *p = it->second.second;
+                c.total -= bytes;
+                c.blocks.erase(it);
+                return cudaSuccess;
+            }
+    }
+    return cudaMalloc(p, bytes);
+}
+
+void state_release(void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes <= kStateCacheBlock) {
+        // the buffer's own device (a state may be destroyed on any thread,
+        // after its context); cached once that device has drained -- what
+        // cudaFree would have waited for anyway
+        cudaPointerAttributes at{};
+        int cur = 0;
+        if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeDevice &&
+            cudaGetDevice(&cur) == cudaSuccess) {
+            const bool other = at.device != cur;
+            bool ok = !other || cudaSetDevice(at.device) == cudaSuccess;
+            ok = ok && cudaDeviceSynchronize() == cudaSuccess;
+            if (other) cudaSetDevice(cur);
+            if (ok) {
+                StateCache &c = state_cache();
+                std::lock_guard<std::mutex> lk(c.mu);
+                if (c.total + bytes <= kStateCacheTotal) {
+                    c.blocks.emplace(bytes, std::make_pair(at.device, p));
+                    c.total += bytes;
+                    return;
+                }
+            }
+        }
+        cudaGetLastError();
+    }
+    cudaFree(p);
+}
+
 void reduce_z_all(State &st, double *host_out) {
     const int rows = st.batch;
     const int CL = st.nlocal >= 4 ? 4 : 0;

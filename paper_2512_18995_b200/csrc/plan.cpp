@@ -28,8 +28,10 @@ Ctx::~Ctx() {
 
 State::~State() {
     if (p2p_opened.size() || d_peers || d_barrier) dist_p2p_release(*this);
-    if (d) cudaFree(d);
-    if (scratch) cudaFree(scratch);
+    const size_t bytes = local_amps * amp_bytes() * static_cast<size_t>(batch);
+    // buffers once exported to peers (IPC) are freed, never recycled
+    if (d) state_release(d, p2p ? SIZE_MAX : bytes);
+    if (scratch) state_release(scratch, p2p ? SIZE_MAX : bytes);
 }
 
 bool plan_uses_jit(const Plan &p);
@@ -637,7 +639,7 @@ namespace {
 void ensure_scratch(State &st) {
     if (!st.scratch) {
         const size_t bytes = st.local_amps * st.amp_bytes() * static_cast<size_t>(st.batch);
-        if (cudaMalloc(&st.scratch, bytes) != cudaSuccess) {
+        if (state_alloc(&st.scratch, bytes) != cudaSuccess) {
             cudaGetLastError();
             st.scratch = nullptr;
             fail(QSV_ERR_INTERNAL, "out-of-place pass: cannot allocate the scratch state (" + std::to_string(bytes) +

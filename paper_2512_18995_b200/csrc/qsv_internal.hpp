@@ -428,6 +428,9 @@ void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaS
 // per-row, per-bit product-state vectors of a from-|0> plan into p.d_prefix
 void launch_prefix(const Plan &p, int rows, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
+// state buffers: recycled per device up to 256 MiB each (engine.cu)
+cudaError_t state_alloc(void **p, size_t bytes);
+void state_release(void *p, size_t bytes);
 // one gate as one sweep kernel (single GPU, k <= 2, not encoded); false = not eligible
 bool apply_direct(State &st, const GateRec &g);
 void launch_convert(void *dst, int dst_dtype, const void *src, int src_dtype, uint64_t count, cudaStream_t s);

@@ -124,13 +124,31 @@ void sample_counts(const double *probs, int k, int shots, uint64_t seed, const c
         cdf[i] = acc;
     }
     std::fill(counts, counts + np, 0ull);
-    uint64_t c = counter ? *counter : 0;
-    for (int s = 0; s < shots; ++s) {
-        const double u = to_unit(mix(key + kPhi * ++c)) * acc;
-        const size_t idx = std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin();
-        counts[std::min(idx, np - 1)] += 1;
+    const uint64_t c0 = counter ? *counter : 0;
+    // shot s draws the stream's (c0 + s + 1)-th value (counter-based), so
+    // shot ranges are independent: large batches fan out over host threads
+    // and the histogram is the same as the sequential loop's
+    auto run = [&](int s0, int s1, bool atomic) {
+        for (int s = s0; s < s1; ++s) {
+            const double u = to_unit(mix(key + kPhi * (c0 + static_cast<uint64_t>(s) + 1))) * acc;
+            const size_t idx = std::min<size_t>(std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin(), np - 1);
+            if (atomic) __atomic_fetch_add(&counts[idx], 1ull, __ATOMIC_RELAXED);
+            else counts[idx] += 1;
+        }
+    };
+    const int hw = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int nt = shots >= (1 << 16) ? std::min(hw, 16) : 1;
+    if (nt == 1) run(0, shots, false);
+    else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+            th.emplace_back([&, t] {
+                run(static_cast<int>(static_cast<int64_t>(shots) * t / nt),
+                    static_cast<int>(static_cast<int64_t>(shots) * (t + 1) / nt), true);
+            });
+        for (auto &x : th) x.join();
     }
-    if (counter) *counter = c;
+    if (counter) *counter = c0 + static_cast<uint64_t>(shots);
 }
 
 } // namespace qsv

@@ -969,22 +969,32 @@ def bits_to_string(outcome: int, k: int) -> str:
     return "".join("1" if (outcome >> (k - 1 - i)) & 1 else "0" for i in range(k))
 
 
+def measure_counts(state: QubitState, shots: int, wires, rng: "Rng", batch_index: int = 0):
+    """qsv_measure as arrays: (counts[2^k] uint64, probs[2^k]) -- the
+    marginals on the device, the reference's seeded sampling in the library
+    (identical histograms), continuing this Rng's stream. Pure states,
+    1 <= k <= 26 wires."""
+    if shots < 1:
+        raise InvalidInput("measure: shots must be >= 1")
+    k = len(wires)
+    w = (C.c_int32 * max(1, k))(*wires)
+    counts = np.zeros(1 << k, dtype=np.uint64)
+    probs = np.zeros(1 << k)
+    ctr = C.c_uint64(rng.counter)
+    check(lib().qsv_measure(state.h, batch_index, k, w, int(shots), C.c_uint64(rng.seed0),
+                            None if rng.label is None else rng.label.encode(), C.byref(ctr), _ptr(counts),
+                            _ptr(probs)))
+    rng.counter = ctr.value
+    return counts, probs
+
+
 def measure(state: QubitState, shots: int, wires, rng: "Rng", with_prob: bool = False, batch_index: int = 0):
     """circuit.hpp:217-244: CDF sampling over the device-computed marginals."""
     if shots < 1:
         raise InvalidInput("measure: shots must be >= 1")
     k = len(wires)
     if not state.is_mixed() and 1 <= k <= 26:
-        # qsv_measure: the marginals on the device, the seeded sampling in the
-        # library, continuing this Rng's stream
-        w = (C.c_int32 * k)(*wires)
-        counts = np.zeros(1 << k, dtype=np.uint64)
-        probs = np.zeros(1 << k)
-        ctr = C.c_uint64(rng.counter)
-        check(lib().qsv_measure(state.h, batch_index, k, w, int(shots), C.c_uint64(rng.seed0),
-                                None if rng.label is None else rng.label.encode(), C.byref(ctr), _ptr(counts),
-                                _ptr(probs)))
-        rng.counter = ctr.value
+        counts, probs = measure_counts(state, shots, wires, rng, batch_index)
         out: dict = {}
         for i in np.nonzero(counts)[0]:
             out[bits_to_string(int(i), k)] = {"count": int(counts[i]), "probability": 0.0}

@@ -179,6 +179,24 @@ def test_measure_matches_seeded_reference_histogram():  # test_dist.cpp:207-222 
     assert abs(counts["00"]["count"] - 50000) < 5 * math.sqrt(0.25 * 100000)
 
 
+def test_measure_counts_many_shots_match_reference():
+    """10^5 shots (the library samples them on several host threads, each
+    shot its own counter of the stream): the histogram equals the
+    reference's, and the Rng continues after the last shot."""
+    rng = Rng(21, "many-shots")
+    n = 16
+    psi = random_state(rng, n)
+    s = QubitState.from_amplitudes(n, psi)
+    wires = [0, 3, 5, 7, 9, 11, 13, 15, 2, 4, 6, 8]
+    r = Rng(9, "hist-many")
+    counts, probs = qsv.measure_counts(s, 100000, wires, r)
+    assert r.counter == 100000 and int(counts.sum()) == 100000
+    assert np.max(np.abs(probs - O.port_marginal(n, psi, wires))) < 1e-12
+    if O.REF_LIB.exists():
+        want = O.ref_measure(n, psi, 100000, wires, 9, "hist-many")
+        assert np.array_equal(counts, want)
+
+
 # ----------------------------------------------- random / fused paths ----
 @pytest.mark.parametrize("dtype", [C128, C64])
 @pytest.mark.parametrize("jit", [-1, 1])
