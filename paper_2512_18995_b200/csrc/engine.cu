@@ -571,7 +571,22 @@ cudaError_t state_alloc(void **p, size_t bytes) {
                 return cudaSuccess;
             }
     }
-    return cudaMalloc(p, bytes);
+    e = cudaMalloc(p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        // give the cached buffers of this device back and retry once
+        cudaGetLastError();
+        StateCache &c = state_cache();
+        std::lock_guard<std::mutex> lk(c.mu);
+        for (auto it = c.blocks.begin(); it != c.blocks.end();) {
+            if (it->second.first == dev) {
+                cudaFree(it->second.second);
+                c.total -= it->first;
+                it = c.blocks.erase(it);
+            } else ++it;
+        }
+        e = cudaMalloc(p, bytes);
+    }
+    return e;
 }
 
 void state_release(void *p, size_t bytes) {
