@@ -127,6 +127,13 @@ typedef struct qsv_opts {
                                multi-qubit gates (deep local circuits, where it is
                                measured 2.7-5.4x faster); the BASELINE configs stay on
                                the FFMA passes */
+    int32_t lazy_layout;    /* one GPU: swap gates stay qubit relabelings past the end of
+                               the execute -- the state keeps its permuted physical
+                               layout (its wire -> bit map travels with it) instead of
+                               paying a layout-restoring pass; the next execute plans
+                               from that layout, and anything that reads amplitudes in
+                               logical order (downloads, device_ptr, density calls)
+                               restores it first (one permutation pass). 0 = off */
 } qsv_opts;
 
 /* What a plan does, for measurement (bench.py roofline). */

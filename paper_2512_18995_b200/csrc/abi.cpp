@@ -186,6 +186,17 @@ void download_f64(State &st, const void *src, double *host, uint64_t count) {
     }
 }
 
+// Lazy layouts: a whole-state overwrite makes any layout canonical; a
+// one-row upload into a batch first restores the other rows' layout.
+void reset_layout(State &st) {
+    for (int w = 0; w < st.n; ++w) st.perm[w] = st.n - 1 - w;
+}
+void upload_layout(State &st) {
+    if (st.ctx->world != 1 || layout_canonical(st)) return;
+    if (st.batch == 1) reset_layout(st);
+    else normalize_layout(st);
+}
+
 void *row_ptr(State &st, int row) {
     require(row >= 0 && row < st.batch, "batch index out of range");
     return static_cast<unsigned char *>(st.d) + static_cast<size_t>(row) * st.local_amps * st.amp_bytes();
@@ -499,6 +510,7 @@ int qsv_state_set_basis(qsv_state *st, uint64_t index) {
             return;
         }
         const uint64_t owner = index >> st->nlocal;
+        if (st->ctx->world == 1) reset_layout(*st);  // every row is overwritten
         launch_set_basis(*st, index & (st->local_amps - 1), owner == static_cast<uint64_t>(st->ctx->rank));
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
     });
@@ -512,6 +524,7 @@ int qsv_state_upload(qsv_state *st, int row, const double *host, uint64_t count)
                 return qsv_state_upload(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        upload_layout(*st);
         upload_f64(*st, row_ptr(*st, row), host, count);
     });
 }
@@ -524,6 +537,7 @@ int qsv_state_download(qsv_state *st, int row, double *host, uint64_t count) {
                 return qsv_state_download(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        normalize_layout(*st);  // lazy layouts: amplitudes leave in logical order
         download_f64(*st, row_ptr(*st, row), host, count);
     });
 }
@@ -536,6 +550,7 @@ int qsv_state_upload_raw(qsv_state *st, int row, const void *host, uint64_t coun
                 return qsv_state_upload_raw(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        upload_layout(*st);
         QSV_CUDA(cudaMemcpyAsync(row_ptr(*st, row), host, count * st->amp_bytes(), cudaMemcpyHostToDevice,
                                  st->ctx->stream));
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));  // the caller may reuse `host` on return
@@ -550,6 +565,7 @@ int qsv_state_upload_raw_async(qsv_state *st, int row, const void *host, uint64_
                 return qsv_state_upload_raw_async(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        upload_layout(*st);
         QSV_CUDA(cudaMemcpyAsync(row_ptr(*st, row), host, count * st->amp_bytes(), cudaMemcpyHostToDevice,
                                  st->ctx->stream));
     });
@@ -563,6 +579,7 @@ int qsv_state_download_raw_async(qsv_state *st, int row, void *host, uint64_t co
                 return qsv_state_download_raw_async(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        normalize_layout(*st);  // lazy layouts: amplitudes leave in logical order
         QSV_CUDA(cudaMemcpyAsync(host, row_ptr(*st, row), count * st->amp_bytes(), cudaMemcpyDeviceToHost,
                                  st->ctx->stream));
     });
@@ -576,6 +593,7 @@ int qsv_state_download_raw(qsv_state *st, int row, void *host, uint64_t count) {
                 return qsv_state_download_raw(x, row, h, c);
             });
         require(count == st->local_amps, "QubitState: amplitude length mismatch");
+        normalize_layout(*st);  // lazy layouts: amplitudes leave in logical order
         QSV_CUDA(cudaMemcpyAsync(host, row_ptr(*st, row), count * st->amp_bytes(), cudaMemcpyDeviceToHost,
                                  st->ctx->stream));
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
@@ -613,6 +631,7 @@ int qsv_state_device_ptr(qsv_state *st, int row, void **ptr) {
     return guard([&] {
         require(st && ptr, "null argument");
         require(!is_group(st), "device_ptr: a multi-device state has one pointer per rank (use the rank contexts)");
+        normalize_layout(*st);  // the pointer's amplitudes are in logical order
         *ptr = row_ptr(*st, row);
     });
 }
@@ -1048,8 +1067,9 @@ int qsv_measure(qsv_state *st, int row, int k, const int32_t *wires, int shots, 
 }
 
 namespace {
-void require_canonical_density(const qsv_state *st) {
+void require_canonical_density(qsv_state *st) {
     require(!is_group(st), "density: mixed states run on one GPU");
+    normalize_layout(*st);
     require(st->n % 2 == 0 && st->n >= 2, "density: a mixed state of m qubits is held on 2m engine qubits");
     require(st->nlocal == st->n, "density: mixed states run on one GPU");
     for (int w = 0; w < st->n; ++w)

@@ -449,7 +449,20 @@ void extract_prefix(Plan &p) {
 }
 } // namespace
 
+namespace {
+void build_plan_at(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts,
+                   const std::vector<int> *layout);
+}
+
 void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts) {
+    build_plan_at(pl, ctx, n, dtype, std::move(gates), nslots, opts, nullptr);
+}
+
+namespace {
+// `layout` (lazy layouts, one GPU): the wire -> physical bit map of the
+// states this plan runs on; nullptr = canonical.
+void build_plan_at(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates, int nslots, const qsv_opts *opts,
+                   const std::vector<int> *layout) {
     require(n >= 1 && n <= kMaxQubits, "plan: nqubit out of range");
     require(dtype == QSV_C64 || dtype == QSV_C128, "plan: bad dtype");
     Plan *p = &pl;
@@ -478,7 +491,14 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
     cfg.R = p->opts.reg_slots > 0 ? std::min(p->opts.reg_slots, kMaxSlots) : 0; // 0: per pass (planner.cpp)
     require(cfg.K - cfg.L >= 2 || cfg.K == p->nlocal, "plan: tile too small (need tile_bits - low_bits >= 2)");
     p->perm_in = canonical_perm(n);
-    if (p->opts.dense_blocks == 0 && dtype == QSV_C64 && ctx->world == 1 && p->nslots == 0 && p->nlocal >= kDenseTile &&
+    const bool lazy = p->opts.lazy_layout != 0 && ctx->world == 1 && !p->opts.from_zero;
+    if (layout) {
+        require(ctx->world == 1 && static_cast<int>(layout->size()) == n, "plan: layouts are single-GPU");
+        p->perm_in = *layout;
+    }
+    const bool canon_in = p->perm_in == canonical_perm(n);
+    if (lazy && canon_in) p->src_gates = p->gates;  // the base plan: variants are re-planned from these
+    if (canon_in && p->opts.dense_blocks == 0 && dtype == QSV_C64 && ctx->world == 1 && p->nslots == 0 && p->nlocal >= kDenseTile &&
         cfg.fuse && p->opts.jit >= 0 && !p->gates.empty()) {
         // auto: tensor-core blocks when the fused 5-qubit blocks are deep in
         // genuinely dense gates (measured: ~40 dense two-qubit
@@ -508,7 +528,7 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
             }
         }
     }
-    if (p->opts.dense_blocks > 0) {
+    if (p->opts.dense_blocks > 0 && canon_in) {
         // dense-block plan (tensor cores): every gate fused into <= 5-qubit
         // blocks on physical bits (canonical layout: wire w is bit n-1-w)
         require(dtype == QSV_C64, "dense blocks: complex64 plans only (tf32 tensor cores)");
@@ -562,14 +582,26 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
             const char *e = std::getenv("QSV_SCATTER_OUT");
             cfg.scatter_out = relabel && e && e[0] == '1';
         }
+        p->perm_out = p->perm_in;
         if (relabel) {
             std::vector<int> fin;
             gl = relabel_swaps(p->gates, p->perm_in, fin);
             for (int b = 0; b < n; ++b) phys[b] = b; // gates now name physical bits
-            out_perm.assign(n, 0);
-            for (int w = 0; w < n; ++w) out_perm[fin[w]] = p->perm_in[w];
+            if (lazy) {
+                p->perm_out = fin;  // the state leaves in the relabelled layout
+            } else {                // restore the canonical layout in the last pass
+                const std::vector<int> canon = canonical_perm(n);
+                p->perm_out = canon;
+                out_perm.assign(n, 0);
+                bool moved = false;
+                for (int w = 0; w < n; ++w) {
+                    out_perm[fin[w]] = canon[w];
+                    moved = moved || fin[w] != canon[w];
+                }
+                if (!moved) out_perm.clear();
+            }
         }
-        if (!p->gates.empty()) {
+        if (!gl.empty() || !out_perm.empty()) {
             const size_t encs0 = p->encs.size();
             auto passes = plan_passes(gl, phys, cfg, p->encs, out_perm);
             // complex64, default geometry: a memory-bound circuit (at most
@@ -606,12 +638,12 @@ void build_plan(Plan &pl, Ctx *ctx, int n, int dtype, std::vector<GateRec> gates
                 p->steps.push_back(std::move(s));
             }
         }
-        p->perm_out = p->perm_in;
     } else {
         schedule_dist(*p, cfg);
     }
     if (ctx->stream || ctx->device >= 0) upload_plan(*p); // dry runs (qsv_plan_dry) stay on the host
 }
+} // namespace
 
 void build_plan_from_abi(Plan &p, Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ngates,
                          const qsv_opts *opts) {
@@ -926,7 +958,70 @@ bool execute_graph(Plan &p, State &st) {
     return true;
 }
 
+bool layout_canonical(const State &st) {
+    for (int w = 0; w < st.n; ++w)
+        if (st.perm[w] != st.n - 1 - w) return false;
+    return true;
+}
+
+// One permutation-only pass (out of place, balanced read / write runs) from
+// the state's layout to the canonical one; the plan is kept per context and
+// input layout (a lazily laid-out state meets only a few).
+void normalize_layout(State &st) {
+    if (st.ctx->world != 1 || layout_canonical(st)) return;
+    Ctx &c = *st.ctx;
+    Plan *q = nullptr;
+    for (auto &e : c.layout_plans)
+        if (e.first == st.perm && e.second->dtype == st.dtype && e.second->n == st.n) q = e.second.get();
+    if (!q) {
+        auto np = std::make_shared<Plan>();
+        qsv_opts o{};
+        o.fuse = 1;
+        o.jit = 1;  // the permuting pass is a specialised kernel
+        build_plan_at(*np, st.ctx, st.n, st.dtype, {}, 0, &o, &st.perm);
+        require(np->perm_out == canonical_perm(st.n) && !np->passes.empty(),
+                "layout restore: needs a second state buffer (relabelled layouts)");
+        if (c.layout_plans.size() >= 8) c.layout_plans.erase(c.layout_plans.begin());
+        c.layout_plans.emplace_back(st.perm, np);
+        q = np.get();
+    }
+    execute_plan(*q, st, nullptr, 0, 0);
+}
+
+namespace {
+// The plan that runs on the state's current layout: p itself, or (lazy
+// layouts) p re-planned from that layout, once per layout met.
+Plan &plan_for_layout(Plan &p, State &st) {
+    if (p.ctx->world != 1 || st.perm == p.perm_in) return p;
+    if (p.opts.from_zero) {  // the state's contents are replaced: any layout will do
+        st.perm = p.perm_in;
+        return p;
+    }
+    if (p.src_gates.empty() && p.ngates > 0) {  // not a lazy-layout plan
+        normalize_layout(st);
+        require(st.perm == p.perm_in, "plan: state layout");
+        return p;
+    }
+    for (auto &v : p.variants)
+        if (v.first == st.perm) return *v.second;
+    auto v = std::make_unique<Plan>();
+    build_plan_at(*v, p.ctx, p.n, p.dtype, p.src_gates, p.nslots, &p.opts, &st.perm);
+    p.variants.emplace_back(st.perm, std::move(v));
+    return *p.variants.back().second;
+}
+void execute_plan_body(Plan &p, State &st, const double *data, int rows, int slots, double *zout);
+} // namespace
+
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout) {
+    require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
+    require(st.ctx == p.ctx, "plan/state belong to different contexts");
+    Plan &q = plan_for_layout(p, st);
+    execute_plan_body(q, st, data, rows, slots, zout);
+    if (p.ctx->world == 1) st.perm = q.perm_out;
+}
+
+namespace {
+void execute_plan_body(Plan &p, State &st, const double *data, int rows, int slots, double *zout) {
     require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
     require(st.ctx == p.ctx, "plan/state belong to different contexts");
     if (rows == 0) {
@@ -977,6 +1072,7 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     }
     execute_steps(p, st, enc_table, rows, zout);
 }
+} // namespace
 
 namespace {
 void execute_steps(Plan &p, State &st, const void *enc_table, int rows, double *zout) {
@@ -1023,10 +1119,14 @@ bool z_fusable(Plan &p) {
 }
 } // namespace
 
-void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots, double *host_out) {
+void execute_plan_z(Plan &p0, State &st, const double *data, int rows, int slots, double *host_out) {
+    require(st.n == p0.n && st.dtype == p0.dtype, "plan/state mismatch (nqubit or dtype)");
+    require(st.ctx == p0.ctx, "plan/state belong to different contexts");
+    Plan &p = plan_for_layout(p0, st);
     const int n = st.n, K1 = p.nlocal + 1;
     if (!z_fusable(p)) {
-        execute_plan(p, st, data, rows, slots);
+        execute_plan_body(p, st, data, rows, slots, nullptr);
+        if (p.ctx->world == 1) st.perm = p.perm_out;
         std::vector<double> z(static_cast<size_t>(st.batch) * 41);
         reduce_z_all(st, z.data());
         for (int b = 0; b < st.batch; ++b)
@@ -1046,7 +1146,8 @@ void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots,
         QSV_CUDA(cudaMalloc(&p.d_z, zbytes));
         p.d_z_cap = zbytes;
     }
-    execute_plan(p, st, data, rows, slots, static_cast<double *>(p.d_z));
+    execute_plan_body(p, st, data, rows, slots, static_cast<double *>(p.d_z));
+    if (p.ctx->world == 1) st.perm = p.perm_out;
     std::vector<double> z(static_cast<size_t>(st.batch) * K1);
     cudaStream_t s = p.ctx->stream;
     QSV_CUDA(cudaMemcpyAsync(z.data(), p.d_z, zbytes, cudaMemcpyDeviceToHost, s));
@@ -1057,9 +1158,19 @@ void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots,
                 z[static_cast<size_t>(b) * K1] - 2.0 * z[static_cast<size_t>(b) * K1 + 1 + st.perm[w]];
 }
 
-void profile_plan(Plan &p, State &st, double *launch_ms) {
-    require(st.n == p.n && st.dtype == p.dtype, "plan/state mismatch (nqubit or dtype)");
-    require(p.nslots == 0, "profile: encoded plans not supported");
+void profile_plan(Plan &p0, State &st, double *launch_ms) {
+    require(st.n == p0.n && st.dtype == p0.dtype, "plan/state mismatch (nqubit or dtype)");
+    require(p0.nslots == 0, "profile: encoded plans not supported");
+    Plan &p = plan_for_layout(p0, st);
+    // launch_ms holds one entry per step of p0 (qsv_plan_info / qsv_plan_steps)
+    require(p.steps.size() == p0.steps.size(), "profile: this layout's plan has another step count");
+    struct SetLayout {  // the state leaves in the plan's output layout
+        Plan &p;
+        State &st;
+        ~SetLayout() {
+            if (p.ctx->world == 1) st.perm = p.perm_out;
+        }
+    } set_layout{p, st};
     cudaStream_t s = p.ctx->stream;
     if (p.dense) {
         dense_execute(p, st, s, launch_ms);

@@ -285,6 +285,8 @@ struct Ctx {
     // every rank is driven from this process (qsv_ctx_create_multi): peer
     // memory is shared by raw pointers instead of CUDA IPC handles
     bool in_process = false;
+    // permutation-only plans restoring the canonical layout, by input layout
+    std::vector<std::pair<std::vector<int>, std::shared_ptr<struct Plan>>> layout_plans;
     ~Ctx();
 };
 
@@ -379,6 +381,10 @@ struct Plan {
     std::vector<DenseBlock> dblocks;
     std::vector<DensePass> dpasses;
     DenseDev *ddev = nullptr;
+    // opts.lazy_layout: the source gates, and one plan per input layout met
+    // so far (a lazily laid-out state alternates between a few layouts)
+    std::vector<GateRec> src_gates;
+    std::vector<std::pair<std::vector<int>, std::unique_ptr<Plan>>> variants;
     ~Plan();
 };
 
@@ -424,6 +430,11 @@ void run_pass(const DevPass &dp, int dtype, State &st, cudaStream_t s, double *z
 // reduction pass.
 void execute_plan_z(Plan &p, State &st, const double *data, int rows, int slots, double *host_out);
 void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, double *zout = nullptr);
+// Lazy layouts (opts.lazy_layout): whether the state's wire -> bit map is the
+// canonical one (wire w at bit n-1-w), and the permutation pass restoring it
+// (a no-op when it is; single GPU).
+bool layout_canonical(const State &st);
+void normalize_layout(State &st);
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
 // per-row, per-bit product-state vectors of a from-|0> plan into p.d_prefix
 void launch_prefix(const Plan &p, int rows, cudaStream_t s);

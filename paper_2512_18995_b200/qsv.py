@@ -82,7 +82,7 @@ class qsv_opts(C.Structure):
     _fields_ = [("fuse", C.c_int32), ("tile_bits", C.c_int32), ("low_bits", C.c_int32), ("use_graph", C.c_int32),
                 ("no_fuse_1q", C.c_int32), ("no_phase_flush", C.c_int32), ("jit", C.c_int32), ("reg_slots", C.c_int32),
                 ("no_relabel", C.c_int32), ("from_zero", C.c_int32), ("super_bits", C.c_int32),
-                ("dense_blocks", C.c_int32)]
+                ("dense_blocks", C.c_int32), ("lazy_layout", C.c_int32)]
 
 
 class qsv_plan_info(C.Structure):
