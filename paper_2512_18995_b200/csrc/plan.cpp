@@ -1017,7 +1017,10 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
     require(st.ctx == p.ctx, "plan/state belong to different contexts");
     Plan &q = plan_for_layout(p, st);
     execute_plan_body(q, st, data, rows, slots, zout);
-    if (p.ctx->world == 1) st.perm = q.perm_out;
+    if (p.ctx->world == 1) {
+        require(q.perm_out.size() == static_cast<size_t>(st.n), "plan: output layout");
+        st.perm = q.perm_out;
+    }
 }
 
 namespace {
