@@ -866,7 +866,10 @@ struct Gen {
               << " c) { return mk(c.x + a.x * b.x - a.y * b.y, c.y + a.x * b.y + a.y * b.x); }\n";
         }
         // a +-1 factor as a sign mask (0 or 0x80000000 on the high word of each component)
-        if (f32)
+        const char *nosign_dbg = std::getenv("QSV_DEBUG_NOSIGN");  // diagnostics only: wrong results
+        if (nosign_dbg && nosign_dbg[0] == '1')
+            c << "static __device__ __forceinline__ " << V << " sxor(" << V << " v, unsigned s) { (void)s; return v; }\n";
+        else if (f32)
             c << "static __device__ __forceinline__ cf sxor(cf v, unsigned s) { return mk(__uint_as_float(__float_as_uint(v.x) ^ s), "
                  "__uint_as_float(__float_as_uint(v.y) ^ s)); }\n";
         else
