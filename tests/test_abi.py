@@ -179,3 +179,36 @@ def test_dense_block_planning_on_host():
         qsv.plan_dry(14, W.dense_brickwork_circuit(14, 2).gates(), dtype=qsv.C128, opts={"dense_blocks": 1})
     with pytest.raises(qsv.InvalidInput):
         qsv.plan_dry(10, W.dense_brickwork_circuit(10, 2).gates(), dtype=qsv.C64, opts={"dense_blocks": 1})
+
+
+def header_struct_fields(name):
+    """Field names of `typedef struct name { ... } name;` in include/qsv.h, in
+    declaration order (array fields by their name)."""
+    text = HEADER.read_text()
+    body = re.search(r"typedef struct %s \{(.*?)\} %s;" % (name, name), text, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    return re.findall(r"(\w+)\s*(?:\[[^\]]*\])?\s*;", body)
+
+
+@pytest.mark.parametrize("name", ["qsv_gate", "qsv_obs", "qsv_opts", "qsv_plan_info"])
+def test_ctypes_structs_mirror_the_header(name):
+    """The Python mirror's ctypes structs lay out the header's fields in the
+    same order (an option added to one and not the other would shift every
+    later field across the boundary)."""
+    py = [f for f, _ in getattr(qsv, name)._fields_]
+    assert py == header_struct_fields(name), (py, header_struct_fields(name))
+
+
+def test_lazy_layout_plans_the_qft_in_three_12bit_passes():
+    """Host-only planning (qsv_plan_dry): with lazy layouts the 30q QFT + swaps
+    needs no layout-restoring pass, so 12-bit complex128 tiles take it in 3
+    passes (9 + 9 + 12 Hadamard wires) where the eager plan needs 4
+    (DESIGN.md 4.1g); the default 11-bit geometry needs 4 either way."""
+    from paper_2512_18995_b200 import workloads as W
+
+    gates = W.cfg3_circuit(30).gates()
+    npass = lambda o: qsv.plan_dry(30, gates, qsv.C128, 1, o)[0]["npasses"]
+    assert npass({"tile_bits": 12, "lazy_layout": 1}) == 3
+    assert npass({"tile_bits": 12}) == 4
+    assert npass({"lazy_layout": 1}) == 4
+    assert npass({}) == 4
