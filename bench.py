@@ -634,7 +634,7 @@ def main():
     hbm_peak, peak_kind = peaks()
     achieved = bytes_per_launch / (avg_launch_ms / 1e3) / 1e9
     traffic = None  # DRAM bytes per launch from the committed ncu --set full capture of this workload
-    tp = ROOT / "profiles" / "r02_traffic_cfg3_30q.json"
+    tp = ROOT / "profiles" / "r02_traffic_cfg3_30q_final.json"
     if tp.exists() and n == N_QUBITS and world == 1:
         traffic = json.loads(tp.read_text())["traffic_per_launch_bytes"]
 
@@ -721,7 +721,7 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                          "frac_nominal": achieved / NOMINAL_HBM_GBS, "peak_nominal": NOMINAL_HBM_GBS,
-                         "traffic_source": "profiles/r02_traffic_cfg3_30q.json (ncu --set full dram__bytes_read+write per launch)",
+                         "traffic_source": "profiles/r02_traffic_cfg3_30q_final.json (ncu --set full dram__bytes_read+write per launch)",
                          "kernel": "qsv_pass (NVRTC-specialised fused tile pass)", "bytes_per_launch": bytes_per_launch,
                          "avg_launch_ms": avg_launch_ms,
                          "per_pass_ms": [round(float(x), 4) for x in lm.mean(axis=0)]},

@@ -46,3 +46,18 @@ def test_stratified_sample_keeps_the_circuit_mix():
     assert len(gl) == 480
     kinds = [g.name for g in bench.stratified_sample(gl, 25)]
     assert len(kinds) == 25 and kinds.count("h") == 2 and kinds.count("swap") == 1 and kinds.count("p") == 22
+
+
+def test_bench_traffic_file_exists():
+    """bench.py's roofline.traffic comes from a committed ncu capture; a
+    renamed or missing file would silently report null."""
+    import re
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    src = (root / "bench.py").read_text()
+    name = re.search(r'tp = ROOT / "profiles" / "([^"]+)"', src).group(1)
+    import json
+
+    d = json.loads((root / "profiles" / name).read_text())
+    assert d["traffic_per_launch_bytes"] > 3e10
