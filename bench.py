@@ -486,9 +486,10 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
                      "hbm_floor_ms": p.info["npasses"] * bpl / (hbm_peak * 1e9) * 1e3,
                      "bound": ("FP64 pipe (ncu: 57-66 % busy, profiles/r02_ncu_cfg4f_28q_passenger.txt)" if dt == qsv.C128
                                else "FMA pipe / latency (ncu: FMA 40-52 %, profiles/r02_ncu_cfg5f_28q.txt)"),
-                     "note": "passes fuse more gates each than in round 1 (32q cfg4: 17 passes vs 32), so per-pass GB/s "
-                             "is lower while the forward is faster; the passes are compute-bound, the HBM fraction "
-                             "is not their roofline"}
+                     "note": ("passes fuse more gates each than in round 1 (" +
+                              ("32q cfg4: 17 passes vs 32" if dt == qsv.C128 else "33q cfg5: 18 passes vs 20") +
+                              "), so per-pass GB/s is lower while the forward is faster; the passes are "
+                              "compute-bound, the HBM fraction is not their roofline")}
         launches += 4 * p.info["npasses"]
         del st, p
     # ---- north_star (2)'s tensor-core blocks, measured where they are
