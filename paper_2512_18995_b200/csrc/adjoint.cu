@@ -152,7 +152,7 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t x, int b) {
 template <typename T, int K>
 __global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *__restrict__ psi,
                                                        typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
-                                                       const AdjGate g, double *__restrict__ grads) {
+                                                       const AdjGate g, double *__restrict__ part, int pb) {
     constexpr int D = 1 << K;
     double acc[3] = {0.0, 0.0, 0.0};
     const int lo = K == 2 ? (g.t0 < g.t1 ? g.t0 : g.t1) : g.t0, hi = K == 2 ? (g.t0 < g.t1 ? g.t1 : g.t0) : g.t0;
@@ -225,7 +225,108 @@ __global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *_
     if (threadIdx.x < g.nq) {
         double s = 0.0;
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
-        atomicAdd(grads + g.slot + threadIdx.x, 2.0 * s);
+        part[static_cast<size_t>(g.slot + threadIdx.x) * pb + blockIdx.x] = 2.0 * s;
+    }
+}
+
+// A run of single-qubit gates on one wire under one control mask (cfg1's rx,
+// ry, rz per wire and layer): the reverse-sweep steps of every gate of the
+// run on the thread's amplitude pair in registers -- psi and lambda loaded
+// and stored once per run instead of once per gate. Per gate in sweep order:
+// psi <- U^dag psi, each parameter's Re conj(lambda) dU psi, lambda <- U^dag
+// lambda (adjoint.hpp:93-108); the pair stays in FP64 between the gates.
+constexpr int kRunMax = 8;  // gates per run, and parameters per run
+constexpr int kRunMinBlocks = 3;  // 256-thread blocks per SM the register budget must allow
+struct AdjRun {
+    int t0 = 0, n = 0, nacc = 0;
+    uint64_t cmask = 0;
+    int first[kRunMax + 1];    // gate k's parameters are accumulators [first[k], first[k + 1])
+    int accslot[kRunMax];      // gradient slot of accumulator j
+    double u[kRunMax][8];      // U^dagger of gate k, 2 x 2 row-major (re, im)
+    double du[kRunMax][8];     // d U / d param of accumulator j
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256, kRunMinBlocks) adj_run_kernel(typename Vec2<T>::type *__restrict__ psi,
+                                                      typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
+                                                      const AdjRun g, double *__restrict__ part, int pb) {
+    double acc[kRunMax];
+#pragma unroll
+    for (int j = 0; j < kRunMax; ++j) acc[j] = 0.0;
+    for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < ngroups;
+         gi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t b0 = insert_zero(gi, g.t0);
+        if ((b0 & g.cmask) != g.cmask) continue;
+        const uint64_t b1 = b0 | (1ull << g.t0);
+        const auto a0 = psi[b0], a1 = psi[b1], c0 = lam[b0], c1 = lam[b1];
+        double p0r = a0.x, p0i = a0.y, p1r = a1.x, p1i = a1.y;
+        double l0r = c0.x, l0i = c0.y, l1r = c1.x, l1i = c1.y;
+#pragma unroll
+        for (int k = 0; k < kRunMax; ++k) {
+            if (k >= g.n) break;
+            const double *u = g.u[k];
+            const double n0r = u[0] * p0r - u[1] * p0i + u[2] * p1r - u[3] * p1i;
+            const double n0i = u[0] * p0i + u[1] * p0r + u[2] * p1i + u[3] * p1r;
+            const double n1r = u[4] * p0r - u[5] * p0i + u[6] * p1r - u[7] * p1i;
+            const double n1i = u[4] * p0i + u[5] * p0r + u[6] * p1i + u[7] * p1r;
+#pragma unroll
+            for (int j = 0; j < kRunMax; ++j) {
+                if (j < g.first[k] || j >= g.first[k + 1]) continue;
+                const double *d = g.du[j];
+                const double m0r = d[0] * n0r - d[1] * n0i + d[2] * n1r - d[3] * n1i;
+                const double m0i = d[0] * n0i + d[1] * n0r + d[2] * n1i + d[3] * n1r;
+                const double m1r = d[4] * n0r - d[5] * n0i + d[6] * n1r - d[7] * n1i;
+                const double m1i = d[4] * n0i + d[5] * n0r + d[6] * n1i + d[7] * n1r;
+                acc[j] += l0r * m0r + l0i * m0i + l1r * m1r + l1i * m1i;  // Re(conj(lambda) mu)
+            }
+            const double x0r = u[0] * l0r - u[1] * l0i + u[2] * l1r - u[3] * l1i;
+            const double x0i = u[0] * l0i + u[1] * l0r + u[2] * l1i + u[3] * l1r;
+            const double x1r = u[4] * l0r - u[5] * l0i + u[6] * l1r - u[7] * l1i;
+            const double x1i = u[4] * l0i + u[5] * l0r + u[6] * l1i + u[7] * l1r;
+            p0r = n0r, p0i = n0i, p1r = n1r, p1i = n1i;
+            l0r = x0r, l0i = x0i, l1r = x1r, l1i = x1i;
+        }
+        typename Vec2<T>::type v;
+        v.x = static_cast<T>(p0r), v.y = static_cast<T>(p0i);
+        psi[b0] = v;
+        v.x = static_cast<T>(p1r), v.y = static_cast<T>(p1i);
+        psi[b1] = v;
+        v.x = static_cast<T>(l0r), v.y = static_cast<T>(l0i);
+        lam[b0] = v;
+        v.x = static_cast<T>(l1r), v.y = static_cast<T>(l1i);
+        lam[b1] = v;
+    }
+    if (g.nacc == 0) return;
+    __shared__ double red[kRunMax][8];
+#pragma unroll
+    for (int j = 0; j < kRunMax; ++j) {
+        if (j >= g.nacc) break;
+        const double v = dev::warp_sum(acc[j]);
+        if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < g.nacc) {
+        double s = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
+        part[static_cast<size_t>(g.accslot[threadIdx.x]) * pb + blockIdx.x] = 2.0 * s;
+    }
+}
+
+// Gradient slot q = sum of its launch's per-block partials part[q * pb + b]
+// (the other entries stay zero): a fixed-order sum, no atomics contending on
+// one slot while the sweep runs.
+__global__ void __launch_bounds__(256) partial_sum_kernel(const double *__restrict__ part, int pb,
+                                                          double *__restrict__ grads) {
+    double s = 0.0;
+    for (int b = threadIdx.x; b < pb; b += blockDim.x) s += part[static_cast<size_t>(blockIdx.x) * pb + b];
+    __shared__ double red[8];
+    s = dev::warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += red[w];
+        grads[blockIdx.x] = t;
     }
 }
 
@@ -379,12 +480,82 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
     QSV_CUDA(cudaGetLastError());
     // gradient slots: params, then data slots
     const int nslots = static_cast<int>(dg.size());
+    const int ngrad = std::max(1, nparams + nslots);
     double *d_grad = nullptr;
-    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_grad), sizeof(double) * std::max(1, nparams + nslots), s));
-    QSV_CUDA(cudaMemsetAsync(d_grad, 0, sizeof(double) * std::max(1, nparams + nslots), s));
+    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_grad), sizeof(double) * ngrad, s));
+    QSV_CUDA(cudaMemsetAsync(d_grad, 0, sizeof(double) * ngrad, s));
+    static const int bps = [] {  // gradient launches: blocks per SM (QSV_ADJ_BLOCKS_PER_SM)
+        const char *e = std::getenv("QSV_ADJ_BLOCKS_PER_SM");
+        return e ? std::max(1, std::min(8, std::atoi(e))) : kRunMinBlocks;
+    }();
+    // per-block gradient partials: [slot][block], zero where a launch had
+    // fewer blocks; summed once after the sweep
+    const int pb = ctx->sm_count * 8;
+    double *d_part = nullptr;
+    QSV_CUDA(cudaMallocAsync(reinterpret_cast<void **>(&d_part), sizeof(double) * ngrad * pb, s));
+    QSV_CUDA(cudaMemsetAsync(d_part, 0, sizeof(double) * ngrad * pb, s));
+    static const bool no_runs = [] {  // QSV_ADJ_NO_RUNS=1: one kernel per gate (A/B)
+        const char *e = std::getenv("QSV_ADJ_NO_RUNS");
+        return e && e[0] == '1';
+    }();
+    auto nparams_of = [&](int x) { return pbase[x] >= 0 || dbase[x] >= 0 ? bound[x].nparams : 0; };
+    auto cmask_of = [&](int x) {
+        uint64_t m = 0;
+        for (int c : recs[x].ctls) m |= 1ull << perm[c];
+        return m;
+    };
     for (int i = static_cast<int>(recs.size()) - 1; i >= 0; --i) {
         const GateRec &g = recs[i];
         require(g.k >= 1 && g.k <= 2, "adjoint_gradients: gates act on 1 or 2 targets");
+        if (g.k == 1 && !no_runs && nparams_of(i) <= 3) {  // a run of single-qubit gates on this wire
+            const int t0 = perm[g.wires[0]];
+            const uint64_t cm = cmask_of(i);
+            int j = i, np = nparams_of(i);
+            while (j > 0 && i - j + 1 < kRunMax && recs[j - 1].k == 1 && perm[recs[j - 1].wires[0]] == t0 &&
+                   cmask_of(j - 1) == cm && nparams_of(j - 1) <= 3 && np + nparams_of(j - 1) <= kRunMax) {
+                --j;
+                np += nparams_of(j);
+            }
+            if (j < i) {
+                AdjRun r;
+                r.t0 = t0;
+                r.cmask = cm;
+                r.n = i - j + 1;
+                int acc = 0;
+                for (int k = 0; k < r.n; ++k) {
+                    const int x = i - k;  // sweep order
+                    const GateRec &h = recs[x];
+                    for (int rr = 0; rr < 2; ++rr)
+                        for (int c = 0; c < 2; ++c) {
+                            const cplx v = std::conj(h.m[c * 2 + rr]);
+                            r.u[k][2 * (rr * 2 + c)] = v.real();
+                            r.u[k][2 * (rr * 2 + c) + 1] = v.imag();
+                        }
+                    r.first[k] = acc;
+                    const int base = pbase[x] >= 0 ? pbase[x] : dbase[x] >= 0 ? nparams + dbase[x] : -1;
+                    for (int q = 0; q < nparams_of(x); ++q) {
+                        cplx dm[16];
+                        dmatrix(bound[x], q, dm);
+                        for (int e = 0; e < 4; ++e) r.du[acc][2 * e] = dm[e].real(), r.du[acc][2 * e + 1] = dm[e].imag();
+                        r.accslot[acc++] = base + q;
+                    }
+                }
+                r.first[r.n] = acc;
+                r.nacc = acc;
+                const uint64_t groups = N >> 1;
+                const int blocks = static_cast<int>(std::max<uint64_t>(
+                    1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * (acc ? bps : 8))));
+                if (dtype == QSV_C64)
+                    adj_run_kernel<float><<<blocks, 256, 0, s>>>(static_cast<float2 *>(psi.st.d),
+                                                                 static_cast<float2 *>(lam.st.d), groups, r, d_part, pb);
+                else
+                    adj_run_kernel<double><<<blocks, 256, 0, s>>>(static_cast<double2 *>(psi.st.d),
+                                                                  static_cast<double2 *>(lam.st.d), groups, r, d_part, pb);
+                QSV_CUDA(cudaGetLastError());
+                i = j;  // the loop's --i continues below the run
+                continue;
+            }
+        }
         const int d = 1 << g.k;
         AdjGate a;
         a.k = g.k;
@@ -412,27 +583,28 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
         const uint64_t groups = N >> g.k;
         // gradient gates: fewer, fuller blocks (one atomic per block and
         // parameter lands on the same slot); QSV_ADJ_BLOCKS_PER_SM overrides
-        static const int bps = [] {
-            const char *e = std::getenv("QSV_ADJ_BLOCKS_PER_SM");
-            return e ? std::max(1, std::atoi(e)) : 2;
-        }();
         const int blocks = static_cast<int>(
             std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * (a.nq ? bps : 8))));
         if (dtype == QSV_C64) {
             auto *P = static_cast<float2 *>(psi.st.d);
             auto *Lm = static_cast<float2 *>(lam.st.d);
-            if (g.k == 1) adj_gate_kernel<float, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
-            else adj_gate_kernel<float, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+            if (g.k == 1) adj_gate_kernel<float, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            else adj_gate_kernel<float, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
         } else {
             auto *P = static_cast<double2 *>(psi.st.d);
             auto *Lm = static_cast<double2 *>(lam.st.d);
-            if (g.k == 1) adj_gate_kernel<double, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
-            else adj_gate_kernel<double, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_grad);
+            if (g.k == 1) adj_gate_kernel<double, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            else adj_gate_kernel<double, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
         }
         QSV_CUDA(cudaGetLastError());
     }
-    std::vector<double> h(std::max(1, nparams + nslots));
+    if (nparams + nslots > 0) {
+        partial_sum_kernel<<<nparams + nslots, 256, 0, s>>>(d_part, pb, d_grad);
+        QSV_CUDA(cudaGetLastError());
+    }
+    std::vector<double> h(ngrad);
     QSV_CUDA(cudaMemcpyAsync(h.data(), d_grad, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, s));
+    QSV_CUDA(cudaFreeAsync(d_part, s));
     QSV_CUDA(cudaFreeAsync(d_grad, s));
     QSV_CUDA(cudaFreeAsync(dtab, s));
     QSV_CUDA(cudaStreamSynchronize(s));
