@@ -226,6 +226,60 @@ void run_single(State &st, const GateRec &g) {
     QSV_CUDA(cudaStreamSynchronize(st.ctx->stream));
 }
 
+// Trainable gates as run-time parameters (Circuit::forward in a training
+// loop: new angles every call). A copy of the gate list with every trainable
+// parametric gate marked encoded, and data rows rewritten in slot order --
+// the caller's encode values and the trainable parameters interleaved as the
+// gates come, one row per state row. The pass kernels then do not depend on
+// the trainable values (the bind kernel forms their matrices on the device),
+// so new angles reuse the compiled passes and the plan cache entry instead
+// of a code-generation + NVRTC compile per call.
+struct Lifted {
+    std::vector<qsv_gate> gates;
+    std::vector<double> data;
+    int rows = 0, slots = 0;
+};
+bool liftable(const qsv_gate &g) {
+    return g.trainable && !g.encode && g.nparams > 0 && std::strncmp(g.name, "custom", sizeof(g.name)) != 0;
+}
+bool lift_trainable(const qsv_gate *gates, int ngates, int n, const double *data, int rows, int slots, int batch,
+                    Lifted &out) {
+    bool any = false;
+    for (int i = 0; i < ngates; ++i) any = any || liftable(gates[i]);
+    if (!any) return false;
+    out.gates.assign(gates, gates + ngates);
+    int user = 0, total = 0;
+    for (qsv_gate &g : out.gates) {
+        if (liftable(g)) {
+            int scratch = 0;
+            (void)resolve_gate(g, n, &scratch);  // the constant gate's own checks and messages
+            g.encode = 1;
+        }
+        if (g.encode && g.nparams > 0) total += g.nparams;
+    }
+    for (int i = 0; i < ngates; ++i)
+        if (gates[i].encode && gates[i].nparams > 0) user += gates[i].nparams;
+    require(rows == 0 || slots == user, "data length " + std::to_string(slots) + " != encode slots " +
+                                            std::to_string(user));  // circuit.hpp:134-136
+    require(rows > 0 || user == 0, "circuit has encode slots but no data given");  // circuit.hpp:125
+    out.rows = rows > 0 ? rows : batch;
+    out.slots = total;
+    out.data.resize(static_cast<size_t>(out.rows) * total);
+    for (int r = 0; r < out.rows; ++r) {
+        double *dst = out.data.data() + static_cast<size_t>(r) * total;
+        const double *src = rows > 0 ? data + static_cast<size_t>(r) * slots : nullptr;
+        for (int i = 0; i < ngates; ++i) {
+            const qsv_gate &g = gates[i];
+            if (g.encode && g.nparams > 0) {
+                for (int q = 0; q < g.nparams; ++q) *dst++ = *src++;
+            } else if (liftable(g)) {
+                for (int q = 0; q < g.nparams; ++q) *dst++ = g.params[q];
+            }
+        }
+    }
+    return true;
+}
+
 // A group's host view is the whole state: rank r takes amplitudes
 // [r * 2^(n-g), (r + 1) * 2^(n-g)).
 template <typename Ptr, typename F> void group_slices(qsv_state *st, Ptr host, uint64_t count, size_t elem, F &&f) {
@@ -739,6 +793,42 @@ int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const doub
             const char *e = std::getenv("QSV_NO_PLAN_CACHE");
             return e && e[0] == '1';
         }();
+        static const bool nolift = [] {  // QSV_NO_LIFT=1: trainable angles stay compile-time constants
+            const char *e = std::getenv("QSV_NO_LIFT");
+            return e && e[0] == '1';
+        }();
+        Lifted lf;
+        bool lift = false;
+        if (!nolift && !(opts && opts->dense_blocks > 0) && ngates > 0 && gates) {
+            std::string sk, vk;  // structure (everything but the trainable values) and those values
+            auto put = [](std::string &k, const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
+            put(sk, &st->n, sizeof(int));
+            put(sk, &st->dtype, sizeof(int));
+            if (opts) put(sk, opts, sizeof(qsv_opts));
+            bool any = false;
+            for (int i = 0; i < ngates; ++i) {
+                const qsv_gate &g = gates[i];
+                const bool l = liftable(g);
+                any = any || l;
+                put(sk, g.name, sizeof(g.name));
+                put(sk, &g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
+                                       sizeof(g.nparams));
+                put(sk, &g.trainable, sizeof(g.trainable) + sizeof(g.encode));
+                if (l) put(vk, g.params, sizeof(g.params));
+                else if (!g.encode) put(sk, g.params, sizeof(g.params));
+                if (g.custom) {
+                    const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
+                    put(sk, g.custom, sizeof(double) * 2 * (1u << (2 * k)));
+                }
+            }
+            lift = any && lift_policy(*c, sk, vk);
+        }
+        if (lift && lift_trainable(gates, ngates, st->n, data, rows, slots, st->batch, lf)) {
+            gates = lf.gates.data();
+            data = lf.data.data();
+            rows = lf.rows;
+            slots = lf.slots;
+        }
         if (nocache || c->world != 1 || ngates > 4096) {
             Plan p;
             build_plan_from_abi(p, st->ctx, st->n, st->dtype, gates, ngates, opts);

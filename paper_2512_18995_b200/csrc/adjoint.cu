@@ -660,11 +660,60 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
     } else {
         launch_set_basis(psi.st, 0, ctx->rank == 0);
     }
-    // forward sweep, fused
+    // forward sweep, fused. The trainable and data-bound values are
+    // compile-time constants the first time this circuit structure is met;
+    // once it comes back with other values (a training loop) they enter as
+    // run-time parameters bound on the device (lift_policy), so new values
+    // reuse the compiled passes instead of an NVRTC compile per call
     {
+        auto variable = [&](int i) {
+            return (pbase[i] >= 0 || dbase[i] >= 0) && bound[i].nparams > 0 &&
+                   std::strncmp(bound[i].name, "custom", sizeof(bound[i].name)) != 0;
+        };
+        bool lift = false;
+        {
+            std::string sk("adjoint"), vk;
+            auto put = [](std::string &k, const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
+            put(sk, &n, sizeof(int));
+            put(sk, &dtype, sizeof(int));
+            bool any = false;
+            for (int i = 0; i < ngates; ++i) {
+                const qsv_gate &g = gates[i];
+                put(sk, g.name, sizeof(g.name));
+                put(sk, &g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
+                                       sizeof(g.nparams));
+                put(sk, &g.trainable, sizeof(g.trainable) + sizeof(g.encode));
+                if (variable(i)) {
+                    any = true;
+                    put(vk, bound[i].params, sizeof(double) * bound[i].nparams);
+                } else {
+                    put(sk, g.params, sizeof(g.params));
+                }
+                if (g.custom) {
+                    const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
+                    put(sk, g.custom, sizeof(double) * 2 * (1u << (2 * k)));
+                }
+            }
+            static const bool nolift = [] {
+                const char *e = std::getenv("QSV_NO_LIFT");
+                return e && e[0] == '1';
+            }();
+            lift = any && !nolift && lift_policy(*ctx, sk, vk);
+        }
+        std::vector<GateRec> fwd;
+        std::vector<double> vals;
+        int cur = 0;
+        for (int i = 0; i < ngates; ++i) {
+            qsv_gate g = bound[i];
+            if (lift && variable(i)) {
+                g.encode = 1;
+                for (int q = 0; q < g.nparams; ++q) vals.push_back(g.params[q]);
+            }
+            fwd.push_back(resolve_gate(g, n, &cur));
+        }
         Plan fw;
-        build_plan(fw, ctx, n, dtype, recs, 0, nullptr);
-        execute_plan(fw, psi.st, nullptr, 0, 0);
+        build_plan(fw, ctx, n, dtype, std::move(fwd), cur, nullptr);
+        execute_plan(fw, psi.st, cur ? vals.data() : nullptr, cur ? 1 : 0, cur);
     }
     pg.assign(nparams, 0.0);
     dg.assign(nslots, 0.0);

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <complex>
+#include <map>
+#include <mutex>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -265,6 +267,13 @@ void dense_free(struct Plan &p);
 // ---- runtime objects ----------------------------------------------------
 struct Nccl;  // dlopen'd NCCL
 
+// Circuit structures met on a context and whether their trainable values
+// have varied (lift_policy).
+struct LiftSeen {
+    std::mutex mu;
+    std::map<std::string, std::pair<std::string, bool>> m;  // structure -> (last values, varied)
+};
+
 struct Ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -287,6 +296,7 @@ struct Ctx {
     bool in_process = false;
     // permutation-only plans restoring the canonical layout, by input layout
     std::vector<std::pair<std::vector<int>, std::shared_ptr<struct Plan>>> layout_plans;
+    std::shared_ptr<LiftSeen> lift_seen = std::make_shared<LiftSeen>();
     ~Ctx();
 };
 
@@ -434,6 +444,22 @@ void execute_plan(Plan &p, State &st, const double *data, int rows, int slots, d
 // canonical one (wire w at bit n-1-w), and the permutation pass restoring it
 // (a no-op when it is; single GPU).
 bool layout_canonical(const State &st);
+// Trainable values as compile-time constants (specialised passes) the first
+// time a circuit structure is met on a context, as run-time parameters bound
+// on the device (encoded slots: no new code per value) once the same
+// structure comes back with other values -- a training loop.
+inline bool lift_policy(Ctx &c, const std::string &structure, const std::string &values) {
+    std::lock_guard<std::mutex> lk(c.lift_seen->mu);
+    auto &m = c.lift_seen->m;
+    auto it = m.find(structure);
+    if (it == m.end()) {
+        if (m.size() >= 256) m.clear();
+        m.emplace(structure, std::make_pair(values, false));
+        return false;
+    }
+    if (!it->second.second && it->second.first != values) it->second.second = true;
+    return it->second.second;
+}
 void normalize_layout(State &st);
 void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaStream_t s);
 // per-row, per-bit product-state vectors of a from-|0> plan into p.d_prefix
