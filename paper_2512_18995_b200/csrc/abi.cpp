@@ -280,6 +280,34 @@ bool lift_trainable(const qsv_gate *gates, int ngates, int n, const double *data
     return true;
 }
 
+// lift_policy's keys for a gate list: the structure (everything but the
+// trainable values) and those values.
+bool want_lift(Ctx &c, int n, int dtype, const qsv_opts *opts, const qsv_gate *gates, int ngates) {
+    if ((opts && opts->dense_blocks > 0) || ngates <= 0 || !gates) return false;  // dense blocks: no encoded gates
+    std::string sk, vk;
+    auto put = [](std::string &k, const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
+    put(sk, &n, sizeof(int));
+    put(sk, &dtype, sizeof(int));
+    if (opts) put(sk, opts, sizeof(qsv_opts));
+    bool any = false;
+    for (int i = 0; i < ngates; ++i) {
+        const qsv_gate &g = gates[i];
+        const bool l = liftable(g);
+        any = any || l;
+        put(sk, g.name, sizeof(g.name));
+        put(sk, &g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
+                               sizeof(g.nparams));
+        put(sk, &g.trainable, sizeof(g.trainable) + sizeof(g.encode));
+        if (l) put(vk, g.params, sizeof(g.params));
+        else if (!g.encode) put(sk, g.params, sizeof(g.params));
+        if (g.custom) {
+            const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
+            put(sk, g.custom, sizeof(double) * 2 * (1u << (2 * k)));
+        }
+    }
+    return any && lift_policy(c, sk, vk);
+}
+
 // A group's host view is the whole state: rank r takes amplitudes
 // [r * 2^(n-g), (r + 1) * 2^(n-g)).
 template <typename Ptr, typename F> void group_slices(qsv_state *st, Ptr host, uint64_t count, size_t elem, F &&f) {
@@ -310,6 +338,17 @@ void detail_run_rows(qsv_ctx *c, int n, int dtype, const qsv_gate *gates, int ng
     auto chk = [](int rc) {
         if (rc) fail(rc, g_err);
     };
+    static const bool nolift = [] {  // QSV_NO_LIFT=1: trainable values stay compile-time constants
+        const char *e = std::getenv("QSV_NO_LIFT");
+        return e && e[0] == '1';
+    }();
+    Lifted lf;  // a training loop's new shared angles: bound on the device
+    if (!nolift && want_lift(*c, n, dtype, &o, gates, ngates) &&
+        lift_trainable(gates, ngates, n, data, slots ? rows : 0, slots, rows, lf)) {
+        gates = lf.gates.data();
+        data = lf.data.data();
+        slots = lf.slots;
+    }
     chk(qsv_plan_create(c, n, dtype, gates, ngates, &o, pp));
     chk(qsv_state_create(c, n, rows, dtype, ps));
     chk(qsv_plan_execute_expect_z(*pp, *ps, slots ? data : nullptr, slots ? rows : 0, slots, out));
@@ -798,31 +837,7 @@ int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const doub
             return e && e[0] == '1';
         }();
         Lifted lf;
-        bool lift = false;
-        if (!nolift && !(opts && opts->dense_blocks > 0) && ngates > 0 && gates) {
-            std::string sk, vk;  // structure (everything but the trainable values) and those values
-            auto put = [](std::string &k, const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
-            put(sk, &st->n, sizeof(int));
-            put(sk, &st->dtype, sizeof(int));
-            if (opts) put(sk, opts, sizeof(qsv_opts));
-            bool any = false;
-            for (int i = 0; i < ngates; ++i) {
-                const qsv_gate &g = gates[i];
-                const bool l = liftable(g);
-                any = any || l;
-                put(sk, g.name, sizeof(g.name));
-                put(sk, &g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
-                                       sizeof(g.nparams));
-                put(sk, &g.trainable, sizeof(g.trainable) + sizeof(g.encode));
-                if (l) put(vk, g.params, sizeof(g.params));
-                else if (!g.encode) put(sk, g.params, sizeof(g.params));
-                if (g.custom) {
-                    const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
-                    put(sk, g.custom, sizeof(double) * 2 * (1u << (2 * k)));
-                }
-            }
-            lift = any && lift_policy(*c, sk, vk);
-        }
+        const bool lift = !nolift && want_lift(*c, st->n, st->dtype, opts, gates, ngates);
         if (lift && lift_trainable(gates, ngates, st->n, data, rows, slots, st->batch, lf)) {
             gates = lf.gates.data();
             data = lf.data.data();

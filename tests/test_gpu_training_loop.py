@@ -87,3 +87,26 @@ def test_adjoint_with_new_angles_every_call(dtype):
         want, _ = O.ref_adjoint(n, cir.gates(), [(o.wires, o.basis) for o in cir.observables()], [])
         err = float(np.max(np.abs(np.asarray(g.param_grads) - np.asarray(want))))
         assert err <= (1e-11 if dtype == C128 else 2e-4), (step, err)
+
+
+def test_batched_rows_expect_z_with_new_shared_angles():
+    """cfg2-style batched circuits (qsv_run_rows_expect_z): encoded data per
+    row, trainable U3 angles shared by the rows and new every call."""
+    n, rows = 6, 16
+    rng = np.random.default_rng(11)
+    for step in range(3):
+        cir = Circuit(n)
+        for q in range(n):
+            cir.add(make_gate("ry", [q], [], [0.0], False, True))
+        for _ in range(2):
+            for q in range(n):
+                cir.add(make_gate("u3", [q], [], list(rng.uniform(0, 2 * math.pi, 3)), True))
+            for q in range(n):
+                cir.cz(q, (q + 1) % n)
+        data = rng.uniform(-math.pi, math.pi, (rows, n))
+        z = np.asarray(qsv.run_rows_expect_z(cir, data, dtype=C128))
+        amps = np.asarray(ref_forward(n, cir.gates(), data=data.tolist()))
+        p = np.abs(amps) ** 2
+        idx = np.arange(1 << n)
+        want = np.stack([(p * (1 - 2 * ((idx >> (n - 1 - w)) & 1))).sum(axis=1) for w in range(n)], axis=1)
+        assert np.max(np.abs(z.reshape(rows, n) - want)) <= 1e-12, step
