@@ -390,7 +390,64 @@ def run_aux(ctx, stream, hbm_peak, want_cpu):
         adj["cpu_reference"] = {"ms_per_gradient": 1e3 * (_t.perf_counter() - t0), "cores": 1,
                                 "protocol": "1 run of quasar::qubit::adjoint_gradients (oracle/_ref)"}
         adj["max_abs_err_vs_reference"] = float(np.max(np.abs(np.asarray(ag.param_grads) - want)))
+    adj["note"] = ("runs of single-qubit gates on one wire as one reverse-sweep kernel (the psi/lambda pair in "
+                   "registers through the run), other gates one kernel each: psi' = U^dag psi, every parameter's "
+                   "Re<lambda|dU psi'>, lambda' = U^dag lambda (DESIGN.md 4.1c)")
     aux["adjoint_20q"] = adj
+    # ---- training loops: the same structure with NEW trainable values every
+    # step: steps 0-1 compile (the values in, then the
+    # device-bound form), later steps reuse the passes ----
+    def loop_steps(make, call, steps=5):
+        out = []
+        for k in range(steps):
+            c = make(k)
+            t0 = _t.perf_counter()
+            call(c)
+            out.append(1e3 * (_t.perf_counter() - t0))
+        return out
+
+    lrng = np.random.default_rng(0)
+
+    def adj_circ(_k):
+        c = qsv.Circuit(n_adj)
+        for _ in range(10):
+            for q in range(n_adj):
+                c.rx(q, lrng.uniform(0, 2 * np.pi), True)
+                c.ry(q, lrng.uniform(0, 2 * np.pi), True)
+                c.rz(q, lrng.uniform(0, 2 * np.pi), True)
+        for q in range(n_adj - 1):
+            c.cnot(q, q + 1)
+        for q in range(n_adj):
+            c.observable([q], "z")
+        return c
+
+    t_adj = loop_steps(adj_circ, lambda c: qsv.adjoint_gradients(c))
+    t_fwd = loop_steps(adj_circ, lambda c: c.forward())
+    d2 = lrng.uniform(-np.pi, np.pi, (4096, 12))
+
+    def cfg2_circ(_k):
+        c = qsv.Circuit(12)
+        for q in range(12):
+            c.add(qsv.make_gate("ry", [q], [], [0.0], False, True))
+        for _ in range(6):
+            for q in range(12):
+                c.add(qsv.make_gate("u3", [q], [], list(lrng.uniform(0, 2 * np.pi, 3)), True))
+            for q in range(12):
+                c.cz(q, (q + 1) % 12)
+        return c
+
+    t_c2 = loop_steps(cfg2_circ, lambda c: qsv.run_rows_expect_z(c, d2))
+    launches += 3 * 5 * 2 * len(adj_circ(0).gates())
+    aux["training_loops"] = {
+        "workload": "new trainable values every step, host wall clock per step: adjoint_gradients and "
+                    "Circuit.forward of the cfg1-shaped circuit at 20q c128 (600 trainable rotations), and cfg2 "
+                    "(4096 rows x 12q c64, new shared U3 angles) through run_rows_expect_z",
+        "adjoint_20q_ms_per_step": [round(x, 2) for x in t_adj],
+        "forward_20q_ms_per_step": [round(x, 2) for x in t_fwd],
+        "cfg2_ms_per_step": [round(x, 2) for x in t_c2],
+        "note": "steps 0-1 include code generation + NVRTC (values compiled in, then the device-bound form); "
+                "from step 2 on no compile: the reference's own CPU path takes ~17 s per 20q gradient and "
+                "~0.9 s per cfg2 step on 16 cores (aux.adjoint_20q / aux.cfg2)"}
     # ---- seeded measurement (circuit.hpp:217-244): marginals
     # over 20 wires of a 24-qubit state on the device, 10^6 shots sampled on
     # the host with the reference's Rng stream; the histogram must equal the
