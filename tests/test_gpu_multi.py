@@ -304,3 +304,33 @@ def test_cfg2_rows_sharded_over_devices_match_one_device():
     for r in range(8):
         wz = [O.port_expectation(12, want[r], [q], "z")[0] for q in range(12)]
         assert np.max(np.abs(four[r] - wz)) <= 1e-5
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_training_loop_values_bound_on_device_across_ranks(world):
+    """The same structure with new trainable values every call (DESIGN.md
+    4.1h): from the second set on the trainable gates run as device-bound
+    (encoded) parameters through the distributed schedule; forward and
+    adjoint gradients still match the reference on every call."""
+    import math
+
+    ctx = multi(world)
+    rng = np.random.default_rng(world)
+    n = 6
+    for step in range(3):
+        c = qsv.Circuit(n)
+        for q in range(n):
+            c.rx(q, rng.uniform(0, 2 * math.pi), True)
+            c.ry(q, rng.uniform(0, 2 * math.pi), True)
+        for q in range(n - 1):
+            c.cnot(q, q + 1)
+        c.add(qsv.make_gate("u3", [0], [], list(rng.uniform(0, 2 * math.pi, 3)), True))
+        c.add(qsv.make_gate("rzz", [0, n - 1], [], [rng.uniform(0, 2 * math.pi)], True))
+        c.observable([0], "z")
+        c.observable([n - 1], "x")
+        got = c.forward(ctx=ctx).amplitudes()
+        assert np.max(np.abs(got - ref_state(n, c.gates()))) <= 1e-12, (world, step)
+        want, _ = O.ref_adjoint(n, c.gates(), [([0], "z"), ([n - 1], "x")])
+        g = qsv.adjoint_gradients(c, ctx=ctx)
+        assert np.max(np.abs(np.array(g.param_grads) - want)) <= 1e-10, (world, step)
+    ctx.close()
