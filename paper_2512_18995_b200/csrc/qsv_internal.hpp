@@ -271,7 +271,7 @@ struct Nccl;  // dlopen'd NCCL
 // have varied (lift_policy).
 struct LiftSeen {
     std::mutex mu;
-    std::map<std::string, std::pair<std::string, bool>> m;  // structure -> (last values, varied)
+    std::map<size_t, std::pair<size_t, bool>> m;  // hash(structure) -> (hash(last values), varied)
 };
 
 struct Ctx {
@@ -449,15 +449,19 @@ bool layout_canonical(const State &st);
 // on the device (encoded slots: no new code per value) once the same
 // structure comes back with other values -- a training loop.
 inline bool lift_policy(Ctx &c, const std::string &structure, const std::string &values) {
+    // hashes only: a collision costs a compile or a device-bound run, never a
+    // wrong result (both forms compute the same circuit)
+    const size_t hs = std::hash<std::string>{}(structure), hv = std::hash<std::string>{}(values);
     std::lock_guard<std::mutex> lk(c.lift_seen->mu);
     auto &m = c.lift_seen->m;
-    auto it = m.find(structure);
+    auto it = m.find(hs);
     if (it == m.end()) {
-        if (m.size() >= 256) m.clear();
-        m.emplace(structure, std::make_pair(values, false));
+        if (m.size() >= 1024) m.clear();
+        m.emplace(hs, std::make_pair(hv, false));
         return false;
     }
-    if (!it->second.second && it->second.first != values) it->second.second = true;
+    const size_t &values_seen = it->second.first;
+    if (!it->second.second && values_seen != hv) it->second.second = true;
     return it->second.second;
 }
 void normalize_layout(State &st);
