@@ -137,6 +137,15 @@ void init_ctx(Ctx &c, int device) {
     c.sm_count = prop.multiProcessorCount;
     c.smem_optin = prop.sharedMemPerBlockOptin;
     QSV_CUDA(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    // stream-ordered scratch (reductions, adjoint gradient partials): keep up
+    // to 256 MiB in the device's pool across synchronisations instead of
+    // unmapping and remapping it on every call
+    cudaMemPool_t pool = nullptr;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = 256ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    cudaGetLastError();
 }
 
 // Device staging owned for the scope of one transfer (freed on every path,

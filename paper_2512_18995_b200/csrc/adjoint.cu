@@ -671,8 +671,8 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
                    std::strncmp(bound[i].name, "custom", sizeof(bound[i].name)) != 0;
         };
         bool lift = false;
+        std::string sk("adjoint"), vk;
         {
-            std::string sk("adjoint"), vk;
             auto put = [](std::string &k, const void *p, size_t b) { k.append(static_cast<const char *>(p), b); };
             put(sk, &n, sizeof(int));
             put(sk, &dtype, sizeof(int));
@@ -711,9 +711,24 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
             }
             fwd.push_back(resolve_gate(g, n, &cur));
         }
-        Plan fw;
-        build_plan(fw, ctx, n, dtype, std::move(fwd), cur, nullptr);
-        execute_plan(fw, psi.st, cur ? vals.data() : nullptr, cur ? 1 : 0, cur);
+        // forward plans kept per context: a device-bound plan by structure
+        // (it does not depend on the values), a constant one by structure
+        // and values (planning 600+ gates costs more than the 20q sweep)
+        const std::string key = lift ? sk : sk + std::string(1, '\1') + vk;
+        std::shared_ptr<Plan> fw;
+        {
+            std::lock_guard<std::mutex> lk(ctx->lift_seen->mu);
+            for (auto &e : ctx->adj_plans)
+                if (e.first == key) fw = e.second;
+        }
+        if (!fw) {
+            fw = std::make_shared<Plan>();
+            build_plan(*fw, ctx, n, dtype, std::move(fwd), cur, nullptr);
+            std::lock_guard<std::mutex> lk(ctx->lift_seen->mu);
+            if (ctx->adj_plans.size() >= 4) ctx->adj_plans.erase(ctx->adj_plans.begin());
+            ctx->adj_plans.emplace_back(key, fw);
+        }
+        execute_plan(*fw, psi.st, cur ? vals.data() : nullptr, cur ? 1 : 0, cur);
     }
     pg.assign(nparams, 0.0);
     dg.assign(nslots, 0.0);

@@ -297,6 +297,8 @@ struct Ctx {
     // permutation-only plans restoring the canonical layout, by input layout
     std::vector<std::pair<std::vector<int>, std::shared_ptr<struct Plan>>> layout_plans;
     std::shared_ptr<LiftSeen> lift_seen = std::make_shared<LiftSeen>();
+    // adjoint forward plans of device-bound (lifted) structures, by structure
+    std::vector<std::pair<std::string, std::shared_ptr<struct Plan>>> adj_plans;
     ~Ctx();
 };
 
