@@ -327,6 +327,49 @@ template <typename Ptr, typename F> void group_slices(qsv_state *st, Ptr host, u
     });
 }
 
+// The context's plan for (n, dtype, options, gates), planned and specialised
+// on first use: the key is everything build_plan reads -- n, dtype, the
+// options and every gate field except the encoded parameters' values (bound
+// per row at execute) and `trainable`; custom matrices by value. `lk` holds
+// the cache (and so the plan) while the caller executes it.
+Plan &cached_plan(qsv_ctx *c, int n, int dtype, const qsv_opts *opts, const qsv_gate *gates, int ngates,
+                  std::unique_lock<std::mutex> &lk) {
+    std::string key;
+    auto put = [&](const void *p, size_t b) { key.append(static_cast<const char *>(p), b); };
+    put(&n, sizeof(int));
+    put(&dtype, sizeof(int));
+    const int has_opts = opts != nullptr;
+    put(&has_opts, sizeof(int));
+    if (opts) put(opts, sizeof(qsv_opts));
+    require(ngates >= 0 && (ngates == 0 || gates != nullptr), "plan: bad gate list");
+    for (int i = 0; i < ngates; ++i) {
+        const qsv_gate &g = gates[i];
+        put(g.name, sizeof(g.name));
+        put(&g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
+                           sizeof(g.nparams));
+        put(&g.encode, sizeof(g.encode));
+        if (!g.encode) put(g.params, sizeof(g.params));
+        if (g.custom) {
+            const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
+            put(g.custom, sizeof(double) * 2 * (1u << (2 * k)));
+        }
+    }
+    lk = std::unique_lock<std::mutex>(c->plans->mu);
+    auto &lru = c->plans->lru;
+    auto it = std::find_if(lru.begin(), lru.end(), [&](const auto &e) { return e.first == key; });
+    if (it == lru.end()) {
+        auto np = std::make_unique<Plan>();
+        build_plan_from_abi(*np, c, n, dtype, gates, ngates, opts);
+        lru.emplace_front(std::move(key), std::move(np));
+        if (lru.size() > PlanCache::kCap) lru.pop_back();
+        it = lru.begin();
+    } else if (it != lru.begin()) {
+        lru.splice(lru.begin(), lru, it);
+        it = lru.begin();
+    }
+    return *it->second;
+}
+
 // Batched circuit on one context: forward from |0...0> with the rows' encode
 // data, then every <Z_w> per row (the fused epilogue when the pass holds a
 // whole row); the plan and state are freed on every path.
@@ -358,9 +401,11 @@ void detail_run_rows(qsv_ctx *c, int n, int dtype, const qsv_gate *gates, int ng
         data = lf.data.data();
         slots = lf.slots;
     }
-    chk(qsv_plan_create(c, n, dtype, gates, ngates, &o, pp));
+    (void)pp;
     chk(qsv_state_create(c, n, rows, dtype, ps));
-    chk(qsv_plan_execute_expect_z(*pp, *ps, slots ? data : nullptr, slots ? rows : 0, slots, out));
+    std::unique_lock<std::mutex> lk;
+    Plan &plan = cached_plan(c, n, dtype, &o, gates, ngates, lk);  // a training loop re-plans once
+    execute_plan_z(plan, **ps, slots ? data : nullptr, slots ? rows : 0, slots, out);
 }
 
 } // namespace
@@ -860,43 +905,9 @@ int qsv_run_circuit(qsv_state *st, const qsv_gate *gates, int ngates, const doub
             QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
             return;
         }
-        // key: everything build_plan reads -- n, dtype, the options and every
-        // gate field except the encoded parameters' values (bound per row at
-        // execute) and `trainable`; custom matrices by value
-        std::string key;
-        auto put = [&](const void *p, size_t b) { key.append(static_cast<const char *>(p), b); };
-        put(&st->n, sizeof(int));
-        put(&st->dtype, sizeof(int));
-        const int has_opts = opts != nullptr;
-        put(&has_opts, sizeof(int));
-        if (opts) put(opts, sizeof(qsv_opts));
-        require(ngates >= 0 && (ngates == 0 || gates != nullptr), "plan: bad gate list");
-        for (int i = 0; i < ngates; ++i) {
-            const qsv_gate &g = gates[i];
-            put(g.name, sizeof(g.name));
-            put(&g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
-                               sizeof(g.nparams));
-            put(&g.encode, sizeof(g.encode));
-            if (!g.encode) put(g.params, sizeof(g.params));
-            if (g.custom) {
-                const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
-                put(g.custom, sizeof(double) * 2 * (1u << (2 * k)));
-            }
-        }
-        std::lock_guard<std::mutex> lk(c->plans->mu);
-        auto &lru = c->plans->lru;
-        auto it = std::find_if(lru.begin(), lru.end(), [&](const auto &e) { return e.first == key; });
-        if (it == lru.end()) {
-            auto np = std::make_unique<Plan>();
-            build_plan_from_abi(*np, st->ctx, st->n, st->dtype, gates, ngates, opts);
-            lru.emplace_front(std::move(key), std::move(np));
-            if (lru.size() > PlanCache::kCap) lru.pop_back();
-            it = lru.begin();
-        } else if (it != lru.begin()) {
-            lru.splice(lru.begin(), lru, it);
-            it = lru.begin();
-        }
-        execute_plan(*it->second, *st, data, rows, slots);
+        std::unique_lock<std::mutex> lk;
+        Plan &plan = cached_plan(c, st->n, st->dtype, opts, gates, ngates, lk);
+        execute_plan(plan, *st, data, rows, slots);
         QSV_CUDA(cudaStreamSynchronize(st->ctx->stream));
     });
 }
