@@ -462,6 +462,32 @@ bool apply_direct(State &st, const GateRec &g) {
     return true;
 }
 
+// <Z_w> of every row from the fused epilogue's sums: z[b][0] is the row's
+// total |a|^2, z[b][1 + bit] the |a|^2 with that physical bit set.
+struct ZPerm {
+    int bit[kMaxQubits];
+};
+__global__ void z_finish_kernel(const double *__restrict__ z, int k1, int rows, int n, const ZPerm perm,
+                                double *__restrict__ out) {
+    const int total = rows * n;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int b = i / n, w = i - b * n;
+        const double *zb = z + static_cast<size_t>(b) * k1;
+        out[i] = zb[0] - 2.0 * zb[1 + perm.bit[w]];
+    }
+}
+
+void launch_z_finish(const double *z, int k1, int rows, int n, const std::vector<int> &perm, double *out,
+                     cudaStream_t s) {
+    require(n <= kMaxQubits, "z_finish: too many qubits");
+    ZPerm pm{};
+    for (int w = 0; w < n; ++w) pm.bit[w] = perm[w];
+    const int total = rows * n;
+    const int blocks = std::max(1, std::min((total + 255) / 256, 1024));
+    z_finish_kernel<<<blocks, 256, 0, s>>>(z, k1, rows, n, pm, out);
+    QSV_CUDA(cudaGetLastError());
+}
+
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank) {
     const uint64_t total = st.local_amps * st.batch;
     const int g = grid_for(total, 256, st.ctx->sm_count);

@@ -47,6 +47,8 @@ Plan::~Plan() {
     cudaFree(d_prefix_mats);
     cudaFree(d_prefix);
     cudaFree(d_sync);
+    cudaFree(d_zout);
+    cudaFreeHost(h_zout);
     for (auto &g : graphs)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     dense_free(*this);
@@ -1151,14 +1153,24 @@ void execute_plan_z(Plan &p0, State &st, const double *data, int rows, int slots
     }
     execute_plan_body(p, st, data, rows, slots, static_cast<double *>(p.d_z));
     if (p.ctx->world == 1) st.perm = p.perm_out;
-    std::vector<double> z(static_cast<size_t>(st.batch) * K1);
+    // <Z_w> formed on the device, read back through pinned staging
     cudaStream_t s = p.ctx->stream;
-    QSV_CUDA(cudaMemcpyAsync(z.data(), p.d_z, zbytes, cudaMemcpyDeviceToHost, s));
+    const size_t obytes = sizeof(double) * static_cast<size_t>(st.batch) * n;
+    if (obytes > p.zout_cap) {
+        QSV_CUDA(cudaStreamSynchronize(s));
+        cudaFree(p.d_zout);
+        cudaFreeHost(p.h_zout);
+        p.d_zout = nullptr;
+        p.h_zout = nullptr;
+        p.zout_cap = 0;
+        QSV_CUDA(cudaMalloc(reinterpret_cast<void **>(&p.d_zout), obytes));
+        QSV_CUDA(cudaMallocHost(reinterpret_cast<void **>(&p.h_zout), obytes));
+        p.zout_cap = obytes;
+    }
+    launch_z_finish(static_cast<const double *>(p.d_z), K1, st.batch, n, st.perm, p.d_zout, s);
+    QSV_CUDA(cudaMemcpyAsync(p.h_zout, p.d_zout, obytes, cudaMemcpyDeviceToHost, s));
     QSV_CUDA(cudaStreamSynchronize(s));
-    for (int b = 0; b < st.batch; ++b)
-        for (int w = 0; w < n; ++w)
-            host_out[static_cast<size_t>(b) * n + w] =
-                z[static_cast<size_t>(b) * K1] - 2.0 * z[static_cast<size_t>(b) * K1 + 1 + st.perm[w]];
+    std::memcpy(host_out, p.h_zout, obytes);
 }
 
 void profile_plan(Plan &p0, State &st, double *launch_ms) {

@@ -376,6 +376,8 @@ struct Plan {
     void *d_prefix_prog = nullptr, *d_prefix_mats = nullptr, *d_prefix = nullptr;
     size_t prefix_rows = 0;
     size_t d_z_cap = 0;
+    double *d_zout = nullptr, *h_zout = nullptr;  // fused <Z>: device result, pinned staging
+    size_t zout_cap = 0;
     void *d_sync = nullptr;    // L2 super-passes: per-chunk counters + the item ticket
     size_t d_sync_cap = 0;
     // opts.use_graph: the launch sequence captured per (state buffers, rows)
@@ -471,6 +473,9 @@ void launch_bind(const Plan &p, const double *d_data, int rows, int slots, cudaS
 // per-row, per-bit product-state vectors of a from-|0> plan into p.d_prefix
 void launch_prefix(const Plan &p, int rows, cudaStream_t s);
 void launch_set_basis(State &st, uint64_t local_index, bool on_this_rank);
+// out[b * n + w] = z[b * k1] - 2 z[b * k1 + 1 + perm[w]] (device arrays)
+void launch_z_finish(const double *z, int k1, int rows, int n, const std::vector<int> &perm, double *out,
+                     cudaStream_t s);
 // state buffers: recycled per device up to 256 MiB each (engine.cu)
 cudaError_t state_alloc(void **p, size_t bytes);
 void state_release(void *p, size_t bytes);
