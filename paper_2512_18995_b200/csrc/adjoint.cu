@@ -13,6 +13,7 @@
 //     (fused_sweep below); across ranks the steps run as whole-state
 //     operations through one-gate plans.
 // The derivative matrices restate gate_dmatrix (gate.hpp:157-190).
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
@@ -312,6 +313,108 @@ __global__ void __launch_bounds__(256, kRunMinBlocks) adj_run_kernel(typename Ve
     }
 }
 
+// One run's steps on one amplitude pair: p = (psi0, psi1), l = (lambda0,
+// lambda1) as (re, im, re, im), in place; acc: the run's parameter sums.
+__device__ __forceinline__ void adj_run_steps(const AdjRun &g, double *p, double *l, double *acc) {
+#pragma unroll
+    for (int k = 0; k < kRunMax; ++k) {
+        if (k >= g.n) break;
+        const double *u = g.u[k];
+        const double n0r = u[0] * p[0] - u[1] * p[1] + u[2] * p[2] - u[3] * p[3];
+        const double n0i = u[0] * p[1] + u[1] * p[0] + u[2] * p[3] + u[3] * p[2];
+        const double n1r = u[4] * p[0] - u[5] * p[1] + u[6] * p[2] - u[7] * p[3];
+        const double n1i = u[4] * p[1] + u[5] * p[0] + u[6] * p[3] + u[7] * p[2];
+        for (int j = g.first[k]; j < g.first[k + 1]; ++j) {
+            const double *d = g.du[j];
+            const double m0r = d[0] * n0r - d[1] * n0i + d[2] * n1r - d[3] * n1i;
+            const double m0i = d[0] * n0i + d[1] * n0r + d[2] * n1i + d[3] * n1r;
+            const double m1r = d[4] * n0r - d[5] * n0i + d[6] * n1r - d[7] * n1i;
+            const double m1i = d[4] * n0i + d[5] * n0r + d[6] * n1i + d[7] * n1r;
+            acc[j] += l[0] * m0r + l[1] * m0i + l[2] * m1r + l[3] * m1i;  // Re(conj(lambda) mu)
+        }
+        const double x0r = u[0] * l[0] - u[1] * l[1] + u[2] * l[2] - u[3] * l[3];
+        const double x0i = u[0] * l[1] + u[1] * l[0] + u[2] * l[3] + u[3] * l[2];
+        const double x1r = u[4] * l[0] - u[5] * l[1] + u[6] * l[2] - u[7] * l[3];
+        const double x1i = u[4] * l[1] + u[5] * l[0] + u[6] * l[3] + u[7] * l[2];
+        p[0] = n0r, p[1] = n0i, p[2] = n1r, p[3] = n1i;
+        l[0] = x0r, l[1] = x0i, l[2] = x1r, l[3] = x1i;
+    }
+}
+
+// Runs on up to 3 different wires, consecutive in the sweep and without
+// controls (cfg1: the rx, ry, rz runs of neighbouring wires in a layer): the
+// thread holds the 2^W amplitudes spanned by the W wires for psi and lambda
+// and applies run 0 on local bit 0 (its wire), then run 1 on local bit 1,
+// ... -- the sweep order -- so W runs cost one state round trip. Gradient
+// sums per thread in shared memory (registers go to the 4 W amplitudes).
+constexpr int kRunsMax = 3;
+struct AdjRuns {
+    int w = 0;
+    int sorted[kRunsMax];  // the wires' bits, ascending (index insertion order)
+    AdjRun r[kRunsMax];    // sweep order; run k acts on local bit k
+};
+
+template <typename T, int W>
+__global__ void __launch_bounds__(256, 2) adj_runs_kernel(typename Vec2<T>::type *__restrict__ psi,
+                                                          typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
+                                                          const AdjRuns g, double *__restrict__ part, int pb) {
+    constexpr int A = 1 << W, S = W * kRunMax;
+    __shared__ double sacc[256 * S];
+    double *acc = sacc + threadIdx.x * S;
+#pragma unroll
+    for (int j = 0; j < S; ++j) acc[j] = 0.0;
+    uint64_t off[A];
+#pragma unroll
+    for (int j = 0; j < A; ++j) {
+        off[j] = 0;
+#pragma unroll
+        for (int k = 0; k < W; ++k)
+            if ((j >> k) & 1) off[j] |= 1ull << g.r[k].t0;
+    }
+    for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < ngroups;
+         gi += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        uint64_t base = gi;
+#pragma unroll
+        for (int k = 0; k < W; ++k) base = insert_zero(base, g.sorted[k]);
+        double p[A][2], l[A][2];
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+            const auto a = psi[base | off[j]];
+            const auto b = lam[base | off[j]];
+            p[j][0] = a.x, p[j][1] = a.y, l[j][0] = b.x, l[j][1] = b.y;
+        }
+#pragma unroll
+        for (int r = 0; r < W; ++r)
+#pragma unroll
+            for (int j0 = 0; j0 < A; ++j0) {
+                if ((j0 >> r) & 1) continue;
+                const int j1 = j0 | (1 << r);
+                double pp[4] = {p[j0][0], p[j0][1], p[j1][0], p[j1][1]};
+                double ll[4] = {l[j0][0], l[j0][1], l[j1][0], l[j1][1]};
+                adj_run_steps(g.r[r], pp, ll, acc + r * kRunMax);
+                p[j0][0] = pp[0], p[j0][1] = pp[1], p[j1][0] = pp[2], p[j1][1] = pp[3];
+                l[j0][0] = ll[0], l[j0][1] = ll[1], l[j1][0] = ll[2], l[j1][1] = ll[3];
+            }
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+            typename Vec2<T>::type a, b;
+            a.x = static_cast<T>(p[j][0]), a.y = static_cast<T>(p[j][1]);
+            b.x = static_cast<T>(l[j][0]), b.y = static_cast<T>(l[j][1]);
+            psi[base | off[j]] = a;
+            lam[base | off[j]] = b;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < S) {
+        const int r = threadIdx.x / kRunMax, j = threadIdx.x % kRunMax;
+        if (j < g.r[r].nacc) {
+            double t = 0.0;
+            for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += sacc[i * S + threadIdx.x];
+            part[static_cast<size_t>(g.r[r].accslot[j]) * pb + blockIdx.x] = 2.0 * t;
+        }
+    }
+}
+
 // Gradient slot q = sum of its launch's per-block partials part[q * pb + b]
 // (the other entries stay zero): a fixed-order sum, no atomics contending on
 // one slot while the sweep runs.
@@ -498,6 +601,14 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
         const char *e = std::getenv("QSV_ADJ_NO_RUNS");
         return e && e[0] == '1';
     }();
+    static const int max_wires = [] {  // QSV_ADJ_RUN_WIRES=2|3: wires per multi-run kernel (A/B)
+        const char *e = std::getenv("QSV_ADJ_RUN_WIRES");
+        return e ? std::max(2, std::min(kRunsMax, std::atoi(e))) : kRunsMax;
+    }();
+    static const bool no_multi = [] {  // QSV_ADJ_NO_MULTI=1: one kernel per run (A/B)
+        const char *e = std::getenv("QSV_ADJ_NO_MULTI");
+        return e && e[0] == '1';
+    }();
     auto nparams_of = [&](int x) { return pbase[x] >= 0 || dbase[x] >= 0 ? bound[x].nparams : 0; };
     auto cmask_of = [&](int x) {
         uint64_t m = 0;
@@ -508,22 +619,26 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
         const GateRec &g = recs[i];
         require(g.k >= 1 && g.k <= 2, "adjoint_gradients: gates act on 1 or 2 targets");
         if (g.k == 1 && !no_runs && nparams_of(i) <= 3) {  // a run of single-qubit gates on this wire
-            const int t0 = perm[g.wires[0]];
-            const uint64_t cm = cmask_of(i);
-            int j = i, np = nparams_of(i);
-            while (j > 0 && i - j + 1 < kRunMax && recs[j - 1].k == 1 && perm[recs[j - 1].wires[0]] == t0 &&
-                   cmask_of(j - 1) == cm && nparams_of(j - 1) <= 3 && np + nparams_of(j - 1) <= kRunMax) {
-                --j;
-                np += nparams_of(j);
-            }
-            if (j < i) {
+            // the run of gates i, i-1, ..., j on gate i's wire and control mask
+            auto extent = [&](int top) {
+                const int t0 = perm[recs[top].wires[0]];
+                const uint64_t cm = cmask_of(top);
+                int j = top, np = nparams_of(top);
+                while (j > 0 && top - j + 1 < kRunMax && recs[j - 1].k == 1 && perm[recs[j - 1].wires[0]] == t0 &&
+                       cmask_of(j - 1) == cm && nparams_of(j - 1) <= 3 && np + nparams_of(j - 1) <= kRunMax) {
+                    --j;
+                    np += nparams_of(j);
+                }
+                return j;
+            };
+            auto make_run = [&](int top, int j) {
                 AdjRun r;
-                r.t0 = t0;
-                r.cmask = cm;
-                r.n = i - j + 1;
+                r.t0 = perm[recs[top].wires[0]];
+                r.cmask = cmask_of(top);
+                r.n = top - j + 1;
                 int acc = 0;
                 for (int k = 0; k < r.n; ++k) {
-                    const int x = i - k;  // sweep order
+                    const int x = top - k;  // sweep order
                     const GateRec &h = recs[x];
                     for (int rr = 0; rr < 2; ++rr)
                         for (int c = 0; c < 2; ++c) {
@@ -542,6 +657,47 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
                 }
                 r.first[r.n] = acc;
                 r.nacc = acc;
+                return r;
+            };
+            // consecutive uncontrolled runs on different wires: one kernel for up to 3
+            if (!no_multi && cmask_of(i) == 0) {
+                AdjRuns rs;
+                int top = i;
+                while (rs.w < max_wires && top >= 0 && recs[top].k == 1 && cmask_of(top) == 0 && nparams_of(top) <= 3) {
+                    const int t0 = perm[recs[top].wires[0]];
+                    bool dup = false;
+                    for (int k = 0; k < rs.w; ++k) dup = dup || rs.r[k].t0 == t0;
+                    if (dup) break;
+                    const int j = extent(top);
+                    rs.r[rs.w++] = make_run(top, j);
+                    top = j - 1;
+                }
+                if (rs.w >= 2) {
+                    for (int k = 0; k < rs.w; ++k) rs.sorted[k] = rs.r[k].t0;
+                    std::sort(rs.sorted, rs.sorted + rs.w);
+                    const uint64_t groups = N >> rs.w;
+                    const int blocks = static_cast<int>(
+                        std::max<uint64_t>(1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * 2)));
+                    auto *P64 = static_cast<float2 *>(psi.st.d);
+                    auto *L64 = static_cast<float2 *>(lam.st.d);
+                    auto *P128 = static_cast<double2 *>(psi.st.d);
+                    auto *L128 = static_cast<double2 *>(lam.st.d);
+                    if (dtype == QSV_C64) {
+                        if (rs.w == 2) adj_runs_kernel<float, 2><<<blocks, 256, 0, s>>>(P64, L64, groups, rs, d_part, pb);
+                        else adj_runs_kernel<float, 3><<<blocks, 256, 0, s>>>(P64, L64, groups, rs, d_part, pb);
+                    } else {
+                        if (rs.w == 2) adj_runs_kernel<double, 2><<<blocks, 256, 0, s>>>(P128, L128, groups, rs, d_part, pb);
+                        else adj_runs_kernel<double, 3><<<blocks, 256, 0, s>>>(P128, L128, groups, rs, d_part, pb);
+                    }
+                    QSV_CUDA(cudaGetLastError());
+                    i = top + 1;  // the loop's --i continues below the runs
+                    continue;
+                }
+            }
+            const int j = extent(i);
+            if (j < i) {
+                AdjRun r = make_run(i, j);
+                const int acc = r.nacc;
                 const uint64_t groups = N >> 1;
                 const int blocks = static_cast<int>(std::max<uint64_t>(
                     1, std::min<uint64_t>((groups + 255) / 256, ctx->sm_count * (acc ? bps : 8))));
