@@ -150,7 +150,7 @@ __device__ __forceinline__ uint64_t insert_zero(uint64_t x, int b) {
     return ((x >> b) << (b + 1)) | lo;
 }
 
-template <typename T, int K>
+template <typename T, int K, bool G>  // G: the gate has gradient parameters
 __global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *__restrict__ psi,
                                                        typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
                                                        const AdjGate g, double *__restrict__ part, int pb) {
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *_
             }
             nr[r] = xr, ni[r] = xi;
         }
-        for (int q = 0; q < g.nq; ++q) {
+        for (int q = 0; G && q < g.nq; ++q) {
             double s = 0.0;
 #pragma unroll
             for (int r = 0; r < D; ++r) {
@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256) adj_gate_kernel(typename Vec2<T>::type *_
             lam[base | off[r]] = b;
         }
     }
-    if (g.nq == 0) return;
+    if (!G || g.nq == 0) return;
     __shared__ double red[3][8];
     for (int q = 0; q < g.nq; ++q) {
         const double v = dev::warp_sum(acc[q]);
@@ -744,13 +744,13 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
         if (dtype == QSV_C64) {
             auto *P = static_cast<float2 *>(psi.st.d);
             auto *Lm = static_cast<float2 *>(lam.st.d);
-            if (g.k == 1) adj_gate_kernel<float, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
-            else adj_gate_kernel<float, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            if (g.k == 1) (a.nq ? adj_gate_kernel<float, 1, true> : adj_gate_kernel<float, 1, false>)<<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            else (a.nq ? adj_gate_kernel<float, 2, true> : adj_gate_kernel<float, 2, false>)<<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
         } else {
             auto *P = static_cast<double2 *>(psi.st.d);
             auto *Lm = static_cast<double2 *>(lam.st.d);
-            if (g.k == 1) adj_gate_kernel<double, 1><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
-            else adj_gate_kernel<double, 2><<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            if (g.k == 1) (a.nq ? adj_gate_kernel<double, 1, true> : adj_gate_kernel<double, 1, false>)<<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
+            else (a.nq ? adj_gate_kernel<double, 2, true> : adj_gate_kernel<double, 2, false>)<<<blocks, 256, 0, s>>>(P, Lm, groups, a, d_part, pb);
         }
         QSV_CUDA(cudaGetLastError());
     }
