@@ -245,13 +245,75 @@ struct AdjRun {
     int accslot[kRunMax];      // gradient slot of accumulator j
     double u[kRunMax][8];      // U^dagger of gate k, 2 x 2 row-major (re, im)
     double du[kRunMax][8];     // d U / d param of accumulator j
+    int ut[kRunMax];           // sparsity class of u[k] (mat_class), of du[j]
+    int dt[kRunMax];
 };
+
+// Sparsity class of a 2 x 2 complex matrix (re, im row-major): 1 diagonal
+// (rz, p), 2 real (ry), 3 real diagonal with imaginary off-diagonal (rx),
+// 0 general -- the products with exact zeros are not issued (FP64-bound
+// sweep; without fast-math a multiply by 0.0 is not folded).
+inline int mat_class(const double *m) {
+    if (m[2] == 0 && m[3] == 0 && m[4] == 0 && m[5] == 0) return 1;
+    if (m[1] == 0 && m[3] == 0 && m[5] == 0 && m[7] == 0) return 2;
+    if (m[1] == 0 && m[7] == 0 && m[2] == 0 && m[4] == 0) return 3;
+    return 0;
+}
+
+// y = M x for a 2 x 2 complex M of class ty; x, y = (x0r, x0i, x1r, x1i)
+__device__ __forceinline__ void cmv2(int ty, const double *m, const double *x, double *y) {
+    switch (ty) {
+    case 1:
+        y[0] = m[0] * x[0] - m[1] * x[1];
+        y[1] = m[0] * x[1] + m[1] * x[0];
+        y[2] = m[6] * x[2] - m[7] * x[3];
+        y[3] = m[6] * x[3] + m[7] * x[2];
+        break;
+    case 2:
+        y[0] = m[0] * x[0] + m[2] * x[2];
+        y[1] = m[0] * x[1] + m[2] * x[3];
+        y[2] = m[4] * x[0] + m[6] * x[2];
+        y[3] = m[4] * x[1] + m[6] * x[3];
+        break;
+    case 3:
+        y[0] = m[0] * x[0] - m[3] * x[3];
+        y[1] = m[0] * x[1] + m[3] * x[2];
+        y[2] = m[6] * x[2] - m[5] * x[1];
+        y[3] = m[6] * x[3] + m[5] * x[0];
+        break;
+    default:
+        y[0] = m[0] * x[0] - m[1] * x[1] + m[2] * x[2] - m[3] * x[3];
+        y[1] = m[0] * x[1] + m[1] * x[0] + m[2] * x[3] + m[3] * x[2];
+        y[2] = m[4] * x[0] - m[5] * x[1] + m[6] * x[2] - m[7] * x[3];
+        y[3] = m[4] * x[1] + m[5] * x[0] + m[6] * x[3] + m[7] * x[2];
+    }
+}
+
+// One run's steps on one amplitude pair: p = (psi0, psi1), l = (lambda0,
+// lambda1) as (re, im, re, im), in place; acc: the run's parameter sums.
+__device__ __forceinline__ void adj_run_steps(const AdjRun &g, double *p, double *l, double *acc) {
+#pragma unroll
+    for (int k = 0; k < kRunMax; ++k) {
+        if (k >= g.n) break;
+        double nv[4], xv[4];
+        cmv2(g.ut[k], g.u[k], p, nv);  // psi' = U^dag psi
+        for (int j = g.first[k]; j < g.first[k + 1]; ++j) {
+            double mv[4];
+            cmv2(g.dt[j], g.du[j], nv, mv);
+            acc[j] += l[0] * mv[0] + l[1] * mv[1] + l[2] * mv[2] + l[3] * mv[3];  // Re(conj(lambda) mu)
+        }
+        cmv2(g.ut[k], g.u[k], l, xv);  // lambda' = U^dag lambda
+        p[0] = nv[0], p[1] = nv[1], p[2] = nv[2], p[3] = nv[3];
+        l[0] = xv[0], l[1] = xv[1], l[2] = xv[2], l[3] = xv[3];
+    }
+}
 
 template <typename T>
 __global__ void __launch_bounds__(256, kRunMinBlocks) adj_run_kernel(typename Vec2<T>::type *__restrict__ psi,
                                                       typename Vec2<T>::type *__restrict__ lam, uint64_t ngroups,
                                                       const AdjRun g, double *__restrict__ part, int pb) {
-    double acc[kRunMax];
+    __shared__ double sacc[256 * kRunMax];  // per-thread gradient sums (indexed at run time)
+    double *acc = sacc + threadIdx.x * kRunMax;
 #pragma unroll
     for (int j = 0; j < kRunMax; ++j) acc[j] = 0.0;
     for (uint64_t gi = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; gi < ngroups;
@@ -260,33 +322,10 @@ __global__ void __launch_bounds__(256, kRunMinBlocks) adj_run_kernel(typename Ve
         if ((b0 & g.cmask) != g.cmask) continue;
         const uint64_t b1 = b0 | (1ull << g.t0);
         const auto a0 = psi[b0], a1 = psi[b1], c0 = lam[b0], c1 = lam[b1];
-        double p0r = a0.x, p0i = a0.y, p1r = a1.x, p1i = a1.y;
-        double l0r = c0.x, l0i = c0.y, l1r = c1.x, l1i = c1.y;
-#pragma unroll
-        for (int k = 0; k < kRunMax; ++k) {
-            if (k >= g.n) break;
-            const double *u = g.u[k];
-            const double n0r = u[0] * p0r - u[1] * p0i + u[2] * p1r - u[3] * p1i;
-            const double n0i = u[0] * p0i + u[1] * p0r + u[2] * p1i + u[3] * p1r;
-            const double n1r = u[4] * p0r - u[5] * p0i + u[6] * p1r - u[7] * p1i;
-            const double n1i = u[4] * p0i + u[5] * p0r + u[6] * p1i + u[7] * p1r;
-#pragma unroll
-            for (int j = 0; j < kRunMax; ++j) {
-                if (j < g.first[k] || j >= g.first[k + 1]) continue;
-                const double *d = g.du[j];
-                const double m0r = d[0] * n0r - d[1] * n0i + d[2] * n1r - d[3] * n1i;
-                const double m0i = d[0] * n0i + d[1] * n0r + d[2] * n1i + d[3] * n1r;
-                const double m1r = d[4] * n0r - d[5] * n0i + d[6] * n1r - d[7] * n1i;
-                const double m1i = d[4] * n0i + d[5] * n0r + d[6] * n1i + d[7] * n1r;
-                acc[j] += l0r * m0r + l0i * m0i + l1r * m1r + l1i * m1i;  // Re(conj(lambda) mu)
-            }
-            const double x0r = u[0] * l0r - u[1] * l0i + u[2] * l1r - u[3] * l1i;
-            const double x0i = u[0] * l0i + u[1] * l0r + u[2] * l1i + u[3] * l1r;
-            const double x1r = u[4] * l0r - u[5] * l0i + u[6] * l1r - u[7] * l1i;
-            const double x1i = u[4] * l0i + u[5] * l0r + u[6] * l1i + u[7] * l1r;
-            p0r = n0r, p0i = n0i, p1r = n1r, p1i = n1i;
-            l0r = x0r, l0i = x0i, l1r = x1r, l1i = x1i;
-        }
+        double p[4] = {a0.x, a0.y, a1.x, a1.y}, l[4] = {c0.x, c0.y, c1.x, c1.y};
+        adj_run_steps(g, p, l, acc);
+        const double p0r = p[0], p0i = p[1], p1r = p[2], p1i = p[3];
+        const double l0r = l[0], l0i = l[1], l1r = l[2], l1i = l[3];
         typename Vec2<T>::type v;
         v.x = static_cast<T>(p0r), v.y = static_cast<T>(p0i);
         psi[b0] = v;
@@ -297,47 +336,11 @@ __global__ void __launch_bounds__(256, kRunMinBlocks) adj_run_kernel(typename Ve
         v.x = static_cast<T>(l1r), v.y = static_cast<T>(l1i);
         lam[b1] = v;
     }
-    if (g.nacc == 0) return;
-    __shared__ double red[kRunMax][8];
-#pragma unroll
-    for (int j = 0; j < kRunMax; ++j) {
-        if (j >= g.nacc) break;
-        const double v = dev::warp_sum(acc[j]);
-        if ((threadIdx.x & 31) == 0) red[j][threadIdx.x >> 5] = v;
-    }
     __syncthreads();
     if (threadIdx.x < g.nacc) {
-        double s = 0.0;
-        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[threadIdx.x][w];
-        part[static_cast<size_t>(g.accslot[threadIdx.x]) * pb + blockIdx.x] = 2.0 * s;
-    }
-}
-
-// One run's steps on one amplitude pair: p = (psi0, psi1), l = (lambda0,
-// lambda1) as (re, im, re, im), in place; acc: the run's parameter sums.
-__device__ __forceinline__ void adj_run_steps(const AdjRun &g, double *p, double *l, double *acc) {
-#pragma unroll
-    for (int k = 0; k < kRunMax; ++k) {
-        if (k >= g.n) break;
-        const double *u = g.u[k];
-        const double n0r = u[0] * p[0] - u[1] * p[1] + u[2] * p[2] - u[3] * p[3];
-        const double n0i = u[0] * p[1] + u[1] * p[0] + u[2] * p[3] + u[3] * p[2];
-        const double n1r = u[4] * p[0] - u[5] * p[1] + u[6] * p[2] - u[7] * p[3];
-        const double n1i = u[4] * p[1] + u[5] * p[0] + u[6] * p[3] + u[7] * p[2];
-        for (int j = g.first[k]; j < g.first[k + 1]; ++j) {
-            const double *d = g.du[j];
-            const double m0r = d[0] * n0r - d[1] * n0i + d[2] * n1r - d[3] * n1i;
-            const double m0i = d[0] * n0i + d[1] * n0r + d[2] * n1i + d[3] * n1r;
-            const double m1r = d[4] * n0r - d[5] * n0i + d[6] * n1r - d[7] * n1i;
-            const double m1i = d[4] * n0i + d[5] * n0r + d[6] * n1i + d[7] * n1r;
-            acc[j] += l[0] * m0r + l[1] * m0i + l[2] * m1r + l[3] * m1i;  // Re(conj(lambda) mu)
-        }
-        const double x0r = u[0] * l[0] - u[1] * l[1] + u[2] * l[2] - u[3] * l[3];
-        const double x0i = u[0] * l[1] + u[1] * l[0] + u[2] * l[3] + u[3] * l[2];
-        const double x1r = u[4] * l[0] - u[5] * l[1] + u[6] * l[2] - u[7] * l[3];
-        const double x1i = u[4] * l[1] + u[5] * l[0] + u[6] * l[3] + u[7] * l[2];
-        p[0] = n0r, p[1] = n0i, p[2] = n1r, p[3] = n1i;
-        l[0] = x0r, l[1] = x0i, l[2] = x1r, l[3] = x1i;
+        double t = 0.0;
+        for (int i = 0; i < static_cast<int>(blockDim.x); ++i) t += sacc[i * kRunMax + threadIdx.x];
+        part[static_cast<size_t>(g.accslot[threadIdx.x]) * pb + blockIdx.x] = 2.0 * t;
     }
 }
 
@@ -384,17 +387,30 @@ __global__ void __launch_bounds__(256, 2) adj_runs_kernel(typename Vec2<T>::type
             p[j][0] = a.x, p[j][1] = a.y, l[j][0] = b.x, l[j][1] = b.y;
         }
 #pragma unroll
-        for (int r = 0; r < W; ++r)
+        for (int r = 0; r < W; ++r) {
+            const AdjRun &rr = g.r[r];
+            for (int k = 0; k < rr.n; ++k) {  // the run's gates in sweep order, every pair along local bit r
+                const double *u = rr.u[k];
+                const int ut = rr.ut[k];
 #pragma unroll
-            for (int j0 = 0; j0 < A; ++j0) {
-                if ((j0 >> r) & 1) continue;
-                const int j1 = j0 | (1 << r);
-                double pp[4] = {p[j0][0], p[j0][1], p[j1][0], p[j1][1]};
-                double ll[4] = {l[j0][0], l[j0][1], l[j1][0], l[j1][1]};
-                adj_run_steps(g.r[r], pp, ll, acc + r * kRunMax);
-                p[j0][0] = pp[0], p[j0][1] = pp[1], p[j1][0] = pp[2], p[j1][1] = pp[3];
-                l[j0][0] = ll[0], l[j0][1] = ll[1], l[j1][0] = ll[2], l[j1][1] = ll[3];
+                for (int j0 = 0; j0 < A; ++j0) {
+                    if ((j0 >> r) & 1) continue;
+                    const int j1 = j0 | (1 << r);
+                    const double pp[4] = {p[j0][0], p[j0][1], p[j1][0], p[j1][1]};
+                    const double ll[4] = {l[j0][0], l[j0][1], l[j1][0], l[j1][1]};
+                    double nv[4], xv[4];
+                    cmv2(ut, u, pp, nv);
+                    for (int j = rr.first[k]; j < rr.first[k + 1]; ++j) {
+                        double mv[4];
+                        cmv2(rr.dt[j], rr.du[j], nv, mv);
+                        acc[r * kRunMax + j] += ll[0] * mv[0] + ll[1] * mv[1] + ll[2] * mv[2] + ll[3] * mv[3];
+                    }
+                    cmv2(ut, u, ll, xv);
+                    p[j0][0] = nv[0], p[j0][1] = nv[1], p[j1][0] = nv[2], p[j1][1] = nv[3];
+                    l[j0][0] = xv[0], l[j0][1] = xv[1], l[j1][0] = xv[2], l[j1][1] = xv[3];
+                }
             }
+        }
 #pragma unroll
         for (int j = 0; j < A; ++j) {
             typename Vec2<T>::type a, b;
@@ -657,6 +673,8 @@ void fused_sweep(Ctx *ctx, int n, int dtype, const std::vector<qsv_gate> &bound,
                 }
                 r.first[r.n] = acc;
                 r.nacc = acc;
+                for (int k = 0; k < r.n; ++k) r.ut[k] = mat_class(r.u[k]);
+                for (int q = 0; q < acc; ++q) r.dt[q] = mat_class(r.du[q]);
                 return r;
             };
             // consecutive uncontrolled runs on different wires: one kernel for up to 3
