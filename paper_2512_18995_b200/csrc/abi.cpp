@@ -248,6 +248,11 @@ struct Lifted {
     std::vector<double> data;
     int rows = 0, slots = 0;
 };
+// Bytes of the parameters a gate uses (cache and policy keys: entries past
+// nparams may hold anything a C caller left there).
+size_t used_params(const qsv_gate &g) {
+    return sizeof(double) * static_cast<size_t>(std::min(3, std::max(0, static_cast<int>(g.nparams))));
+}
 bool liftable(const qsv_gate &g) {
     return g.trainable && !g.encode && g.nparams > 0 && std::strncmp(g.name, "custom", sizeof(g.name)) != 0;
 }
@@ -307,8 +312,8 @@ bool want_lift(Ctx &c, int n, int dtype, const qsv_opts *opts, const qsv_gate *g
         put(sk, &g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
                                sizeof(g.nparams));
         put(sk, &g.trainable, sizeof(g.trainable) + sizeof(g.encode));
-        if (l) put(vk, g.params, sizeof(g.params));
-        else if (!g.encode) put(sk, g.params, sizeof(g.params));
+        if (l) put(vk, g.params, used_params(g));
+        else if (!g.encode) put(sk, g.params, used_params(g));
         if (g.custom) {
             const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
             put(sk, g.custom, sizeof(double) * 2 * (1u << (2 * k)));
@@ -348,7 +353,7 @@ Plan &cached_plan(qsv_ctx *c, int n, int dtype, const qsv_opts *opts, const qsv_
         put(&g.nwires, sizeof(g.nwires) + sizeof(g.wires) + sizeof(g.ncontrols) + sizeof(g.controls) +
                            sizeof(g.nparams));
         put(&g.encode, sizeof(g.encode));
-        if (!g.encode) put(g.params, sizeof(g.params));
+        if (!g.encode) put(g.params, used_params(g));
         if (g.custom) {
             const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
             put(g.custom, sizeof(double) * 2 * (1u << (2 * k)));

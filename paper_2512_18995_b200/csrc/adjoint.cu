@@ -861,7 +861,7 @@ void adjoint_gradients(Ctx *ctx, int n, int dtype, const qsv_gate *gates, int ng
                     any = true;
                     put(vk, bound[i].params, sizeof(double) * bound[i].nparams);
                 } else {
-                    put(sk, g.params, sizeof(g.params));
+                    put(sk, g.params, sizeof(double) * std::min(3, std::max(0, static_cast<int>(g.nparams))));
                 }
                 if (g.custom) {
                     const int k = std::max(1, std::min(2, static_cast<int>(g.nwires)));
